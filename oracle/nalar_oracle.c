@@ -1,0 +1,281 @@
+/* nalar_oracle.c -- TEST INFRASTRUCTURE ONLY (see nalar_oracle.h).
+ *
+ * Plain, slow, single-threaded CPU oracle of the Nalar global controller's
+ * policy epoch (arXiv 2601.05109).  Written step by step in the order of the
+ * epoch definition (readings Q1-Q22 listed in
+ * DESIGN.md "Readings of the paper").  No blocking, fusion or reordering; the
+ * only library routine used is qsort (O6/O7 sort by the total order of O4).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section in brackets).
+ *
+ * Pins (tests/test_oracle_pins.py), each reaching the answer another way:
+ * brute-force path enumeration (depth), forward reachability (doom), closed
+ * forms (chains, fan-out/fan-in, the hand-derived C1 golden file
+ * tests/golden/c1_srtf.txt), brute-force subset enumeration of feasible
+ * admissions (lexicographically greatest admitted set), the closed-form slot
+ * list for phase B, SPEC worked examples, and invariants I1-I10.
+ */
+#include "nalar_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+enum { S_PENDING = 0, S_QUEUED = 1, S_RUNNING = 2, S_RESOLVED = 3, S_FAILED = 4 };
+enum { A_NONE = 0, A_SESSION = 1, A_STATEFUL = 2 };
+enum { O_RESOLVED = 0, O_FAILED = 1, O_INFLIGHT = 2, O_WAITING = 3, O_DOOMED = 4,
+       O_INELIGIBLE = 5, O_DEFERRED = 6, O_ASSIGNED = 7 };
+#define CALL_BIT 0x80000000u
+
+/* ------------------------------------------------------------------------ */
+/* Validation: the input contract of the "live future table" (Q1).           */
+/* Every dependency is write-once and must exist when its consumer is created */
+/* (SPEC S:50-52), so every edge points to an EARLIER row of the SAME workflow */
+/* (creation order is a topological order).                                   */
+/* ------------------------------------------------------------------------ */
+int oracle_validate(const oracle_table* t, int64_t* err_row) {
+    int64_t bad = -1;
+    uint32_t N = t->n_futures, W = t->n_workflows, I = t->n_instances, T = t->n_types;
+    if (err_row) *err_row = -1;
+    if (t->levels < 1 || t->levels > 256) return -1;
+    if (t->wf_fut_off[0] != 0 || t->wf_fut_off[W] != N) return -1;
+    for (uint32_t w = 0; w < W; ++w) {
+        if (t->wf_fut_off[w + 1] < t->wf_fut_off[w]) return -1;
+        if (w > 0 && t->wf_id[w] <= t->wf_id[w - 1]) return -1;
+    }
+    if (t->f_edge_off[0] != 0 || t->f_edge_off[N] != t->n_edges) return -1;
+    for (uint32_t f = 0; f < N; ++f)
+        if (t->f_edge_off[f + 1] < t->f_edge_off[f]) return -1;
+    for (uint32_t i = 0; i < I; ++i)
+        if (t->i_type[i] >= T) return -1;
+    for (uint32_t k = 0; k < T; ++k)
+        if (t->t_affinity[k] > A_STATEFUL) return -1;
+    for (uint32_t w = 0; w < W && bad < 0; ++w) {
+        for (uint32_t f = t->wf_fut_off[w]; f < t->wf_fut_off[w + 1]; ++f) {
+            int ok = 1;
+            uint8_t st = t->f_state[f], ty = t->f_type[f];
+            int pin = t->f_pin[f], ex = t->f_executor[f];
+            if (st > S_FAILED) ok = 0;
+            if (ty >= T) ok = 0;
+            if (ok && pin != -1 && (pin < 0 || (uint32_t)pin >= I || t->i_type[pin] != ty)) ok = 0;
+            if (ok && (st == S_QUEUED || st == S_RUNNING) &&
+                (ex < 0 || (uint32_t)ex >= I || t->i_type[ex] != ty)) ok = 0;
+            for (uint32_t e = t->f_edge_off[f]; ok && e < t->f_edge_off[f + 1]; ++e) {
+                uint32_t s = t->edges[e] & ~CALL_BIT;
+                if (s < t->wf_fut_off[w] || s >= f) ok = 0;
+            }
+            if (!ok) { bad = f; break; }
+        }
+    }
+    if (bad >= 0) { if (err_row) *err_row = bad; return -1; }
+    return 0;
+}
+
+/* total order of O4: f before g iff level[f] > level[g], or equal levels and
+ * f < g (tie-break by future id / row = (workflow_id, seq), Q8). */
+static const uint8_t* g_level;
+static int cmp_order(const void* a, const void* b) {
+    uint32_t f = *(const uint32_t*)a, g = *(const uint32_t*)b;
+    if (g_level[f] != g_level[g]) return g_level[f] > g_level[g] ? -1 : 1;
+    return f < g ? -1 : (f > g ? 1 : 0);
+}
+
+int oracle_epoch(const oracle_table* t, int policy, oracle_out* o) {
+    uint32_t N = t->n_futures, W = t->n_workflows, I = t->n_instances, T = t->n_types;
+    int64_t dummy;
+    if (oracle_validate(t, &dummy) != 0) return -1;
+
+    uint8_t* doomed = (uint8_t*)calloc(N ? N : 1, 1);
+    uint8_t* ready = (uint8_t*)calloc(N ? N : 1, 1);
+    uint8_t* eligible = (uint8_t*)calloc(N ? N : 1, 1);
+    uint32_t* wf_of = (uint32_t*)calloc(N ? N : 1, sizeof(uint32_t));
+    for (uint32_t w = 0; w < W; ++w)
+        for (uint32_t f = t->wf_fut_off[w]; f < t->wf_fut_off[w + 1]; ++f) wf_of[f] = w;
+
+    /* O1 topological sweep in row order (rows are topologically ordered, Q1).
+     * depth: longest path from a root over DEP u CALL edges; SRTF "later
+     *   stages of the graph" P:691 [§6.2], SPEC S:460 creation-chain depth (Q4);
+     *   u16 saturating (Q22).
+     * doomed: PENDING with a DEP predecessor FAILED or doomed, transitively
+     *   (failures are delivered like values; P:580-581 [§5]) (Q3).
+     * ready: PENDING, not doomed, every DEP predecessor RESOLVED -- push-based
+     *   readiness P:462-465 [§4.3.1], SPEC S:268-276 (Q2; CALL edges do not gate). */
+    for (uint32_t f = 0; f < N; ++f) {
+        uint32_t e0 = t->f_edge_off[f], e1 = t->f_edge_off[f + 1];
+        uint32_t d = 0;
+        int dm = 0, allres = 1;
+        for (uint32_t e = e0; e < e1; ++e) {
+            uint32_t s = t->edges[e] & ~CALL_BIT;
+            int is_call = (t->edges[e] & CALL_BIT) != 0;
+            uint32_t cand = (uint32_t)o->depth[s] + 1u;
+            if (cand > d) d = cand;
+            if (!is_call) {
+                if (t->f_state[s] == S_FAILED || doomed[s]) dm = 1;
+                if (t->f_state[s] != S_RESOLVED) allres = 0;
+            }
+        }
+        o->depth[f] = (uint16_t)(d > 65535u ? 65535u : d);
+        doomed[f] = (uint8_t)(t->f_state[f] == S_PENDING && dm);
+        ready[f] = (uint8_t)(t->f_state[f] == S_PENDING && !doomed[f] && allres);
+    }
+
+    /* O2 per-workflow aggregates ("aggregating metrics and metadata", P:338
+     * [§4.1]; per-session summaries SPEC S:365) and per-(w,t) facts used by
+     * eligibility. */
+    uint8_t* inflight_wt = (uint8_t*)calloc((size_t)(W ? W : 1) * (T ? T : 1), 1);
+    int64_t* first_pending = (int64_t*)malloc(sizeof(int64_t) * (size_t)(W ? W : 1) * (T ? T : 1));
+    int64_t* first_ready_unp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(W ? W : 1) * (T ? T : 1));
+    for (size_t k = 0; k < (size_t)W * T; ++k) { first_pending[k] = -1; first_ready_unp[k] = -1; }
+    for (uint32_t w = 0; w < W; ++w) {
+        uint32_t* a = o->wf_agg + (size_t)w * 10;
+        memset(a, 0, 10 * sizeof(uint32_t));
+        for (uint32_t f = t->wf_fut_off[w]; f < t->wf_fut_off[w + 1]; ++f) {
+            uint8_t st = t->f_state[f];
+            size_t wt = (size_t)w * T + t->f_type[f];
+            a[0] += 1;                                             /* total          */
+            if (st == S_PENDING) a[1] += 1;                        /* pending        */
+            if (ready[f]) a[2] += 1;                               /* ready          */
+            if (st == S_QUEUED || st == S_RUNNING) a[3] += 1;      /* in flight      */
+            if (st == S_RESOLVED) a[4] += 1;                       /* resolved       */
+            if (st == S_FAILED) a[5] += 1;                         /* failed         */
+            if (doomed[f]) a[6] += 1;                              /* doomed         */
+            if (st == S_PENDING && t->f_pin[f] != -1) a[7] += 1;   /* pinned pending */
+            if (o->depth[f] > a[8]) a[8] = o->depth[f];            /* max depth      */
+            if (t->f_round[f] > a[9]) a[9] = t->f_round[f];        /* max round      */
+            if (st == S_QUEUED || st == S_RUNNING) inflight_wt[wt] = 1;
+            if (st == S_PENDING && !doomed[f] && first_pending[wt] < 0) first_pending[wt] = f;
+            if (ready[f] && t->f_pin[f] == -1 && first_ready_unp[wt] < 0) first_ready_unp[wt] = f;
+        }
+    }
+
+    /* O3 eligibility of ready futures.
+     * stateful: "a single user request and a single session are scheduled in
+     *   order and routed to the same agent instance" P:267-268 [§3.4]; scope
+     *   (workflow, type), fence SPEC S:222 (Q12).
+     * managed state (SESSION): all requests of a session go to the same
+     *   instance P:575 [§5]; an unpinned session places only its first ready
+     *   future, the assignment creates the pin (Q13). */
+    uint32_t n_ready = 0, n_elig = 0, n_doomed = 0;
+    for (uint32_t f = 0; f < N; ++f) {
+        if (doomed[f]) n_doomed++;
+        if (!ready[f]) continue;
+        n_ready++;
+        size_t wt = (size_t)wf_of[f] * T + t->f_type[f];
+        uint8_t aff = t->t_affinity[t->f_type[f]];
+        int el;
+        if (aff == A_STATEFUL) el = !inflight_wt[wt] && first_pending[wt] == (int64_t)f;
+        else if (aff == A_SESSION && t->f_pin[f] == -1) el = first_ready_unp[wt] == (int64_t)f;
+        else el = 1;
+        eligible[f] = (uint8_t)el;
+        n_elig += (uint32_t)el;
+    }
+
+    /* O4 priority level of every non-terminal future (Q15):
+     *   level = clamp(prio[w] + score, 0, Lv-1) in 64-bit (Q7);
+     *   set_priority(session, value) P:389 [§4.2 tab:scheduling-API];
+     *   score: FCFS 0; SRTF depth (P:691 [§6.2]); LPT max round of the
+     *   workflow ("jobs that re-enter the graph", P:696 [§6.2]) (Q6). */
+    for (uint32_t f = 0; f < N; ++f) {
+        uint8_t st = t->f_state[f];
+        if (st == S_RESOLVED || st == S_FAILED) { o->level[f] = 0; continue; }
+        int64_t score = 0;
+        if (policy == 1) score = o->depth[f];
+        else if (policy == 2) score = o->wf_agg[(size_t)wf_of[f] * 10 + 9];
+        int64_t lv = (int64_t)t->wf_prio[wf_of[f]] + score;
+        if (lv < 0) lv = 0;
+        if (lv > (int64_t)t->levels - 1) lv = (int64_t)t->levels - 1;
+        o->level[f] = (uint8_t)lv;
+    }
+
+    /* O5 load and spare per instance: queue lengths + running (P:332-334
+     * [§4.1]); spare = max(0, cap - load), capacity hard (Q9). */
+    int64_t* spare = (int64_t*)calloc(I ? I : 1, sizeof(int64_t));
+    for (uint32_t i = 0; i < I; ++i) {
+        uint64_t load = t->i_base_load[i];
+        for (uint32_t f = 0; f < N; ++f)
+            if ((t->f_state[f] == S_QUEUED || t->f_state[f] == S_RUNNING) && t->f_executor[f] == (int)i)
+                load += 1;
+        o->i_load[i] = (uint32_t)(load > 0xFFFFFFFFull ? 0xFFFFFFFFull : load);
+        spare[i] = (int64_t)t->i_cap[i] - (int64_t)load;
+        if (spare[i] < 0) spare[i] = 0;
+        o->i_spare[i] = (uint32_t)spare[i];
+        o->i_assigned[i] = 0;
+    }
+
+    /* statuses before admission */
+    for (uint32_t f = 0; f < N; ++f) {
+        uint8_t st = t->f_state[f];
+        o->instance[f] = -1;
+        o->new_pin[f] = 0;
+        if (st == S_RESOLVED) o->status[f] = O_RESOLVED;
+        else if (st == S_FAILED) o->status[f] = O_FAILED;
+        else if (st == S_QUEUED || st == S_RUNNING) { o->status[f] = O_INFLIGHT; o->instance[f] = t->f_executor[f]; }
+        else if (doomed[f]) o->status[f] = O_DOOMED;
+        else if (!ready[f]) o->status[f] = O_WAITING;
+        else if (!eligible[f]) o->status[f] = O_INELIGIBLE;
+        else o->status[f] = O_DEFERRED;
+    }
+
+    uint32_t* buf = (uint32_t*)malloc(sizeof(uint32_t) * (N ? N : 1));
+    uint32_t na = 0;
+    g_level = o->level;
+
+    /* O6 phase A: pinned futures, route(session, agent-type, agent-instance)
+     * P:387 [§4.2]; a pin overrides weighted rules (Q10).
+     * Each instance independently admits its first min(|A|, spare) futures in
+     * the O4 order. */
+    for (uint32_t p = 0; p < I; ++p) {
+        uint32_t n = 0;
+        for (uint32_t f = 0; f < N; ++f)
+            if (eligible[f] && t->f_pin[f] == (int)p) buf[n++] = f;
+        qsort(buf, n, sizeof(uint32_t), cmp_order);
+        uint32_t adm = 0;
+        for (uint32_t k = 0; k < n; ++k) {
+            if ((int64_t)adm < spare[p]) {
+                uint32_t f = buf[k];
+                o->status[f] = O_ASSIGNED;
+                o->instance[f] = (int16_t)p;
+                o->assign_row[na] = f;
+                o->assign_inst[na] = (int16_t)p;
+                na++;
+                adm++;
+            }
+        }
+        spare[p] -= adm;
+        o->i_assigned[p] += adm;
+    }
+
+    /* O7 phase B: unpinned futures, weighted route(agent-type, instances,
+     * weights) P:388 with weights proportional to spare in its
+     * exact-integer form: literal sequential greedy, each future in O4 order
+     * goes to the instance of its type with the most spare, ties to the lowest
+     * instance id ("actively balances load ... through routing") (Q11). */
+    for (uint32_t ty = 0; ty < T; ++ty) {
+        uint32_t n = 0;
+        for (uint32_t f = 0; f < N; ++f)
+            if (eligible[f] && t->f_pin[f] == -1 && t->f_type[f] == ty) buf[n++] = f;
+        qsort(buf, n, sizeof(uint32_t), cmp_order);
+        for (uint32_t k = 0; k < n; ++k) {
+            uint32_t f = buf[k];
+            int64_t best = -1, best_sp = 0;
+            for (uint32_t i = 0; i < I; ++i)
+                if (t->i_type[i] == ty && spare[i] > best_sp) { best = i; best_sp = spare[i]; }
+            if (best < 0) continue;                       /* no spare: DEFERRED */
+            spare[best] -= 1;
+            o->i_assigned[best] += 1;
+            o->status[f] = O_ASSIGNED;
+            o->instance[f] = (int16_t)best;
+            o->new_pin[f] = (uint8_t)(t->t_affinity[ty] != A_NONE);
+            o->assign_row[na] = f;
+            o->assign_inst[na] = (int16_t)best;
+            na++;
+        }
+    }
+
+    o->n_assigned = na;
+    o->n_ready = n_ready;
+    o->n_eligible = n_elig;
+    o->n_doomed = n_doomed;
+    free(buf); free(spare); free(inflight_wt); free(first_pending); free(first_ready_unp);
+    free(doomed); free(ready); free(eligible); free(wf_of);
+    return 0;
+}

@@ -1,0 +1,61 @@
+/* nalar_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * The plain, slow, single-threaded CPU oracle of the Nalar policy epoch
+ * (arXiv 2601.05109).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it.  It shares no code,
+ * header, table or constant with the CUDA library (include/nalar.h); the two
+ * meet only at the input data format defined in nalar_gen/snapshot.py.
+ */
+#ifndef NALAR_ORACLE_H
+#define NALAR_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    uint32_t n_futures, n_edges, n_workflows, n_instances, n_types, levels;
+    const uint64_t* wf_id;      /* [W]   */
+    const uint32_t* wf_fut_off; /* [W+1] */
+    const int32_t*  wf_prio;    /* [W]   */
+    const uint8_t*  f_state;    /* [N]   */
+    const uint8_t*  f_type;
+    const uint8_t*  f_round;
+    const int16_t*  f_executor;
+    const int16_t*  f_pin;
+    const uint32_t* f_edge_off; /* [N+1] */
+    const uint32_t* edges;      /* [E]   */
+    const uint8_t*  i_type;     /* [I]   */
+    const uint32_t* i_cap;
+    const uint32_t* i_base_load;
+    const uint8_t*  t_affinity; /* [T]   */
+} oracle_table;
+
+typedef struct {
+    uint8_t*  status;     /* [N] */
+    uint8_t*  level;      /* [N] */
+    uint16_t* depth;      /* [N] */
+    int16_t*  instance;   /* [N] */
+    uint8_t*  new_pin;    /* [N] */
+    uint32_t* wf_agg;     /* [W*10] */
+    uint32_t* i_load;     /* [I] */
+    uint32_t* i_spare;    /* [I] spare before admission */
+    uint32_t* i_assigned; /* [I] */
+    uint32_t* assign_row; /* [N] capacity; (resource, global rank) order */
+    int16_t*  assign_inst;/* [N] */
+    uint32_t  n_assigned; /* out */
+    uint32_t  n_ready, n_eligible, n_doomed; /* out */
+} oracle_out;
+
+/* 0 = valid, -1 = invalid; *err_row = smallest offending future row, or -1
+ * when the violation is not attributable to a row. */
+int oracle_validate(const oracle_table* t, int64_t* err_row);
+
+/* policy: 0 FCFS, 1 SRTF, 2 LPT.  Returns 0, or -1 on an invalid table. */
+int oracle_epoch(const oracle_table* t, int policy, oracle_out* o);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,105 @@
+"""ctypes loader for oracle/liboracle.so (TEST INFRASTRUCTURE ONLY).
+
+Builds the C oracle with gcc -O2 (no SIMD intrinsics, no threads) on first
+use.  Inputs are nalar_gen.Snapshot objects; outputs are numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SRC = os.path.join(HERE, "nalar_oracle.c")
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+
+POLICIES = {"fcfs": 0, "srtf": 1, "lpt": 2}
+
+
+class _Table(C.Structure):
+    _fields_ = [("n_futures", C.c_uint32), ("n_edges", C.c_uint32), ("n_workflows", C.c_uint32),
+                ("n_instances", C.c_uint32), ("n_types", C.c_uint32), ("levels", C.c_uint32),
+                ("wf_id", C.c_void_p), ("wf_fut_off", C.c_void_p), ("wf_prio", C.c_void_p),
+                ("f_state", C.c_void_p), ("f_type", C.c_void_p), ("f_round", C.c_void_p),
+                ("f_executor", C.c_void_p), ("f_pin", C.c_void_p), ("f_edge_off", C.c_void_p),
+                ("edges", C.c_void_p), ("i_type", C.c_void_p), ("i_cap", C.c_void_p),
+                ("i_base_load", C.c_void_p), ("t_affinity", C.c_void_p)]
+
+
+class _Out(C.Structure):
+    _fields_ = [("status", C.c_void_p), ("level", C.c_void_p), ("depth", C.c_void_p),
+                ("instance", C.c_void_p), ("new_pin", C.c_void_p), ("wf_agg", C.c_void_p),
+                ("i_load", C.c_void_p), ("i_spare", C.c_void_p), ("i_assigned", C.c_void_p),
+                ("assign_row", C.c_void_p), ("assign_inst", C.c_void_p),
+                ("n_assigned", C.c_uint32), ("n_ready", C.c_uint32), ("n_eligible", C.c_uint32),
+                ("n_doomed", C.c_uint32)]
+
+
+_lib = None
+
+
+def build_oracle(force: bool = False) -> str:
+    if force or not os.path.exists(ORACLE_SO) or \
+            os.path.getmtime(ORACLE_SO) < os.path.getmtime(ORACLE_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", ORACLE_SO,
+                               ORACLE_SRC])
+    return ORACLE_SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        _lib = C.CDLL(ORACLE_SO)
+        _lib.oracle_validate.argtypes = [C.POINTER(_Table), C.POINTER(C.c_int64)]
+        _lib.oracle_epoch.argtypes = [C.POINTER(_Table), C.c_int, C.POINTER(_Out)]
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p) if a.size else C.c_void_p(0)
+
+
+def _table(s, levels):
+    arrs = s.arrays()
+    t = _Table(s.n_futures, s.n_edges, s.n_workflows, s.n_instances, s.n_types, levels,
+               *[_ptr(arrs[k]) for k in ("wf_id", "wf_fut_off", "wf_prio", "f_state", "f_type",
+                                         "f_round", "f_executor", "f_pin", "f_edge_off", "edges",
+                                         "i_type", "i_cap", "i_base_load", "t_affinity")])
+    return t, arrs   # keep arrays alive
+
+
+def oracle_validate(s, levels: int = 256):
+    lib = _load()
+    t, keep = _table(s, levels)
+    err = C.c_int64(-1)
+    rc = lib.oracle_validate(C.byref(t), C.byref(err))
+    return rc, err.value
+
+
+def oracle_epoch(s, policy="srtf", levels: int = 256) -> dict:
+    lib = _load()
+    pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+    t, keep = _table(s, levels)
+    N, W, I = s.n_futures, s.n_workflows, s.n_instances
+    out = {
+        "status": np.zeros(N, np.uint8), "level": np.zeros(N, np.uint8),
+        "depth": np.zeros(N, np.uint16), "instance": np.zeros(N, np.int16),
+        "new_pin": np.zeros(N, np.uint8), "wf_agg": np.zeros((W, 10), np.uint32),
+        "i_load": np.zeros(I, np.uint32), "i_spare": np.zeros(I, np.uint32),
+        "i_assigned": np.zeros(I, np.uint32), "assign_row": np.zeros(max(N, 1), np.uint32),
+        "assign_inst": np.zeros(max(N, 1), np.int16),
+    }
+    o = _Out(*[_ptr(out[k]) for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg",
+                                      "i_load", "i_spare", "i_assigned", "assign_row",
+                                      "assign_inst")], 0, 0, 0, 0)
+    rc = lib.oracle_epoch(C.byref(t), pol, C.byref(o))
+    if rc != 0:
+        raise ValueError("oracle: invalid table")
+    na = o.n_assigned
+    out["assign_row"] = out["assign_row"][:na].copy()
+    out["assign_inst"] = out["assign_inst"][:na].copy()
+    out["n_ready"], out["n_eligible"], out["n_doomed"] = o.n_ready, o.n_eligible, o.n_doomed
+    return out

@@ -1,0 +1,379 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+Each test pins the oracle to something other than itself: a hand-derived
+golden file, brute-force enumeration, closed forms, SPEC worked examples and
+invariants.  Citations: P:n = PAPER.md line n; S:n = SPEC.md line n.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from nalar_gen import (AFF_NONE, AFF_SESSION, AFF_STATEFUL, FAILED, PENDING, QUEUED, RESOLVED,
+                       RUNNING, TableBuilder, c1, c2, c4, random_table)
+from oracle import oracle_epoch, oracle_validate
+from tests import bruteforce as bf
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "c1_srtf.txt")
+S_RES, S_FAIL, S_INF, S_WAIT, S_DOOM, S_INEL, S_DEF, S_ASG = range(8)
+
+
+def _read_golden():
+    rows, kv = [], {}
+    for line in open(GOLD):
+        line = line.split("#")[0].strip()
+        if not line:
+            continue
+        parts = line.split()
+        if parts[0].isdigit():
+            rows.append([int(x) for x in parts[2:]])
+        else:
+            kv[parts[0]] = [int(x) for x in parts[1:]]
+    return np.array(rows), kv
+
+
+# --------------------------------------------------------------------------
+# C1: hand-derived golden output (tests/golden/c1_srtf.txt)
+# --------------------------------------------------------------------------
+def test_c1_golden_srtf():
+    rows, kv = _read_golden()
+    o = oracle_epoch(c1(), "srtf")
+    assert o["status"].tolist() == rows[:, 0].tolist()
+    assert o["depth"].tolist() == rows[:, 1].tolist()
+    assert o["level"].tolist() == rows[:, 2].tolist()
+    assert o["instance"].tolist() == rows[:, 3].tolist()
+    assert o["new_pin"].tolist() == rows[:, 4].tolist()
+    assert o["wf_agg"][0].tolist() == kv["wf_agg"]
+    assert o["i_load"].tolist() == kv["i_load"]
+    assert o["i_spare"].tolist() == kv["i_spare"]
+    assert o["i_assigned"].tolist() == kv["i_assigned"]
+    assert o["assign_row"].tolist() == kv["assign_row"]
+    assert o["assign_inst"].tolist() == kv["assign_inst"]
+    assert set(o["status"].tolist()) == set(range(8))       # every status occurs
+
+
+@pytest.mark.parametrize("pol,key", [("lpt", "lpt_level"), ("fcfs", "fcfs_level")])
+def test_c1_golden_other_policies(pol, key):
+    rows, kv = _read_golden()
+    o = oracle_epoch(c1(), pol)
+    assert o["level"].tolist() == kv[key]
+    assert o["status"].tolist() == rows[:, 0].tolist()
+    assert o["instance"].tolist() == rows[:, 3].tolist()
+
+
+# --------------------------------------------------------------------------
+# O1: depth / doom / readiness against brute force
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", range(300))
+def test_depth_doom_ready_bruteforce(seed):
+    s = random_table(seed, n_workflows=3, max_rows=9, max_preds=3)
+    o = oracle_epoch(s, "srtf")
+    doomed = bf.doomed_by_reachability(s)
+    for f in range(s.n_futures):
+        assert o["depth"][f] == bf.depth_by_path_enumeration(s, f), (seed, f)
+        st = int(s.f_state[f])
+        ready = st == PENDING and not doomed[f] and all(
+            s.f_state[p] == RESOLVED for (p, _) in bf.preds(s, f, "dep"))
+        if st == RESOLVED:
+            assert o["status"][f] == S_RES
+        elif st == FAILED:
+            assert o["status"][f] == S_FAIL
+        elif st in (QUEUED, RUNNING):
+            assert o["status"][f] == S_INF and o["instance"][f] == s.f_executor[f]
+        elif doomed[f]:
+            assert o["status"][f] == S_DOOM, (seed, f)
+        elif not ready:
+            assert o["status"][f] == S_WAIT, (seed, f)
+        else:
+            assert o["status"][f] in (S_INEL, S_DEF, S_ASG), (seed, f)
+
+
+def _chain(n, prio=0, call_every=0, rounds=None):
+    tb = TableBuilder(i_type=[0], i_cap=[0], i_base_load=[0], t_affinity=[AFF_NONE])
+    rows = []
+    for j in range(n):
+        preds = [] if j == 0 else [(j - 1, bool(call_every and j % call_every == 0))]
+        rows.append((PENDING, 0, 0 if rounds is None else rounds[j], -1, -1, preds))
+    tb.add_workflow(1, prio, rows)
+    return tb.build()
+
+
+def test_depth_chain_closed_form_and_saturation():
+    # a chain of n has depth n-1 at its tail; levels saturate at Lv-1 (Q7)
+    s = _chain(300, prio=-5, call_every=7)
+    o = oracle_epoch(s, "srtf")
+    assert o["depth"].tolist() == list(range(300))
+    assert o["level"].tolist() == [min(255, max(0, d - 5)) for d in range(300)]
+    o = oracle_epoch(s, "srtf", levels=16)
+    assert o["level"].max() == 15
+
+
+def test_c2_depth_closed_form():
+    # Financial Analyst shape: plan 0 / specialists 1 / summarize 2 (fan-out/fan-in)
+    s = c2(seed=2, n_workflows=50)
+    o = oracle_epoch(s, "srtf")
+    assert o["depth"].reshape(50, 10).tolist() == [[0] + [1] * 8 + [2]] * 50
+
+
+def test_readiness_spec_examples():
+    # {d1,d2}: d1 delivered -> still waiting; both -> queued(ready);
+    # a duplicated dependency is idempotent.
+    def table(st1, st2, dup):
+        tb = TableBuilder(i_type=[0], i_cap=[5], i_base_load=[0], t_affinity=[AFF_NONE])
+        p = [(0, False), (1, False)] + ([(0, False)] if dup else [])
+        tb.add_workflow(1, 0, [(st1, 0, 0, 0 if st1 == RUNNING else -1, -1, []),
+                               (st2, 0, 0, 0 if st2 == RUNNING else -1, -1, []),
+                               (PENDING, 0, 0, -1, -1, p)])
+        return tb.build()
+    assert oracle_epoch(table(RESOLVED, RUNNING, False))["status"][2] == S_WAIT
+    assert oracle_epoch(table(RESOLVED, RESOLVED, False))["status"][2] == S_ASG
+    assert oracle_epoch(table(RESOLVED, RESOLVED, True))["status"][2] == S_ASG
+    # CALL edges do not gate readiness (Q2) but count for depth (Q4)
+    tb = TableBuilder(i_type=[0], i_cap=[5], i_base_load=[0], t_affinity=[AFF_NONE])
+    tb.add_workflow(1, 0, [(RUNNING, 0, 0, 0, -1, []), (PENDING, 0, 0, -1, -1, [(0, True)])])
+    o = oracle_epoch(tb.build())
+    assert o["status"][1] == S_ASG and o["depth"][1] == 1
+
+
+# --------------------------------------------------------------------------
+# O4 order: SPEC worked examples
+# --------------------------------------------------------------------------
+def _one_slot_table(entries, aff=AFF_NONE, cap=1):
+    """entries: list of (prio, depth_chain_len, round) -> one workflow each whose
+    last row is a ready future of type 0; one instance with `cap` spare."""
+    tb = TableBuilder(i_type=[0], i_cap=[cap], i_base_load=[0], t_affinity=[aff])
+    for w, (prio, d, rd) in enumerate(entries):
+        rows = [(RESOLVED, 0, rd, 0, -1, [] if j == 0 else [(j - 1, False)]) for j in range(d)]
+        rows.append((PENDING, 0, rd, -1, -1, [(d - 1, False)] if d else []))
+        tb.add_workflow(w + 1, prio, rows)
+    return tb.build()
+
+
+def _winner(s, pol):
+    o = oracle_epoch(s, pol)
+    return [int(r) for r in np.nonzero(o["status"] == S_ASG)[0]]
+
+
+def test_spec_priority_and_fifo():
+    # S:284 queue [p=0 t=1, p=5 t=2] -> picks p=5 (set_priority P:389)
+    s = _one_slot_table([(0, 0, 0), (5, 0, 0)])
+    assert _winner(s, "fcfs") == [1]
+    # S:285 equal priorities -> earlier one wins (tie-break by future id, Q8)
+    s = _one_slot_table([(3, 0, 0), (3, 0, 0)])
+    assert _winner(s, "fcfs") == [0]
+
+
+def test_spec_srtf_depth():
+    # S:464 futures at depths 1 and 3 -> depth-3 future first
+    s = _one_slot_table([(0, 1, 0), (0, 3, 0)])
+    assert _winner(s, "srtf") == [2 + 3]      # rows: w0 = 0..1, w1 = 2..5
+    assert _winner(s, "fcfs") == [1]
+
+
+def test_spec_lpt_reentry():
+    # S:475 session with 2 requeues vs fresh -> requeued first
+    s = _one_slot_table([(0, 0, 0), (0, 0, 2)])
+    assert _winner(s, "lpt") == [1]
+    assert _winner(s, "fcfs") == [0]
+
+
+# --------------------------------------------------------------------------
+# O6/O7 admission + placement: brute force on tiny tables
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", range(400))
+def test_admission_bruteforce(seed):
+    s = random_table(1000 + seed, n_workflows=3, max_rows=5, n_types=2, inst_per_type=(0, 2),
+                     max_cap=3, max_base=2)
+    o = oracle_epoch(s, ["fcfs", "srtf", "lpt"][seed % 3])
+    I = s.n_instances
+    elig = [f for f in range(s.n_futures) if o["status"][f] in (S_DEF, S_ASG)]
+    if len(elig) > 10:
+        pytest.skip("too many for brute force")
+    key = lambda f: (-int(o["level"][f]), f)
+    order = sorted(elig, key=key)                   # library sort (O4 order)
+    # load / spare from the definition, counted independently
+    load = [int(s.i_base_load[i]) + sum(1 for f in range(s.n_futures)
+                                         if s.f_state[f] in (QUEUED, RUNNING)
+                                         and s.f_executor[f] == i) for i in range(I)]
+    spare = [max(0, int(s.i_cap[i]) - load[i]) for i in range(I)]
+    assert o["i_load"].tolist() == load and o["i_spare"].tolist() == spare
+    # phase A: lexicographically greatest admitted set under per-pin capacity
+    pinned = [f for f in order if s.f_pin[f] >= 0]
+    admA = bf.lexmax_admission(pinned, {f: int(s.f_pin[f]) for f in pinned},
+                               {i: spare[i] for i in range(I)})
+    for f in pinned:
+        assert (o["status"][f] == S_ASG) == (f in admA), (seed, f)
+        if f in admA:
+            assert o["instance"][f] == s.f_pin[f]
+    spare2 = list(spare)
+    for f in admA:
+        spare2[int(s.f_pin[f])] -= 1
+    # phase B per type: lexmax under the type's total spare; placement = slot list
+    for t in range(s.n_types):
+        inst = [i for i in range(I) if s.i_type[i] == t]
+        unp = [f for f in order if s.f_pin[f] < 0 and s.f_type[f] == t]
+        admB = bf.lexmax_admission(unp, {f: t for f in unp}, {t: sum(spare2[i] for i in inst)})
+        slots = bf.slot_list([spare2[i] for i in inst])
+        k = 0
+        for f in unp:
+            assert (o["status"][f] == S_ASG) == (f in admB), (seed, f)
+            if f in admB:
+                assert o["instance"][f] == inst[slots[k]], (seed, f)
+                assert o["new_pin"][f] == int(s.t_affinity[t] != AFF_NONE)
+                k += 1
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_water_fill_equals_slot_enumeration(seed):
+    rng = np.random.default_rng(seed)
+    n_i = int(rng.integers(1, 6))
+    caps = rng.integers(0, 6, n_i)
+    n_f = int(rng.integers(0, 20))
+    tb = TableBuilder(i_type=[0] * n_i, i_cap=caps, i_base_load=[0] * n_i, t_affinity=[AFF_NONE])
+    tb.add_workflow(1, 0, [(PENDING, 0, 0, -1, -1, [])] * n_f)
+    o = oracle_epoch(tb.build(), "fcfs")
+    got = [int(o["instance"][f]) for f in range(n_f) if o["status"][f] == S_ASG]
+    assert got == bf.slot_list([int(c) for c in caps])[:n_f]
+
+
+def test_water_fill_hand_check():
+    # spares (3,1,3) -> i0,i2,i0,i2,i0,i1,i2
+    assert bf.slot_list([3, 1, 3]) == [0, 2, 0, 2, 0, 1, 2]
+    tb = TableBuilder(i_type=[0] * 3, i_cap=[3, 1, 3], i_base_load=[0] * 3, t_affinity=[AFF_NONE])
+    tb.add_workflow(1, 0, [(PENDING, 0, 0, -1, -1, [])] * 8)
+    o = oracle_epoch(tb.build(), "fcfs")
+    assert o["instance"].tolist() == [0, 2, 0, 2, 0, 1, 2, -1]
+    assert o["status"][7] == S_DEF
+
+
+def test_spec_load_balance_examples():
+    # S:434 queues (0,0) -> equal share; S:435 queues (4,0), C=4 -> all to the
+    # idle instance; S:436 single instance -> everything to it.
+    def run(caps, bases, n):
+        tb = TableBuilder(i_type=[0] * len(caps), i_cap=caps, i_base_load=bases,
+                          t_affinity=[AFF_NONE])
+        tb.add_workflow(1, 0, [(PENDING, 0, 0, -1, -1, [])] * n)
+        return oracle_epoch(tb.build(), "fcfs")["instance"].tolist()
+    assert run([4, 4], [0, 0], 4) == [0, 1, 0, 1]
+    assert run([4, 4], [4, 0], 4) == [1, 1, 1, 1]
+    assert run([4], [0], 3) == [0, 0, 0]
+
+
+def test_spec_pin_precedence_and_stateful():
+    # a pinned session goes to its pin even when a peer has more spare.
+    tb = TableBuilder(i_type=[0, 0], i_cap=[1, 5], i_base_load=[0, 0], t_affinity=[AFF_SESSION])
+    tb.add_workflow(1, 0, [(PENDING, 0, 0, -1, 0, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"][0] == S_ASG and o["instance"][0] == 0 and o["new_pin"][0] == 0
+    # S:256 / P:267: stateful -- a second future of the same session is not
+    # placed while the first is in flight; then it goes to the same instance.
+    tb = TableBuilder(i_type=[0, 0], i_cap=[5, 5], i_base_load=[0, 0], t_affinity=[AFF_STATEFUL])
+    tb.add_workflow(1, 0, [(RUNNING, 0, 0, 1, 1, []), (PENDING, 0, 0, -1, 1, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"][1] == S_INEL
+    tb = TableBuilder(i_type=[0, 0], i_cap=[5, 5], i_base_load=[0, 0], t_affinity=[AFF_STATEFUL])
+    tb.add_workflow(1, 0, [(RESOLVED, 0, 0, 1, 1, []), (PENDING, 0, 0, -1, 1, []),
+                           (PENDING, 0, 0, -1, 1, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"].tolist() == [S_RES, S_ASG, S_INEL] and o["instance"][1] == 1
+    # stateful in-order: the lowest pending future must go first even if a
+    # later one is ready (fence S:222)
+    tb = TableBuilder(i_type=[0], i_cap=[5], i_base_load=[0], t_affinity=[AFF_STATEFUL])
+    tb.add_workflow(1, 0, [(RUNNING, 0, 0, 0, -1, []), (PENDING, 0, 0, -1, -1, [(0, False)]),
+                           (PENDING, 0, 0, -1, -1, [])])
+    tb.add_workflow(2, 0, [(PENDING, 0, 0, -1, -1, []), (PENDING, 0, 0, -1, -1, [(0, True)])])
+    o = oracle_epoch(tb.build())
+    assert o["status"].tolist() == [S_INF, S_WAIT, S_INEL, S_ASG, S_INEL]
+    # a doomed future never runs, so it does not fence its session (Q3, Q12)
+    tb = TableBuilder(i_type=[0], i_cap=[5], i_base_load=[0], t_affinity=[AFF_STATEFUL])
+    tb.add_workflow(1, 0, [(FAILED, 0, 0, 0, -1, []), (PENDING, 0, 0, -1, -1, [(0, False)]),
+                           (PENDING, 0, 0, -1, -1, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"].tolist() == [S_FAIL, S_DOOM, S_ASG]
+
+
+# --------------------------------------------------------------------------
+# invariants I1-I10 on generated workloads
+# --------------------------------------------------------------------------
+def _check_invariants(s, o):
+    N, I = s.n_futures, s.n_instances
+    st = o["status"]
+    # I10 conservation
+    assert np.bincount(st, minlength=8).sum() == N
+    agg = o["wf_agg"]
+    assert agg[:, 0].sum() == N
+    assert (agg[:, 1] + agg[:, 3] + agg[:, 4] + agg[:, 5] == agg[:, 0]).all()
+    sizes = np.diff(s.wf_fut_off.astype(np.int64))
+    assert (agg[:, 0] == sizes).all()
+    asg = np.nonzero(st == S_ASG)[0]
+    for f in asg:
+        # I1 readiness safety
+        assert s.f_state[f] == PENDING
+        for (p, _) in bf.preds(s, int(f), "dep"):
+            assert s.f_state[p] == RESOLVED
+        # I7 pinned futures only go to their pin; instance type matches
+        if s.f_pin[f] >= 0:
+            assert o["instance"][f] == s.f_pin[f]
+        assert s.i_type[o["instance"][f]] == s.f_type[f]
+    # I2 capacity
+    cnt = np.bincount(o["instance"][asg].astype(np.int64), minlength=I) if I else np.zeros(0)
+    assert (cnt == o["i_assigned"]).all()
+    load = o["i_load"].astype(np.int64)
+    assert (load + cnt <= np.maximum(s.i_cap.astype(np.int64), load)).all()
+    # I4 no inversion inside a resource, I5 work conservation
+    after = o["i_spare"].astype(np.int64) - cnt
+    assert (after >= 0).all()
+    lv = o["level"].astype(np.int64)
+    for f in np.nonzero(st == S_DEF)[0]:
+        if s.f_pin[f] >= 0:
+            same = asg[s.f_pin[asg] == s.f_pin[f]]
+            assert after[s.f_pin[f]] == 0
+        else:
+            same = asg[(s.f_pin[asg] < 0) & (s.f_type[asg] == s.f_type[f])]
+            assert (after[s.i_type == s.f_type[f]] == 0).all()
+        for g in same:
+            assert (lv[g], -g) > (lv[f], -f)
+    # I6 stateful: at most one placed per (w, stateful type), none if one is in flight
+    wf = np.repeat(np.arange(s.n_workflows), np.diff(s.wf_fut_off.astype(np.int64)))
+    for t in np.nonzero(s.t_affinity == AFF_STATEFUL)[0]:
+        for w in range(s.n_workflows):
+            m = (wf == w) & (s.f_type == t)
+            if (m & (st == S_ASG)).sum():
+                assert (m & (st == S_ASG)).sum() == 1 and (m & (st == S_INF)).sum() == 0
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_invariants_random(seed):
+    s = random_table(5000 + seed, n_workflows=6, max_rows=12, n_types=3, consistent=seed % 2 == 0)
+    o = oracle_epoch(s, ["fcfs", "srtf", "lpt"][seed % 3])
+    _check_invariants(s, o)
+
+
+def test_invariants_c2_c4():
+    for s in (c2(seed=1), c4(seed=2)):
+        for pol in ("srtf", "lpt"):
+            o = oracle_epoch(s, pol)
+            _check_invariants(s, o)
+            # I9 run-to-run bit identity
+            o2 = oracle_epoch(s, pol)
+            for k in ("status", "level", "depth", "instance", "new_pin", "assign_row"):
+                assert (o[k] == o2[k]).all()
+
+
+# --------------------------------------------------------------------------
+# input contract (Q1): invalid tables are rejected with the first bad row
+# --------------------------------------------------------------------------
+def test_validation():
+    assert oracle_validate(c1()) == (0, -1)
+    s = c1(); s.edges[3] = 23                      # row 3 (test0) -> later row
+    assert oracle_validate(s) == (-1, 3)
+    s = c1(); s.f_pin[7] = 0                       # TOOL future pinned to an LLM instance
+    assert oracle_validate(s) == (-1, 7)
+    s = c1(); s.f_executor[3] = -1                 # RUNNING without executor
+    assert oracle_validate(s) == (-1, 3)
+    s = c1(); s.f_state[4] = 9
+    assert oracle_validate(s) == (-1, 4)
+    s = c2(seed=1, n_workflows=3); s.edges[-1] = 5  # edge into another workflow
+    assert oracle_validate(s)[0] == -1 and oracle_validate(s)[1] == 29
+    s = c2(seed=1, n_workflows=3); s.wf_id[2] = s.wf_id[1]
+    assert oracle_validate(s) == (-1, -1)
