@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the policy epoch: futures/s and epoch latency (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl nalar|reference]
+
+Workload: the SWE-recursive future table (SURVEY §8(d) C4/C5 recipe, DESIGN.md
+"Input recipe") with 2^17 futures per GPU -- at N=1 exactly the paper-scale
+C4 table (131,072 futures, 64 instances, state affinity), at N=8 the C5 scale-
+out table (2^20 futures) sharded by workflow id.  One step = one policy epoch
+(SRTF, the paper's scalability policy) over the whole table:
+K1 sweep -> [NCCL allreduce] -> K4 assign.  Inputs are resident in HBM before
+the timed region; L2 is flushed (256 MB memset, untimed) before every epoch.
+Under torchrun each rank owns one shard, NCCL carries the per-epoch exchange.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FUT_PER_GPU = 1 << 17
+METRIC = "futures scheduled/sec and policy-epoch latency at 130K futures, 1/2/4/8 B200"
+
+
+def nearest_rank(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = max(1, int(np.ceil(q / 100.0 * len(xs))))
+    return xs[k - 1]
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_table(n_gpus, seed):
+    from nalar_gen import swe_table
+    return swe_table(n_gpus * FUT_PER_GPU, seed=seed, name="C4" if n_gpus == 1 else "C5")
+
+
+def workload_config(n_gpus, table, policy):
+    return {"workload": ("C4 paper-scale SWE-recursive future table" if n_gpus == 1 else
+                         f"C5 scale-out SWE-recursive table sharded by workflow id over {n_gpus} GPUs"),
+            "futures_total": table.n_futures, "futures_per_gpu": FUT_PER_GPU,
+            "workflows": table.n_workflows, "edges": table.n_edges,
+            "instances": table.n_instances, "types": table.n_types, "policy": policy.upper(),
+            "levels": 256, "l2": "flushed between epochs (256 MB memset, untimed)",
+            "parallelism": f"workflow-sharded x{n_gpus}" + (" + NCCL allreduce" if n_gpus > 1 else "")}
+
+
+def oracle_time(s, policy, budget_s, min_runs=1, max_runs=10**6):
+    """Time the CPU oracle as it stands on one host core."""
+    from oracle import oracle_epoch
+    try:
+        cpus = sorted(os.sched_getaffinity(0))
+        os.sched_setaffinity(0, {cpus[-1]})
+    except Exception:
+        cpus = None
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while (len(times) < min_runs or time.perf_counter() < t_end) and len(times) < max_runs:
+        t0 = time.perf_counter()
+        oracle_epoch(s, policy)
+        times.append(time.perf_counter() - t0)
+    if cpus:
+        os.sched_setaffinity(0, set(cpus))
+    return times
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except Exception:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def k1_algorithmic_bytes(s, n_elig):
+    """SURVEY §8(d) byte model recomputed for this layout:
+    per future 11 B read (state, type, round, executor, pin, edge_off) + 7 B
+    written (status, level, depth, instance, new_pin); 4 B per edge; per
+    workflow 48 B (offset, prio, 10 aggregates); 8 B per eligible item."""
+    return 18 * s.n_futures + 4 * s.n_edges + 48 * s.n_workflows + 8 * n_elig
+
+
+def k4_algorithmic_bytes(R, levels, G, n_elig, n_asg):
+    return 4 * R * levels * G + 8 * n_elig + 10 * n_asg
+
+
+def load_traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle (this tier's reference arm) on host cores."""
+    if rank != 0:
+        return
+    table = make_table(world, args.seed)
+    from oracle import build_oracle
+    build_oracle()
+    oracle_time(table, args.policy, 0, min_runs=args.warmup, max_runs=args.warmup)
+    times = oracle_time(table, args.policy, 0, min_runs=args.steps, max_runs=args.steps)
+    mean = float(np.mean(times))
+    value = table.n_futures / mean
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "futures/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": workload_config(world, table, args.policy),
+            "cpu_baseline": {"value": value, "unit": "futures/s", "cores": 1, "kind": "oracle",
+                             "sample": f"full table ({table.n_futures} futures) x {args.steps} epochs, "
+                                       f"single-threaded C oracle (gcc -O2) on 1 core of {cpu_model()}"},
+            "e2e": {"value": value, "unit": "futures/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "epoch_ms_p50": nearest_rank([t * 1e3 for t in times], 50),
+            "epoch_ms_p99": nearest_rank([t * 1e3 for t in times], 99)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="nalar", choices=["nalar", "reference"])
+    ap.add_argument("--policy", default="srtf", choices=["fcfs", "srtf", "lpt"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--e2e-steps", type=int, default=30)
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if world == 1:
+        world = 1
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2601_05109_b200 import nalar
+    from paper_2601_05109_b200.sharding import shard_bounds
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    table = make_table(world, args.seed)
+    w0, w1 = shard_bounds(table.wf_fut_off, world)[rank]
+    s = table.slice_workflows(w0, w1) if world > 1 else table
+    pol = nalar.POLICIES[args.policy]
+
+    nccl_id = None
+    if world > 1:
+        obj = [nalar.nalar_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def new_ctx(flags=0):
+        return nalar.Context(max(s.n_futures, 1), max(s.n_edges, 1), max(s.n_workflows, 1),
+                             s.n_instances, s.n_types, device=local, rank=rank, world=world,
+                             nccl_id=nccl_id, flags=flags)
+
+    ctx = new_ctx()
+    ctx.upload(s)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed_epochs(n, do_flush, clocks=None):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(n)]
+        barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for a, b in ev:
+                if do_flush:
+                    flush.zero_()
+                a.record(stream)
+                ctx.epoch(pol)
+                b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        t = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
+    # warm-up (also builds the CUDA graph)
+    timed_epochs(args.warmup, True)
+    with ClockSampler(local) as clk:
+        ms = timed_epochs(args.steps, True)
+    ms_warm = timed_epochs(args.steps, False)
+    st = ctx.stats()
+    mean_ms = float(np.mean(ms))
+    total_fut = table.n_futures
+    value = total_fut / (mean_ms / 1e3)
+
+    # per-kernel device times (CUDA events captured inside the epoch graph)
+    tctx = new_ctx(flags=nalar.NALAR_F_TIMING)
+    tctx.upload(s)
+    k1, k4, coll = [], [], []
+    tstream = torch.cuda.ExternalStream(tctx.stream)
+    for i in range(args.warmup + args.steps):
+        with torch.cuda.stream(tstream):
+            flush.zero_()
+        tctx.epoch(pol)
+        ts = tctx.stats()
+        if i >= args.warmup:
+            k1.append(ts.k1_us); k4.append(ts.k4_us); coll.append(ts.coll_us)
+    tctx.close()
+    k1_us, k4_us, coll_us = float(np.mean(k1)), float(np.mean(k4)), float(np.mean(coll))
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    R = s.n_instances + s.n_types
+    b1 = k1_algorithmic_bytes(s, st.n_eligible)
+    b4 = k4_algorithmic_bytes(R, 256, world, st.n_eligible, st.n_assigned)
+    dom, dom_us, dom_b = ("k1_sweep", k1_us, b1) if k1_us >= k4_us else ("k4_assign", k4_us, b4)
+    achieved = dom_b / (dom_us * 1e-6) / 1e9
+    traffic = load_traffic(dom)
+
+    # end to end through the public API: pinned host table -> upload (H2D +
+    # validate) -> epoch -> fetch decisions (D2H), every step
+    keep = []
+
+    def pinned_like(a):
+        t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        keep.append(t)
+        v = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+        v[...] = a
+        return v
+    from nalar_gen import Snapshot
+    sp = Snapshot(global_row_base=s.global_row_base, name=s.name,
+                  **{k: pinned_like(a) for k, a in s.arrays().items()})
+    h2d = sum(a.nbytes for a in sp.arrays().values())
+
+    def pin_alloc(n, dt):
+        return pinned_like(np.zeros(n, dt))
+    outb = ctx.output_buffers(("status", "instance", "assign"), alloc=pin_alloc)
+    e2e_t = []
+    n_asg = 0
+    for i in range(3 + args.e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        ctx.upload(sp)
+        ctx.epoch(pol)
+        r = ctx.fetch(("status", "instance", "assign"), out=outb)
+        dt = time.perf_counter() - t0
+        n_asg = r["n_assigned"]
+        if i >= 3:
+            e2e_t.append(dt)
+    et = torch.tensor(e2e_t, dtype=torch.float64)
+    if world > 1:
+        et = et.cuda()
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_mean = float(et.cpu().mean())
+    d2h = 3 * s.n_futures + 6 * n_asg + 32
+
+    line = {"metric": METRIC, "value": value, "unit": "futures/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": workload_config(world, table, args.policy),
+            "epoch_us_p50": nearest_rank(list(ms * 1e3), 50),
+            "epoch_us_p99": nearest_rank(list(ms * 1e3), 99),
+            "warm_l2": {"ms_per_step": float(np.mean(ms_warm)),
+                        "value": total_fut / (float(np.mean(ms_warm)) / 1e3)},
+            "kernels_us": {"k1_sweep": k1_us, "allreduce": coll_us, "k4_assign": k4_us},
+            "counts": {"ready": st.n_ready, "eligible": st.n_eligible, "assigned": st.n_assigned,
+                       "doomed": st.n_doomed},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": dom_b, "peak_source": peak_src},
+            "e2e": {"value": total_fut / e2e_mean, "unit": "futures/s", "ms_per_step": e2e_mean * 1e3,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+            "paper_context": "464 ms per global-control-loop at 131K futures, Python+gRPC+Redis on "
+                             "64 emulated CPU nodes (PAPER.md:715); context, not the target"}
+    if rank == 0 and world == 1:
+        from oracle import build_oracle
+        build_oracle()
+        times = oracle_time(table, args.policy, args.cpu_budget, min_runs=3)
+        line["cpu_baseline"] = {"value": table.n_futures / float(np.mean(times)), "unit": "futures/s",
+                                "cores": 1, "kind": "oracle",
+                                "sample": f"C4 full table ({table.n_futures} futures) x {len(times)} "
+                                          f"epochs (~{args.cpu_budget:.0f} s), single-threaded C "
+                                          f"oracle on 1 core of {cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/* nalar.h -- C ABI of the B200 policy-epoch library (libnalar.so).
+ *
+ * The data-parallel hot path of Nalar's global controller (arXiv 2601.05109):
+ * one POLICY EPOCH over the live future table.  "Running periodically, the
+ * global controller tracks the global state ... by aggregating metrics and
+ * metadata from component-level controllers ..., computing decisions related
+ * (for request routing, prioritization, and resource allocation) and pushing
+ * the computed decisions" (PAPER.md:338 [§4.1]); the single-threaded policy loop
+ * (PAPER.md:364 [§4.2]) is re-expressed as sm_100a kernels that reproduce its
+ * sequential definition bit for bit (readings Q1-Q22).
+ *
+ * Three calls carry the path:
+ *   nalar_snapshot_upload  -- the "collect" hand-off: host SoA table -> HBM,
+ *                             validated
+ *   nalar_policy_epoch     -- readiness, depth, doom, per-workflow aggregates,
+ *                             priority key, load, capacity-limited assignment
+ *   nalar_fetch_decisions  -- the "push" hand-off: decisions -> host
+ *                             (route / set_priority)
+ *
+ * Conventions
+ *  - Every function returns NALAR_OK (0) or a negative nalar_err.  Nothing
+ *    throws or aborts; nalar_last_error(ctx) describes the last failure.
+ *  - Ownership: the library owns all device memory it allocates (sized once at
+ *    nalar_create from the reservations in nalar_config), or carves it out of
+ *    caller memory given in nalar_config.workspace.  Input host pointers are
+ *    borrowed only for the duration of a call.  Outputs go to caller buffers.
+ *  - Call order: upload -> epoch -> fetch; fetch/epoch before any successful
+ *    upload return NALAR_E_STATE.  A ctx is not thread-safe.
+ *  - Multi-GPU: one ctx per GPU/rank; every rank uploads its contiguous
+ *    workflow range (plus the replicated instance and type tables) and calls
+ *    every function; nalar_policy_epoch is then a collective.
+ *  - No CPU fallback: without a usable sm_100 device nalar_create fails.
+ */
+#ifndef NALAR_H
+#define NALAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NALAR_ABI_VERSION 1
+
+/* limits (DESIGN.md §3 "Data layout") */
+#define NALAR_MAX_LEVELS     256      /* level is u8                          */
+#define NALAR_MAX_TYPES      64
+#define NALAR_MAX_INSTANCES  1024     /* instance ids are i16; R = I + T       */
+#define NALAR_MAX_ROWS       0x7FFFFFFFu /* edge rows use 31 bits              */
+#define NALAR_CALL_EDGE      0x80000000u /* edges[] bit 31: CALL (creator) edge */
+#define NALAR_WF_AGG_FIELDS  10
+
+typedef struct nalar_ctx nalar_ctx; /* opaque; one per GPU / rank */
+
+enum nalar_err {
+    NALAR_OK = 0,
+    NALAR_E_INVAL = -1,   /* malformed snapshot or argument (see upload)     */
+    NALAR_E_STATE = -2,   /* call out of order                               */
+    NALAR_E_NOMEM = -3,   /* snapshot exceeds the reservation / alloc failed */
+    NALAR_E_SIZE = -4,    /* caller output buffer too small (sizes written)  */
+    NALAR_E_CUDA = -5,    /* CUDA runtime error / no sm_100 device           */
+    NALAR_E_COMM = -6,    /* NCCL error                                      */
+    NALAR_E_NOTIMPL = -7
+};
+
+/* per-future lifecycle, collapsed from SPEC S:46-53 (DESIGN.md Q-state) */
+enum nalar_state { NALAR_PENDING = 0, NALAR_QUEUED = 1, NALAR_RUNNING = 2,
+                   NALAR_RESOLVED = 3, NALAR_FAILED = 4 };
+/* per-type state-placement directive: managed state = SESSION,
+ * `stateful` directive = STATEFUL */
+enum nalar_aff { NALAR_AFF_NONE = 0, NALAR_AFF_SESSION = 1, NALAR_AFF_STATEFUL = 2 };
+/* priority score: FCFS, SRTF "later stages of the graph",
+ * LPT "jobs that re-enter the graph" */
+enum nalar_policy { NALAR_FCFS = 0, NALAR_SRTF = 1, NALAR_LPT = 2 };
+/* per-future decision */
+enum nalar_status { NALAR_S_RESOLVED = 0, NALAR_S_FAILED = 1, NALAR_S_INFLIGHT = 2,
+                    NALAR_S_WAITING = 3, NALAR_S_DOOMED = 4, NALAR_S_INELIGIBLE = 5,
+                    NALAR_S_DEFERRED = 6, NALAR_S_ASSIGNED = 7 };
+/* how ranks exchange the per-epoch histogram / load buffer (world > 1) */
+enum nalar_collective { NALAR_COLL_NONE = 0,     /* world == 1                       */
+                        NALAR_COLL_NCCL = 1,     /* library-owned ncclComm, in-graph */
+                        NALAR_COLL_EXTERNAL = 2  /* caller sums the exchange buffer
+                                                    between epoch_begin / finish      */ };
+/* nalar_config.flags */
+#define NALAR_F_TIMING          1u  /* record per-kernel CUDA events (stats)      */
+#define NALAR_F_NO_GRAPH        2u  /* launch kernels directly, no CUDA graph     */
+#define NALAR_F_FORCE_UNSTAGED  4u  /* test knob: K1 reads HBM, no smem staging   */
+
+typedef struct {
+    int      device;          /* CUDA ordinal                                      */
+    int      rank, world;     /* world == 1: single GPU                            */
+    int      collective;      /* nalar_collective                                  */
+    unsigned char nccl_id[128]; /* ncclUniqueId from nalar_nccl_unique_id() on rank 0,
+                                 broadcast by the caller (NALAR_COLL_NCCL only)    */
+    void*    stream;          /* cudaStream_t to run on (e.g. torch's), NULL = own */
+    void*    workspace;       /* optional caller device memory, >= nalar_workspace_bytes() */
+    size_t   workspace_bytes;
+    uint32_t levels;          /* Lv, 1..256 (default 256 when 0)                   */
+    uint32_t max_futures, max_edges, max_workflows, max_instances, max_types;
+    uint32_t flags;           /* NALAR_F_*                                         */
+} nalar_config;
+
+/* The live future table, structure-of-arrays, rows in (workflow_id, seq) order
+ * (creation order within a workflow).  HOST pointers (pageable or pinned),
+ * borrowed for the call.  Field meanings: future metadata PAPER.md:469-485
+ * (dependencies, creator, executor), session ids PAPER.md:519, instance metrics
+ * PAPER.md:332-334, directives PAPER.md:242-258.
+ *   wf_fut_off[W+1]: rows of workflow w are [wf_fut_off[w], wf_fut_off[w+1])
+ *   f_edge_off[N+1], edges[E]: CSR predecessor lists; edges[e] bits 0..30 =
+ *     predecessor row (an EARLIER row of the SAME workflow), bit 31 =
+ *     NALAR_CALL_EDGE for the creator (CALL) edge, 0 for a DEP (argument) edge
+ *   f_executor: instance a QUEUED/RUNNING future sits at (-1 otherwise)
+ *   f_pin: session home instance of the future (state placement), -1 none
+ *   global_row_base: index of row 0 in the all-rank row order (multi-GPU)   */
+typedef struct {
+    uint32_t n_futures, n_edges, n_workflows, n_instances, n_types;
+    uint64_t global_row_base;
+    const uint64_t* wf_id;       /* [W] strictly increasing                  */
+    const uint32_t* wf_fut_off;  /* [W+1]                                    */
+    const int32_t*  wf_prio;     /* [W] set_priority value     */
+    const uint8_t*  f_state;     /* [N] nalar_state                          */
+    const uint8_t*  f_type;      /* [N] < n_types                            */
+    const uint8_t*  f_round;     /* [N] retry round (LPT input)              */
+    const int16_t*  f_executor;  /* [N]                                      */
+    const int16_t*  f_pin;       /* [N]                                      */
+    const uint32_t* f_edge_off;  /* [N+1]                                    */
+    const uint32_t* edges;       /* [E]                                      */
+    const uint8_t*  i_type;      /* [I] < n_types                            */
+    const uint32_t* i_cap;       /* [I] capacity (queue + running)           */
+    const uint32_t* i_base_load; /* [I] load outside the table               */
+    const uint8_t*  t_affinity;  /* [T] nalar_aff                            */
+} nalar_snapshot;
+
+/* Caller-allocated HOST output buffers; any pointer may be NULL (skipped).
+ * *_cap = capacity in elements.  On NALAR_E_SIZE the n_* fields hold the
+ * required sizes and nothing is copied. */
+typedef struct {
+    uint8_t*  status;     /* [N] nalar_status                                  */
+    uint8_t*  level;      /* [N] priority level, 0 for terminal futures        */
+    uint16_t* depth;      /* [N] longest DEP u CALL path from a root (sat. u16) */
+    int16_t*  instance;   /* [N] executor (INFLIGHT) / assigned (ASSIGNED) / -1 */
+    uint8_t*  new_pin;    /* [N] 1 = assignment creates the session's pin       */
+    uint32_t  f_cap;
+    uint32_t* wf_agg;     /* [W][10] total, pending, ready, inflight, resolved,
+                             failed, doomed, pinned_pending, max_depth, max_round */
+    uint32_t  wf_cap;
+    uint32_t* i_load;     /* [I] base_load + in-flight futures of ALL ranks      */
+    uint32_t* i_spare;    /* [I] max(0, cap - load) before this epoch's admission */
+    uint32_t* i_assigned; /* [I] futures of ALL ranks assigned this epoch        */
+    uint32_t  i_cap;
+    uint32_t* assign_row; /* [n_assigned] this rank's assigned rows, ordered by
+                             (resource, global rank); resource = pin for pinned
+                             futures, I + type for unpinned ones               */
+    int16_t*  assign_inst;/* [n_assigned] their instances                      */
+    uint32_t  a_cap;
+    uint32_t  n_f, n_w, n_i, n_assigned;  /* out */
+} nalar_decisions;
+
+/* TickReport analog. */
+typedef struct {
+    float    epoch_us;        /* device time of the last epoch (NALAR_F_TIMING)  */
+    float    k1_us, coll_us, k4_us;
+    uint32_t n_futures, n_ready, n_eligible, n_assigned, n_deferred, n_doomed, n_instances;
+} nalar_epoch_stats;
+
+/* Bytes of device workspace nalar_create needs for cfg's reservations. */
+size_t nalar_workspace_bytes(const nalar_config* cfg);
+
+/* Fill out[128] with a fresh ncclUniqueId (call on rank 0 only; loads NCCL). */
+int nalar_nccl_unique_id(unsigned char out[128]);
+
+/* Create a context on cfg->device: allocate/carve device memory, create the
+ * stream (if none given) and, for NALAR_COLL_NCCL, the communicator
+ * (collective over all ranks).  E_INVAL on bad limits, E_CUDA without an
+ * sm_100 device, E_COMM on NCCL failure. */
+int nalar_create(nalar_ctx** out, const nalar_config* cfg);
+int nalar_destroy(nalar_ctx* ctx);
+
+/* Copy a snapshot to HBM and validate it (stream-ordered, then synchronises).
+ * E_NOMEM if a size exceeds the reservation; E_INVAL if: offsets are not
+ * monotone / do not start at 0 / end at N or E; wf_id not strictly
+ * increasing; a state > 4, type >= T, affinity > 2 or instance type >= T; a
+ * pin not naming an instance of the future's type; a QUEUED/RUNNING future
+ * without an executor of its type; an edge not pointing to an earlier row of
+ * the same workflow.  *err_row (may be NULL) = smallest offending row, or -1
+ * when the error is not attributable to a row. */
+int nalar_snapshot_upload(nalar_ctx* ctx, const nalar_snapshot* snap, int64_t* err_row);
+
+/* One policy epoch over the uploaded table (nalar_policy).  Asynchronous on
+ * the ctx stream; a collective over all ranks when world > 1 (NCCL mode).
+ * Repeated epochs on the same upload are idempotent. */
+int nalar_policy_epoch(nalar_ctx* ctx, int policy);
+
+/* NALAR_COLL_EXTERNAL: the epoch in two halves around a caller-side sum of
+ * the exchange buffer (u32 words, slot-disjoint histogram + per-instance load,
+ * DESIGN.md §5) over all ranks.  *dev_ptr is device memory owned by ctx. */
+int nalar_epoch_begin(nalar_ctx* ctx, int policy);
+int nalar_exchange_buffer(nalar_ctx* ctx, void** dev_ptr, size_t* n_words);
+int nalar_epoch_finish(nalar_ctx* ctx);
+
+/* Copy decisions to caller host buffers; synchronises the ctx stream. */
+int nalar_fetch_decisions(nalar_ctx* ctx, nalar_decisions* out);
+
+/* Counters (and kernel times with NALAR_F_TIMING) of the last epoch; syncs. */
+int nalar_epoch_stats_get(nalar_ctx* ctx, nalar_epoch_stats* stats);
+
+/* Device stream the ctx runs on (cudaStream_t). */
+void* nalar_stream(nalar_ctx* ctx);
+
+const char* nalar_last_error(const nalar_ctx* ctx);
+int nalar_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NALAR_H */

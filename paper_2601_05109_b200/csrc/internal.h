@@ -1,0 +1,104 @@
+// internal.h -- device-side parameter blocks and launch declarations shared by
+// the host context (nalar_ctx.cu) and the kernels (k_*.cu) of libnalar.so.
+// Nothing here is part of the C ABI (see include/nalar.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define NALAR_MAX_INSTANCES_DEV 1024
+
+namespace nalar {
+
+constexpr int kK0Threads = 256;          // validate: warp per workflow
+constexpr int kK1Threads = 256;          // sweep: warp per workflow inside a block
+constexpr int kK1Warps = kK1Threads / 32;
+constexpr int kK4Threads = 256;          // assign: one block per resource
+constexpr int kK4Warps = kK4Threads / 32;
+
+// per-row flags produced by the sweep
+enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4 };
+
+// indices into the per-epoch counters array (scratch)
+enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_TICKET = 4, C_NUM = 8 };
+
+// bytes of K1 shared memory that do not scale with the block's rows
+size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
+// bytes of K1 shared memory needed to stage a block of `rows` rows / `edges` edges
+size_t k1_staged_smem(uint32_t rows, uint32_t edges);
+
+struct ValidateParams {
+    const uint32_t* wf_fut_off;
+    const uint8_t* f_state;
+    const uint8_t* f_type;
+    const int16_t* f_exec;
+    const int16_t* f_pin;
+    const uint32_t* f_edge_off;
+    const uint32_t* edges;
+    const uint8_t* i_type;
+    uint32_t n_wf, n_fut, n_edges, n_types, n_inst;
+    unsigned long long* err;   // [0] = min bad row (init ~0), [1] = structural flag
+};
+
+struct SweepParams {
+    const uint32_t* wf_fut_off;
+    const int32_t* wf_prio;
+    const uint8_t* f_state;
+    const uint8_t* f_type;
+    const uint8_t* f_round;
+    const int16_t* f_exec;
+    const int16_t* f_pin;
+    const uint32_t* f_edge_off;
+    const uint32_t* edges;
+    const uint8_t* t_aff;
+    const uint32_t* blk_wf;     // [B+1] workflow range of each block
+    const uint32_t* blk_row0;   // [B+1] first row of each block
+    const uint32_t* blk_edge0;  // [B+1] first edge of each block
+    const uint8_t* blk_staged;  // [B]   1 = rows staged in shared memory by TMA
+    uint32_t B, n_types, n_inst, R, levels, policy;
+    uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
+    uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
+    // outputs
+    uint8_t* status;
+    uint8_t* level;
+    uint16_t* depth;
+    int16_t* instance;
+    uint8_t* new_pin;
+    uint32_t* wf_agg;           // [W][10]
+    uint32_t* H;                // this rank's histogram slot [R][Lv]
+    uint32_t* load_part;        // [I] in-flight counts of this rank's rows
+    uint2* items;               // [N] eligible (row, level), per-block regions
+    uint32_t* cnt_rb;           // [R][B]
+    uint32_t* off_rb;           // [R][B]
+    uint32_t* counters;         // C_*
+};
+
+struct AssignParams {
+    const uint32_t* H;          // [G][R][Lv] summed over ranks
+    const uint32_t* load_sum;   // [I] summed over ranks
+    uint32_t G, slot, R, n_inst, n_types, levels, B;
+    const uint8_t* i_type;
+    const uint32_t* i_cap;
+    const uint32_t* i_base;
+    const uint8_t* t_aff;
+    const uint32_t* cnt_rb;
+    const uint32_t* off_rb;
+    const uint32_t* blk_row0;
+    const uint2* items;
+    // outputs
+    uint8_t* status;
+    int16_t* instance;
+    uint8_t* new_pin;
+    uint32_t* i_load;
+    uint32_t* i_spare;
+    uint32_t* i_assigned;
+    uint32_t* assign_row;
+    int16_t* assign_inst;
+    uint32_t* adm_pub;          // [R] published per-resource admitted counts
+    uint32_t* counters;
+};
+
+cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);
+cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s);
+cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
+
+}  // namespace nalar

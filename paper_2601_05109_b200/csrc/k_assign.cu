@@ -1,0 +1,328 @@
+// k_assign.cu -- K4: capacity-constrained assignment, one CTA per resource.
+//
+// Resource r < I is instance r (phase A: futures pinned to it, route(session,
+// agent-type, agent-instance) PAPER.md:387); resource I + t is type t (phase B:
+// unpinned futures, route(agent-type, instances, weights) PAPER.md:388, with
+// weights proportional to spare in exact integer water-fill form, "actively
+// balances load ... through routing" PAPER.md:663).
+//
+// The sequential definition (admit futures in (level desc, row
+// asc) order while spare remains; phase B to the most-spare instance, ties to
+// the lowest id) is reproduced data-parallel from each future's GLOBAL rank in
+// its resource:
+//   g(f) = #{level > lv(f)} over all ranks + #{level == lv(f)} on lower ranks
+//          + stable rank of f among this rank's (resource, level) bucket,
+// all read from the (allreduced) histogram H[G][R][Lv].  f is admitted iff
+// g(f) < bound(r) (bound = spare for phase A, sum of phase-A-residual spare over
+// the type for phase B); a phase-B future takes slot g(f) of the list
+// [(s, i): 1 <= s <= spare2_i] sorted by (s desc, i asc), which equals the
+// sequential greedy (tests/test_oracle_pins.py::test_water_fill_*).
+// Stable ranks come from scans over the row-ordered bucket lists K1 wrote;
+// atomics only ever produce counts.
+#include "internal.h"
+
+namespace nalar {
+
+namespace {
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename Tv>
+__device__ __forceinline__ Tv block_sum(Tv v, Tv* red) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    Tv s = 0;
+    for (int k = 0; k < kK4Warps; ++k) s += red[k];
+    return s;
+}
+
+// number of slots with spare-level > s among the type's instances
+__device__ __forceinline__ uint64_t slots_above(const uint64_t* sp2, uint32_t n, uint64_t s) {
+    uint64_t a = 0;
+    for (uint32_t k = 0; k < n; ++k) a += sp2[k] > s ? sp2[k] - s : 0ull;
+    return a;
+}
+
+// slot g -> (level s, index j among instances with spare2 >= s)
+__device__ __forceinline__ void locate_slot(const uint64_t* sp2, uint32_t n, uint64_t maxs, uint64_t g,
+                                            uint64_t* s_out, uint64_t* j_out) {
+    uint64_t lo = 1, hi = maxs;
+    while (lo < hi) {
+        const uint64_t mid = lo + ((hi - lo) >> 1);
+        if (slots_above(sp2, n, mid) <= g) hi = mid;
+        else lo = mid + 1;
+    }
+    *s_out = lo;
+    *j_out = g - slots_above(sp2, n, lo);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
+    __shared__ uint32_t s_r;
+    __shared__ uint32_t s_inst[NALAR_MAX_INSTANCES_DEV];
+    __shared__ uint64_t s_spare[NALAR_MAX_INSTANCES_DEV];   // spare before phase A
+    __shared__ uint64_t s_sp2[NALAR_MAX_INSTANCES_DEV];     // spare after phase A
+    __shared__ uint64_t s_A[256];                           // global count above level
+    __shared__ uint64_t s_before[256];                      // same level, lower ranks
+    __shared__ uint32_t s_LA[256];                          // local count above level
+    __shared__ uint32_t s_Hg[256];
+    __shared__ uint32_t s_Hl[256];
+    __shared__ uint32_t s_run[256];
+    __shared__ uint32_t s_wc[kK4Warps][256];
+    __shared__ uint64_t s_red64[kK4Warps];
+    __shared__ uint32_t s_red32[kK4Warps];
+    __shared__ uint32_t s_pref[kK4Threads + 1];
+    __shared__ uint32_t s_ni;
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
+    if (tid == 0) s_r = atomicAdd(&p.counters[C_TICKET], 1u);   // resources in ticket order
+    __syncthreads();
+    const uint32_t r = s_r;
+    const bool is_type = r >= I;
+    const uint32_t t = is_type ? r - I : p.i_type[r];
+
+    // ---- instances of type t (ascending id), their load and spare ----------
+    if (tid == 0) s_ni = 0;
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < I; i0 += kK4Threads) {
+        const uint32_t i = i0 + tid;
+        const bool m = i < I && p.i_type[i] == t;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+        if (lane == 0) s_red32[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t base = s_ni;
+        for (uint32_t k = 0; k < warp; ++k) base += s_red32[k];
+        if (m) s_inst[base + __popc(bal & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t tot = 0;
+            for (int k = 0; k < kK4Warps; ++k) tot += s_red32[k];
+            s_ni += tot;
+        }
+        __syncthreads();
+    }
+    const uint32_t ni = s_ni;
+    // warp per instance: load, spare, phase-A admissions (all ranks)
+    for (uint32_t k = warp; k < ni; k += kK4Warps) {
+        const uint32_t i = s_inst[k];
+        uint64_t ha = 0;
+        for (uint32_t x = lane; x < G * Lv; x += 32) {
+            const uint32_t s = x / Lv, lv = x - s * Lv;
+            ha += p.H[((size_t)s * R + i) * Lv + lv];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ha += __shfl_xor_sync(0xFFFFFFFFu, ha, o);
+        if (lane == 0) {
+            const uint64_t load = (uint64_t)p.i_base[i] + p.load_sum[i];
+            const uint64_t cap = p.i_cap[i];
+            const uint64_t spare = cap > load ? cap - load : 0ull;
+            const uint64_t adm = ha < spare ? ha : spare;
+            s_spare[k] = spare;
+            s_sp2[k] = spare - adm;
+            if (is_type) {
+                p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
+                p.i_spare[i] = (uint32_t)spare;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- bound of this resource -------------------------------------------
+    uint64_t bound = 0, maxs = 0;
+    if (is_type) {
+        uint64_t sum = 0, mx = 0;
+        for (uint32_t k = tid; k < ni; k += kK4Threads) { sum += s_sp2[k]; mx = max(mx, s_sp2[k]); }
+        bound = block_sum<uint64_t>(sum, s_red64);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        __syncthreads();
+        if (lane == 0) s_red64[warp] = mx;
+        __syncthreads();
+        for (int k = 0; k < kK4Warps; ++k) maxs = max(maxs, s_red64[k]);
+    } else {
+        for (uint32_t k = 0; k < ni; ++k)
+            if (s_inst[k] == r) bound = s_spare[k];
+    }
+
+    // ---- level histogram of r: global, lower-ranks, local ------------------
+    for (uint32_t lv = tid; lv < 256; lv += kK4Threads) {
+        uint32_t hg = 0, hb = 0, hl = 0;
+        if (lv < Lv) {
+            for (uint32_t s = 0; s < G; ++s) {
+                const uint32_t h = p.H[((size_t)s * R + r) * Lv + lv];
+                hg += h;
+                if (s < p.slot) hb += h;
+                if (s == p.slot) hl = h;
+            }
+        }
+        s_Hg[lv] = hg;
+        s_Hl[lv] = hl;
+        s_before[lv] = hb;
+        s_run[lv] = 0;
+        for (int k = 0; k < kK4Warps; ++k) s_wc[k][lv] = 0;
+    }
+    __syncthreads();
+    // suffix sums (levels above): small, one thread
+    if (tid == 0) {
+        uint64_t a = 0;
+        uint32_t la = 0;
+        for (int lv = 255; lv >= 0; --lv) {
+            s_A[lv] = a;
+            s_LA[lv] = la;
+            a += s_Hg[lv];
+            la += s_Hl[lv];
+        }
+    }
+    __syncthreads();
+    // number of this rank's futures admitted on r
+    uint32_t adm_lv = 0;
+    for (uint32_t lv = tid; lv < Lv; lv += kK4Threads) {
+        const uint64_t pre = s_A[lv] + s_before[lv];
+        if (pre < bound) {
+            const uint64_t room = bound - pre;
+            adm_lv = (uint32_t)(room < s_Hl[lv] ? room : s_Hl[lv]);
+        }
+    }
+    const uint32_t n_adm = block_sum<uint32_t>(adm_lv, s_red32);
+
+    // ---- publish n_adm, look back for the assignment-list offset -----------
+    if (tid == 0) st_release(&p.adm_pub[r], 0x80000000u | n_adm);
+    uint32_t base_part = 0;
+    for (uint32_t q = tid; q < r; q += kK4Threads) {
+        uint32_t v;
+        do { v = ld_acquire(&p.adm_pub[q]); } while (!(v & 0x80000000u));
+        base_part += v & 0x7FFFFFFFu;
+    }
+    const uint32_t list_base = block_sum<uint32_t>(base_part, s_red32);
+    if (tid == 0 && n_adm) atomicAdd(&p.counters[C_ASSIGNED], n_adm);
+
+    // ---- per-instance assigned counts (type blocks own their instances) ----
+    if (is_type) {
+        uint64_t n_t = 0;
+        for (uint32_t lv = 0; lv < Lv; ++lv) n_t += s_Hg[lv];
+        const uint64_t used = n_t < bound ? n_t : bound;
+        uint64_t s0 = 0, j0 = 0;
+        if (used) locate_slot(s_sp2, ni, maxs, used - 1, &s0, &j0);
+        for (uint32_t k = tid; k < ni; k += kK4Threads) {
+            uint64_t asg = s_spare[k] - s_sp2[k];     // phase A
+            if (used) {
+                const uint64_t sp = s_sp2[k];
+                asg += sp > s0 ? sp - s0 : 0ull;
+                if (sp >= s0) {
+                    uint64_t idx = 0;
+                    for (uint32_t q = 0; q < k; ++q) idx += s_sp2[q] >= s0;
+                    asg += idx <= j0;
+                }
+            }
+            p.i_assigned[s_inst[k]] = (uint32_t)asg;
+        }
+    }
+    if (n_adm == 0) return;
+
+    // ---- walk this rank's futures of r in row order --------------------------
+    const uint8_t aff = is_type ? p.t_aff[t] : 0;
+    uint32_t found = 0;
+    uint32_t carry = 0;      // positions of earlier block-chunks
+    for (uint32_t b0 = 0; b0 < B && found < n_adm; b0 += kK4Threads) {
+        // prefix of per-K1-block counts for blocks [b0, b0 + 256)
+        const uint32_t bb = b0 + tid;
+        const uint32_t c = bb < B ? p.cnt_rb[(size_t)r * B + bb] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        __syncthreads();
+        if (lane == 31) s_red32[warp] = incl;
+        __syncthreads();
+        uint32_t wb = 0;
+        for (uint32_t k = 0; k < warp; ++k) wb += s_red32[k];
+        s_pref[tid] = wb + incl - c;
+        if (tid == kK4Threads - 1) s_pref[kK4Threads] = wb + incl;
+        __syncthreads();
+        const uint32_t total = s_pref[kK4Threads];
+        const uint32_t nb = min((uint32_t)kK4Threads, B - b0);
+        for (uint32_t q0 = 0; q0 < total && found < n_adm; q0 += kK4Threads) {
+            const uint32_t q = q0 + tid;
+            bool live = false;
+            uint32_t row = 0, lv = 0xFFFFu;
+            if (q < total) {
+                // owning K1 block: last k with s_pref[k] <= q
+                uint32_t lo = 0, hi = nb - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    if (s_pref[mid] <= q) lo = mid;
+                    else hi = mid - 1;
+                }
+                const uint32_t kb = b0 + lo;
+                const uint2 it = p.items[p.blk_row0[kb] + p.off_rb[(size_t)r * B + kb] + (q - s_pref[lo])];
+                row = it.x;
+                lv = it.y;
+                live = s_A[lv] + s_before[lv] < bound;
+                if (!live) lv = 0xFFFFu;
+            }
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv);
+            const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
+            if (live && (__ffs(peers) - 1) == (int)lane) s_wc[warp][lv] = __popc(peers);
+            __syncthreads();
+            bool adm = false;
+            uint32_t rank = 0;
+            if (live) {
+                rank = s_run[lv] + wrank;
+                for (uint32_t k = 0; k < warp; ++k) rank += s_wc[k][lv];
+                adm = s_A[lv] + s_before[lv] + rank < bound;
+            }
+            __syncthreads();
+            for (uint32_t j = tid; j < 256; j += kK4Threads) {
+                uint32_t add = 0;
+                for (int k = 0; k < kK4Warps; ++k) { add += s_wc[k][j]; s_wc[k][j] = 0; }
+                s_run[j] += add;
+            }
+            if (adm) {
+                const uint64_t g = s_A[lv] + s_before[lv] + rank;
+                int16_t inst = (int16_t)r;
+                if (is_type) {
+                    uint64_t s, j;
+                    locate_slot(s_sp2, ni, maxs, g, &s, &j);
+                    for (uint32_t k = 0; k < ni; ++k) {
+                        if (s_sp2[k] >= s) {
+                            if (j == 0) { inst = (int16_t)s_inst[k]; break; }
+                            --j;
+                        }
+                    }
+                }
+                p.status[row] = 7;
+                p.instance[row] = inst;
+                p.new_pin[row] = (uint8_t)(is_type && aff != 0);
+                const uint32_t pos = list_base + s_LA[lv] + rank;
+                p.assign_row[pos] = row;
+                p.assign_inst[pos] = inst;
+            }
+            found += __syncthreads_count(adm);
+        }
+        carry += total;
+    }
+    (void)carry;
+}
+
+cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
+    if (p.R == 0) return cudaSuccess;
+    k4_assign<<<p.R, kK4Threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace nalar

@@ -1,0 +1,460 @@
+// k_sweep.cu -- K1: the per-workflow sweep of the policy epoch.
+//
+// One CTA owns a contiguous range of whole workflows (balanced by rows on the
+// host at upload).  Its slice of the SoA future table is staged into shared
+// memory with 1-D TMA bulk copies (cp.async.bulk + mbarrier); each warp then
+// takes whole workflows and sweeps their rows in creation order, 32 rows per
+// step, computing:
+//   depth  -- longest DEP u CALL path from a root (SRTF stage, PAPER.md:691;
+//             SPEC S:460), saturating u16
+//   doomed -- PENDING with a FAILED / doomed DEP predecessor (failures are
+//             delivered like values)
+//   ready  -- PENDING, not doomed, all DEP predecessors RESOLVED (push-based
+//             readiness)
+//   eligibility -- stateful in-order fence and first
+//             placement of managed-state sessions
+//   per-workflow aggregates ("aggregating metrics and metadata")
+//   level  -- clamp(prio + score, 0, Lv-1) (set_priority PAPER.md:389; SRTF
+//             PAPER.md:691; LPT PAPER.md:696)
+//   per-instance in-flight counts (queue lengths)
+// Predecessors in earlier 32-row steps are final; predecessors inside the
+// current step are resolved by warp-synchronous Bellman-Ford rounds (edges
+// point to earlier rows, so rounds <= longest intra-step chain).
+// Finally the CTA buckets its eligible futures by resource (pin, or I + type)
+// in row order -- a stable counting sort whose positions come from scans, never
+// from atomics -- and adds them to the (resource, level) histogram that the
+// assignment pass (and, for G > 1, the allreduce) consumes.
+#include "internal.h"
+
+namespace nalar {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared, completion counted on `bar` (TMA engine).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// plan of one staged array: aligned global window copied into smem
+struct Win {
+    const uint8_t* src;
+    uint32_t pre, bytes;
+};
+__device__ __forceinline__ Win window(const void* base, size_t elem, size_t lo, size_t hi) {
+    const uint8_t* s = (const uint8_t*)base + lo * elem;
+    const uint8_t* a = (const uint8_t*)((uintptr_t)s & ~(uintptr_t)15);
+    Win w;
+    w.src = a;
+    w.pre = (uint32_t)(s - a);
+    w.bytes = (uint32_t)align16(w.pre + (hi - lo) * elem);
+    return w;
+}
+
+}  // namespace
+
+size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
+    size_t b = 64;                                  // mbarrier, ticket, counters
+    b += (size_t)kK1Warps * (8 + 8 * (size_t)T);    // infl mask + first_pending + first_ready_unp
+    b += 4 * (size_t)I;                             // in-flight counts
+    b += 8 * (size_t)R;                             // per-resource count / offset
+    b += 4 * (size_t)kK1Threads + 4 * kK1Warps;     // compaction list + warp counts
+    b += (size_t)T;                                 // affinity
+    return (b + 127) & ~(size_t)127;
+}
+
+size_t k1_staged_smem(uint32_t rows, uint32_t edges) {
+    return 2 * align16(rows + 32) + align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
+           align16(4 * (size_t)edges + 32) + align16(2 * (size_t)rows) + align16(rows);
+}
+
+__global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t b = blockIdx.x;
+    const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Lv = p.levels;
+
+    const uint32_t w0 = p.blk_wf[b], w1 = p.blk_wf[b + 1];
+    const uint32_t r0 = p.blk_row0[b], r1 = p.blk_row0[b + 1];
+    const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
+    const uint32_t nr = r1 - r0, ne = e1 - e0;
+    const bool staged = p.blk_staged[b] != 0;
+
+    // ---- carve the fixed part --------------------------------------------
+    uint8_t* sp = smem;
+    uint64_t* mbar = (uint64_t*)sp;
+    uint32_t* s_ticket = (uint32_t*)(sp + 8);
+    uint32_t* s_cnt = (uint32_t*)(sp + 16);      // [0] ready [1] elig [2] doomed
+    sp += 64;
+    unsigned long long* s_infl = (unsigned long long*)sp;
+    sp += 8 * kK1Warps;
+    uint32_t* s_fp = (uint32_t*)sp;               // [warps][T]
+    sp += 4 * (size_t)kK1Warps * T;
+    uint32_t* s_fru = (uint32_t*)sp;              // [warps][T]
+    sp += 4 * (size_t)kK1Warps * T;
+    uint32_t* s_load = (uint32_t*)sp;
+    sp += 4 * (size_t)I;
+    uint32_t* s_rcnt = (uint32_t*)sp;
+    sp += 4 * (size_t)R;
+    uint32_t* s_roff = (uint32_t*)sp;
+    sp += 4 * (size_t)R;
+    uint32_t* s_list = (uint32_t*)sp;
+    sp += 4 * kK1Threads;
+    uint32_t* s_wc = (uint32_t*)sp;
+    sp += 4 * kK1Warps;
+    uint8_t* s_aff = sp;
+
+    // ---- row arrays: staged in smem (TMA) or read in place ----------------
+    const uint8_t* st;
+    const uint8_t* ty;
+    const int16_t* pn;
+    const uint32_t* eo;   // absolute edge offsets, indexed by local row
+    const uint32_t* ed;   // edges, indexed by (edge - e0)
+    uint16_t* dep;
+    uint8_t* flg;
+    if (staged) {
+        uint8_t* q = smem + p.fixed_smem;
+        const Win ws = window(p.f_state, 1, r0, r1), wt = window(p.f_type, 1, r0, r1);
+        const Win wp = window(p.f_pin, 2, r0, r1), we = window(p.f_edge_off, 4, r0, r1 + 1);
+        const Win wg = window(p.edges, 4, e0, e1);
+        uint8_t* d_s = q;   q += align16(nr + 32);
+        uint8_t* d_t = q;   q += align16(nr + 32);
+        uint8_t* d_p = q;   q += align16(2 * (size_t)nr + 32);
+        uint8_t* d_e = q;   q += align16(4 * ((size_t)nr + 1) + 32);
+        uint8_t* d_g = q;   q += align16(4 * (size_t)ne + 32);
+        dep = (uint16_t*)q; q += align16(2 * (size_t)nr);
+        flg = q;
+        if (tid == 0) {
+            mbar_init(mbar, 1);
+            const uint32_t total = ws.bytes + wt.bytes + wp.bytes + we.bytes + (ne ? wg.bytes : 0u);
+            mbar_arrive_expect_tx(mbar, total);
+            bulk_g2s(d_s, ws.src, ws.bytes, mbar);
+            bulk_g2s(d_t, wt.src, wt.bytes, mbar);
+            bulk_g2s(d_p, wp.src, wp.bytes, mbar);
+            bulk_g2s(d_e, we.src, we.bytes, mbar);
+            if (ne) bulk_g2s(d_g, wg.src, wg.bytes, mbar);
+        }
+        st = d_s + ws.pre;
+        ty = d_t + wt.pre;
+        pn = (const int16_t*)(d_p + wp.pre);
+        eo = (const uint32_t*)(d_e + we.pre);
+        ed = (const uint32_t*)(d_g + wg.pre);
+    } else {
+        st = p.f_state + r0;
+        ty = p.f_type + r0;
+        pn = p.f_pin + r0;
+        eo = p.f_edge_off + r0;
+        ed = p.edges + e0;
+        dep = p.depth + r0;
+        flg = p.g_flags + r0;
+    }
+
+    // ---- zero block state while the copies are in flight ------------------
+    for (uint32_t i = tid; i < I; i += kK1Threads) s_load[i] = 0;
+    for (uint32_t r = tid; r < R; r += kK1Threads) s_rcnt[r] = 0;
+    for (uint32_t t = tid; t < T; t += kK1Threads) s_aff[t] = p.t_aff[t];
+    if (tid == 0) {
+        *s_ticket = 0;
+        s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
+    }
+    __syncthreads();
+    if (staged) mbar_wait(mbar, 0);
+
+    const uint32_t pol = p.policy;
+    unsigned long long* infl = s_infl + warp;
+    uint32_t* fp = s_fp + warp * T;
+    uint32_t* fru = s_fru + warp * T;
+    uint32_t n_ready = 0, n_doom = 0;
+
+    // ---- warps take whole workflows ---------------------------------------
+    for (;;) {
+        uint32_t wi = 0;
+        if (lane == 0) wi = atomicAdd(s_ticket, 1u);
+        wi = __shfl_sync(0xFFFFFFFFu, wi, 0);
+        const uint32_t w = w0 + wi;
+        if (w >= w1) break;
+        const uint32_t fa = p.wf_fut_off[w] - r0, fb = p.wf_fut_off[w + 1] - r0;
+
+        for (uint32_t t = lane; t < T; t += 32) { fp[t] = 0xFFFFFFFFu; fru[t] = 0xFFFFFFFFu; }
+        if (lane == 0) *infl = 0ull;
+        __syncwarp();
+
+        uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
+        uint32_t m_dep = 0, m_rnd = 0;
+
+        for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
+            const uint32_t f = c0 + lane;
+            const bool valid = f < fb;
+            const uint32_t stf = valid ? st[f] : 3u;
+            const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
+            uint32_t d = 0;
+            bool dm = false, allres = true, intra = false;
+            for (uint32_t e = eb; e < ee; ++e) {
+                const uint32_t v = ed[e];
+                const uint32_t s = (v & 0x7FFFFFFFu) - r0;
+                const bool call = (v >> 31) != 0;
+                if (s >= c0) {                       // inside this step: resolved below
+                    intra = true;
+                    if (!call) {
+                        const uint32_t ss = st[s];
+                        dm |= ss == 4u;
+                        allres &= ss == 3u;
+                    }
+                    continue;
+                }
+                d = max(d, (uint32_t)dep[s] + 1u);
+                if (!call) {
+                    const uint32_t ss = st[s];
+                    dm |= (ss == 4u) || (flg[s] & FL_DOOMED);
+                    allres &= ss == 3u;
+                }
+            }
+            if (ee > eb) d = max(d, 1u);
+            d = min(d, 65535u);
+            const bool pend = stf == 0u;
+            bool doom = pend && dm;
+            if (valid) { dep[f] = (uint16_t)d; flg[f] = doom ? FL_DOOMED : 0; }
+            __syncwarp();
+            if (__any_sync(0xFFFFFFFFu, intra)) {
+                for (;;) {
+                    uint32_t nd = d;
+                    bool ndm = doom;
+                    if (intra) {
+                        for (uint32_t e = eb; e < ee; ++e) {
+                            const uint32_t v = ed[e];
+                            const uint32_t s = (v & 0x7FFFFFFFu) - r0;
+                            if (s < c0) continue;
+                            nd = max(nd, (uint32_t)dep[s] + 1u);
+                            if (!(v >> 31) && pend) ndm |= (flg[s] & FL_DOOMED) != 0;
+                        }
+                        nd = min(nd, 65535u);
+                    }
+                    const bool ch = (nd != d) || (ndm != doom);
+                    __syncwarp();
+                    if (ch) { d = nd; doom = ndm; dep[f] = (uint16_t)d; flg[f] = doom ? FL_DOOMED : 0; }
+                    __syncwarp();
+                    if (!__any_sync(0xFFFFFFFFu, ch)) break;
+                }
+            }
+            if (valid) {
+                const uint32_t tyf = ty[f];
+                const int pinf = pn[f];
+                const uint32_t aff = s_aff[tyf];
+                const bool ready = pend && !doom && allres;
+                uint8_t fl = doom ? FL_DOOMED : 0;
+                if (ready) fl |= FL_READY;
+                if (ready && (aff == 0u || (aff == 1u && pinf >= 0))) fl |= FL_ELIG;
+                if (stf == 1u || stf == 2u) {
+                    atomicOr(infl, 1ull << tyf);
+                    atomicAdd(&s_load[p.f_exec[r0 + f]], 1u);
+                }
+                if (pend && !doom) atomicMin(&fp[tyf], f);
+                if (ready && pinf < 0) atomicMin(&fru[tyf], f);
+                flg[f] = fl;
+                c_pend += pend;
+                c_ready += ready;
+                c_infl += (stf == 1u || stf == 2u);
+                c_res += stf == 3u;
+                c_fail += stf == 4u;
+                c_doom += doom;
+                c_pinp += pend && pinf >= 0;
+                m_dep = max(m_dep, d);
+                m_rnd = max(m_rnd, (uint32_t)p.f_round[r0 + f]);
+            }
+            __syncwarp();
+        }
+
+        // stateful fence and first placement
+        const unsigned long long im = *infl;
+        for (uint32_t t = lane; t < T; t += 32) {
+            const uint32_t aff = s_aff[t];
+            if (aff == 2u) {
+                const uint32_t f = fp[t];
+                if (f != 0xFFFFFFFFu && !((im >> t) & 1ull) && (flg[f] & FL_READY)) flg[f] |= FL_ELIG;
+            } else if (aff == 1u) {
+                const uint32_t f = fru[t];
+                if (f != 0xFFFFFFFFu) flg[f] |= FL_ELIG;
+            }
+        }
+        c_pend = __reduce_add_sync(0xFFFFFFFFu, c_pend);
+        c_ready = __reduce_add_sync(0xFFFFFFFFu, c_ready);
+        c_infl = __reduce_add_sync(0xFFFFFFFFu, c_infl);
+        c_res = __reduce_add_sync(0xFFFFFFFFu, c_res);
+        c_fail = __reduce_add_sync(0xFFFFFFFFu, c_fail);
+        c_doom = __reduce_add_sync(0xFFFFFFFFu, c_doom);
+        c_pinp = __reduce_add_sync(0xFFFFFFFFu, c_pinp);
+        m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
+        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
+        __syncwarp();
+        n_ready += c_ready;
+        n_doom += c_doom;
+        if (lane < 10) {
+            const uint32_t vals[10] = {fb - fa, c_pend, c_ready, c_infl, c_res, c_fail, c_doom, c_pinp, m_dep, m_rnd};
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 10; ++k) v = (lane == (uint32_t)k) ? vals[k] : v;
+            p.wf_agg[(size_t)w * 10 + lane] = v;
+        }
+
+        // levels, statuses and per-row outputs
+        const int64_t prio = p.wf_prio[w];
+        for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
+            const uint32_t f = c0 + lane;
+            if (f >= fb) break;
+            const uint32_t g = r0 + f;
+            const uint32_t stf = st[f];
+            const uint32_t fl = flg[f];
+            const uint32_t d = dep[f];
+            uint32_t lv = 0, status;
+            int16_t inst = -1;
+            if (stf < 3u) {
+                const int64_t score = pol == 1u ? (int64_t)d : (pol == 2u ? (int64_t)m_rnd : 0);
+                int64_t x = prio + score;
+                x = x < 0 ? 0 : (x > (int64_t)Lv - 1 ? (int64_t)Lv - 1 : x);
+                lv = (uint32_t)x;
+            }
+            if (stf == 3u) status = 0;
+            else if (stf == 4u) status = 1;
+            else if (stf != 0u) { status = 2; inst = p.f_exec[g]; }
+            else if (fl & FL_DOOMED) status = 4;
+            else if (!(fl & FL_READY)) status = 3;
+            else if (!(fl & FL_ELIG)) status = 5;
+            else status = 6;
+            p.status[g] = (uint8_t)status;
+            p.level[g] = (uint8_t)lv;
+            if (staged) p.depth[g] = (uint16_t)d;
+            p.instance[g] = inst;
+            p.new_pin[g] = 0;
+            if (fl & FL_ELIG) {
+                const int pinf = pn[f];
+                const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + ty[f];
+                atomicAdd(&p.H[(size_t)r * Lv + lv], 1u);
+                atomicAdd(&s_rcnt[r], 1u);
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        atomicAdd(&s_cnt[0], n_ready);
+        atomicAdd(&s_cnt[2], n_doom);
+    }
+    __syncthreads();
+
+    // ---- block epilogue: loads, per-resource offsets, stable bucketing ------
+    for (uint32_t i = tid; i < I; i += kK1Threads)
+        if (s_load[i]) atomicAdd(&p.load_part[i], s_load[i]);
+    // exclusive scan of s_rcnt over R (serial per thread chunk + warp scan)
+    {
+        const uint32_t per = (R + kK1Threads - 1) / kK1Threads;
+        const uint32_t lo = min(R, tid * per), hi = min(R, lo + per);
+        uint32_t sum = 0;
+        for (uint32_t r = lo; r < hi; ++r) sum += s_rcnt[r];
+        // block exclusive scan of `sum`
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        if (lane == 31) s_wc[warp] = incl;
+        __syncthreads();
+        uint32_t wbase = 0;
+        for (uint32_t k = 0; k < warp; ++k) wbase += s_wc[k];
+        uint32_t run = wbase + incl - sum;
+        for (uint32_t r = lo; r < hi; ++r) {
+            const uint32_t c = s_rcnt[r];
+            s_roff[r] = run;
+            p.cnt_rb[(size_t)r * p.B + b] = c;
+            p.off_rb[(size_t)r * p.B + b] = run;
+            run += c;
+            s_rcnt[r] = 0;   // reused as the running rank counter below
+        }
+        __syncthreads();
+    }
+    uint32_t n_elig = 0;
+    for (uint32_t t0 = 0; t0 < nr; t0 += kK1Threads) {
+        const uint32_t f = t0 + tid;
+        const bool el = f < nr && (flg[f] & FL_ELIG);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, el);
+        if (lane == 0) s_wc[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t base = 0, tot = 0;
+        for (uint32_t k = 0; k < (uint32_t)kK1Warps; ++k) {
+            const uint32_t c = s_wc[k];
+            base += k < warp ? c : 0u;
+            tot += c;
+        }
+        if (el) s_list[base + __popc(bal & ((1u << lane) - 1u))] = f;
+        __syncthreads();
+        if (warp == 0) {
+            for (uint32_t j0 = 0; j0 < tot; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const bool ok = j < tot;
+                uint32_t r = 0xFFFFFFFFu, ff = 0;
+                if (ok) {
+                    ff = s_list[j];
+                    const int pinf = pn[ff];
+                    r = pinf >= 0 ? (uint32_t)pinf : I + ty[ff];
+                }
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, r);
+                const uint32_t rank = ok ? s_rcnt[r] + __popc(peers & ((1u << lane) - 1u)) : 0u;
+                __syncwarp();
+                if (ok) {
+                    const uint32_t g = r0 + ff;
+                    p.items[r0 + s_roff[r] + rank] = make_uint2(g, p.level[g]);
+                    if ((__ffs(peers) - 1) == (int)lane) s_rcnt[r] += __popc(peers);
+                }
+                __syncwarp();
+            }
+        }
+        n_elig += tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        atomicAdd(&p.counters[C_READY], s_cnt[0]);
+        atomicAdd(&p.counters[C_ELIG], n_elig);
+        atomicAdd(&p.counters[C_DOOMED], s_cnt[2]);
+    }
+}
+
+cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s) {
+    if (p.B == 0) return cudaSuccess;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    k1_sweep<<<p.B, kK1Threads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace nalar

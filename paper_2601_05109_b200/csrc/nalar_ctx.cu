@@ -1,0 +1,622 @@
+// nalar_ctx.cu -- host side of libnalar.so: the C ABI of include/nalar.h.
+//
+// Owns device memory (one arena), the stream, the per-policy CUDA graph of the
+// epoch (memset -> K1 sweep -> [NCCL allreduce] -> K4 assign) and, in
+// NALAR_COLL_NCCL mode, a library-owned NCCL communicator (NCCL is dlopen'ed,
+// so the library loads on machines without it).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/nalar.h"
+#include "internal.h"
+
+using namespace nalar;
+
+namespace {
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+    bool load(std::string* err) {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) { *err = std::string("dlopen libnccl failed: ") + dlerror(); return false; }
+        getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+        commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+        commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !getErrorString) {
+            *err = "libnccl: missing symbols";
+            return false;
+        }
+        return true;
+    }
+};
+NcclApi g_nccl;
+
+constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
+constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
+constexpr uint32_t kMaxBlocks = 16384;
+
+struct Key {
+    uint32_t N, E, W, I, T, B, R, policy;
+    size_t smem;
+    bool operator==(const Key& o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
+};
+
+}  // namespace
+
+struct nalar_ctx {
+    nalar_config cfg{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint8_t* arena = nullptr;
+    bool own_arena = false;
+    size_t arena_bytes = 0;
+    uint32_t Lv = 256, Rmax = 0, Bmax = 0;
+    // inputs
+    uint32_t *d_wf_off = nullptr, *d_eoff = nullptr, *d_edges = nullptr, *d_icap = nullptr, *d_ibase = nullptr;
+    int32_t* d_wf_prio = nullptr;
+    uint8_t *d_state = nullptr, *d_type = nullptr, *d_round = nullptr, *d_itype = nullptr, *d_taff = nullptr;
+    int16_t *d_exec = nullptr, *d_pin = nullptr;
+    uint32_t *d_blk_wf = nullptr, *d_blk_row0 = nullptr, *d_blk_edge0 = nullptr;
+    uint8_t* d_blk_staged = nullptr;
+    // outputs
+    uint8_t *d_status = nullptr, *d_level = nullptr, *d_newpin = nullptr, *d_gflags = nullptr;
+    uint16_t* d_depth = nullptr;
+    int16_t *d_inst = nullptr, *d_ainst = nullptr;
+    uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
+    // intermediates
+    uint2* d_items = nullptr;
+    uint32_t *d_cnt_rb = nullptr, *d_off_rb = nullptr;
+    uint32_t* d_x = nullptr;          // exchange: H[G][R][Lv] then load[I]
+    size_t x_words = 0;
+    uint32_t* d_scr = nullptr;        // counters[C_NUM] then adm_pub[Rmax]; contiguous with d_x
+    size_t zero_bytes = 0;            // bytes to clear per epoch from d_x
+    unsigned long long* d_err = nullptr;
+    // host pinned
+    uint32_t* h_cnt = nullptr;
+    unsigned long long* h_err = nullptr;
+    // current table
+    uint32_t N = 0, E = 0, W = 0, I = 0, T = 0, B = 0, R = 0;
+    size_t smem = 0, fixed_smem = 0;
+    bool uploaded = false, epoch_done = false, in_epoch = false;
+    int last_policy = -1;
+    // graphs / timing
+    cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
+    Key gkey[3]{};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    ncclComm_t comm = nullptr;
+    std::string err;
+};
+
+namespace {
+
+int fail(nalar_ctx* c, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) return fail(c, NALAR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct Layout {
+    size_t off = 0;
+    template <typename T>
+    size_t take(size_t n) {
+        const size_t o = off;
+        off += ((n * sizeof(T) + 64) + 255) & ~(size_t)255;   // +64 B pad: TMA windows may over-read
+        return o;
+    }
+};
+
+struct Plan {
+    size_t wf_off, wf_prio, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
+    size_t blk_wf, blk_row0, blk_edge0, blk_staged;
+    size_t status, level, newpin, gflags, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
+    size_t items, cnt_rb, off_rb, x, scr, err;
+    size_t x_words, total;
+    uint32_t Rmax, Bmax;
+};
+
+bool plan_layout(const nalar_config* cfg, Plan* p) {
+    const uint32_t Lv = cfg->levels ? cfg->levels : 256;
+    const size_t N = cfg->max_futures, E = cfg->max_edges, W = cfg->max_workflows;
+    const size_t I = cfg->max_instances, T = cfg->max_types;
+    const uint32_t G = cfg->world > 0 ? (uint32_t)cfg->world : 1u;
+    p->Rmax = (uint32_t)(I + T);
+    p->Bmax = (uint32_t)std::min<size_t>(std::max<size_t>(W, 1), kMaxBlocks);
+    Layout L;
+    p->wf_off = L.take<uint32_t>(W + 1);
+    p->wf_prio = L.take<int32_t>(W);
+    p->state = L.take<uint8_t>(N);
+    p->type = L.take<uint8_t>(N);
+    p->round = L.take<uint8_t>(N);
+    p->exec = L.take<int16_t>(N);
+    p->pin = L.take<int16_t>(N);
+    p->eoff = L.take<uint32_t>(N + 1);
+    p->edges = L.take<uint32_t>(E);
+    p->itype = L.take<uint8_t>(I);
+    p->icap = L.take<uint32_t>(I);
+    p->ibase = L.take<uint32_t>(I);
+    p->taff = L.take<uint8_t>(T);
+    p->blk_wf = L.take<uint32_t>(p->Bmax + 1);
+    p->blk_row0 = L.take<uint32_t>(p->Bmax + 1);
+    p->blk_edge0 = L.take<uint32_t>(p->Bmax + 1);
+    p->blk_staged = L.take<uint8_t>(p->Bmax);
+    p->status = L.take<uint8_t>(N);
+    p->level = L.take<uint8_t>(N);
+    p->newpin = L.take<uint8_t>(N);
+    p->gflags = L.take<uint8_t>(N);
+    p->depth = L.take<uint16_t>(N);
+    p->inst = L.take<int16_t>(N);
+    p->ainst = L.take<int16_t>(N);
+    p->wfagg = L.take<uint32_t>(W * NALAR_WF_AGG_FIELDS);
+    p->iload = L.take<uint32_t>(I);
+    p->ispare = L.take<uint32_t>(I);
+    p->iasg = L.take<uint32_t>(I);
+    p->arow = L.take<uint32_t>(N);
+    p->items = L.take<uint2>(N);
+    p->cnt_rb = L.take<uint32_t>((size_t)p->Rmax * p->Bmax);
+    p->off_rb = L.take<uint32_t>((size_t)p->Rmax * p->Bmax);
+    p->x_words = (size_t)G * p->Rmax * Lv + I;
+    // exchange buffer and scratch are contiguous so one memset clears both
+    p->x = L.off;
+    L.off += p->x_words * 4;
+    p->scr = L.off;
+    L.off += (C_NUM + (size_t)p->Rmax) * 4;
+    L.off = (L.off + 255) & ~(size_t)255;
+    p->err = L.take<unsigned long long>(2);
+    p->total = L.off + 256;
+    return true;
+}
+
+template <typename T>
+T* at(uint8_t* base, size_t off) { return reinterpret_cast<T*>(base + off); }
+
+void destroy_graphs(nalar_ctx* c) {
+    for (auto& g : c->gexec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+// Greedy partition of whole workflows into K1 blocks, balanced by rows.
+void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* eoff, std::vector<uint32_t>& bw,
+               std::vector<uint32_t>& br, std::vector<uint32_t>& be, std::vector<uint8_t>& bs, size_t* max_smem) {
+    const uint32_t W = c->W, N = c->N;
+    uint32_t target = std::max<uint32_t>(64u, (N + kSmSplit - 1) / kSmSplit);
+    for (;;) {
+        bw.clear(); br.clear(); be.clear(); bs.clear();
+        size_t mx = 0;
+        uint32_t w = 0;
+        while (w < W) {
+            const uint32_t ws = w;
+            uint32_t rows = 0;
+            while (w < W) {
+                const uint32_t wr = wf_off[w + 1] - wf_off[w];
+                const uint32_t e_if = eoff[wf_off[w + 1]] - eoff[wf_off[ws]];
+                if (w > ws && k1_staged_smem(rows + wr, e_if) > kStageBudget) break;
+                rows += wr;
+                ++w;
+                if (rows >= target) break;
+            }
+            const uint32_t ra = wf_off[ws], rb = wf_off[w];
+            const size_t need = k1_staged_smem(rb - ra, eoff[rb] - eoff[ra]);
+            const bool staged = need <= kStageBudget && !(c->cfg.flags & NALAR_F_FORCE_UNSTAGED);
+            if (staged) mx = std::max(mx, need);
+            bw.push_back(ws); br.push_back(ra); be.push_back(eoff[ra]); bs.push_back(staged ? 1 : 0);
+        }
+        bw.push_back(W); br.push_back(wf_off[W]); be.push_back(eoff[wf_off[W]]);
+        if (bw.size() - 1 <= c->Bmax) { *max_smem = mx; return; }
+        target *= 2;
+    }
+}
+
+int run_k1(nalar_ctx* c, int policy) {
+    SweepParams p{};
+    p.wf_fut_off = c->d_wf_off; p.wf_prio = c->d_wf_prio;
+    p.f_state = c->d_state; p.f_type = c->d_type; p.f_round = c->d_round;
+    p.f_exec = c->d_exec; p.f_pin = c->d_pin; p.f_edge_off = c->d_eoff; p.edges = c->d_edges;
+    p.t_aff = c->d_taff;
+    p.blk_wf = c->d_blk_wf; p.blk_row0 = c->d_blk_row0; p.blk_edge0 = c->d_blk_edge0;
+    p.blk_staged = c->d_blk_staged;
+    p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
+    p.fixed_smem = (uint32_t)c->fixed_smem;
+    p.g_flags = c->d_gflags;
+    p.status = c->d_status; p.level = c->d_level; p.depth = c->d_depth; p.instance = c->d_inst;
+    p.new_pin = c->d_newpin; p.wf_agg = c->d_wfagg;
+    const uint32_t slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
+    p.H = c->d_x + (size_t)slot * c->R * c->Lv;
+    const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
+    p.load_part = c->d_x + (size_t)G * c->R * c->Lv;
+    p.items = c->d_items; p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb;
+    p.counters = c->d_scr;
+    CK(launch_sweep(p, c->smem, c->stream));
+    return NALAR_OK;
+}
+
+int run_k4(nalar_ctx* c) {
+    AssignParams p{};
+    const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
+    p.H = c->d_x;
+    p.load_sum = c->d_x + (size_t)G * c->R * c->Lv;
+    p.G = G; p.slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
+    p.R = c->R; p.n_inst = c->I; p.n_types = c->T; p.levels = c->Lv; p.B = c->B;
+    p.i_type = c->d_itype; p.i_cap = c->d_icap; p.i_base = c->d_ibase; p.t_aff = c->d_taff;
+    p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb; p.blk_row0 = c->d_blk_row0; p.items = c->d_items;
+    p.status = c->d_status; p.instance = c->d_inst; p.new_pin = c->d_newpin;
+    p.i_load = c->d_iload; p.i_spare = c->d_ispare; p.i_assigned = c->d_iasg;
+    p.assign_row = c->d_arow; p.assign_inst = c->d_ainst;
+    p.adm_pub = c->d_scr + C_NUM;
+    p.counters = c->d_scr;
+    CK(launch_assign(p, c->stream));
+    return NALAR_OK;
+}
+
+size_t x_used_words(nalar_ctx* c) {
+    const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
+    return (size_t)G * c->R * c->Lv + c->I;
+}
+
+int enqueue_first_half(nalar_ctx* c, int policy) {
+    const bool timing = c->cfg.flags & NALAR_F_TIMING;
+    // clear exchange buffer (used part) + counters + adm_pub; contiguous region
+    CK(cudaMemsetAsync(c->d_x, 0, c->x_words * 4 + (C_NUM + (size_t)c->Rmax) * 4, c->stream));
+    if (timing) CK(cudaEventRecord(c->ev[0], c->stream));
+    int rc = run_k1(c, policy);
+    if (rc) return rc;
+    if (timing) CK(cudaEventRecord(c->ev[1], c->stream));
+    return NALAR_OK;
+}
+
+int enqueue_collective(nalar_ctx* c) {
+    if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_NCCL) {
+        // NOTE: the full reservation-sized layout keeps slot offsets identical on all ranks
+        const ncclResult_t r = g_nccl.allReduce(c->d_x, c->d_x, x_used_words(c), ncclUint32, ncclSum, c->comm,
+                                                c->stream);
+        if (r != ncclSuccess) return fail(c, NALAR_E_COMM, "ncclAllReduce: %s", g_nccl.getErrorString(r));
+    }
+    return NALAR_OK;
+}
+
+int enqueue_second_half(nalar_ctx* c) {
+    const bool timing = c->cfg.flags & NALAR_F_TIMING;
+    if (timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    int rc = run_k4(c);
+    if (rc) return rc;
+    if (timing) CK(cudaEventRecord(c->ev[3], c->stream));
+    return NALAR_OK;
+}
+
+int enqueue_epoch(nalar_ctx* c, int policy) {
+    int rc = enqueue_first_half(c, policy);
+    if (!rc) rc = enqueue_collective(c);
+    if (!rc) rc = enqueue_second_half(c);
+    return rc;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+int nalar_abi_version(void) { return NALAR_ABI_VERSION; }
+
+size_t nalar_workspace_bytes(const nalar_config* cfg) {
+    if (!cfg) return 0;
+    Plan p;
+    plan_layout(cfg, &p);
+    return p.total;
+}
+
+int nalar_nccl_unique_id(unsigned char out[128]) {
+    std::string e;
+    if (!out) return NALAR_E_INVAL;
+    if (!g_nccl.load(&e)) return NALAR_E_COMM;
+    ncclUniqueId id;
+    if (g_nccl.getUniqueId(&id) != ncclSuccess) return NALAR_E_COMM;
+    memcpy(out, id.internal, 128);
+    return NALAR_OK;
+}
+
+int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
+    if (!out || !cfg) return NALAR_E_INVAL;
+    *out = nullptr;
+    nalar_ctx* c = new (std::nothrow) nalar_ctx();
+    if (!c) return NALAR_E_NOMEM;
+    c->cfg = *cfg;
+    c->Lv = cfg->levels ? cfg->levels : 256;
+    auto bail = [&](int code) { nalar_destroy(c); return code; };
+    if (c->Lv > NALAR_MAX_LEVELS || cfg->max_types > NALAR_MAX_TYPES || cfg->max_instances > NALAR_MAX_INSTANCES ||
+        cfg->max_futures > NALAR_MAX_ROWS || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world ||
+        (cfg->world > 1 && cfg->collective == NALAR_COLL_NONE))
+        return bail(NALAR_E_INVAL);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return bail(NALAR_E_CUDA);
+    if (cfg->device < 0 || cfg->device >= ndev) return bail(NALAR_E_INVAL);
+    cudaDeviceProp prop;
+    if (cudaSetDevice(cfg->device) != cudaSuccess || cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess)
+        return bail(NALAR_E_CUDA);
+    if (prop.major != 10) return bail(NALAR_E_CUDA);   // built for sm_100a only
+    Plan p;
+    plan_layout(cfg, &p);
+    c->Rmax = p.Rmax;
+    c->Bmax = p.Bmax;
+    c->x_words = p.x_words;
+    if (cfg->workspace) {
+        if (cfg->workspace_bytes < p.total) return bail(NALAR_E_NOMEM);
+        c->arena = (uint8_t*)(((uintptr_t)cfg->workspace + 255) & ~(uintptr_t)255);
+        if ((size_t)(c->arena - (uint8_t*)cfg->workspace) + p.total - 256 > cfg->workspace_bytes)
+            return bail(NALAR_E_NOMEM);
+    } else {
+        if (cudaMalloc(&c->arena, p.total) != cudaSuccess) return bail(NALAR_E_NOMEM);
+        c->own_arena = true;
+    }
+    c->arena_bytes = p.total;
+    uint8_t* a = c->arena;
+    c->d_wf_off = at<uint32_t>(a, p.wf_off); c->d_wf_prio = at<int32_t>(a, p.wf_prio);
+    c->d_state = at<uint8_t>(a, p.state); c->d_type = at<uint8_t>(a, p.type); c->d_round = at<uint8_t>(a, p.round);
+    c->d_exec = at<int16_t>(a, p.exec); c->d_pin = at<int16_t>(a, p.pin);
+    c->d_eoff = at<uint32_t>(a, p.eoff); c->d_edges = at<uint32_t>(a, p.edges);
+    c->d_itype = at<uint8_t>(a, p.itype); c->d_icap = at<uint32_t>(a, p.icap); c->d_ibase = at<uint32_t>(a, p.ibase);
+    c->d_taff = at<uint8_t>(a, p.taff);
+    c->d_blk_wf = at<uint32_t>(a, p.blk_wf); c->d_blk_row0 = at<uint32_t>(a, p.blk_row0);
+    c->d_blk_edge0 = at<uint32_t>(a, p.blk_edge0); c->d_blk_staged = at<uint8_t>(a, p.blk_staged);
+    c->d_status = at<uint8_t>(a, p.status); c->d_level = at<uint8_t>(a, p.level);
+    c->d_newpin = at<uint8_t>(a, p.newpin); c->d_gflags = at<uint8_t>(a, p.gflags);
+    c->d_depth = at<uint16_t>(a, p.depth); c->d_inst = at<int16_t>(a, p.inst); c->d_ainst = at<int16_t>(a, p.ainst);
+    c->d_wfagg = at<uint32_t>(a, p.wfagg); c->d_iload = at<uint32_t>(a, p.iload);
+    c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
+    c->d_items = at<uint2>(a, p.items); c->d_cnt_rb = at<uint32_t>(a, p.cnt_rb); c->d_off_rb = at<uint32_t>(a, p.off_rb);
+    c->d_x = at<uint32_t>(a, p.x); c->d_scr = at<uint32_t>(a, p.scr);
+    c->d_err = at<unsigned long long>(a, p.err);
+    if (cfg->stream) {
+        c->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NALAR_E_CUDA);
+        c->own_stream = true;
+    }
+    if (cudaMallocHost(&c->h_cnt, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess)
+        return bail(NALAR_E_NOMEM);
+    for (auto& e : c->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
+    if (cfg->world > 1 && cfg->collective == NALAR_COLL_NCCL) {
+        if (!g_nccl.load(&c->err)) return bail(NALAR_E_COMM);
+        ncclUniqueId id;
+        memcpy(id.internal, cfg->nccl_id, 128);
+        if (g_nccl.commInitRank(&c->comm, cfg->world, id, cfg->rank) != ncclSuccess) return bail(NALAR_E_COMM);
+    }
+    *out = c;
+    return NALAR_OK;
+}
+
+int nalar_destroy(nalar_ctx* c) {
+    if (!c) return NALAR_OK;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    destroy_graphs(c);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->comm) g_nccl.commDestroy(c->comm);
+    if (c->own_arena && c->arena) cudaFree(c->arena);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->h_cnt) cudaFreeHost(c->h_cnt);
+    if (c->h_err) cudaFreeHost(c->h_err);
+    delete c;
+    return NALAR_OK;
+}
+
+void* nalar_stream(nalar_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row) {
+    if (err_row) *err_row = -1;
+    if (!c || !s) return NALAR_E_INVAL;
+    c->uploaded = false;
+    c->epoch_done = false;
+    const nalar_config& k = c->cfg;
+    if (s->n_futures > k.max_futures || s->n_edges > k.max_edges || s->n_workflows > k.max_workflows ||
+        s->n_instances > k.max_instances || s->n_types > k.max_types)
+        return fail(c, NALAR_E_NOMEM, "snapshot exceeds reservation");
+    const uint32_t N = s->n_futures, E = s->n_edges, W = s->n_workflows, I = s->n_instances, T = s->n_types;
+    if (!s->wf_fut_off || !s->f_edge_off || (W && (!s->wf_id || !s->wf_prio)) ||
+        (N && (!s->f_state || !s->f_type || !s->f_round || !s->f_executor || !s->f_pin)) || (E && !s->edges) ||
+        (I && (!s->i_type || !s->i_cap || !s->i_base_load)) || (T && !s->t_affinity))
+        return fail(c, NALAR_E_INVAL, "null array");
+    // structural checks that need no per-row work (host, O(W + I + T))
+    if (s->wf_fut_off[0] != 0 || s->wf_fut_off[W] != N) return fail(c, NALAR_E_INVAL, "wf_fut_off bounds");
+    for (uint32_t w = 0; w < W; ++w) {
+        if (s->wf_fut_off[w + 1] < s->wf_fut_off[w]) return fail(c, NALAR_E_INVAL, "wf_fut_off not monotone");
+        if (w && s->wf_id[w] <= s->wf_id[w - 1]) return fail(c, NALAR_E_INVAL, "wf_id not increasing");
+    }
+    if (s->f_edge_off[0] != 0 || s->f_edge_off[N] != E) return fail(c, NALAR_E_INVAL, "f_edge_off bounds");
+    for (uint32_t i = 0; i < I; ++i)
+        if (s->i_type[i] >= T) return fail(c, NALAR_E_INVAL, "instance type out of range");
+    for (uint32_t t = 0; t < T; ++t)
+        if (s->t_affinity[t] > NALAR_AFF_STATEFUL) return fail(c, NALAR_E_INVAL, "affinity out of range");
+    if (N && T == 0) return fail(c, NALAR_E_INVAL, "futures without types");
+
+    c->N = N; c->E = E; c->W = W; c->I = I; c->T = T; c->R = I + T;
+    std::vector<uint32_t> bw, br, be;
+    std::vector<uint8_t> bs;
+    size_t mx = 0;
+    partition(c, s->wf_fut_off, s->f_edge_off, bw, br, be, bs, &mx);
+    c->B = (uint32_t)bs.size();
+    c->fixed_smem = k1_fixed_smem(T, I, c->R);
+    c->smem = c->fixed_smem + mx;
+
+    cudaStream_t st = c->stream;
+    auto h2d = [&](void* d, const void* h, size_t bytes) -> cudaError_t {
+        return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    };
+    CK(h2d(c->d_wf_off, s->wf_fut_off, 4ull * (W + 1)));
+    CK(h2d(c->d_wf_prio, s->wf_prio, 4ull * W));
+    CK(h2d(c->d_state, s->f_state, N));
+    CK(h2d(c->d_type, s->f_type, N));
+    CK(h2d(c->d_round, s->f_round, N));
+    CK(h2d(c->d_exec, s->f_executor, 2ull * N));
+    CK(h2d(c->d_pin, s->f_pin, 2ull * N));
+    CK(h2d(c->d_eoff, s->f_edge_off, 4ull * (N + 1)));
+    CK(h2d(c->d_edges, s->edges, 4ull * E));
+    CK(h2d(c->d_itype, s->i_type, I));
+    CK(h2d(c->d_icap, s->i_cap, 4ull * I));
+    CK(h2d(c->d_ibase, s->i_base_load, 4ull * I));
+    CK(h2d(c->d_taff, s->t_affinity, T));
+    CK(h2d(c->d_blk_wf, bw.data(), 4ull * bw.size()));
+    CK(h2d(c->d_blk_row0, br.data(), 4ull * br.size()));
+    CK(h2d(c->d_blk_edge0, be.data(), 4ull * be.size()));
+    CK(h2d(c->d_blk_staged, bs.data(), bs.size()));
+    CK(cudaMemsetAsync(c->d_err, 0xFF, 8, st));
+    CK(cudaMemsetAsync(c->d_err + 1, 0, 8, st));
+    ValidateParams v{};
+    v.wf_fut_off = c->d_wf_off; v.f_state = c->d_state; v.f_type = c->d_type; v.f_exec = c->d_exec;
+    v.f_pin = c->d_pin; v.f_edge_off = c->d_eoff; v.edges = c->d_edges; v.i_type = c->d_itype;
+    v.n_wf = W; v.n_fut = N; v.n_edges = E; v.n_types = T; v.n_inst = I; v.err = c->d_err;
+    CK(launch_validate(v, st));
+    CK(cudaMemcpyAsync(c->h_err, c->d_err, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c->h_err[1]) return fail(c, NALAR_E_INVAL, "edge offsets not monotone");
+    if (c->h_err[0] != ~0ull) {
+        if (err_row) *err_row = (int64_t)c->h_err[0];
+        return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
+    }
+    c->uploaded = true;
+    return NALAR_OK;
+}
+
+int nalar_policy_epoch(nalar_ctx* c, int policy) {
+    if (!c) return NALAR_E_INVAL;
+    if (!c->uploaded) return fail(c, NALAR_E_STATE, "epoch before upload");
+    if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
+    if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
+        return fail(c, NALAR_E_STATE, "external collective: use nalar_epoch_begin/finish");
+    int rc;
+    if (c->cfg.flags & NALAR_F_NO_GRAPH) {
+        rc = enqueue_epoch(c, policy);
+    } else {
+        Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->smem};
+        cudaGraphExec_t& ge = c->gexec[policy];
+        if (!ge || !(c->gkey[policy] == key)) {
+            if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            rc = enqueue_epoch(c, policy);
+            cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+            if (rc) { if (e == cudaSuccess) cudaGraphDestroy(g); return rc; }
+            CK(e);
+            e = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            CK(e);
+            c->gkey[policy] = key;
+        }
+        CK(cudaGraphLaunch(ge, c->stream));
+        rc = NALAR_OK;
+    }
+    if (!rc) { c->epoch_done = true; c->last_policy = policy; }
+    return rc;
+}
+
+int nalar_epoch_begin(nalar_ctx* c, int policy) {
+    if (!c) return NALAR_E_INVAL;
+    if (!c->uploaded) return fail(c, NALAR_E_STATE, "epoch before upload");
+    if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
+    int rc = enqueue_first_half(c, policy);
+    if (!rc) { c->in_epoch = true; c->last_policy = policy; }
+    return rc;
+}
+
+int nalar_exchange_buffer(nalar_ctx* c, void** dev_ptr, size_t* n_words) {
+    if (!c || !dev_ptr || !n_words) return NALAR_E_INVAL;
+    *dev_ptr = c->d_x;
+    *n_words = c->uploaded ? x_used_words(c) : c->x_words;
+    return NALAR_OK;
+}
+
+int nalar_epoch_finish(nalar_ctx* c) {
+    if (!c) return NALAR_E_INVAL;
+    if (!c->in_epoch) return fail(c, NALAR_E_STATE, "finish without begin");
+    c->in_epoch = false;
+    int rc = enqueue_second_half(c);
+    if (!rc) c->epoch_done = true;
+    return rc;
+}
+
+int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
+    if (!c || !o) return NALAR_E_INVAL;
+    if (!c->epoch_done) return fail(c, NALAR_E_STATE, "fetch before epoch");
+    cudaStream_t st = c->stream;
+    CK(cudaMemcpyAsync(c->h_cnt, c->d_scr, C_NUM * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint32_t na = c->h_cnt[C_ASSIGNED];
+    o->n_f = c->N; o->n_w = c->W; o->n_i = c->I; o->n_assigned = na;
+    const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
+    const bool wbad = o->wf_agg && o->wf_cap < c->W;
+    const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
+    const bool abad = (o->assign_row || o->assign_inst) && o->a_cap < na;
+    if (fbad || wbad || ibad || abad) return fail(c, NALAR_E_SIZE, "output buffer too small");
+    auto d2h = [&](void* h, const void* d, size_t bytes) -> cudaError_t {
+        return (h && bytes) ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+    };
+    CK(d2h(o->status, c->d_status, c->N));
+    CK(d2h(o->level, c->d_level, c->N));
+    CK(d2h(o->depth, c->d_depth, 2ull * c->N));
+    CK(d2h(o->instance, c->d_inst, 2ull * c->N));
+    CK(d2h(o->new_pin, c->d_newpin, c->N));
+    CK(d2h(o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W));
+    CK(d2h(o->i_load, c->d_iload, 4ull * c->I));
+    CK(d2h(o->i_spare, c->d_ispare, 4ull * c->I));
+    CK(d2h(o->i_assigned, c->d_iasg, 4ull * c->I));
+    CK(d2h(o->assign_row, c->d_arow, 4ull * na));
+    CK(d2h(o->assign_inst, c->d_ainst, 2ull * na));
+    CK(cudaStreamSynchronize(st));
+    return NALAR_OK;
+}
+
+int nalar_epoch_stats_get(nalar_ctx* c, nalar_epoch_stats* s) {
+    if (!c || !s) return NALAR_E_INVAL;
+    if (!c->epoch_done) return fail(c, NALAR_E_STATE, "stats before epoch");
+    memset(s, 0, sizeof *s);
+    CK(cudaMemcpyAsync(c->h_cnt, c->d_scr, C_NUM * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    s->n_futures = c->N;
+    s->n_ready = c->h_cnt[C_READY];
+    s->n_eligible = c->h_cnt[C_ELIG];
+    s->n_doomed = c->h_cnt[C_DOOMED];
+    s->n_assigned = c->h_cnt[C_ASSIGNED];
+    s->n_deferred = s->n_eligible - s->n_assigned;
+    s->n_instances = c->I;
+    if (c->cfg.flags & NALAR_F_TIMING) {
+        CK(cudaEventElapsedTime(&s->epoch_us, c->ev[0], c->ev[3]));
+        CK(cudaEventElapsedTime(&s->k1_us, c->ev[0], c->ev[1]));
+        CK(cudaEventElapsedTime(&s->coll_us, c->ev[1], c->ev[2]));
+        CK(cudaEventElapsedTime(&s->k4_us, c->ev[2], c->ev[3]));
+        s->epoch_us *= 1000.f; s->k1_us *= 1000.f; s->coll_us *= 1000.f; s->k4_us *= 1000.f;
+    }
+    return NALAR_OK;
+}
+
+}  // extern "C"

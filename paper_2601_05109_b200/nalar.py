@@ -1,0 +1,320 @@
+"""Thin ctypes binding of include/nalar.h (argument marshalling only).
+
+Every step of the policy epoch runs in libnalar.so's sm_100a kernels; this
+module only lays out structs, passes pointers and wraps results as numpy
+arrays.  PyTorch is used for device memory (the library's workspace can be a
+torch CUDA tensor) and streams.  There is no CPU fallback: if libnalar.so is
+missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnalar.so")
+
+NALAR_OK, NALAR_E_INVAL, NALAR_E_STATE, NALAR_E_NOMEM, NALAR_E_SIZE, NALAR_E_CUDA, NALAR_E_COMM, \
+    NALAR_E_NOTIMPL = 0, -1, -2, -3, -4, -5, -6, -7
+NALAR_FCFS, NALAR_SRTF, NALAR_LPT = 0, 1, 2
+NALAR_COLL_NONE, NALAR_COLL_NCCL, NALAR_COLL_EXTERNAL = 0, 1, 2
+NALAR_F_TIMING, NALAR_F_NO_GRAPH, NALAR_F_FORCE_UNSTAGED = 1, 2, 4
+POLICIES = {"fcfs": NALAR_FCFS, "srtf": NALAR_SRTF, "lpt": NALAR_LPT}
+ERR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_STATE", -3: "E_NOMEM", -4: "E_SIZE", -5: "E_CUDA",
+             -6: "E_COMM", -7: "E_NOTIMPL"}
+WF_AGG_FIELDS = ("total", "pending", "ready", "inflight", "resolved", "failed", "doomed",
+                 "pinned_pending", "max_depth", "max_round")
+EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id", "nalar_create",
+           "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
+           "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
+           "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error")
+
+
+class nalar_config(C.Structure):
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("collective", C.c_int),
+                ("nccl_id", C.c_ubyte * 128), ("stream", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("levels", C.c_uint32),
+                ("max_futures", C.c_uint32), ("max_edges", C.c_uint32),
+                ("max_workflows", C.c_uint32), ("max_instances", C.c_uint32),
+                ("max_types", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class nalar_snapshot(C.Structure):
+    _fields_ = [("n_futures", C.c_uint32), ("n_edges", C.c_uint32), ("n_workflows", C.c_uint32),
+                ("n_instances", C.c_uint32), ("n_types", C.c_uint32),
+                ("global_row_base", C.c_uint64),
+                ("wf_id", C.c_void_p), ("wf_fut_off", C.c_void_p), ("wf_prio", C.c_void_p),
+                ("f_state", C.c_void_p), ("f_type", C.c_void_p), ("f_round", C.c_void_p),
+                ("f_executor", C.c_void_p), ("f_pin", C.c_void_p), ("f_edge_off", C.c_void_p),
+                ("edges", C.c_void_p), ("i_type", C.c_void_p), ("i_cap", C.c_void_p),
+                ("i_base_load", C.c_void_p), ("t_affinity", C.c_void_p)]
+
+
+class nalar_decisions(C.Structure):
+    _fields_ = [("status", C.c_void_p), ("level", C.c_void_p), ("depth", C.c_void_p),
+                ("instance", C.c_void_p), ("new_pin", C.c_void_p), ("f_cap", C.c_uint32),
+                ("wf_agg", C.c_void_p), ("wf_cap", C.c_uint32),
+                ("i_load", C.c_void_p), ("i_spare", C.c_void_p), ("i_assigned", C.c_void_p),
+                ("i_cap", C.c_uint32),
+                ("assign_row", C.c_void_p), ("assign_inst", C.c_void_p), ("a_cap", C.c_uint32),
+                ("n_f", C.c_uint32), ("n_w", C.c_uint32), ("n_i", C.c_uint32),
+                ("n_assigned", C.c_uint32)]
+
+
+class nalar_epoch_stats(C.Structure):
+    _fields_ = [("epoch_us", C.c_float), ("k1_us", C.c_float), ("coll_us", C.c_float),
+                ("k4_us", C.c_float), ("n_futures", C.c_uint32), ("n_ready", C.c_uint32),
+                ("n_eligible", C.c_uint32), ("n_assigned", C.c_uint32),
+                ("n_deferred", C.c_uint32), ("n_doomed", C.c_uint32), ("n_instances", C.c_uint32)]
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise RuntimeError(f"libnalar.so not built ({path}); run __graft_entry__.build() -- "
+                           "there is no CPU fallback")
+    lib = C.CDLL(path)
+    P = C.POINTER
+    lib.nalar_abi_version.restype = C.c_int
+    lib.nalar_workspace_bytes.argtypes = [P(nalar_config)]
+    lib.nalar_workspace_bytes.restype = C.c_size_t
+    lib.nalar_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.nalar_create.argtypes = [P(C.c_void_p), P(nalar_config)]
+    lib.nalar_destroy.argtypes = [C.c_void_p]
+    lib.nalar_snapshot_upload.argtypes = [C.c_void_p, P(nalar_snapshot), P(C.c_int64)]
+    lib.nalar_policy_epoch.argtypes = [C.c_void_p, C.c_int]
+    lib.nalar_epoch_begin.argtypes = [C.c_void_p, C.c_int]
+    lib.nalar_exchange_buffer.argtypes = [C.c_void_p, P(C.c_void_p), P(C.c_size_t)]
+    lib.nalar_epoch_finish.argtypes = [C.c_void_p]
+    lib.nalar_fetch_decisions.argtypes = [C.c_void_p, P(nalar_decisions)]
+    lib.nalar_epoch_stats_get.argtypes = [C.c_void_p, P(nalar_epoch_stats)]
+    lib.nalar_stream.argtypes = [C.c_void_p]
+    lib.nalar_stream.restype = C.c_void_p
+    lib.nalar_last_error.argtypes = [C.c_void_p]
+    lib.nalar_last_error.restype = C.c_char_p
+    for name in ("nalar_create", "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch",
+                 "nalar_epoch_begin", "nalar_exchange_buffer", "nalar_epoch_finish",
+                 "nalar_fetch_decisions", "nalar_epoch_stats_get", "nalar_nccl_unique_id"):
+        getattr(lib, name).restype = C.c_int
+    return lib
+
+
+_lib = load_library()
+
+
+class NalarError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data if a.size else None
+
+
+# ---------------------------------------------------------------------------
+# same-name wrappers of the C ABI (plain marshalling)
+# ---------------------------------------------------------------------------
+def nalar_abi_version() -> int:
+    return _lib.nalar_abi_version()
+
+
+def nalar_workspace_bytes(cfg: nalar_config) -> int:
+    return _lib.nalar_workspace_bytes(C.byref(cfg))
+
+
+def nalar_nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    rc = _lib.nalar_nccl_unique_id(C.addressof(buf))
+    if rc:
+        raise NalarError(rc, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def nalar_create(cfg: nalar_config) -> C.c_void_p:
+    h = C.c_void_p()
+    rc = _lib.nalar_create(C.byref(h), C.byref(cfg))
+    if rc:
+        raise NalarError(rc, "nalar_create failed (no sm_100 device, bad limits or NCCL init)")
+    return h
+
+
+def nalar_destroy(h) -> int:
+    return _lib.nalar_destroy(h)
+
+
+def nalar_last_error(h) -> str:
+    return (_lib.nalar_last_error(h) or b"").decode()
+
+
+def _check(h, rc, what):
+    if rc:
+        raise NalarError(rc, f"{what}: {nalar_last_error(h)}")
+
+
+def snapshot_struct(s) -> tuple:
+    """nalar_snapshot over a nalar_gen.Snapshot-like object (numpy arrays)."""
+    a = s.arrays()
+    st = nalar_snapshot(s.n_futures, s.n_edges, s.n_workflows, s.n_instances, s.n_types,
+                        int(getattr(s, "global_row_base", 0)),
+                        *[_ptr(a[k]) for k in ("wf_id", "wf_fut_off", "wf_prio", "f_state", "f_type",
+                                               "f_round", "f_executor", "f_pin", "f_edge_off",
+                                               "edges", "i_type", "i_cap", "i_base_load",
+                                               "t_affinity")])
+    return st, a
+
+
+def nalar_snapshot_upload(h, snap: nalar_snapshot) -> tuple[int, int]:
+    err = C.c_int64(-1)
+    rc = _lib.nalar_snapshot_upload(h, C.byref(snap), C.byref(err))
+    return rc, err.value
+
+
+def nalar_policy_epoch(h, policy: int) -> int:
+    return _lib.nalar_policy_epoch(h, int(policy))
+
+
+def nalar_epoch_begin(h, policy: int) -> int:
+    return _lib.nalar_epoch_begin(h, int(policy))
+
+
+def nalar_exchange_buffer(h) -> tuple[int, int]:
+    p = C.c_void_p()
+    n = C.c_size_t()
+    _check(h, _lib.nalar_exchange_buffer(h, C.byref(p), C.byref(n)), "exchange_buffer")
+    return p.value, n.value
+
+
+def nalar_epoch_finish(h) -> int:
+    return _lib.nalar_epoch_finish(h)
+
+
+def nalar_fetch_decisions(h, d: nalar_decisions) -> int:
+    return _lib.nalar_fetch_decisions(h, C.byref(d))
+
+
+def nalar_epoch_stats_get(h) -> nalar_epoch_stats:
+    s = nalar_epoch_stats()
+    _check(h, _lib.nalar_epoch_stats_get(h, C.byref(s)), "epoch_stats_get")
+    return s
+
+
+def nalar_stream(h) -> int:
+    return _lib.nalar_stream(h) or 0
+
+
+# ---------------------------------------------------------------------------
+# convenience context (still marshalling only)
+# ---------------------------------------------------------------------------
+class Context:
+    """One ctx on one GPU.  Device memory comes from a torch CUDA tensor."""
+
+    def __init__(self, max_futures, max_edges, max_workflows, max_instances, max_types,
+                 device=0, rank=0, world=1, collective=None, nccl_id=None, levels=256,
+                 flags=0, use_torch_memory=True, stream=None):
+        cfg = nalar_config()
+        cfg.device, cfg.rank, cfg.world = device, rank, world
+        cfg.collective = (NALAR_COLL_NONE if world == 1 else NALAR_COLL_NCCL) \
+            if collective is None else collective
+        if nccl_id is not None:
+            C.memmove(cfg.nccl_id, nccl_id, 128)
+        cfg.levels = levels
+        cfg.max_futures, cfg.max_edges, cfg.max_workflows = max_futures, max_edges, max_workflows
+        cfg.max_instances, cfg.max_types, cfg.flags = max_instances, max_types, flags
+        self._ws = None
+        if use_torch_memory:
+            import torch
+            nbytes = nalar_workspace_bytes(cfg)
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+            cfg.workspace, cfg.workspace_bytes = self._ws.data_ptr(), nbytes
+        if stream is not None:
+            cfg.stream = stream
+        self.cfg = cfg
+        self.h = nalar_create(cfg)
+        self.n = None
+
+    @classmethod
+    def for_snapshot(cls, s, **kw):
+        return cls(max(s.n_futures, 1), max(s.n_edges, 1), max(s.n_workflows, 1),
+                   max(s.n_instances, 1), max(s.n_types, 1), **kw)
+
+    def close(self):
+        if self.h:
+            nalar_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, s) -> None:
+        st, keep = snapshot_struct(s)
+        rc, row = nalar_snapshot_upload(self.h, st)
+        if rc:
+            e = NalarError(rc, f"upload: {nalar_last_error(self.h)}")
+            e.err_row = row
+            raise e
+        self.n = (s.n_futures, s.n_workflows, s.n_instances)
+
+    def epoch(self, policy="srtf") -> None:
+        pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        _check(self.h, nalar_policy_epoch(self.h, pol), "policy_epoch")
+
+    def begin(self, policy="srtf"):
+        pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        _check(self.h, nalar_epoch_begin(self.h, pol), "epoch_begin")
+
+    def finish(self):
+        _check(self.h, nalar_epoch_finish(self.h), "epoch_finish")
+
+    def exchange_buffer(self):
+        return nalar_exchange_buffer(self.h)
+
+    def stats(self) -> nalar_epoch_stats:
+        return nalar_epoch_stats_get(self.h)
+
+    def output_buffers(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg",
+                                     "i_load", "i_spare", "i_assigned", "assign"), alloc=None):
+        """Host buffers for fetch(); ``alloc(n, dtype)`` may return pinned memory."""
+        N, W, I = self.n
+        alloc = alloc or (lambda n, dt: np.zeros(n, dt))
+        spec = {"status": (N, np.uint8), "level": (N, np.uint8), "depth": (N, np.uint16),
+                "instance": (N, np.int16), "new_pin": (N, np.uint8),
+                "wf_agg": (W * 10, np.uint32), "i_load": (I, np.uint32),
+                "i_spare": (I, np.uint32), "i_assigned": (I, np.uint32)}
+        out = {k: alloc(n, dt) for k, (n, dt) in spec.items() if k in fields}
+        if "assign" in fields:
+            out["assign_row"] = alloc(max(N, 1), np.uint32)
+            out["assign_inst"] = alloc(max(N, 1), np.int16)
+        return out
+
+    def fetch(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
+                            "i_spare", "i_assigned", "assign"), out=None) -> dict:
+        N, W, I = self.n
+        bufs = out if out is not None else self.output_buffers(fields)
+        d = nalar_decisions()
+        for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
+                  "i_spare", "i_assigned", "assign_row", "assign_inst"):
+            if k in bufs:
+                setattr(d, k, _ptr(bufs[k]))
+        d.f_cap, d.wf_cap, d.i_cap = N, W, I
+        if "assign_row" in bufs:
+            d.a_cap = min(len(bufs["assign_row"]), len(bufs["assign_inst"]))
+        _check(self.h, nalar_fetch_decisions(self.h, d), "fetch_decisions")
+        res = dict(bufs)
+        if "wf_agg" in res:
+            res["wf_agg"] = res["wf_agg"].reshape(W, 10)
+        if "assign_row" in res:
+            res["assign_row"] = res["assign_row"][:d.n_assigned]
+            res["assign_inst"] = res["assign_inst"][:d.n_assigned]
+        res["n_assigned"] = d.n_assigned
+        return res
+
+    @property
+    def stream(self) -> int:
+        return nalar_stream(self.h)

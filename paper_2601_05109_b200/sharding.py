@@ -1,0 +1,36 @@
+"""Host-side sharding of the future table by workflow id (multi-GPU).
+
+Every dependency edge stays inside its workflow (Q1), so contiguous
+workflow ranges are independent for the sweep; ranks exchange only the
+(resource, level) histogram slots and per-instance in-flight counts.  Shards
+are contiguous in row order, balanced by future count: shard k starts at the
+first workflow w with wf_fut_off[w] >= k * N / G.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_bounds(wf_fut_off: np.ndarray, G: int) -> list[tuple[int, int]]:
+    """Workflow ranges [(w0, w1), ...] of the G shards (some may be empty)."""
+    off = np.asarray(wf_fut_off, dtype=np.int64)
+    W = len(off) - 1
+    N = int(off[-1]) if W >= 0 else 0
+    starts = [0]
+    for k in range(1, G):
+        target = -(-k * N // G)                 # ceil(k * N / G)
+        w = int(np.searchsorted(off[:W], target, side="left"))
+        starts.append(max(w, starts[-1]))
+    starts.append(W)
+    return [(starts[k], starts[k + 1]) for k in range(G)]
+
+
+def exchange_words(G: int, R: int, levels: int, n_inst: int) -> int:
+    """u32 words of the per-epoch exchange buffer: H[G][R][Lv] then load[I]."""
+    return G * R * levels + n_inst
+
+
+def slot_view(buf: np.ndarray, G: int, R: int, levels: int):
+    """(H[G][R][Lv], load[I]) views of an exchange buffer (numpy, host side)."""
+    h = buf[:G * R * levels].reshape(G, R, levels)
+    return h, buf[G * R * levels:]
