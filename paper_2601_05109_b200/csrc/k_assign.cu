@@ -175,18 +175,28 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         for (int k = 0; k < kK4Warps; ++k) s_wc[k][lv] = 0;
     }
     __syncthreads();
-    // suffix sums (levels above): small, one thread
-    if (tid == 0) {
-        uint64_t a = 0;
-        uint32_t la = 0;
-        for (int lv = 255; lv >= 0; --lv) {
-            s_A[lv] = a;
-            s_LA[lv] = la;
-            a += s_Hg[lv];
-            la += s_Hl[lv];
+    // suffix sums over levels (count strictly above each level): warp
+    // suffix scans + per-warp totals; thread tid owns level tid
+    {
+        static_assert(kK4Threads == 256, "one thread per level");
+        const uint32_t hg = s_Hg[tid], hl = s_Hl[tid];
+        uint32_t xg = hg, xl = hl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yg = __shfl_down_sync(0xFFFFFFFFu, xg, o);
+            const uint32_t yl = __shfl_down_sync(0xFFFFFFFFu, xl, o);
+            if (lane + o < 32) { xg += yg; xl += yl; }
         }
+        if (lane == 0) { s_wc[0][warp] = xg; s_wc[1][warp] = xl; }
+        __syncthreads();
+        uint32_t ag = xg - hg, al = xl - hl;
+        for (uint32_t k = warp + 1; k < (uint32_t)kK4Warps; ++k) { ag += s_wc[0][k]; al += s_wc[1][k]; }
+        s_A[tid] = ag;
+        s_LA[tid] = al;
+        __syncthreads();
+        if (tid < 2 * kK4Warps) s_wc[tid >> 3][tid & 7] = 0;
+        __syncthreads();
     }
-    __syncthreads();
     // number of this rank's futures admitted on r
     uint32_t adm_lv = 0;
     for (uint32_t lv = tid; lv < Lv; lv += kK4Threads) {
@@ -211,8 +221,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
 
     // ---- per-instance assigned counts (type blocks own their instances) ----
     if (is_type) {
-        uint64_t n_t = 0;
-        for (uint32_t lv = 0; lv < Lv; ++lv) n_t += s_Hg[lv];
+        const uint64_t n_t = s_A[0] + s_Hg[0];
         const uint64_t used = n_t < bound ? n_t : bound;
         uint64_t s0 = 0, j0 = 0;
         if (used) locate_slot(s_sp2, ni, maxs, used - 1, &s0, &j0);

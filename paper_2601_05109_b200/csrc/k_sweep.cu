@@ -17,9 +17,10 @@
 //   level  -- clamp(prio + score, 0, Lv-1) (set_priority PAPER.md:389; SRTF
 //             PAPER.md:691; LPT PAPER.md:696)
 //   per-instance in-flight counts (queue lengths)
-// Predecessors in earlier 32-row steps are final; predecessors inside the
-// current step are resolved by warp-synchronous Bellman-Ford rounds (edges
-// point to earlier rows, so rounds <= longest intra-step chain).
+// Predecessors in earlier 32-row steps are final (shared memory); those inside
+// the current step are settled in rounds: a lane settles once all its in-step
+// predecessors have, taking their depths by warp shuffles and their doom by
+// ballots (edges point to earlier rows, so rounds = longest in-step chain).
 // Finally the CTA buckets its eligible futures by resource (pin, or I + type)
 // in row order -- a stable counting sort whose positions come from scans, never
 // from atomics -- and adds them to the (resource, level) histogram that the
@@ -215,15 +216,20 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const bool valid = f < fb;
             const uint32_t stf = valid ? st[f] : 3u;
             const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
-            uint32_t d = 0;
-            bool dm = false, allres = true, intra = false;
+            // predecessors before this step are final in smem; those inside the
+            // step are recorded as lane masks (all / DEP) + up to 4 lane slots
+            uint32_t d = 0, need = 0, need_dep = 0, pk = 0, np = 0;
+            bool dm = false, allres = true, many = false;
             for (uint32_t e = eb; e < ee; ++e) {
                 const uint32_t v = ed[e];
                 const uint32_t s = (v & 0x7FFFFFFFu) - r0;
                 const bool call = (v >> 31) != 0;
-                if (s >= c0) {                       // inside this step: resolved below
-                    intra = true;
+                if (s >= c0) {
+                    const uint32_t k = s - c0;
+                    need |= 1u << k;
+                    if (np < 4) { pk |= k << (5 * np); ++np; } else { many = true; }
                     if (!call) {
+                        need_dep |= 1u << k;
                         const uint32_t ss = st[s];
                         dm |= ss == 4u;
                         allres &= ss == 3u;
@@ -241,34 +247,49 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             d = min(d, 65535u);
             const bool pend = stf == 0u;
             bool doom = pend && dm;
-            if (valid) { dep[f] = (uint16_t)d; flg[f] = doom ? FL_DOOMED : 0; }
-            __syncwarp();
-            if (__any_sync(0xFFFFFFFFu, intra)) {
+            // intra-step resolution: a lane settles once all its in-step
+            // predecessors have settled (rounds = longest in-step chain);
+            // depth values move by shuffles, doom by ballots
+            bool fin = need == 0u;
+            if (!__all_sync(0xFFFFFFFFu, fin)) {
+                const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
+                const bool wide = __any_sync(0xFFFFFFFFu, many);
                 for (;;) {
+                    const uint32_t F = __ballot_sync(0xFFFFFFFFu, fin);
+                    if (F == 0xFFFFFFFFu) break;
+                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+                    const bool can = !fin && (need & ~F) == 0u;
                     uint32_t nd = d;
-                    bool ndm = doom;
-                    if (intra) {
-                        for (uint32_t e = eb; e < ee; ++e) {
-                            const uint32_t v = ed[e];
-                            const uint32_t s = (v & 0x7FFFFFFFu) - r0;
-                            if (s < c0) continue;
-                            nd = max(nd, (uint32_t)dep[s] + 1u);
-                            if (!(v >> 31) && pend) ndm |= (flg[s] & FL_DOOMED) != 0;
+                    if (wide) {
+                        for (uint32_t k = 0; k < 32; ++k) {
+                            const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
+                            if ((need >> k) & 1u) nd = max(nd, x + 1u);
                         }
-                        nd = min(nd, 65535u);
+                    } else {
+                        for (uint32_t k = 0; k < K; ++k) {
+                            const uint32_t src = k < np ? (pk >> (5 * k)) & 31u : lane;
+                            const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, src);
+                            if (k < np) nd = max(nd, x + 1u);
+                        }
                     }
-                    const bool ch = (nd != d) || (ndm != doom);
-                    __syncwarp();
-                    if (ch) { d = nd; doom = ndm; dep[f] = (uint16_t)d; flg[f] = doom ? FL_DOOMED : 0; }
-                    __syncwarp();
-                    if (!__any_sync(0xFFFFFFFFu, ch)) break;
+                    if (can) {
+                        d = min(nd, 65535u);
+                        doom = pend && (dm || (need_dep & D) != 0u);
+                        fin = true;
+                    }
                 }
             }
+            // first PENDING non-doomed / first ready unpinned row per type:
+            // rows rise with lane, so the lowest lane of each type group wins
+            const uint32_t tyf = valid ? ty[f] : 0u;
+            const int pinf = valid ? pn[f] : -1;
+            const bool ready = pend && !doom && allres;
+            const uint32_t kp = (valid && pend && !doom) ? tyf : 0xFFFFu;
+            const uint32_t kr = (valid && ready && pinf < 0) ? tyf : 0xFFFFu;
+            const uint32_t mp = __match_any_sync(0xFFFFFFFFu, kp);
+            const uint32_t mr = __match_any_sync(0xFFFFFFFFu, kr);
             if (valid) {
-                const uint32_t tyf = ty[f];
-                const int pinf = pn[f];
                 const uint32_t aff = s_aff[tyf];
-                const bool ready = pend && !doom && allres;
                 uint8_t fl = doom ? FL_DOOMED : 0;
                 if (ready) fl |= FL_READY;
                 if (ready && (aff == 0u || (aff == 1u && pinf >= 0))) fl |= FL_ELIG;
@@ -276,8 +297,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                     atomicOr(infl, 1ull << tyf);
                     atomicAdd(&s_load[p.f_exec[r0 + f]], 1u);
                 }
-                if (pend && !doom) atomicMin(&fp[tyf], f);
-                if (ready && pinf < 0) atomicMin(&fru[tyf], f);
+                dep[f] = (uint16_t)d;
                 flg[f] = fl;
                 c_pend += pend;
                 c_ready += ready;
@@ -288,6 +308,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 c_pinp += pend && pinf >= 0;
                 m_dep = max(m_dep, d);
                 m_rnd = max(m_rnd, (uint32_t)p.f_round[r0 + f]);
+                if (kp != 0xFFFFu && (__ffs(mp) - 1) == (int)lane) atomicMin(&fp[tyf], f);
+                if (kr != 0xFFFFu && (__ffs(mr) - 1) == (int)lane) atomicMin(&fru[tyf], f);
             }
             __syncwarp();
         }

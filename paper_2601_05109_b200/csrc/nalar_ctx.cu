@@ -286,10 +286,10 @@ int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
     // clear exchange buffer (used part) + counters + adm_pub; contiguous region
     CK(cudaMemsetAsync(c->d_x, 0, c->x_words * 4 + (C_NUM + (size_t)c->Rmax) * 4, c->stream));
-    if (timing) CK(cudaEventRecord(c->ev[0], c->stream));
+    if (timing) CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
     int rc = run_k1(c, policy);
     if (rc) return rc;
-    if (timing) CK(cudaEventRecord(c->ev[1], c->stream));
+    if (timing) CK(cudaEventRecordWithFlags(c->ev[1], c->stream, cudaEventRecordExternal));
     return NALAR_OK;
 }
 
@@ -305,10 +305,10 @@ int enqueue_collective(nalar_ctx* c) {
 
 int enqueue_second_half(nalar_ctx* c) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
-    if (timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    if (timing) CK(cudaEventRecordWithFlags(c->ev[2], c->stream, cudaEventRecordExternal));
     int rc = run_k4(c);
     if (rc) return rc;
-    if (timing) CK(cudaEventRecord(c->ev[3], c->stream));
+    if (timing) CK(cudaEventRecordWithFlags(c->ev[3], c->stream, cudaEventRecordExternal));
     return NALAR_OK;
 }
 
