@@ -66,6 +66,7 @@ struct SweepParams {
     uint32_t* wf_agg;           // [W][10]
     uint32_t* H;                // this rank's histogram slot [R][Lv]
     uint32_t* load_part;        // [I] in-flight counts of this rank's rows
+    uint32_t* tot;              // [R] eligible futures per resource (this rank)
     uint2* items;               // [N] eligible (row, level), per-block regions
     uint32_t* cnt_rb;           // [R][B]
     uint32_t* off_rb;           // [R][B]
@@ -75,6 +76,9 @@ struct SweepParams {
 struct AssignParams {
     const uint32_t* H;          // [G][R][Lv] summed over ranks
     const uint32_t* load_sum;   // [I] summed over ranks
+    const uint32_t* tot;        // [R] eligible futures per resource, summed over ranks
+    const uint32_t* type_off;   // [T+1] instances of type t: type_inst[type_off[t] ..]
+    const uint32_t* type_inst;  // [I]   instance ids grouped by type, ascending
     uint32_t G, slot, R, n_inst, n_types, levels, B;
     const uint8_t* i_type;
     const uint32_t* i_cap;

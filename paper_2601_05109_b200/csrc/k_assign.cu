@@ -25,9 +25,11 @@ namespace nalar {
 
 namespace {
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+constexpr uint32_t kSlotCap = 4096;   // phase-B slot table kept in smem up to this size
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
@@ -43,6 +45,7 @@ __device__ __forceinline__ Tv block_sum(Tv v, Tv* red) {
     if (lane == 0) red[warp] = v;
     __syncthreads();
     Tv s = 0;
+#pragma unroll
     for (int k = 0; k < kK4Warps; ++k) s += red[k];
     return s;
 }
@@ -67,6 +70,18 @@ __device__ __forceinline__ void locate_slot(const uint64_t* sp2, uint32_t n, uin
     *j_out = g - slots_above(sp2, n, lo);
 }
 
+__device__ __forceinline__ uint32_t slot_instance(const uint64_t* sp2, const uint32_t* inst, uint32_t n,
+                                                  uint64_t maxs, uint64_t g) {
+    uint64_t s, j;
+    locate_slot(sp2, n, maxs, g, &s, &j);
+    for (uint32_t k = 0; k < n; ++k)
+        if (sp2[k] >= s) {
+            if (j == 0) return inst[k];
+            --j;
+        }
+    return 0xFFFFFFFFu;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
@@ -74,17 +89,18 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     __shared__ uint32_t s_inst[NALAR_MAX_INSTANCES_DEV];
     __shared__ uint64_t s_spare[NALAR_MAX_INSTANCES_DEV];   // spare before phase A
     __shared__ uint64_t s_sp2[NALAR_MAX_INSTANCES_DEV];     // spare after phase A
-    __shared__ uint64_t s_A[256];                           // global count above level
-    __shared__ uint64_t s_before[256];                      // same level, lower ranks
+    __shared__ uint32_t s_A[256];                           // global count above level
+    __shared__ uint32_t s_before[256];                      // same level, lower ranks
     __shared__ uint32_t s_LA[256];                          // local count above level
     __shared__ uint32_t s_Hg[256];
     __shared__ uint32_t s_Hl[256];
     __shared__ uint32_t s_run[256];
     __shared__ uint32_t s_wc[kK4Warps][256];
-    __shared__ uint64_t s_red64[kK4Warps];
+    __shared__ uint64_t s_red64[2 * kK4Warps];
     __shared__ uint32_t s_red32[kK4Warps];
     __shared__ uint32_t s_pref[kK4Threads + 1];
-    __shared__ uint32_t s_ni;
+    __shared__ uint16_t s_slot[kSlotCap];
+    __shared__ uint64_t s_bound;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
@@ -94,71 +110,32 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     const bool is_type = r >= I;
     const uint32_t t = is_type ? r - I : p.i_type[r];
 
-    // ---- instances of type t (ascending id), their load and spare ----------
-    if (tid == 0) s_ni = 0;
-    __syncthreads();
-    for (uint32_t i0 = 0; i0 < I; i0 += kK4Threads) {
-        const uint32_t i = i0 + tid;
-        const bool m = i < I && p.i_type[i] == t;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
-        if (lane == 0) s_red32[warp] = __popc(bal);
-        __syncthreads();
-        uint32_t base = s_ni;
-        for (uint32_t k = 0; k < warp; ++k) base += s_red32[k];
-        if (m) s_inst[base + __popc(bal & ((1u << lane) - 1u))] = i;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t tot = 0;
-            for (int k = 0; k < kK4Warps; ++k) tot += s_red32[k];
-            s_ni += tot;
-        }
-        __syncthreads();
-    }
-    const uint32_t ni = s_ni;
-    // warp per instance: load, spare, phase-A admissions (all ranks)
-    for (uint32_t k = warp; k < ni; k += kK4Warps) {
-        const uint32_t i = s_inst[k];
-        uint64_t ha = 0;
-        for (uint32_t x = lane; x < G * Lv; x += 32) {
-            const uint32_t s = x / Lv, lv = x - s * Lv;
-            ha += p.H[((size_t)s * R + i) * Lv + lv];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ha += __shfl_xor_sync(0xFFFFFFFFu, ha, o);
-        if (lane == 0) {
+    // ---- instances of type t: load, spare, phase-A admissions (all ranks) ----
+    // (per-type instance lists in ascending id are built on the host at upload)
+    uint32_t ni = 0;
+    if (is_type) {
+        const uint32_t k0 = p.type_off[t];
+        ni = p.type_off[t + 1] - k0;
+        for (uint32_t k = tid; k < ni; k += kK4Threads) {
+            const uint32_t i = p.type_inst[k0 + k];
             const uint64_t load = (uint64_t)p.i_base[i] + p.load_sum[i];
             const uint64_t cap = p.i_cap[i];
             const uint64_t spare = cap > load ? cap - load : 0ull;
-            const uint64_t adm = ha < spare ? ha : spare;
+            const uint64_t ha = p.tot[i];
+            s_inst[k] = i;
             s_spare[k] = spare;
-            s_sp2[k] = spare - adm;
-            if (is_type) {
-                p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
-                p.i_spare[i] = (uint32_t)spare;
-            }
+            s_sp2[k] = spare - (ha < spare ? ha : spare);
+            p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
+            p.i_spare[i] = (uint32_t)spare;
         }
+    } else if (tid == 0) {
+        const uint64_t load = (uint64_t)p.i_base[r] + p.load_sum[r];
+        const uint64_t cap = p.i_cap[r];
+        s_bound = cap > load ? cap - load : 0ull;
     }
-    __syncthreads();
-
-    // ---- bound of this resource -------------------------------------------
-    uint64_t bound = 0, maxs = 0;
-    if (is_type) {
-        uint64_t sum = 0, mx = 0;
-        for (uint32_t k = tid; k < ni; k += kK4Threads) { sum += s_sp2[k]; mx = max(mx, s_sp2[k]); }
-        bound = block_sum<uint64_t>(sum, s_red64);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-        __syncthreads();
-        if (lane == 0) s_red64[warp] = mx;
-        __syncthreads();
-        for (int k = 0; k < kK4Warps; ++k) maxs = max(maxs, s_red64[k]);
-    } else {
-        for (uint32_t k = 0; k < ni; ++k)
-            if (s_inst[k] == r) bound = s_spare[k];
-    }
-
     // ---- level histogram of r: global, lower-ranks, local ------------------
-    for (uint32_t lv = tid; lv < 256; lv += kK4Threads) {
+    {
+        const uint32_t lv = tid;
         uint32_t hg = 0, hb = 0, hl = 0;
         if (lv < Lv) {
             for (uint32_t s = 0; s < G; ++s) {
@@ -172,12 +149,17 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         s_Hl[lv] = hl;
         s_before[lv] = hb;
         s_run[lv] = 0;
+#pragma unroll
         for (int k = 0; k < kK4Warps; ++k) s_wc[k][lv] = 0;
     }
     __syncthreads();
-    // suffix sums over levels (count strictly above each level): warp
-    // suffix scans + per-warp totals; thread tid owns level tid
+
+    // ---- bound of this resource; suffix sums over levels ------------------
+    uint64_t bound, maxs = 0;
     {
+        uint64_t sum = 0, mx = 0;
+        for (uint32_t k = tid; k < ni; k += kK4Threads) { sum += s_sp2[k]; mx = max(mx, s_sp2[k]); }
+        // count strictly above each level: warp suffix scans + per-warp totals
         static_assert(kK4Threads == 256, "one thread per level");
         const uint32_t hg = s_Hg[tid], hl = s_Hl[tid];
         uint32_t xg = hg, xl = hl;
@@ -187,23 +169,36 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             const uint32_t yl = __shfl_down_sync(0xFFFFFFFFu, xl, o);
             if (lane + o < 32) { xg += yg; xl += yl; }
         }
-        if (lane == 0) { s_wc[0][warp] = xg; s_wc[1][warp] = xl; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        }
+        if (lane == 0) {
+            s_wc[0][warp] = xg;
+            s_wc[1][warp] = xl;
+            s_red64[warp] = sum;
+            s_red64[kK4Warps + warp] = mx;
+        }
         __syncthreads();
         uint32_t ag = xg - hg, al = xl - hl;
         for (uint32_t k = warp + 1; k < (uint32_t)kK4Warps; ++k) { ag += s_wc[0][k]; al += s_wc[1][k]; }
         s_A[tid] = ag;
         s_LA[tid] = al;
+        uint64_t bs = 0;
+#pragma unroll
+        for (int k = 0; k < kK4Warps; ++k) { bs += s_red64[k]; maxs = max(maxs, s_red64[kK4Warps + k]); }
+        bound = is_type ? bs : s_bound;
         __syncthreads();
         if (tid < 2 * kK4Warps) s_wc[tid >> 3][tid & 7] = 0;
-        __syncthreads();
     }
-    // number of this rank's futures admitted on r
+    // number of this rank's futures admitted on r (closed form per level)
     uint32_t adm_lv = 0;
-    for (uint32_t lv = tid; lv < Lv; lv += kK4Threads) {
-        const uint64_t pre = s_A[lv] + s_before[lv];
+    if (tid < Lv) {
+        const uint64_t pre = (uint64_t)s_A[tid] + s_before[tid];
         if (pre < bound) {
             const uint64_t room = bound - pre;
-            adm_lv = (uint32_t)(room < s_Hl[lv] ? room : s_Hl[lv]);
+            adm_lv = (uint32_t)(room < s_Hl[tid] ? room : s_Hl[tid]);
         }
     }
     const uint32_t n_adm = block_sum<uint32_t>(adm_lv, s_red32);
@@ -213,15 +208,16 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     uint32_t base_part = 0;
     for (uint32_t q = tid; q < r; q += kK4Threads) {
         uint32_t v;
-        do { v = ld_acquire(&p.adm_pub[q]); } while (!(v & 0x80000000u));
+        do { v = ld_relaxed(&p.adm_pub[q]); } while (!(v & 0x80000000u));
         base_part += v & 0x7FFFFFFFu;
     }
     const uint32_t list_base = block_sum<uint32_t>(base_part, s_red32);
     if (tid == 0 && n_adm) atomicAdd(&p.counters[C_ASSIGNED], n_adm);
 
-    // ---- per-instance assigned counts (type blocks own their instances) ----
+    // ---- per-instance assigned counts + phase-B slot table (type blocks) ----
+    const bool table = is_type && bound <= kSlotCap;
     if (is_type) {
-        const uint64_t n_t = s_A[0] + s_Hg[0];
+        const uint64_t n_t = (uint64_t)s_A[0] + s_Hg[0];
         const uint64_t used = n_t < bound ? n_t : bound;
         uint64_t s0 = 0, j0 = 0;
         if (used) locate_slot(s_sp2, ni, maxs, used - 1, &s0, &j0);
@@ -238,13 +234,26 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             }
             p.i_assigned[s_inst[k]] = (uint32_t)asg;
         }
+        if (table && n_adm && warp == 0) {
+            // slots in (level desc, instance asc) order, one level per step
+            uint32_t pos = 0;
+            for (uint64_t sv = maxs; sv >= 1; --sv) {
+                for (uint32_t k0 = 0; k0 < ni; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    const bool in = k < ni && s_sp2[k] >= sv;
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, in);
+                    if (in) s_slot[pos + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)s_inst[k];
+                    pos += __popc(bal);
+                }
+            }
+        }
     }
     if (n_adm == 0) return;
+    __syncthreads();
 
     // ---- walk this rank's futures of r in row order --------------------------
     const uint8_t aff = is_type ? p.t_aff[t] : 0;
     uint32_t found = 0;
-    uint32_t carry = 0;      // positions of earlier block-chunks
     for (uint32_t b0 = 0; b0 < B && found < n_adm; b0 += kK4Threads) {
         // prefix of per-K1-block counts for blocks [b0, b0 + 256)
         const uint32_t bb = b0 + tid;
@@ -281,7 +290,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
                 const uint2 it = p.items[p.blk_row0[kb] + p.off_rb[(size_t)r * B + kb] + (q - s_pref[lo])];
                 row = it.x;
                 lv = it.y;
-                live = s_A[lv] + s_before[lv] < bound;
+                live = (uint64_t)s_A[lv] + s_before[lv] < bound;
                 if (!live) lv = 0xFFFFu;
             }
             const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv);
@@ -293,27 +302,20 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             if (live) {
                 rank = s_run[lv] + wrank;
                 for (uint32_t k = 0; k < warp; ++k) rank += s_wc[k][lv];
-                adm = s_A[lv] + s_before[lv] + rank < bound;
+                adm = (uint64_t)s_A[lv] + s_before[lv] + rank < bound;
             }
             __syncthreads();
-            for (uint32_t j = tid; j < 256; j += kK4Threads) {
+            {
                 uint32_t add = 0;
-                for (int k = 0; k < kK4Warps; ++k) { add += s_wc[k][j]; s_wc[k][j] = 0; }
-                s_run[j] += add;
+#pragma unroll
+                for (int k = 0; k < kK4Warps; ++k) { add += s_wc[k][tid]; s_wc[k][tid] = 0; }
+                s_run[tid] += add;
             }
             if (adm) {
-                const uint64_t g = s_A[lv] + s_before[lv] + rank;
+                const uint64_t g = (uint64_t)s_A[lv] + s_before[lv] + rank;
                 int16_t inst = (int16_t)r;
-                if (is_type) {
-                    uint64_t s, j;
-                    locate_slot(s_sp2, ni, maxs, g, &s, &j);
-                    for (uint32_t k = 0; k < ni; ++k) {
-                        if (s_sp2[k] >= s) {
-                            if (j == 0) { inst = (int16_t)s_inst[k]; break; }
-                            --j;
-                        }
-                    }
-                }
+                if (is_type)
+                    inst = (int16_t)(table ? s_slot[g] : slot_instance(s_sp2, s_inst, ni, maxs, g));
                 p.status[row] = 7;
                 p.instance[row] = inst;
                 p.new_pin[row] = (uint8_t)(is_type && aff != 0);
@@ -323,9 +325,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             }
             found += __syncthreads_count(adm);
         }
-        carry += total;
     }
-    (void)carry;
 }
 
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {

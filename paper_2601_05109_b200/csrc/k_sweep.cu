@@ -217,17 +217,22 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const uint32_t stf = valid ? st[f] : 3u;
             const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
             // predecessors before this step are final in smem; those inside the
-            // step are recorded as lane masks (all / DEP) + up to 4 lane slots
-            uint32_t d = 0, need = 0, need_dep = 0, pk = 0, np = 0;
-            bool dm = false, allres = true, many = false;
+            // step are kept as up to 4 lane slots (+ a mask for any extra ones)
+            uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
+            uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
+            bool dm = false, allres = true;
             for (uint32_t e = eb; e < ee; ++e) {
                 const uint32_t v = ed[e];
                 const uint32_t s = (v & 0x7FFFFFFFu) - r0;
                 const bool call = (v >> 31) != 0;
                 if (s >= c0) {
                     const uint32_t k = s - c0;
-                    need |= 1u << k;
-                    if (np < 4) { pk |= k << (5 * np); ++np; } else { many = true; }
+                    if (np == 0) s0 = k;
+                    else if (np == 1) s1 = k;
+                    else if (np == 2) s2 = k;
+                    else if (np == 3) s3 = k;
+                    else extra |= 1u << k;
+                    ++np;
                     if (!call) {
                         need_dep |= 1u << k;
                         const uint32_t ss = st[s];
@@ -247,38 +252,34 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             d = min(d, 65535u);
             const bool pend = stf == 0u;
             bool doom = pend && dm;
-            // intra-step resolution: a lane settles once all its in-step
-            // predecessors have settled (rounds = longest in-step chain);
-            // depth values move by shuffles, doom by ballots
-            bool fin = need == 0u;
-            if (!__all_sync(0xFFFFFFFFu, fin)) {
-                const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
-                const bool wide = __any_sync(0xFFFFFFFFu, many);
+            // in-step settling: Bellman-Ford rounds on registers -- depths move
+            // by shuffles, doom by ballots; rounds = longest in-step chain + 1
+            if (__any_sync(0xFFFFFFFFu, np != 0u)) {
+                const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
+                const uint32_t m0 = np > 0 ? 0xFFFFFFFFu : 0u, m1 = np > 1 ? 0xFFFFFFFFu : 0u;
+                const uint32_t m2 = np > 2 ? 0xFFFFFFFFu : 0u, m3 = np > 3 ? 0xFFFFFFFFu : 0u;
                 for (;;) {
-                    const uint32_t F = __ballot_sync(0xFFFFFFFFu, fin);
-                    if (F == 0xFFFFFFFFu) break;
+                    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
+                    const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
+                    const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
+                    const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
                     const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
-                    const bool can = !fin && (need & ~F) == 0u;
-                    uint32_t nd = d;
+                    uint32_t nd = max(max((x0 + 1u) & m0, (x1 + 1u) & m1), max((x2 + 1u) & m2, (x3 + 1u) & m3));
                     if (wide) {
                         for (uint32_t k = 0; k < 32; ++k) {
                             const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
-                            if ((need >> k) & 1u) nd = max(nd, x + 1u);
-                        }
-                    } else {
-                        for (uint32_t k = 0; k < K; ++k) {
-                            const uint32_t src = k < np ? (pk >> (5 * k)) & 31u : lane;
-                            const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, src);
-                            if (k < np) nd = max(nd, x + 1u);
+                            if ((extra >> k) & 1u) nd = max(nd, x + 1u);
                         }
                     }
-                    if (can) {
-                        d = min(nd, 65535u);
-                        doom = pend && (dm || (need_dep & D) != 0u);
-                        fin = true;
-                    }
+                    nd = min(max(nd, d), 65535u);
+                    const bool ndm = doom || (pend && (need_dep & D) != 0u);
+                    const bool ch = (nd != d) | (ndm != doom);
+                    d = nd;
+                    doom = ndm;
+                    if (!__any_sync(0xFFFFFFFFu, ch)) break;
                 }
             }
+
             // first PENDING non-doomed / first ready unpinned row per type:
             // rows rise with lane, so the lowest lane of each type group wins
             const uint32_t tyf = valid ? ty[f] : 0u;
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             s_roff[r] = run;
             p.cnt_rb[(size_t)r * p.B + b] = c;
             p.off_rb[(size_t)r * p.B + b] = run;
+            if (c) atomicAdd(&p.tot[r], c);
             run += c;
             s_rcnt[r] = 0;   // reused as the running rank counter below
         }

@@ -78,6 +78,7 @@ struct nalar_ctx {
     int16_t *d_exec = nullptr, *d_pin = nullptr;
     uint32_t *d_blk_wf = nullptr, *d_blk_row0 = nullptr, *d_blk_edge0 = nullptr;
     uint8_t* d_blk_staged = nullptr;
+    uint32_t *d_type_off = nullptr, *d_type_inst = nullptr;
     // outputs
     uint8_t *d_status = nullptr, *d_level = nullptr, *d_newpin = nullptr, *d_gflags = nullptr;
     uint16_t* d_depth = nullptr;
@@ -137,7 +138,7 @@ struct Layout {
 
 struct Plan {
     size_t wf_off, wf_prio, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
-    size_t blk_wf, blk_row0, blk_edge0, blk_staged;
+    size_t blk_wf, blk_row0, blk_edge0, blk_staged, type_off, type_inst;
     size_t status, level, newpin, gflags, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
@@ -169,6 +170,8 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->blk_row0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_edge0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_staged = L.take<uint8_t>(p->Bmax);
+    p->type_off = L.take<uint32_t>(T + 1);
+    p->type_inst = L.take<uint32_t>(I);
     p->status = L.take<uint8_t>(N);
     p->level = L.take<uint8_t>(N);
     p->newpin = L.take<uint8_t>(N);
@@ -184,7 +187,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->items = L.take<uint2>(N);
     p->cnt_rb = L.take<uint32_t>((size_t)p->Rmax * p->Bmax);
     p->off_rb = L.take<uint32_t>((size_t)p->Rmax * p->Bmax);
-    p->x_words = (size_t)G * p->Rmax * Lv + I;
+    p->x_words = (size_t)G * p->Rmax * Lv + I + p->Rmax;
     // exchange buffer and scratch are contiguous so one memset clears both
     p->x = L.off;
     L.off += p->x_words * 4;
@@ -253,6 +256,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.H = c->d_x + (size_t)slot * c->R * c->Lv;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.load_part = c->d_x + (size_t)G * c->R * c->Lv;
+    p.tot = p.load_part + c->I;
     p.items = c->d_items; p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb;
     p.counters = c->d_scr;
     CK(launch_sweep(p, c->smem, c->stream));
@@ -264,6 +268,9 @@ int run_k4(nalar_ctx* c) {
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.H = c->d_x;
     p.load_sum = c->d_x + (size_t)G * c->R * c->Lv;
+    p.tot = p.load_sum + c->I;
+    p.type_off = c->d_type_off;
+    p.type_inst = c->d_type_inst;
     p.G = G; p.slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
     p.R = c->R; p.n_inst = c->I; p.n_types = c->T; p.levels = c->Lv; p.B = c->B;
     p.i_type = c->d_itype; p.i_cap = c->d_icap; p.i_base = c->d_ibase; p.t_aff = c->d_taff;
@@ -279,7 +286,7 @@ int run_k4(nalar_ctx* c) {
 
 size_t x_used_words(nalar_ctx* c) {
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
-    return (size_t)G * c->R * c->Lv + c->I;
+    return (size_t)G * c->R * c->Lv + c->I + c->R;
 }
 
 int enqueue_first_half(nalar_ctx* c, int policy) {
@@ -386,6 +393,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_taff = at<uint8_t>(a, p.taff);
     c->d_blk_wf = at<uint32_t>(a, p.blk_wf); c->d_blk_row0 = at<uint32_t>(a, p.blk_row0);
     c->d_blk_edge0 = at<uint32_t>(a, p.blk_edge0); c->d_blk_staged = at<uint8_t>(a, p.blk_staged);
+    c->d_type_off = at<uint32_t>(a, p.type_off); c->d_type_inst = at<uint32_t>(a, p.type_inst);
     c->d_status = at<uint8_t>(a, p.status); c->d_level = at<uint8_t>(a, p.level);
     c->d_newpin = at<uint8_t>(a, p.newpin); c->d_gflags = at<uint8_t>(a, p.gflags);
     c->d_depth = at<uint16_t>(a, p.depth); c->d_inst = at<int16_t>(a, p.inst); c->d_ainst = at<int16_t>(a, p.ainst);
@@ -490,6 +498,16 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     CK(h2d(c->d_blk_row0, br.data(), 4ull * br.size()));
     CK(h2d(c->d_blk_edge0, be.data(), 4ull * be.size()));
     CK(h2d(c->d_blk_staged, bs.data(), bs.size()));
+    // instances grouped by type (ascending id), for the assignment pass
+    std::vector<uint32_t> toff(T + 1, 0), tinst(I);
+    for (uint32_t i = 0; i < I; ++i) toff[s->i_type[i] + 1]++;
+    for (uint32_t t = 0; t < T; ++t) toff[t + 1] += toff[t];
+    {
+        std::vector<uint32_t> cur(toff.begin(), toff.end() - 1);
+        for (uint32_t i = 0; i < I; ++i) tinst[cur[s->i_type[i]]++] = i;
+    }
+    CK(h2d(c->d_type_off, toff.data(), 4ull * (T + 1)));
+    CK(h2d(c->d_type_inst, tinst.data(), 4ull * I));
     CK(cudaMemsetAsync(c->d_err, 0xFF, 8, st));
     CK(cudaMemsetAsync(c->d_err + 1, 0, 8, st));
     ValidateParams v{};

@@ -26,11 +26,11 @@ def shard_bounds(wf_fut_off: np.ndarray, G: int) -> list[tuple[int, int]]:
 
 
 def exchange_words(G: int, R: int, levels: int, n_inst: int) -> int:
-    """u32 words of the per-epoch exchange buffer: H[G][R][Lv] then load[I]."""
-    return G * R * levels + n_inst
+    """u32 words of the per-epoch exchange buffer: H[G][R][Lv], load[I], tot[R]."""
+    return G * R * levels + n_inst + R
 
 
-def slot_view(buf: np.ndarray, G: int, R: int, levels: int):
-    """(H[G][R][Lv], load[I]) views of an exchange buffer (numpy, host side)."""
-    h = buf[:G * R * levels].reshape(G, R, levels)
-    return h, buf[G * R * levels:]
+def slot_view(buf: np.ndarray, G: int, R: int, levels: int, n_inst: int):
+    """(H[G][R][Lv], load[I], tot[R]) views of an exchange buffer (host side)."""
+    n = G * R * levels
+    return buf[:n].reshape(G, R, levels), buf[n:n + n_inst], buf[n + n_inst:n + n_inst + R]

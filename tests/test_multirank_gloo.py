@@ -63,7 +63,7 @@ def _worker(rank, world, port, which, q):
         assert obj[0] == bytes(range(128))
         # local contribution: slot `rank` of H + in-flight loads of local rows
         buf = np.zeros(exchange_words(world, R, Lv, I), np.int64)
-        H, load = slot_view(buf, world, R, Lv)
+        H, load, tot = slot_view(buf, world, R, Lv, I)
         local = []
         for lf in range(sh.n_futures):
             f = r0 + lf
@@ -72,11 +72,13 @@ def _worker(rank, world, port, which, q):
             if o["status"][f] in (S_DEF, S_ASG):
                 r = int(sh.f_pin[lf]) if sh.f_pin[lf] >= 0 else I + int(sh.f_type[lf])
                 H[rank, r, o["level"][f]] += 1
+                tot[r] += 1
                 local.append((lf, r, int(o["level"][f])))
         t = torch.from_numpy(buf)
         dist.all_reduce(t)
         buf = t.numpy()
-        H, load = slot_view(buf, world, R, Lv)
+        H, load, tot = slot_view(buf, world, R, Lv, I)
+        assert np.array_equal(tot, H.sum(axis=(0, 2)))
         # every rank derives identical spare / bounds from the reduced buffer
         ld = s.i_base_load.astype(np.int64) + load
         spare = np.maximum(0, s.i_cap.astype(np.int64) - ld)
