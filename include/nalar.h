@@ -86,6 +86,7 @@ enum nalar_collective { NALAR_COLL_NONE = 0,     /* world == 1                  
 #define NALAR_F_TIMING          1u  /* record per-kernel CUDA events (stats)      */
 #define NALAR_F_NO_GRAPH        2u  /* launch kernels directly, no CUDA graph     */
 #define NALAR_F_FORCE_UNSTAGED  4u  /* test knob: K1 reads HBM, no smem staging   */
+#define NALAR_F_PROFILE         8u  /* K1 records %globaltimer stamps (diagnostics) */
 
 typedef struct {
     int      device;          /* CUDA ordinal                                      */
@@ -204,6 +205,11 @@ int nalar_fetch_decisions(nalar_ctx* ctx, nalar_decisions* out);
 
 /* Counters (and kernel times with NALAR_F_TIMING) of the last epoch; syncs. */
 int nalar_epoch_stats_get(nalar_ctx* ctx, nalar_epoch_stats* stats);
+
+/* Diagnostics (NALAR_F_PROFILE): copy the last epoch's K1 timeline to host:
+ * words [0, 2W): start/end ns of each workflow's sweep; then per K1 block b
+ * 4 words: staged, swept, bucketed, entered.  *n_words = 2W + 4B. */
+int nalar_debug_profile(nalar_ctx* ctx, uint64_t* host, size_t cap_words, size_t* n_words);
 
 /* Device stream the ctx runs on (cudaStream_t). */
 void* nalar_stream(nalar_ctx* ctx);

@@ -23,8 +23,8 @@ enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_TICKET = 4, C_NU
 
 // bytes of K1 shared memory that do not scale with the block's rows
 size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
-// bytes of K1 shared memory needed to stage a block of `rows` rows / `edges` edges
-size_t k1_staged_smem(uint32_t rows, uint32_t edges);
+// bytes of K1 shared memory needed to stage a block of rows / edges / workflows
+size_t k1_staged_smem(uint32_t rows, uint32_t edges, uint32_t wfs);
 
 struct ValidateParams {
     const uint32_t* wf_fut_off;
@@ -57,6 +57,8 @@ struct SweepParams {
     uint32_t B, n_types, n_inst, R, levels, policy;
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
+    unsigned long long* prof;   // NALAR_F_PROFILE: [W][2] workflow start/end, [B][4] block phases
+    uint32_t n_wf;
     // outputs
     uint8_t* status;
     uint8_t* level;

@@ -63,6 +63,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // plan of one staged array: aligned global window copied into smem
@@ -92,9 +98,10 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-size_t k1_staged_smem(uint32_t rows, uint32_t edges) {
-    return 2 * align16(rows + 32) + align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
-           align16(4 * (size_t)edges + 32) + align16(2 * (size_t)rows) + align16(rows);
+size_t k1_staged_smem(uint32_t rows, uint32_t edges, uint32_t wfs) {
+    return 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
+           align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
+           align16(2 * (size_t)rows) + 2 * align16(rows);
 }
 
 __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
@@ -106,8 +113,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const uint32_t w0 = p.blk_wf[b], w1 = p.blk_wf[b + 1];
     const uint32_t r0 = p.blk_row0[b], r1 = p.blk_row0[b + 1];
     const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
-    const uint32_t nr = r1 - r0, ne = e1 - e0;
+    const uint32_t nr = r1 - r0, ne = e1 - e0, nw = w1 - w0;
     const bool staged = p.blk_staged[b] != 0;
+    if (p.prof && threadIdx.x == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 3] = gtimer();
 
     // ---- carve the fixed part --------------------------------------------
     uint8_t* sp = smem;
@@ -133,49 +141,75 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     sp += 4 * kK1Warps;
     uint8_t* s_aff = sp;
 
-    // ---- row arrays: staged in smem (TMA) or read in place ----------------
-    const uint8_t* st;
+    // ---- the block's slice of the table: staged in smem by TMA, or in place --
+    const uint8_t* st;    // state, type, round, pin, executor: indexed by local row
     const uint8_t* ty;
+    const uint8_t* rd;
     const int16_t* pn;
+    const int16_t* ex;
     const uint32_t* eo;   // absolute edge offsets, indexed by local row
     const uint32_t* ed;   // edges, indexed by (edge - e0)
-    uint16_t* dep;
-    uint8_t* flg;
+    const uint32_t* wfo;  // absolute workflow row offsets, indexed by local workflow
+    const int32_t* wpr;   // workflow priorities, indexed by local workflow
+    uint16_t* dep;        // depth (work / output)
+    uint8_t* flg;         // FL_* (work)
+    uint8_t* lev;         // level (work / output)
     if (staged) {
         uint8_t* q = smem + p.fixed_smem;
         const Win ws = window(p.f_state, 1, r0, r1), wt = window(p.f_type, 1, r0, r1);
-        const Win wp = window(p.f_pin, 2, r0, r1), we = window(p.f_edge_off, 4, r0, r1 + 1);
-        const Win wg = window(p.edges, 4, e0, e1);
+        const Win wr = window(p.f_round, 1, r0, r1);
+        const Win wp = window(p.f_pin, 2, r0, r1), wx = window(p.f_exec, 2, r0, r1);
+        const Win we = window(p.f_edge_off, 4, r0, r1 + 1), wg = window(p.edges, 4, e0, e1);
+        const Win wo = window(p.wf_fut_off, 4, w0, w1 + 1), wq = window(p.wf_prio, 4, w0, w1);
         uint8_t* d_s = q;   q += align16(nr + 32);
         uint8_t* d_t = q;   q += align16(nr + 32);
+        uint8_t* d_r = q;   q += align16(nr + 32);
         uint8_t* d_p = q;   q += align16(2 * (size_t)nr + 32);
+        uint8_t* d_x = q;   q += align16(2 * (size_t)nr + 32);
         uint8_t* d_e = q;   q += align16(4 * ((size_t)nr + 1) + 32);
         uint8_t* d_g = q;   q += align16(4 * (size_t)ne + 32);
+        uint8_t* d_o = q;   q += align16(4 * ((size_t)nw + 1) + 32);
+        uint8_t* d_q = q;   q += align16(4 * (size_t)nw + 32);
         dep = (uint16_t*)q; q += align16(2 * (size_t)nr);
-        flg = q;
+        flg = q;            q += align16(nr);
+        lev = q;
         if (tid == 0) {
             mbar_init(mbar, 1);
-            const uint32_t total = ws.bytes + wt.bytes + wp.bytes + we.bytes + (ne ? wg.bytes : 0u);
+            const uint32_t total = ws.bytes + wt.bytes + wr.bytes + wp.bytes + wx.bytes + we.bytes +
+                                   (ne ? wg.bytes : 0u) + wo.bytes + (nw ? wq.bytes : 0u);
             mbar_arrive_expect_tx(mbar, total);
             bulk_g2s(d_s, ws.src, ws.bytes, mbar);
             bulk_g2s(d_t, wt.src, wt.bytes, mbar);
+            bulk_g2s(d_r, wr.src, wr.bytes, mbar);
             bulk_g2s(d_p, wp.src, wp.bytes, mbar);
+            bulk_g2s(d_x, wx.src, wx.bytes, mbar);
             bulk_g2s(d_e, we.src, we.bytes, mbar);
             if (ne) bulk_g2s(d_g, wg.src, wg.bytes, mbar);
+            bulk_g2s(d_o, wo.src, wo.bytes, mbar);
+            if (nw) bulk_g2s(d_q, wq.src, wq.bytes, mbar);
         }
         st = d_s + ws.pre;
         ty = d_t + wt.pre;
+        rd = d_r + wr.pre;
         pn = (const int16_t*)(d_p + wp.pre);
+        ex = (const int16_t*)(d_x + wx.pre);
         eo = (const uint32_t*)(d_e + we.pre);
         ed = (const uint32_t*)(d_g + wg.pre);
+        wfo = (const uint32_t*)(d_o + wo.pre);
+        wpr = (const int32_t*)(d_q + wq.pre);
     } else {
         st = p.f_state + r0;
         ty = p.f_type + r0;
+        rd = p.f_round + r0;
         pn = p.f_pin + r0;
+        ex = p.f_exec + r0;
         eo = p.f_edge_off + r0;
         ed = p.edges + e0;
+        wfo = p.wf_fut_off + w0;
+        wpr = p.wf_prio + w0;
         dep = p.depth + r0;
         flg = p.g_flags + r0;
+        lev = p.level + r0;
     }
 
     // ---- zero block state while the copies are in flight ------------------
@@ -188,28 +222,37 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     }
     __syncthreads();
     if (staged) mbar_wait(mbar, 0);
+    if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 0] = gtimer();
 
     const uint32_t pol = p.policy;
     unsigned long long* infl = s_infl + warp;
     uint32_t* fp = s_fp + warp * T;
     uint32_t* fru = s_fru + warp * T;
     uint32_t n_ready = 0, n_doom = 0;
+    uint32_t* Hs = p.H;
 
     // ---- warps take whole workflows ---------------------------------------
     for (;;) {
         uint32_t wi = 0;
         if (lane == 0) wi = atomicAdd(s_ticket, 1u);
         wi = __shfl_sync(0xFFFFFFFFu, wi, 0);
+        if (wi >= nw) break;
         const uint32_t w = w0 + wi;
-        if (w >= w1) break;
-        const uint32_t fa = p.wf_fut_off[w] - r0, fb = p.wf_fut_off[w + 1] - r0;
+        const uint32_t fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
+        if (p.prof && lane == 0) p.prof[(size_t)w * 2] = gtimer();
 
         for (uint32_t t = lane; t < T; t += 32) { fp[t] = 0xFFFFFFFFu; fru[t] = 0xFFFFFFFFu; }
         if (lane == 0) *infl = 0ull;
+        // LPT needs the workflow's max round before any level
+        uint32_t m_rnd = 0;
+        for (uint32_t f = fa + lane; f < fb; f += 32) m_rnd = max(m_rnd, (uint32_t)rd[f]);
+        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
+        const int64_t prio = wpr[wi];
+        const int64_t lmax = (int64_t)Lv - 1;
         __syncwarp();
 
         uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
-        uint32_t m_dep = 0, m_rnd = 0;
+        uint32_t m_dep = 0;
 
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
             const uint32_t f = c0 + lane;
@@ -225,6 +268,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 const uint32_t v = ed[e];
                 const uint32_t s = (v & 0x7FFFFFFFu) - r0;
                 const bool call = (v >> 31) != 0;
+                const uint32_t ss = st[s];
+                if (!call) {
+                    dm |= ss == 4u;
+                    allres &= ss == 3u;
+                }
                 if (s >= c0) {
                     const uint32_t k = s - c0;
                     if (np == 0) s0 = k;
@@ -233,20 +281,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                     else if (np == 3) s3 = k;
                     else extra |= 1u << k;
                     ++np;
-                    if (!call) {
-                        need_dep |= 1u << k;
-                        const uint32_t ss = st[s];
-                        dm |= ss == 4u;
-                        allres &= ss == 3u;
-                    }
+                    if (!call) need_dep |= 1u << k;
                     continue;
                 }
                 d = max(d, (uint32_t)dep[s] + 1u);
-                if (!call) {
-                    const uint32_t ss = st[s];
-                    dm |= (ss == 4u) || (flg[s] & FL_DOOMED);
-                    allres &= ss == 3u;
-                }
+                if (!call) dm |= (flg[s] & FL_DOOMED) != 0;
             }
             if (ee > eb) d = max(d, 1u);
             d = min(d, 65535u);
@@ -254,24 +293,32 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             bool doom = pend && dm;
             // in-step settling: Bellman-Ford rounds on registers -- depths move
             // by shuffles, doom by ballots; rounds = longest in-step chain + 1
-            if (__any_sync(0xFFFFFFFFu, np != 0u)) {
-                const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
+            const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
+            if (K) {
                 const uint32_t m0 = np > 0 ? 0xFFFFFFFFu : 0u, m1 = np > 1 ? 0xFFFFFFFFu : 0u;
                 const uint32_t m2 = np > 2 ? 0xFFFFFFFFu : 0u, m3 = np > 3 ? 0xFFFFFFFFu : 0u;
                 for (;;) {
+                    uint32_t nd = d;
                     const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
-                    const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
-                    const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
-                    const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
-                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
-                    uint32_t nd = max(max((x0 + 1u) & m0, (x1 + 1u) & m1), max((x2 + 1u) & m2, (x3 + 1u) & m3));
-                    if (wide) {
+                    nd = max(nd, (x0 + 1u) & m0);
+                    if (K > 1) {
+                        const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
+                        nd = max(nd, (x1 + 1u) & m1);
+                    }
+                    if (K > 2) {
+                        const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
+                        const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
+                        nd = max(nd, max((x2 + 1u) & m2, (x3 + 1u) & m3));
+                    }
+                    if (K > 4) {
+#pragma unroll 1
                         for (uint32_t k = 0; k < 32; ++k) {
                             const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
                             if ((extra >> k) & 1u) nd = max(nd, x + 1u);
                         }
                     }
-                    nd = min(max(nd, d), 65535u);
+                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+                    nd = min(nd, 65535u);
                     const bool ndm = doom || (pend && (need_dep & D) != 0u);
                     const bool ch = (nd != d) | (ndm != doom);
                     d = nd;
@@ -279,7 +326,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                     if (!__any_sync(0xFFFFFFFFu, ch)) break;
                 }
             }
-
             // first PENDING non-doomed / first ready unpinned row per type:
             // rows rise with lane, so the lowest lane of each type group wins
             const uint32_t tyf = valid ? ty[f] : 0u;
@@ -291,40 +337,73 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const uint32_t mr = __match_any_sync(0xFFFFFFFFu, kr);
             if (valid) {
                 const uint32_t aff = s_aff[tyf];
-                uint8_t fl = doom ? FL_DOOMED : 0;
-                if (ready) fl |= FL_READY;
-                if (ready && (aff == 0u || (aff == 1u && pinf >= 0))) fl |= FL_ELIG;
-                if (stf == 1u || stf == 2u) {
-                    atomicOr(infl, 1ull << tyf);
-                    atomicAdd(&s_load[p.f_exec[r0 + f]], 1u);
+                const bool infl_row = stf == 1u || stf == 2u;
+                // eligibility known now unless decided per (workflow, type) below
+                const bool elig = ready && (aff == 0u || (aff == 1u && pinf >= 0));
+                uint32_t lv = 0;
+                if (stf < 3u) {
+                    const int64_t score = pol == 1u ? (int64_t)d : (pol == 2u ? (int64_t)m_rnd : 0);
+                    const int64_t x = prio + score;
+                    lv = (uint32_t)(x < 0 ? 0 : (x > lmax ? lmax : x));
                 }
+                uint32_t status;
+                int16_t inst = -1;
+                if (stf == 3u) status = 0;
+                else if (stf == 4u) status = 1;
+                else if (infl_row) { status = 2; inst = ex[f]; }
+                else if (doom) status = 4;
+                else if (!ready) status = 3;
+                else status = elig ? 6u : 5u;
+                const uint32_t g = r0 + f;
                 dep[f] = (uint16_t)d;
-                flg[f] = fl;
+                flg[f] = (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0) | (elig ? FL_ELIG : 0);
+                lev[f] = (uint8_t)lv;
+                p.status[g] = (uint8_t)status;
+                if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
+                p.instance[g] = inst;
+                p.new_pin[g] = 0;
+                if (infl_row) {
+                    atomicOr(infl, 1ull << tyf);
+                    atomicAdd(&s_load[inst], 1u);
+                }
+                if (elig) {
+                    const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
+                    atomicAdd(&Hs[(size_t)r * Lv + lv], 1u);
+                    atomicAdd(&s_rcnt[r], 1u);
+                }
+                if (kp != 0xFFFFu && (__ffs(mp) - 1) == (int)lane) atomicMin(&fp[tyf], f);
+                if (kr != 0xFFFFu && (__ffs(mr) - 1) == (int)lane) atomicMin(&fru[tyf], f);
                 c_pend += pend;
                 c_ready += ready;
-                c_infl += (stf == 1u || stf == 2u);
+                c_infl += infl_row;
                 c_res += stf == 3u;
                 c_fail += stf == 4u;
                 c_doom += doom;
                 c_pinp += pend && pinf >= 0;
                 m_dep = max(m_dep, d);
-                m_rnd = max(m_rnd, (uint32_t)p.f_round[r0 + f]);
-                if (kp != 0xFFFFu && (__ffs(mp) - 1) == (int)lane) atomicMin(&fp[tyf], f);
-                if (kr != 0xFFFFu && (__ffs(mr) - 1) == (int)lane) atomicMin(&fru[tyf], f);
             }
             __syncwarp();
         }
 
-        // stateful fence and first placement
+        // stateful fence and first placement:
+        // the per-(workflow, type) winner becomes eligible
         const unsigned long long im = *infl;
         for (uint32_t t = lane; t < T; t += 32) {
             const uint32_t aff = s_aff[t];
+            uint32_t f = 0xFFFFFFFFu;
             if (aff == 2u) {
-                const uint32_t f = fp[t];
-                if (f != 0xFFFFFFFFu && !((im >> t) & 1ull) && (flg[f] & FL_READY)) flg[f] |= FL_ELIG;
+                const uint32_t c = fp[t];
+                if (c != 0xFFFFFFFFu && !((im >> t) & 1ull) && (flg[c] & FL_READY)) f = c;
             } else if (aff == 1u) {
-                const uint32_t f = fru[t];
-                if (f != 0xFFFFFFFFu) flg[f] |= FL_ELIG;
+                f = fru[t];
+            }
+            if (f != 0xFFFFFFFFu) {
+                flg[f] |= FL_ELIG;
+                p.status[r0 + f] = 6;
+                const int pinf = pn[f];
+                const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + t;
+                atomicAdd(&Hs[(size_t)r * Lv + lev[f]], 1u);
+                atomicAdd(&s_rcnt[r], 1u);
             }
         }
         c_pend = __reduce_add_sync(0xFFFFFFFFu, c_pend);
@@ -335,54 +414,22 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         c_doom = __reduce_add_sync(0xFFFFFFFFu, c_doom);
         c_pinp = __reduce_add_sync(0xFFFFFFFFu, c_pinp);
         m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
-        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
-        __syncwarp();
         n_ready += c_ready;
         n_doom += c_doom;
         if (lane < 10) {
-            const uint32_t vals[10] = {fb - fa, c_pend, c_ready, c_infl, c_res, c_fail, c_doom, c_pinp, m_dep, m_rnd};
-            uint32_t v = 0;
-#pragma unroll
-            for (int k = 0; k < 10; ++k) v = (lane == (uint32_t)k) ? vals[k] : v;
+            uint32_t v = fb - fa;
+            v = lane == 1 ? c_pend : v;
+            v = lane == 2 ? c_ready : v;
+            v = lane == 3 ? c_infl : v;
+            v = lane == 4 ? c_res : v;
+            v = lane == 5 ? c_fail : v;
+            v = lane == 6 ? c_doom : v;
+            v = lane == 7 ? c_pinp : v;
+            v = lane == 8 ? m_dep : v;
+            v = lane == 9 ? m_rnd : v;
             p.wf_agg[(size_t)w * 10 + lane] = v;
         }
-
-        // levels, statuses and per-row outputs
-        const int64_t prio = p.wf_prio[w];
-        for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
-            const uint32_t f = c0 + lane;
-            if (f >= fb) break;
-            const uint32_t g = r0 + f;
-            const uint32_t stf = st[f];
-            const uint32_t fl = flg[f];
-            const uint32_t d = dep[f];
-            uint32_t lv = 0, status;
-            int16_t inst = -1;
-            if (stf < 3u) {
-                const int64_t score = pol == 1u ? (int64_t)d : (pol == 2u ? (int64_t)m_rnd : 0);
-                int64_t x = prio + score;
-                x = x < 0 ? 0 : (x > (int64_t)Lv - 1 ? (int64_t)Lv - 1 : x);
-                lv = (uint32_t)x;
-            }
-            if (stf == 3u) status = 0;
-            else if (stf == 4u) status = 1;
-            else if (stf != 0u) { status = 2; inst = p.f_exec[g]; }
-            else if (fl & FL_DOOMED) status = 4;
-            else if (!(fl & FL_READY)) status = 3;
-            else if (!(fl & FL_ELIG)) status = 5;
-            else status = 6;
-            p.status[g] = (uint8_t)status;
-            p.level[g] = (uint8_t)lv;
-            if (staged) p.depth[g] = (uint16_t)d;
-            p.instance[g] = inst;
-            p.new_pin[g] = 0;
-            if (fl & FL_ELIG) {
-                const int pinf = pn[f];
-                const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + ty[f];
-                atomicAdd(&p.H[(size_t)r * Lv + lv], 1u);
-                atomicAdd(&s_rcnt[r], 1u);
-            }
-        }
+        if (p.prof && lane == 0) p.prof[(size_t)w * 2 + 1] = gtimer();
         __syncwarp();
     }
     if (lane == 0) {
@@ -390,6 +437,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         atomicAdd(&s_cnt[2], n_doom);
     }
     __syncthreads();
+    if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 1] = gtimer();
 
     // ---- block epilogue: loads, per-resource offsets, stable bucketing ------
     for (uint32_t i = tid; i < I; i += kK1Threads)
@@ -400,7 +448,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         const uint32_t lo = min(R, tid * per), hi = min(R, lo + per);
         uint32_t sum = 0;
         for (uint32_t r = lo; r < hi; ++r) sum += s_rcnt[r];
-        // block exclusive scan of `sum`
         uint32_t incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -452,8 +499,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 const uint32_t rank = ok ? s_rcnt[r] + __popc(peers & ((1u << lane) - 1u)) : 0u;
                 __syncwarp();
                 if (ok) {
-                    const uint32_t g = r0 + ff;
-                    p.items[r0 + s_roff[r] + rank] = make_uint2(g, p.level[g]);
+                    p.items[r0 + s_roff[r] + rank] = make_uint2(r0 + ff, lev[ff]);
                     if ((__ffs(peers) - 1) == (int)lane) s_rcnt[r] += __popc(peers);
                 }
                 __syncwarp();
@@ -462,6 +508,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         n_elig += tot;
         __syncthreads();
     }
+    if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 2] = gtimer();
     if (tid == 0) {
         atomicAdd(&p.counters[C_READY], s_cnt[0]);
         atomicAdd(&p.counters[C_ELIG], n_elig);

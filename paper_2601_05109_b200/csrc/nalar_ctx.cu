@@ -105,6 +105,8 @@ struct nalar_ctx {
     Key gkey[3]{};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ncclComm_t comm = nullptr;
+    unsigned long long* d_prof = nullptr;
+    size_t prof_words = 0;
     std::string err;
 };
 
@@ -222,13 +224,13 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* eoff, std::
             while (w < W) {
                 const uint32_t wr = wf_off[w + 1] - wf_off[w];
                 const uint32_t e_if = eoff[wf_off[w + 1]] - eoff[wf_off[ws]];
-                if (w > ws && k1_staged_smem(rows + wr, e_if) > kStageBudget) break;
+                if (w > ws && k1_staged_smem(rows + wr, e_if, w - ws + 1) > kStageBudget) break;
                 rows += wr;
                 ++w;
                 if (rows >= target) break;
             }
             const uint32_t ra = wf_off[ws], rb = wf_off[w];
-            const size_t need = k1_staged_smem(rb - ra, eoff[rb] - eoff[ra]);
+            const size_t need = k1_staged_smem(rb - ra, eoff[rb] - eoff[ra], w - ws);
             const bool staged = need <= kStageBudget && !(c->cfg.flags & NALAR_F_FORCE_UNSTAGED);
             if (staged) mx = std::max(mx, need);
             bw.push_back(ws); br.push_back(ra); be.push_back(eoff[ra]); bs.push_back(staged ? 1 : 0);
@@ -250,6 +252,8 @@ int run_k1(nalar_ctx* c, int policy) {
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
+    p.prof = c->d_prof;
+    p.n_wf = c->W;
     p.status = c->d_status; p.level = c->d_level; p.depth = c->d_depth; p.instance = c->d_inst;
     p.new_pin = c->d_newpin; p.wf_agg = c->d_wfagg;
     const uint32_t slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
@@ -430,10 +434,21 @@ int nalar_destroy(nalar_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->comm) g_nccl.commDestroy(c->comm);
     if (c->own_arena && c->arena) cudaFree(c->arena);
+    if (c->d_prof) cudaFree(c->d_prof);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
     if (c->h_err) cudaFreeHost(c->h_err);
     delete c;
+    return NALAR_OK;
+}
+
+int nalar_debug_profile(nalar_ctx* c, uint64_t* host, size_t cap, size_t* n_words) {
+    if (!c || !n_words) return NALAR_E_INVAL;
+    if (!c->d_prof) return fail(c, NALAR_E_STATE, "profiling not enabled (NALAR_F_PROFILE)");
+    *n_words = c->prof_words;
+    if (!host || cap < c->prof_words) return NALAR_E_SIZE;
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(host, c->d_prof, 8 * c->prof_words, cudaMemcpyDeviceToHost));
     return NALAR_OK;
 }
 
@@ -521,6 +536,16 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     if (c->h_err[0] != ~0ull) {
         if (err_row) *err_row = (int64_t)c->h_err[0];
         return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
+    }
+    if (k.flags & NALAR_F_PROFILE) {
+        const size_t need = 2ull * W + 4ull * c->B;
+        if (need > c->prof_words) {
+            if (c->d_prof) cudaFree(c->d_prof);
+            c->d_prof = nullptr;
+            CK(cudaMalloc(&c->d_prof, 8 * std::max<size_t>(need, 1)));
+        }
+        c->prof_words = need;
+        CK(cudaMemset(c->d_prof, 0, 8 * std::max<size_t>(need, 1)));
     }
     c->uploaded = true;
     return NALAR_OK;

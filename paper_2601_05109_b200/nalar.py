@@ -20,7 +20,7 @@ NALAR_OK, NALAR_E_INVAL, NALAR_E_STATE, NALAR_E_NOMEM, NALAR_E_SIZE, NALAR_E_CUD
     NALAR_E_NOTIMPL = 0, -1, -2, -3, -4, -5, -6, -7
 NALAR_FCFS, NALAR_SRTF, NALAR_LPT = 0, 1, 2
 NALAR_COLL_NONE, NALAR_COLL_NCCL, NALAR_COLL_EXTERNAL = 0, 1, 2
-NALAR_F_TIMING, NALAR_F_NO_GRAPH, NALAR_F_FORCE_UNSTAGED = 1, 2, 4
+NALAR_F_TIMING, NALAR_F_NO_GRAPH, NALAR_F_FORCE_UNSTAGED, NALAR_F_PROFILE = 1, 2, 4, 8
 POLICIES = {"fcfs": NALAR_FCFS, "srtf": NALAR_SRTF, "lpt": NALAR_LPT}
 ERR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_STATE", -3: "E_NOMEM", -4: "E_SIZE", -5: "E_CUDA",
              -6: "E_COMM", -7: "E_NOTIMPL"}
@@ -29,7 +29,7 @@ WF_AGG_FIELDS = ("total", "pending", "ready", "inflight", "resolved", "failed", 
 EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id", "nalar_create",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
-           "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error")
+           "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile")
 
 
 class nalar_config(C.Structure):
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_epoch_finish.argtypes = [C.c_void_p]
     lib.nalar_fetch_decisions.argtypes = [C.c_void_p, P(nalar_decisions)]
     lib.nalar_epoch_stats_get.argtypes = [C.c_void_p, P(nalar_epoch_stats)]
+    lib.nalar_debug_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]
+    lib.nalar_debug_profile.restype = C.c_int
     lib.nalar_stream.argtypes = [C.c_void_p]
     lib.nalar_stream.restype = C.c_void_p
     lib.nalar_last_error.argtypes = [C.c_void_p]
@@ -200,6 +202,14 @@ def nalar_epoch_stats_get(h) -> nalar_epoch_stats:
     s = nalar_epoch_stats()
     _check(h, _lib.nalar_epoch_stats_get(h, C.byref(s)), "epoch_stats_get")
     return s
+
+
+def nalar_debug_profile(h) -> np.ndarray:
+    n = C.c_size_t(0)
+    _lib.nalar_debug_profile(h, None, 0, C.byref(n))
+    buf = np.zeros(max(n.value, 1), np.uint64)
+    _check(h, _lib.nalar_debug_profile(h, buf.ctypes.data, buf.size, C.byref(n)), "debug_profile")
+    return buf[:n.value]
 
 
 def nalar_stream(h) -> int:

@@ -1,0 +1,60 @@
+"""K1 timeline from NALAR_F_PROFILE stamps: where does the sweep's critical path go?
+
+  python scripts/k1_timeline.py [--n 131072] [--seed 1]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from nalar_gen import swe_table  # noqa: E402
+from oracle import oracle_epoch  # noqa: E402
+from paper_2601_05109_b200 import nalar  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=1 << 17)
+ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--out", default="gpurun_out/k1_timeline.json")
+a = ap.parse_args()
+s = swe_table(a.n, seed=a.seed)
+ctx = nalar.Context.for_snapshot(s, flags=nalar.NALAR_F_PROFILE | nalar.NALAR_F_NO_GRAPH)
+ctx.upload(s)
+for _ in range(5):
+    ctx.epoch("srtf")
+torch.cuda.synchronize()
+prof = nalar.nalar_debug_profile(ctx.h).astype(np.int64)
+W = s.n_workflows
+wf = prof[:2 * W].reshape(W, 2)
+blk = prof[2 * W:].reshape(-1, 4)        # staged, swept, bucketed, entered
+t0 = blk[:, 3].min()
+o = oracle_epoch(s, "srtf")
+sizes = np.diff(s.wf_fut_off.astype(np.int64))
+maxd = o["wf_agg"][:, 8]
+dur = wf[:, 1] - wf[:, 0]
+start = wf[:, 0] - t0
+end = wf[:, 1] - t0
+res = {
+    "kernel_span_ns": int(blk[:, 2].max() - t0),
+    "block_entry_spread_ns": int(blk[:, 3].max() - t0),
+    "stage_ns_mean": float(np.mean(blk[:, 0] - blk[:, 3])), "stage_ns_max": int(np.max(blk[:, 0] - blk[:, 3])),
+    "sweep_ns_max": int(np.max(blk[:, 1] - blk[:, 0])), "sweep_ns_mean": float(np.mean(blk[:, 1] - blk[:, 0])),
+    "bucket_ns_max": int(np.max(blk[:, 2] - blk[:, 1])), "bucket_ns_mean": float(np.mean(blk[:, 2] - blk[:, 1])),
+    "wf_dur_ns_max": int(dur.max()), "wf_dur_ns_mean": float(dur.mean()),
+    "wf_end_ns_max": int(end.max()),
+    "ns_per_row_mean": float(np.sum(dur) / np.sum(sizes)),
+}
+top = np.argsort(-dur)[:10]
+res["slowest"] = [{"w": int(w), "rows": int(sizes[w]), "max_depth": int(maxd[w]), "dur_ns": int(dur[w]),
+                   "start_ns": int(start[w])} for w in top]
+# regression of duration on rows and depth
+A = np.stack([sizes, maxd, np.ones_like(sizes)], 1).astype(np.float64)
+coef, *_ = np.linalg.lstsq(A, dur.astype(np.float64), rcond=None)
+res["fit_ns"] = {"per_row": coef[0], "per_depth": coef[1], "const": coef[2]}
+print(json.dumps(res, indent=1))
+os.makedirs(os.path.dirname(a.out), exist_ok=True)
+json.dump(res, open(a.out, "w"), indent=1)
