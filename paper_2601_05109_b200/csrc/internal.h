@@ -101,6 +101,7 @@ struct AssignParams {
     int16_t* assign_inst;
     uint32_t* adm_pub;          // [R] published per-resource admitted counts
     uint32_t* counters;
+    unsigned long long* prof;   // NALAR_F_PROFILE: [R][4] start, published, based, done
 };
 
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);

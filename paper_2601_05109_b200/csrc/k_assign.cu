@@ -82,6 +82,12 @@ __device__ __forceinline__ uint32_t slot_instance(const uint64_t* sp2, const uin
     return 0xFFFFFFFFu;
 }
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
@@ -107,6 +113,8 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     if (tid == 0) s_r = atomicAdd(&p.counters[C_TICKET], 1u);   // resources in ticket order
     __syncthreads();
     const uint32_t r = s_r;
+    unsigned long long* prof = p.prof ? p.prof + (size_t)r * 4 : nullptr;
+    if (prof && tid == 0) prof[0] = gtimer();
     const bool is_type = r >= I;
     const uint32_t t = is_type ? r - I : p.i_type[r];
 
@@ -204,6 +212,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     const uint32_t n_adm = block_sum<uint32_t>(adm_lv, s_red32);
 
     // ---- publish n_adm, look back for the assignment-list offset -----------
+    if (prof && tid == 0) prof[1] = gtimer();
     if (tid == 0) st_release(&p.adm_pub[r], 0x80000000u | n_adm);
     uint32_t base_part = 0;
     for (uint32_t q = tid; q < r; q += kK4Threads) {
@@ -213,6 +222,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     }
     const uint32_t list_base = block_sum<uint32_t>(base_part, s_red32);
     if (tid == 0 && n_adm) atomicAdd(&p.counters[C_ASSIGNED], n_adm);
+    if (prof && tid == 0) prof[2] = gtimer();
 
     // ---- per-instance assigned counts + phase-B slot table (type blocks) ----
     const bool table = is_type && bound <= kSlotCap;
@@ -248,7 +258,10 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             }
         }
     }
-    if (n_adm == 0) return;
+    if (n_adm == 0) {
+        if (prof && tid == 0) prof[3] = gtimer();
+        return;
+    }
     __syncthreads();
 
     // ---- walk this rank's futures of r in row order --------------------------
@@ -326,6 +339,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             found += __syncthreads_count(adm);
         }
     }
+    if (prof && tid == 0) prof[3] = gtimer();
 }
 
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {

@@ -253,8 +253,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
 
         uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
         uint32_t m_dep = 0;
+        long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = p.prof ? clock64() : 0;
 
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
+            if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
             const uint32_t stf = valid ? st[f] : 3u;
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             d = min(d, 65535u);
             const bool pend = stf == 0u;
             bool doom = pend && dm;
+            if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
             // in-step settling: Bellman-Ford rounds on registers -- depths move
             // by shuffles, doom by ballots; rounds = longest in-step chain + 1
             const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
@@ -326,6 +329,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                     if (!__any_sync(0xFFFFFFFFu, ch)) break;
                 }
             }
+            if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
             // first PENDING non-doomed / first ready unpinned row per type:
             // rows rise with lane, so the lowest lane of each type group wins
             const uint32_t tyf = valid ? ty[f] : 0u;
@@ -429,7 +433,12 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             v = lane == 9 ? m_rnd : v;
             p.wf_agg[(size_t)w * 10 + lane] = v;
         }
-        if (p.prof && lane == 0) p.prof[(size_t)w * 2 + 1] = gtimer();
+        if (p.prof && lane == 0) {
+            p.prof[(size_t)w * 2 + 1] = gtimer();
+            cyc_rest += clock64() - cyc_t;
+            unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 4 + (size_t)p.R * 4 + (size_t)w * 3;
+            c[0] = cyc_edge; c[1] = cyc_round; c[2] = cyc_rest;
+        }
         __syncwarp();
     }
     if (lane == 0) {

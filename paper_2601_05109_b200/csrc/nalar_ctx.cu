@@ -283,6 +283,7 @@ int run_k4(nalar_ctx* c) {
     p.i_load = c->d_iload; p.i_spare = c->d_ispare; p.i_assigned = c->d_iasg;
     p.assign_row = c->d_arow; p.assign_inst = c->d_ainst;
     p.adm_pub = c->d_scr + C_NUM;
+    p.prof = c->d_prof ? c->d_prof + 2ull * c->W + 4ull * c->B : nullptr;
     p.counters = c->d_scr;
     CK(launch_assign(p, c->stream));
     return NALAR_OK;
@@ -538,7 +539,7 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
         return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
     }
     if (k.flags & NALAR_F_PROFILE) {
-        const size_t need = 2ull * W + 4ull * c->B;
+        const size_t need = 2ull * W + 4ull * c->B + 4ull * c->R + 3ull * W;
         if (need > c->prof_words) {
             if (c->d_prof) cudaFree(c->d_prof);
             c->d_prof = nullptr;

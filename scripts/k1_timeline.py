@@ -30,7 +30,11 @@ torch.cuda.synchronize()
 prof = nalar.nalar_debug_profile(ctx.h).astype(np.int64)
 W = s.n_workflows
 wf = prof[:2 * W].reshape(W, 2)
-blk = prof[2 * W:].reshape(-1, 4)        # staged, swept, bucketed, entered
+R = s.n_instances + s.n_types
+cyc = prof[len(prof) - 3 * W:].reshape(W, 3)              # edge loop, rounds, rest (SM cycles)
+prof = prof[:len(prof) - 3 * W]
+blk = prof[2 * W:len(prof) - 4 * R].reshape(-1, 4)        # staged, swept, bucketed, entered
+k4 = prof[len(prof) - 4 * R:].reshape(R, 4)              # start, published, based, done
 t0 = blk[:, 3].min()
 o = oracle_epoch(s, "srtf")
 sizes = np.diff(s.wf_fut_off.astype(np.int64))
@@ -48,9 +52,21 @@ res = {
     "wf_end_ns_max": int(end.max()),
     "ns_per_row_mean": float(np.sum(dur) / np.sum(sizes)),
 }
+res["k4"] = {"start_after_k1_ns": int(k4[:, 0].min() - blk[:, 2].max()),
+             "span_ns": int(k4[:, 3].max() - k4[:, 0].min()),
+             "prologue_ns_max": int((k4[:, 1] - k4[:, 0]).max()),
+             "lookback_ns_max": int((k4[:, 2] - k4[:, 1]).max()),
+             "walk_ns_max": int((k4[:, 3] - k4[:, 2]).max()),
+             "start_spread_ns": int(k4[:, 0].max() - k4[:, 0].min()),
+             "slowest_walk_r": int(np.argmax(k4[:, 3] - k4[:, 2]))}
 top = np.argsort(-dur)[:10]
 res["slowest"] = [{"w": int(w), "rows": int(sizes[w]), "max_depth": int(maxd[w]), "dur_ns": int(dur[w]),
-                   "start_ns": int(start[w])} for w in top]
+                   "start_ns": int(start[w]), "cyc_edge_round_rest": [int(x) for x in cyc[w]]}
+                  for w in top]
+chunks = np.ceil(sizes / 32.0)
+res["cycles_per_chunk"] = {"edge": float(cyc[:, 0].sum() / chunks.sum()),
+                           "round": float(cyc[:, 1].sum() / chunks.sum()),
+                           "rest": float(cyc[:, 2].sum() / chunks.sum())}
 # regression of duration on rows and depth
 A = np.stack([sizes, maxd, np.ones_like(sizes)], 1).astype(np.float64)
 coef, *_ = np.linalg.lstsq(A, dur.astype(np.float64), rcond=None)
