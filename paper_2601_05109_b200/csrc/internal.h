@@ -19,7 +19,7 @@ constexpr int kK4Warps = kK4Threads / 32;
 enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4 };
 
 // indices into the per-epoch counters array (scratch)
-enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_TICKET = 4, C_NUM = 8 };
+enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_NUM = 8 };
 
 // bytes of K1 shared memory that do not scale with the block's rows
 size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
@@ -68,7 +68,8 @@ struct SweepParams {
     uint32_t* wf_agg;           // [W][10]
     uint32_t* H;                // this rank's histogram slot [R][Lv]
     uint32_t* load_part;        // [I] in-flight counts of this rank's rows
-    uint32_t* tot;              // [R] eligible futures per resource (this rank)
+    uint32_t* tot;              // [R] eligible futures per resource (this rank; summed by the allreduce)
+    uint32_t* tot_loc;          // [R] the same, never reduced (assignment-list regions)
     uint2* items;               // [N] eligible (row, level), per-block regions
     uint32_t* cnt_rb;           // [R][B]
     uint32_t* off_rb;           // [R][B]
@@ -99,9 +100,10 @@ struct AssignParams {
     uint32_t* i_assigned;
     uint32_t* assign_row;
     int16_t* assign_inst;
-    uint32_t* adm_pub;          // [R] published per-resource admitted counts
+    const uint32_t* tot_loc;    // [R] this rank's eligible futures per resource
+    uint32_t* n_adm;            // [R] this rank's admitted futures per resource
     uint32_t* counters;
-    unsigned long long* prof;   // NALAR_F_PROFILE: [R][4] start, published, based, done
+    unsigned long long* prof;   // NALAR_F_PROFILE: [R][4] start, bounded, based, done
 };
 
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);

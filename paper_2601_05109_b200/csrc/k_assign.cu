@@ -18,7 +18,9 @@
 // [(s, i): 1 <= s <= spare2_i] sorted by (s desc, i asc), which equals the
 // sequential greedy (tests/test_oracle_pins.py::test_water_fill_*).
 // Stable ranks come from scans over the row-ordered bucket lists K1 wrote;
-// atomics only ever produce counts.
+// atomics only ever produce counts.  Admitted rows go to the resource's region
+// of the assignment list (regions sized by this rank's eligible count per
+// resource, offsets = prefix of K1's per-resource totals; fetch compacts).
 #include "internal.h"
 
 namespace nalar {
@@ -27,14 +29,6 @@ namespace {
 
 constexpr uint32_t kSlotCap = 4096;   // phase-B slot table kept in smem up to this size
 
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <typename Tv>
 __device__ __forceinline__ Tv block_sum(Tv v, Tv* red) {
@@ -51,14 +45,14 @@ __device__ __forceinline__ Tv block_sum(Tv v, Tv* red) {
 }
 
 // number of slots with spare-level > s among the type's instances
-__device__ __forceinline__ uint64_t slots_above(const uint64_t* sp2, uint32_t n, uint64_t s) {
+__device__ __forceinline__ uint64_t slots_above(const uint32_t* sp2, uint32_t n, uint64_t s) {
     uint64_t a = 0;
     for (uint32_t k = 0; k < n; ++k) a += sp2[k] > s ? sp2[k] - s : 0ull;
     return a;
 }
 
 // slot g -> (level s, index j among instances with spare2 >= s)
-__device__ __forceinline__ void locate_slot(const uint64_t* sp2, uint32_t n, uint64_t maxs, uint64_t g,
+__device__ __forceinline__ void locate_slot(const uint32_t* sp2, uint32_t n, uint64_t maxs, uint64_t g,
                                             uint64_t* s_out, uint64_t* j_out) {
     uint64_t lo = 1, hi = maxs;
     while (lo < hi) {
@@ -70,7 +64,7 @@ __device__ __forceinline__ void locate_slot(const uint64_t* sp2, uint32_t n, uin
     *j_out = g - slots_above(sp2, n, lo);
 }
 
-__device__ __forceinline__ uint32_t slot_instance(const uint64_t* sp2, const uint32_t* inst, uint32_t n,
+__device__ __forceinline__ uint32_t slot_instance(const uint32_t* sp2, const uint32_t* inst, uint32_t n,
                                                   uint64_t maxs, uint64_t g) {
     uint64_t s, j;
     locate_slot(sp2, n, maxs, g, &s, &j);
@@ -91,10 +85,9 @@ __device__ __forceinline__ uint64_t gtimer() {
 }  // namespace
 
 __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
-    __shared__ uint32_t s_r;
     __shared__ uint32_t s_inst[NALAR_MAX_INSTANCES_DEV];
-    __shared__ uint64_t s_spare[NALAR_MAX_INSTANCES_DEV];   // spare before phase A
-    __shared__ uint64_t s_sp2[NALAR_MAX_INSTANCES_DEV];     // spare after phase A
+    __shared__ uint32_t s_spare[NALAR_MAX_INSTANCES_DEV];   // spare before phase A
+    __shared__ uint32_t s_sp2[NALAR_MAX_INSTANCES_DEV];     // spare after phase A
     __shared__ uint32_t s_A[256];                           // global count above level
     __shared__ uint32_t s_before[256];                      // same level, lower ranks
     __shared__ uint32_t s_LA[256];                          // local count above level
@@ -105,14 +98,14 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     __shared__ uint64_t s_red64[2 * kK4Warps];
     __shared__ uint32_t s_red32[kK4Warps];
     __shared__ uint32_t s_pref[kK4Threads + 1];
+    __shared__ uint32_t s_base[kK4Threads];
+    __shared__ uint2 s_live[4 * kK4Threads];
     __shared__ uint16_t s_slot[kSlotCap];
     __shared__ uint64_t s_bound;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
-    if (tid == 0) s_r = atomicAdd(&p.counters[C_TICKET], 1u);   // resources in ticket order
-    __syncthreads();
-    const uint32_t r = s_r;
+    const uint32_t r = blockIdx.x;
     unsigned long long* prof = p.prof ? p.prof + (size_t)r * 4 : nullptr;
     if (prof && tid == 0) prof[0] = gtimer();
     const bool is_type = r >= I;
@@ -128,19 +121,22 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             const uint32_t i = p.type_inst[k0 + k];
             const uint64_t load = (uint64_t)p.i_base[i] + p.load_sum[i];
             const uint64_t cap = p.i_cap[i];
-            const uint64_t spare = cap > load ? cap - load : 0ull;
-            const uint64_t ha = p.tot[i];
+            const uint32_t spare = (uint32_t)(cap > load ? cap - load : 0ull);
+            const uint32_t ha = p.tot[i];
             s_inst[k] = i;
             s_spare[k] = spare;
             s_sp2[k] = spare - (ha < spare ? ha : spare);
             p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
-            p.i_spare[i] = (uint32_t)spare;
+            p.i_spare[i] = spare;
         }
     } else if (tid == 0) {
         const uint64_t load = (uint64_t)p.i_base[r] + p.load_sum[r];
         const uint64_t cap = p.i_cap[r];
         s_bound = cap > load ? cap - load : 0ull;
     }
+    // offset of this resource's region of the assignment list
+    uint32_t base_part = 0;
+    for (uint32_t q = tid; q < r; q += kK4Threads) base_part += p.tot_loc[q];
     // ---- level histogram of r: global, lower-ranks, local ------------------
     {
         const uint32_t lv = tid;
@@ -166,7 +162,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     uint64_t bound, maxs = 0;
     {
         uint64_t sum = 0, mx = 0;
-        for (uint32_t k = tid; k < ni; k += kK4Threads) { sum += s_sp2[k]; mx = max(mx, s_sp2[k]); }
+        for (uint32_t k = tid; k < ni; k += kK4Threads) { sum += s_sp2[k]; mx = max(mx, (uint64_t)s_sp2[k]); }
         // count strictly above each level: warp suffix scans + per-warp totals
         static_assert(kK4Threads == 256, "one thread per level");
         const uint32_t hg = s_Hg[tid], hl = s_Hl[tid];
@@ -177,14 +173,17 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             const uint32_t yl = __shfl_down_sync(0xFFFFFFFFu, xl, o);
             if (lane + o < 32) { xg += yg; xl += yl; }
         }
+        uint32_t bp = base_part;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
             mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+            bp += __shfl_xor_sync(0xFFFFFFFFu, bp, o);
         }
         if (lane == 0) {
             s_wc[0][warp] = xg;
             s_wc[1][warp] = xl;
+            s_wc[2][warp] = bp;
             s_red64[warp] = sum;
             s_red64[kK4Warps + warp] = mx;
         }
@@ -194,12 +193,18 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         s_A[tid] = ag;
         s_LA[tid] = al;
         uint64_t bs = 0;
+        base_part = 0;
 #pragma unroll
-        for (int k = 0; k < kK4Warps; ++k) { bs += s_red64[k]; maxs = max(maxs, s_red64[kK4Warps + k]); }
+        for (int k = 0; k < kK4Warps; ++k) {
+            bs += s_red64[k];
+            maxs = max(maxs, s_red64[kK4Warps + k]);
+            base_part += s_wc[2][k];
+        }
         bound = is_type ? bs : s_bound;
         __syncthreads();
-        if (tid < 2 * kK4Warps) s_wc[tid >> 3][tid & 7] = 0;
+        if (tid < 3 * kK4Warps) s_wc[tid >> 3][tid & 7] = 0;
     }
+    const uint32_t list_base = base_part;
     // number of this rank's futures admitted on r (closed form per level)
     uint32_t adm_lv = 0;
     if (tid < Lv) {
@@ -210,19 +215,11 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         }
     }
     const uint32_t n_adm = block_sum<uint32_t>(adm_lv, s_red32);
-
-    // ---- publish n_adm, look back for the assignment-list offset -----------
     if (prof && tid == 0) prof[1] = gtimer();
-    if (tid == 0) st_release(&p.adm_pub[r], 0x80000000u | n_adm);
-    uint32_t base_part = 0;
-    for (uint32_t q = tid; q < r; q += kK4Threads) {
-        uint32_t v;
-        do { v = ld_relaxed(&p.adm_pub[q]); } while (!(v & 0x80000000u));
-        base_part += v & 0x7FFFFFFFu;
+    if (tid == 0) {
+        p.n_adm[r] = n_adm;
+        if (n_adm) atomicAdd(&p.counters[C_ASSIGNED], n_adm);
     }
-    const uint32_t list_base = block_sum<uint32_t>(base_part, s_red32);
-    if (tid == 0 && n_adm) atomicAdd(&p.counters[C_ASSIGNED], n_adm);
-    if (prof && tid == 0) prof[2] = gtimer();
 
     // ---- per-instance assigned counts + phase-B slot table (type blocks) ----
     const bool table = is_type && bound <= kSlotCap;
@@ -258,6 +255,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             }
         }
     }
+    if (prof && tid == 0) prof[2] = gtimer();
     if (n_adm == 0) {
         if (prof && tid == 0) prof[3] = gtimer();
         return;
@@ -265,12 +263,17 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     __syncthreads();
 
     // ---- walk this rank's futures of r in row order --------------------------
+    // pass 1 compacts the live ones (level not yet full), pass 2 ranks them
     const uint8_t aff = is_type ? p.t_aff[t] : 0;
     uint32_t found = 0;
     for (uint32_t b0 = 0; b0 < B && found < n_adm; b0 += kK4Threads) {
-        // prefix of per-K1-block counts for blocks [b0, b0 + 256)
+        // prefix of per-K1-block counts and item bases for blocks [b0, b0 + 256)
         const uint32_t bb = b0 + tid;
-        const uint32_t c = bb < B ? p.cnt_rb[(size_t)r * B + bb] : 0u;
+        uint32_t c = 0;
+        if (bb < B) {
+            c = p.cnt_rb[(size_t)r * B + bb];
+            s_base[tid] = p.blk_row0[bb] + p.off_rb[(size_t)r * B + bb];
+        }
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -287,56 +290,82 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         __syncthreads();
         const uint32_t total = s_pref[kK4Threads];
         const uint32_t nb = min((uint32_t)kK4Threads, B - b0);
-        for (uint32_t q0 = 0; q0 < total && found < n_adm; q0 += kK4Threads) {
-            const uint32_t q = q0 + tid;
-            bool live = false;
-            uint32_t row = 0, lv = 0xFFFFu;
-            if (q < total) {
-                // owning K1 block: last k with s_pref[k] <= q
+        for (uint32_t q0 = 0; q0 < total && found < n_adm; q0 += 4 * kK4Threads) {
+            // pass 1: four consecutive items per thread
+            uint2 it[4];
+            uint32_t nl = 0;
+            const uint32_t qa = q0 + 4 * tid;
+            if (qa < total) {
                 uint32_t lo = 0, hi = nb - 1;
                 while (lo < hi) {
                     const uint32_t mid = (lo + hi + 1) >> 1;
-                    if (s_pref[mid] <= q) lo = mid;
+                    if (s_pref[mid] <= qa) lo = mid;
                     else hi = mid - 1;
                 }
-                const uint32_t kb = b0 + lo;
-                const uint2 it = p.items[p.blk_row0[kb] + p.off_rb[(size_t)r * B + kb] + (q - s_pref[lo])];
-                row = it.x;
-                lv = it.y;
-                live = (uint64_t)s_A[lv] + s_before[lv] < bound;
-                if (!live) lv = 0xFFFFu;
-            }
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv);
-            const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
-            if (live && (__ffs(peers) - 1) == (int)lane) s_wc[warp][lv] = __popc(peers);
-            __syncthreads();
-            bool adm = false;
-            uint32_t rank = 0;
-            if (live) {
-                rank = s_run[lv] + wrank;
-                for (uint32_t k = 0; k < warp; ++k) rank += s_wc[k][lv];
-                adm = (uint64_t)s_A[lv] + s_before[lv] + rank < bound;
-            }
-            __syncthreads();
-            {
-                uint32_t add = 0;
 #pragma unroll
-                for (int k = 0; k < kK4Warps; ++k) { add += s_wc[k][tid]; s_wc[k][tid] = 0; }
-                s_run[tid] += add;
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t q = qa + j;
+                    if (q < total) {
+                        while (lo + 1 < nb && s_pref[lo + 1] <= q) ++lo;
+                        const uint2 x = p.items[s_base[lo] + (q - s_pref[lo])];
+                        if ((uint64_t)s_A[x.y] + s_before[x.y] < bound) it[nl++] = x;
+                    }
+                }
             }
-            if (adm) {
-                const uint64_t g = (uint64_t)s_A[lv] + s_before[lv] + rank;
-                int16_t inst = (int16_t)r;
-                if (is_type)
-                    inst = (int16_t)(table ? s_slot[g] : slot_instance(s_sp2, s_inst, ni, maxs, g));
-                p.status[row] = 7;
-                p.instance[row] = inst;
-                p.new_pin[row] = (uint8_t)(is_type && aff != 0);
-                const uint32_t pos = list_base + s_LA[lv] + rank;
-                p.assign_row[pos] = row;
-                p.assign_inst[pos] = inst;
+            uint32_t li = nl;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, li, o);
+                if (lane >= (uint32_t)o) li += y;
             }
-            found += __syncthreads_count(adm);
+            if (lane == 31) s_red32[warp] = li;
+            __syncthreads();
+            uint32_t lb = 0, n_live = 0;
+            for (uint32_t k = 0; k < (uint32_t)kK4Warps; ++k) {
+                lb += k < warp ? s_red32[k] : 0u;
+                n_live += s_red32[k];
+            }
+            lb += li - nl;
+            for (uint32_t j = 0; j < nl; ++j) s_live[lb + j] = it[j];
+            __syncthreads();
+            // pass 2: stable rank of each live item inside its level
+            for (uint32_t j0 = 0; j0 < n_live; j0 += kK4Threads) {
+                const uint32_t j = j0 + tid;
+                const bool live = j < n_live;
+                uint32_t row = 0, lv = 0xFFFFu;
+                if (live) { row = s_live[j].x; lv = s_live[j].y; }
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv);
+                const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
+                if (live && (__ffs(peers) - 1) == (int)lane) s_wc[warp][lv] = __popc(peers);
+                __syncthreads();
+                bool adm = false;
+                uint32_t rank = 0;
+                if (live) {
+                    rank = s_run[lv] + wrank;
+                    for (uint32_t k = 0; k < warp; ++k) rank += s_wc[k][lv];
+                    adm = (uint64_t)s_A[lv] + s_before[lv] + rank < bound;
+                }
+                __syncthreads();
+                {
+                    uint32_t add = 0;
+#pragma unroll
+                    for (int k = 0; k < kK4Warps; ++k) { add += s_wc[k][tid]; s_wc[k][tid] = 0; }
+                    s_run[tid] += add;
+                }
+                if (adm) {
+                    const uint64_t g = (uint64_t)s_A[lv] + s_before[lv] + rank;
+                    int16_t inst = (int16_t)r;
+                    if (is_type)
+                        inst = (int16_t)(table ? s_slot[g] : slot_instance(s_sp2, s_inst, ni, maxs, g));
+                    p.status[row] = 7;
+                    p.instance[row] = inst;
+                    p.new_pin[row] = (uint8_t)(is_type && aff != 0);
+                    const uint32_t pos = list_base + s_LA[lv] + rank;
+                    p.assign_row[pos] = row;
+                    p.assign_inst[pos] = inst;
+                }
+                found += __syncthreads_count(adm);
+            }
         }
     }
     if (prof && tid == 0) prof[3] = gtimer();

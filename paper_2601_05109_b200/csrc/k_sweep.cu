@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 0] = gtimer();
 
     const uint32_t pol = p.policy;
-    unsigned long long* infl = s_infl + warp;
     uint32_t* fp = s_fp + warp * T;
     uint32_t* fru = s_fru + warp * T;
     uint32_t n_ready = 0, n_doom = 0;
@@ -242,7 +241,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         if (p.prof && lane == 0) p.prof[(size_t)w * 2] = gtimer();
 
         for (uint32_t t = lane; t < T; t += 32) { fp[t] = 0xFFFFFFFFu; fru[t] = 0xFFFFFFFFu; }
-        if (lane == 0) *infl = 0ull;
         // LPT needs the workflow's max round before any level
         uint32_t m_rnd = 0;
         for (uint32_t f = fa + lane; f < fb; f += 32) m_rnd = max(m_rnd, (uint32_t)rd[f]);
@@ -253,6 +251,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
 
         uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
         uint32_t m_dep = 0;
+        uint64_t seen_p = 0, seen_r = 0, im = 0;   // types seen (first pending / ready unpinned), in flight
         long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = p.prof ? clock64() : 0;
 
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
@@ -266,11 +265,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
             uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
             bool dm = false, allres = true;
-            for (uint32_t e = eb; e < ee; ++e) {
-                const uint32_t v = ed[e];
+            // one predecessor edge: loads were issued by the caller
+            auto take = [&](uint32_t v, uint32_t ss, uint32_t ds, uint32_t fs) {
                 const uint32_t s = (v & 0x7FFFFFFFu) - r0;
                 const bool call = (v >> 31) != 0;
-                const uint32_t ss = st[s];
                 if (!call) {
                     dm |= ss == 4u;
                     allres &= ss == 3u;
@@ -284,10 +282,24 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                     else extra |= 1u << k;
                     ++np;
                     if (!call) need_dep |= 1u << k;
-                    continue;
+                } else {
+                    d = max(d, ds + 1u);
+                    if (!call) dm |= (fs & FL_DOOMED) != 0;
                 }
-                d = max(d, (uint32_t)dep[s] + 1u);
-                if (!call) dm |= (flg[s] & FL_DOOMED) != 0;
+            };
+            uint32_t e = eb;
+            for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
+                const uint32_t va = ed[e], vb = ed[e + 1];
+                const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
+                const uint32_t ssa = st[sa], ssb = st[sb], dsa = dep[sa], dsb = dep[sb];
+                const uint32_t fsa = flg[sa], fsb = flg[sb];
+                take(va, ssa, dsa, fsa);
+                take(vb, ssb, dsb, fsb);
+            }
+            if (e < ee) {
+                const uint32_t va = ed[e];
+                const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
+                take(va, st[sa], dep[sa], flg[sa]);
             }
             if (ee > eb) d = max(d, 1u);
             d = min(d, 65535u);
@@ -295,37 +307,35 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             bool doom = pend && dm;
             if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
             // in-step settling: Bellman-Ford rounds on registers -- depths move
-            // by shuffles, doom by ballots; rounds = longest in-step chain + 1
-            const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
-            if (K) {
+            // by shuffles, doom by ballots; two rounds per convergence vote
+            if (__any_sync(0xFFFFFFFFu, np != 0u)) {
+                const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
                 const uint32_t m0 = np > 0 ? 0xFFFFFFFFu : 0u, m1 = np > 1 ? 0xFFFFFFFFu : 0u;
                 const uint32_t m2 = np > 2 ? 0xFFFFFFFFu : 0u, m3 = np > 3 ? 0xFFFFFFFFu : 0u;
-                for (;;) {
-                    uint32_t nd = d;
+                auto round = [&]() -> bool {
                     const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
-                    nd = max(nd, (x0 + 1u) & m0);
-                    if (K > 1) {
-                        const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
-                        nd = max(nd, (x1 + 1u) & m1);
-                    }
-                    if (K > 2) {
-                        const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
-                        const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
-                        nd = max(nd, max((x2 + 1u) & m2, (x3 + 1u) & m3));
-                    }
-                    if (K > 4) {
+                    const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
+                    const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
+                    const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
+                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+                    uint32_t nd = max(max(max(d, (x0 + 1u) & m0), (x1 + 1u) & m1), max((x2 + 1u) & m2, (x3 + 1u) & m3));
+                    if (wide) {
 #pragma unroll 1
                         for (uint32_t k = 0; k < 32; ++k) {
                             const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
                             if ((extra >> k) & 1u) nd = max(nd, x + 1u);
                         }
                     }
-                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
                     nd = min(nd, 65535u);
                     const bool ndm = doom || (pend && (need_dep & D) != 0u);
                     const bool ch = (nd != d) | (ndm != doom);
                     d = nd;
                     doom = ndm;
+                    return ch;
+                };
+                for (;;) {
+                    round();
+                    const bool ch = round();
                     if (!__any_sync(0xFFFFFFFFu, ch)) break;
                 }
             }
@@ -335,10 +345,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const uint32_t tyf = valid ? ty[f] : 0u;
             const int pinf = valid ? pn[f] : -1;
             const bool ready = pend && !doom && allres;
-            const uint32_t kp = (valid && pend && !doom) ? tyf : 0xFFFFu;
-            const uint32_t kr = (valid && ready && pinf < 0) ? tyf : 0xFFFFu;
-            const uint32_t mp = __match_any_sync(0xFFFFFFFFu, kp);
-            const uint32_t mr = __match_any_sync(0xFFFFFFFFu, kr);
+            // types not seen yet in this workflow take an atomicMin (rare)
+            const bool cp = valid && pend && !doom && !((seen_p >> tyf) & 1ull);
+            const bool cr = valid && ready && pinf < 0 && !((seen_r >> tyf) & 1ull);
             if (valid) {
                 const uint32_t aff = s_aff[tyf];
                 const bool infl_row = stf == 1u || stf == 2u;
@@ -366,17 +375,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
                 p.instance[g] = inst;
                 p.new_pin[g] = 0;
-                if (infl_row) {
-                    atomicOr(infl, 1ull << tyf);
-                    atomicAdd(&s_load[inst], 1u);
-                }
+                if (infl_row) atomicAdd(&s_load[inst], 1u);
                 if (elig) {
                     const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
                     atomicAdd(&Hs[(size_t)r * Lv + lv], 1u);
                     atomicAdd(&s_rcnt[r], 1u);
                 }
-                if (kp != 0xFFFFu && (__ffs(mp) - 1) == (int)lane) atomicMin(&fp[tyf], f);
-                if (kr != 0xFFFFu && (__ffs(mr) - 1) == (int)lane) atomicMin(&fru[tyf], f);
+                if (cp) atomicMin(&fp[tyf], f);
+                if (cr) atomicMin(&fru[tyf], f);
                 c_pend += pend;
                 c_ready += ready;
                 c_infl += infl_row;
@@ -386,12 +392,21 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 c_pinp += pend && pinf >= 0;
                 m_dep = max(m_dep, d);
             }
+            {
+                const uint64_t bp = cp ? (1ull << tyf) : 0ull, br = cr ? (1ull << tyf) : 0ull;
+                const uint64_t bi = (valid && (stf == 1u || stf == 2u)) ? (1ull << tyf) : 0ull;
+                seen_p |= ((uint64_t)__reduce_or_sync(0xFFFFFFFFu, (uint32_t)(bp >> 32)) << 32) |
+                          __reduce_or_sync(0xFFFFFFFFu, (uint32_t)bp);
+                seen_r |= ((uint64_t)__reduce_or_sync(0xFFFFFFFFu, (uint32_t)(br >> 32)) << 32) |
+                          __reduce_or_sync(0xFFFFFFFFu, (uint32_t)br);
+                im |= ((uint64_t)__reduce_or_sync(0xFFFFFFFFu, (uint32_t)(bi >> 32)) << 32) |
+                      __reduce_or_sync(0xFFFFFFFFu, (uint32_t)bi);
+            }
             __syncwarp();
         }
 
         // stateful fence and first placement:
         // the per-(workflow, type) winner becomes eligible
-        const unsigned long long im = *infl;
         for (uint32_t t = lane; t < T; t += 32) {
             const uint32_t aff = s_aff[t];
             uint32_t f = 0xFFFFFFFFu;
@@ -473,7 +488,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             s_roff[r] = run;
             p.cnt_rb[(size_t)r * p.B + b] = c;
             p.off_rb[(size_t)r * p.B + b] = run;
-            if (c) atomicAdd(&p.tot[r], c);
+            if (c) { atomicAdd(&p.tot[r], c); atomicAdd(&p.tot_loc[r], c); }
             run += c;
             s_rcnt[r] = 0;   // reused as the running rank counter below
         }

@@ -89,11 +89,14 @@ struct nalar_ctx {
     uint32_t *d_cnt_rb = nullptr, *d_off_rb = nullptr;
     uint32_t* d_x = nullptr;          // exchange: H[G][R][Lv] then load[I]
     size_t x_words = 0;
-    uint32_t* d_scr = nullptr;        // counters[C_NUM] then adm_pub[Rmax]; contiguous with d_x
+    uint32_t* d_scr = nullptr;        // counters[C_NUM], n_adm[Rmax], tot_loc[Rmax]; contiguous with d_x
     size_t zero_bytes = 0;            // bytes to clear per epoch from d_x
     unsigned long long* d_err = nullptr;
     // host pinned
     uint32_t* h_cnt = nullptr;
+    uint32_t* h_reg = nullptr;         // n_adm[Rmax], tot_loc[Rmax]
+    void* h_list = nullptr;
+    size_t h_list_cap = 0;
     unsigned long long* h_err = nullptr;
     // current table
     uint32_t N = 0, E = 0, W = 0, I = 0, T = 0, B = 0, R = 0;
@@ -194,7 +197,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->x = L.off;
     L.off += p->x_words * 4;
     p->scr = L.off;
-    L.off += (C_NUM + (size_t)p->Rmax) * 4;
+    L.off += (C_NUM + 2 * (size_t)p->Rmax) * 4;   // counters, n_adm[R], tot_loc[R]
     L.off = (L.off + 255) & ~(size_t)255;
     p->err = L.take<unsigned long long>(2);
     p->total = L.off + 256;
@@ -262,6 +265,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.load_part = c->d_x + (size_t)G * c->R * c->Lv;
     p.tot = p.load_part + c->I;
     p.items = c->d_items; p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb;
+    p.tot_loc = c->d_scr + C_NUM + c->Rmax;
     p.counters = c->d_scr;
     CK(launch_sweep(p, c->smem, c->stream));
     return NALAR_OK;
@@ -282,7 +286,8 @@ int run_k4(nalar_ctx* c) {
     p.status = c->d_status; p.instance = c->d_inst; p.new_pin = c->d_newpin;
     p.i_load = c->d_iload; p.i_spare = c->d_ispare; p.i_assigned = c->d_iasg;
     p.assign_row = c->d_arow; p.assign_inst = c->d_ainst;
-    p.adm_pub = c->d_scr + C_NUM;
+    p.n_adm = c->d_scr + C_NUM;
+    p.tot_loc = c->d_scr + C_NUM + c->Rmax;
     p.prof = c->d_prof ? c->d_prof + 2ull * c->W + 4ull * c->B : nullptr;
     p.counters = c->d_scr;
     CK(launch_assign(p, c->stream));
@@ -297,7 +302,7 @@ size_t x_used_words(nalar_ctx* c) {
 int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
     // clear exchange buffer (used part) + counters + adm_pub; contiguous region
-    CK(cudaMemsetAsync(c->d_x, 0, c->x_words * 4 + (C_NUM + (size_t)c->Rmax) * 4, c->stream));
+    CK(cudaMemsetAsync(c->d_x, 0, c->x_words * 4 + (C_NUM + 2 * (size_t)c->Rmax) * 4, c->stream));
     if (timing) CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
     int rc = run_k1(c, policy);
     if (rc) return rc;
@@ -413,7 +418,8 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NALAR_E_CUDA);
         c->own_stream = true;
     }
-    if (cudaMallocHost(&c->h_cnt, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess)
+    if (cudaMallocHost(&c->h_cnt, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess ||
+        cudaMallocHost(&c->h_reg, 8ull * std::max<uint32_t>(c->Rmax, 1)) != cudaSuccess)
         return bail(NALAR_E_NOMEM);
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
@@ -439,6 +445,8 @@ int nalar_destroy(nalar_ctx* c) {
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
     if (c->h_err) cudaFreeHost(c->h_err);
+    if (c->h_reg) cudaFreeHost(c->h_reg);
+    if (c->h_list) cudaFreeHost(c->h_list);
     delete c;
     return NALAR_OK;
 }
@@ -634,9 +642,39 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     CK(d2h(o->i_load, c->d_iload, 4ull * c->I));
     CK(d2h(o->i_spare, c->d_ispare, 4ull * c->I));
     CK(d2h(o->i_assigned, c->d_iasg, 4ull * c->I));
-    CK(d2h(o->assign_row, c->d_arow, 4ull * na));
-    CK(d2h(o->assign_inst, c->d_ainst, 2ull * na));
+    // the assignment list lives in per-resource regions on the device
+    // (region r = this rank's eligible futures of r); compact while copying
+    const bool want_list = (o->assign_row || o->assign_inst) && na;
+    if (want_list) {
+        CK(cudaMemcpyAsync(c->h_reg, c->d_scr + C_NUM, 8ull * c->Rmax, cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
+    if (want_list) {
+        const uint32_t* n_adm = c->h_reg;
+        const uint32_t* tot_loc = c->h_reg + c->Rmax;
+        size_t n_el = 0;
+        for (uint32_t r = 0; r < c->R; ++r) n_el += tot_loc[r];
+        if (c->h_list_cap < n_el) {
+            if (c->h_list) cudaFreeHost(c->h_list);
+            c->h_list = nullptr;
+            c->h_list_cap = 0;
+            if (cudaMallocHost(&c->h_list, 6 * std::max<size_t>(n_el, 1)) != cudaSuccess)
+                return fail(c, NALAR_E_NOMEM, "pinned staging for the assignment list");
+            c->h_list_cap = n_el;
+        }
+        uint32_t* hr = (uint32_t*)c->h_list;
+        int16_t* hi = (int16_t*)(hr + n_el);
+        CK(cudaMemcpyAsync(hr, c->d_arow, 4 * n_el, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hi, c->d_ainst, 2 * n_el, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        size_t at = 0, out = 0;
+        for (uint32_t r = 0; r < c->R; ++r) {
+            if (o->assign_row) memcpy(o->assign_row + out, hr + at, 4ull * n_adm[r]);
+            if (o->assign_inst) memcpy(o->assign_inst + out, hi + at, 2ull * n_adm[r]);
+            out += n_adm[r];
+            at += tot_loc[r];
+        }
+    }
     return NALAR_OK;
 }
 

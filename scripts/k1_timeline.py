@@ -55,7 +55,7 @@ res = {
 res["k4"] = {"start_after_k1_ns": int(k4[:, 0].min() - blk[:, 2].max()),
              "span_ns": int(k4[:, 3].max() - k4[:, 0].min()),
              "prologue_ns_max": int((k4[:, 1] - k4[:, 0]).max()),
-             "lookback_ns_max": int((k4[:, 2] - k4[:, 1]).max()),
+             "tables_ns_max": int((k4[:, 2] - k4[:, 1]).max()),
              "walk_ns_max": int((k4[:, 3] - k4[:, 2]).max()),
              "start_spread_ns": int(k4[:, 0].max() - k4[:, 0].min()),
              "slowest_walk_r": int(np.argmax(k4[:, 3] - k4[:, 2]))}
