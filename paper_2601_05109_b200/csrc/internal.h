@@ -16,15 +16,16 @@ constexpr int kK4Threads = 256;          // assign: one block per resource
 constexpr int kK4Warps = kK4Threads / 32;
 
 // per-row flags produced by the sweep
-enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4 };
+enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8, FL_FAILP = 16 };
 
 // indices into the per-epoch counters array (scratch)
 enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_NUM = 8 };
 
 // bytes of K1 shared memory that do not scale with the block's rows
 size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
-// bytes of K1 shared memory needed to stage a block of rows / edges / workflows
-size_t k1_staged_smem(uint32_t rows, uint32_t edges, uint32_t wfs);
+// bytes of K1 shared memory that scale with a block's workflows (and, when
+// staged, with its rows / edges)
+size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged);
 
 struct ValidateParams {
     const uint32_t* wf_fut_off;
@@ -57,6 +58,7 @@ struct SweepParams {
     uint32_t B, n_types, n_inst, R, levels, policy;
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
+    uint16_t* g_wlm;            // [N] row -> local workflow scratch for unstaged blocks
     unsigned long long* prof;   // NALAR_F_PROFILE: [W][2] workflow start/end, [B][4] block phases
     uint32_t n_wf;
     // outputs

@@ -90,7 +90,6 @@ __device__ __forceinline__ Win window(const void* base, size_t elem, size_t lo, 
 
 size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     size_t b = 64;                                  // mbarrier, ticket, counters
-    b += (size_t)kK1Warps * (8 + 8 * (size_t)T);    // infl mask + first_pending + first_ready_unp
     b += 4 * (size_t)I;                             // in-flight counts
     b += 8 * (size_t)R;                             // per-resource count / offset
     b += 4 * (size_t)kK1Threads + 4 * kK1Warps;     // compaction list + warp counts
@@ -98,10 +97,13 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-size_t k1_staged_smem(uint32_t rows, uint32_t edges, uint32_t wfs) {
-    return 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
-           align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
-           align16(2 * (size_t)rows) + 2 * align16(rows);
+size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
+    size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs);   // per-workflow tables
+    if (staged)
+        b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
+             align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
+             2 * align16(2 * (size_t)rows) + 2 * align16(rows);
+    return b;
 }
 
 __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
@@ -115,7 +117,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
     const uint32_t nr = r1 - r0, ne = e1 - e0, nw = w1 - w0;
     const bool staged = p.blk_staged[b] != 0;
-    if (p.prof && threadIdx.x == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 3] = gtimer();
+    unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 4 : nullptr;
+    if (bprof && tid == 0) bprof[3] = gtimer();
 
     // ---- carve the fixed part --------------------------------------------
     uint8_t* sp = smem;
@@ -123,12 +126,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     uint32_t* s_ticket = (uint32_t*)(sp + 8);
     uint32_t* s_cnt = (uint32_t*)(sp + 16);      // [0] ready [1] elig [2] doomed
     sp += 64;
-    unsigned long long* s_infl = (unsigned long long*)sp;
-    sp += 8 * kK1Warps;
-    uint32_t* s_fp = (uint32_t*)sp;               // [warps][T]
-    sp += 4 * (size_t)kK1Warps * T;
-    uint32_t* s_fru = (uint32_t*)sp;              // [warps][T]
-    sp += 4 * (size_t)kK1Warps * T;
     uint32_t* s_load = (uint32_t*)sp;
     sp += 4 * (size_t)I;
     uint32_t* s_rcnt = (uint32_t*)sp;
@@ -141,6 +138,15 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     sp += 4 * kK1Warps;
     uint8_t* s_aff = sp;
 
+    // ---- per-workflow tables (always in smem) -------------------------------
+    uint8_t* q = smem + p.fixed_smem;
+    unsigned long long* s_winfl = (unsigned long long*)q;   // [nw] types with futures in flight
+    uint32_t* s_wfp = (uint32_t*)(q + 8 * (size_t)nw);       // [nw][T] first PENDING non-doomed row
+    uint32_t* s_wfru = s_wfp + (size_t)nw * T;               // [nw][T] first ready unpinned row
+    q += align16((size_t)nw * (8 * (size_t)T + 8));
+    uint32_t* s_wrnd = (uint32_t*)q;                         // [nw] max retry round
+    q += align16(4 * (size_t)nw);
+
     // ---- the block's slice of the table: staged in smem by TMA, or in place --
     const uint8_t* st;    // state, type, round, pin, executor: indexed by local row
     const uint8_t* ty;
@@ -152,10 +158,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const uint32_t* wfo;  // absolute workflow row offsets, indexed by local workflow
     const int32_t* wpr;   // workflow priorities, indexed by local workflow
     uint16_t* dep;        // depth (work / output)
+    uint16_t* wlm;        // local workflow of each row
     uint8_t* flg;         // FL_* (work)
     uint8_t* lev;         // level (work / output)
     if (staged) {
-        uint8_t* q = smem + p.fixed_smem;
         const Win ws = window(p.f_state, 1, r0, r1), wt = window(p.f_type, 1, r0, r1);
         const Win wr = window(p.f_round, 1, r0, r1);
         const Win wp = window(p.f_pin, 2, r0, r1), wx = window(p.f_exec, 2, r0, r1);
@@ -171,6 +177,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         uint8_t* d_o = q;   q += align16(4 * ((size_t)nw + 1) + 32);
         uint8_t* d_q = q;   q += align16(4 * (size_t)nw + 32);
         dep = (uint16_t*)q; q += align16(2 * (size_t)nr);
+        wlm = (uint16_t*)q; q += align16(2 * (size_t)nr);
         flg = q;            q += align16(nr);
         lev = q;
         if (tid == 0) {
@@ -208,6 +215,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         wfo = p.wf_fut_off + w0;
         wpr = p.wf_prio + w0;
         dep = p.depth + r0;
+        wlm = p.g_wlm + r0;
         flg = p.g_flags + r0;
         lev = p.level + r0;
     }
@@ -216,21 +224,45 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     for (uint32_t i = tid; i < I; i += kK1Threads) s_load[i] = 0;
     for (uint32_t r = tid; r < R; r += kK1Threads) s_rcnt[r] = 0;
     for (uint32_t t = tid; t < T; t += kK1Threads) s_aff[t] = p.t_aff[t];
+    for (uint32_t k = tid; k < nw * T; k += kK1Threads) { s_wfp[k] = 0xFFFFFFFFu; s_wfru[k] = 0xFFFFFFFFu; }
+    for (uint32_t k = tid; k < nw; k += kK1Threads) s_winfl[k] = 0ull;
     if (tid == 0) {
         *s_ticket = 0;
         s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
     }
     __syncthreads();
     if (staged) mbar_wait(mbar, 0);
-    if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 0] = gtimer();
+    if (bprof && tid == 0) bprof[0] = gtimer();
 
-    const uint32_t pol = p.policy;
-    uint32_t* fp = s_fp + warp * T;
-    uint32_t* fru = s_fru + warp * T;
+    // ---- P1 (row-parallel): readiness inputs, workflow map, in-flight load ---
+    for (uint32_t f = tid; f < nr; f += kK1Threads) {
+        const uint32_t stf = st[f], tyf = ty[f];
+        const uint32_t eb = eo[f] - e0, ee = eo[f + 1] - e0;
+        bool allres = true, failp = false;
+        for (uint32_t e = eb; e < ee; ++e) {
+            const uint32_t v = ed[e];
+            if (v >> 31) continue;                      // CALL edges never gate (Q2)
+            const uint32_t ss = st[(v & 0x7FFFFFFFu) - r0];
+            allres &= ss == 3u;
+            failp |= ss == 4u;
+        }
+        uint32_t lo = 0, hi = nw - 1;                   // workflow of row f
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (wfo[mid] - r0 <= f) lo = mid;
+            else hi = mid - 1;
+        }
+        wlm[f] = (uint16_t)lo;
+        flg[f] = (allres ? FL_ALLRES : 0) | (failp ? FL_FAILP : 0);
+        if (stf == 1u || stf == 2u) {
+            atomicAdd(&s_load[ex[f]], 1u);
+            atomicOr(&s_winfl[lo], 1ull << tyf);
+        }
+    }
+    __syncthreads();
+
+    // ---- P2 (warp per workflow): depth + doom in creation order ---------------
     uint32_t n_ready = 0, n_doom = 0;
-    uint32_t* Hs = p.H;
-
-    // ---- warps take whole workflows ---------------------------------------
     for (;;) {
         uint32_t wi = 0;
         if (lane == 0) wi = atomicAdd(s_ticket, 1u);
@@ -239,19 +271,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         const uint32_t w = w0 + wi;
         const uint32_t fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
         if (p.prof && lane == 0) p.prof[(size_t)w * 2] = gtimer();
-
-        for (uint32_t t = lane; t < T; t += 32) { fp[t] = 0xFFFFFFFFu; fru[t] = 0xFFFFFFFFu; }
-        // LPT needs the workflow's max round before any level
-        uint32_t m_rnd = 0;
-        for (uint32_t f = fa + lane; f < fb; f += 32) m_rnd = max(m_rnd, (uint32_t)rd[f]);
-        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
-        const int64_t prio = wpr[wi];
-        const int64_t lmax = (int64_t)Lv - 1;
-        __syncwarp();
-
         uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
-        uint32_t m_dep = 0;
-        uint64_t seen_p = 0, seen_r = 0, im = 0;   // types seen (first pending / ready unpinned), in flight
+        uint32_t m_dep = 0, m_rnd = 0;
         long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = p.prof ? clock64() : 0;
 
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
@@ -259,20 +280,16 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
             const uint32_t stf = valid ? st[f] : 3u;
+            const uint32_t fl0 = valid ? flg[f] : (uint32_t)FL_ALLRES;
             const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
             // predecessors before this step are final in smem; those inside the
             // step are kept as up to 4 lane slots (+ a mask for any extra ones)
             uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
             uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
-            bool dm = false, allres = true;
-            // one predecessor edge: loads were issued by the caller
-            auto take = [&](uint32_t v, uint32_t ss, uint32_t ds, uint32_t fs) {
+            bool dm = (fl0 & FL_FAILP) != 0;
+            auto take = [&](uint32_t v, uint32_t ds, uint32_t fs) {
                 const uint32_t s = (v & 0x7FFFFFFFu) - r0;
                 const bool call = (v >> 31) != 0;
-                if (!call) {
-                    dm |= ss == 4u;
-                    allres &= ss == 3u;
-                }
                 if (s >= c0) {
                     const uint32_t k = s - c0;
                     if (np == 0) s0 = k;
@@ -291,15 +308,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
                 const uint32_t va = ed[e], vb = ed[e + 1];
                 const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
-                const uint32_t ssa = st[sa], ssb = st[sb], dsa = dep[sa], dsb = dep[sb];
-                const uint32_t fsa = flg[sa], fsb = flg[sb];
-                take(va, ssa, dsa, fsa);
-                take(vb, ssb, dsb, fsb);
+                const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
+                take(va, dsa, fsa);
+                take(vb, dsb, fsb);
             }
             if (e < ee) {
                 const uint32_t va = ed[e];
                 const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
-                take(va, st[sa], dep[sa], flg[sa]);
+                take(va, dep[sa], flg[sa]);
             }
             if (ee > eb) d = max(d, 1u);
             d = min(d, 65535u);
@@ -340,99 +356,25 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 }
             }
             if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
-            // first PENDING non-doomed / first ready unpinned row per type:
-            // rows rise with lane, so the lowest lane of each type group wins
-            const uint32_t tyf = valid ? ty[f] : 0u;
-            const int pinf = valid ? pn[f] : -1;
-            const bool ready = pend && !doom && allres;
-            // types not seen yet in this workflow take an atomicMin (rare)
-            const bool cp = valid && pend && !doom && !((seen_p >> tyf) & 1ull);
-            const bool cr = valid && ready && pinf < 0 && !((seen_r >> tyf) & 1ull);
+            const bool ready = pend && !doom && (fl0 & FL_ALLRES);
             if (valid) {
-                const uint32_t aff = s_aff[tyf];
-                const bool infl_row = stf == 1u || stf == 2u;
-                // eligibility known now unless decided per (workflow, type) below
-                const bool elig = ready && (aff == 0u || (aff == 1u && pinf >= 0));
-                uint32_t lv = 0;
-                if (stf < 3u) {
-                    const int64_t score = pol == 1u ? (int64_t)d : (pol == 2u ? (int64_t)m_rnd : 0);
-                    const int64_t x = prio + score;
-                    lv = (uint32_t)(x < 0 ? 0 : (x > lmax ? lmax : x));
-                }
-                uint32_t status;
-                int16_t inst = -1;
-                if (stf == 3u) status = 0;
-                else if (stf == 4u) status = 1;
-                else if (infl_row) { status = 2; inst = ex[f]; }
-                else if (doom) status = 4;
-                else if (!ready) status = 3;
-                else status = elig ? 6u : 5u;
-                const uint32_t g = r0 + f;
                 dep[f] = (uint16_t)d;
-                flg[f] = (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0) | (elig ? FL_ELIG : 0);
-                lev[f] = (uint8_t)lv;
-                p.status[g] = (uint8_t)status;
-                if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
-                p.instance[g] = inst;
-                p.new_pin[g] = 0;
-                if (infl_row) atomicAdd(&s_load[inst], 1u);
-                if (elig) {
-                    const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
-                    atomicAdd(&Hs[(size_t)r * Lv + lv], 1u);
-                    atomicAdd(&s_rcnt[r], 1u);
-                }
-                if (cp) atomicMin(&fp[tyf], f);
-                if (cr) atomicMin(&fru[tyf], f);
-                c_pend += pend;
-                c_ready += ready;
-                c_infl += infl_row;
-                c_res += stf == 3u;
-                c_fail += stf == 4u;
-                c_doom += doom;
-                c_pinp += pend && pinf >= 0;
+                flg[f] = (uint8_t)(fl0 | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
                 m_dep = max(m_dep, d);
+                m_rnd = max(m_rnd, (uint32_t)rd[f]);
             }
-            {
-                const uint64_t bp = cp ? (1ull << tyf) : 0ull, br = cr ? (1ull << tyf) : 0ull;
-                const uint64_t bi = (valid && (stf == 1u || stf == 2u)) ? (1ull << tyf) : 0ull;
-                seen_p |= ((uint64_t)__reduce_or_sync(0xFFFFFFFFu, (uint32_t)(bp >> 32)) << 32) |
-                          __reduce_or_sync(0xFFFFFFFFu, (uint32_t)bp);
-                seen_r |= ((uint64_t)__reduce_or_sync(0xFFFFFFFFu, (uint32_t)(br >> 32)) << 32) |
-                          __reduce_or_sync(0xFFFFFFFFu, (uint32_t)br);
-                im |= ((uint64_t)__reduce_or_sync(0xFFFFFFFFu, (uint32_t)(bi >> 32)) << 32) |
-                      __reduce_or_sync(0xFFFFFFFFu, (uint32_t)bi);
-            }
+            // per-workflow aggregates by ballots ("aggregating")
+            c_pend += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend));
+            c_ready += __popc(__ballot_sync(0xFFFFFFFFu, ready));
+            c_infl += __popc(__ballot_sync(0xFFFFFFFFu, valid && (stf == 1u || stf == 2u)));
+            c_res += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 3u));
+            c_fail += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 4u));
+            c_doom += __popc(__ballot_sync(0xFFFFFFFFu, doom));
+            c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pn[f] >= 0));
             __syncwarp();
         }
-
-        // stateful fence and first placement:
-        // the per-(workflow, type) winner becomes eligible
-        for (uint32_t t = lane; t < T; t += 32) {
-            const uint32_t aff = s_aff[t];
-            uint32_t f = 0xFFFFFFFFu;
-            if (aff == 2u) {
-                const uint32_t c = fp[t];
-                if (c != 0xFFFFFFFFu && !((im >> t) & 1ull) && (flg[c] & FL_READY)) f = c;
-            } else if (aff == 1u) {
-                f = fru[t];
-            }
-            if (f != 0xFFFFFFFFu) {
-                flg[f] |= FL_ELIG;
-                p.status[r0 + f] = 6;
-                const int pinf = pn[f];
-                const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + t;
-                atomicAdd(&Hs[(size_t)r * Lv + lev[f]], 1u);
-                atomicAdd(&s_rcnt[r], 1u);
-            }
-        }
-        c_pend = __reduce_add_sync(0xFFFFFFFFu, c_pend);
-        c_ready = __reduce_add_sync(0xFFFFFFFFu, c_ready);
-        c_infl = __reduce_add_sync(0xFFFFFFFFu, c_infl);
-        c_res = __reduce_add_sync(0xFFFFFFFFu, c_res);
-        c_fail = __reduce_add_sync(0xFFFFFFFFu, c_fail);
-        c_doom = __reduce_add_sync(0xFFFFFFFFu, c_doom);
-        c_pinp = __reduce_add_sync(0xFFFFFFFFu, c_pinp);
         m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
+        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
         n_ready += c_ready;
         n_doom += c_doom;
         if (lane < 10) {
@@ -448,6 +390,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             v = lane == 9 ? m_rnd : v;
             p.wf_agg[(size_t)w * 10 + lane] = v;
         }
+        if (lane == 0) s_wrnd[wi] = m_rnd;
         if (p.prof && lane == 0) {
             p.prof[(size_t)w * 2 + 1] = gtimer();
             cyc_rest += clock64() - cyc_t;
@@ -461,9 +404,85 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         atomicAdd(&s_cnt[2], n_doom);
     }
     __syncthreads();
-    if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 1] = gtimer();
+    if (bprof && tid == 0) bprof[1] = gtimer();
 
-    // ---- block epilogue: loads, per-resource offsets, stable bucketing ------
+    // ---- P3 (row-parallel): level, status, outputs, histogram, minima --------
+    const uint32_t pol = p.policy;
+    const int64_t lmax = (int64_t)Lv - 1;
+    for (uint32_t f0 = 0; f0 < nr; f0 += kK1Threads) {
+        const uint32_t f = f0 + tid;
+        uint32_t kp = 0xFFFFFFFFu, kr = 0xFFFFFFFFu, wl = 0, tyf = 0;
+        if (f < nr) {
+            wl = wlm[f];
+            const uint32_t stf = st[f], fl = flg[f], d = dep[f];
+            tyf = ty[f];
+            const int pinf = pn[f];
+            const bool doom = fl & FL_DOOMED, ready = fl & FL_READY, pend = stf == 0u;
+            const uint32_t aff = s_aff[tyf];
+            const bool infl_row = stf == 1u || stf == 2u;
+            // eligibility known now unless decided per (workflow, type) in P4
+            const bool elig = ready && (aff == 0u || (aff == 1u && pinf >= 0));
+            uint32_t lv = 0;
+            if (stf < 3u) {
+                const int64_t score = pol == 1u ? (int64_t)d : (pol == 2u ? (int64_t)s_wrnd[wl] : 0);
+                const int64_t x = (int64_t)wpr[wl] + score;
+                lv = (uint32_t)(x < 0 ? 0 : (x > lmax ? lmax : x));
+            }
+            uint32_t status;
+            int16_t inst = -1;
+            if (stf == 3u) status = 0;
+            else if (stf == 4u) status = 1;
+            else if (infl_row) { status = 2; inst = ex[f]; }
+            else if (doom) status = 4;
+            else if (!ready) status = 3;
+            else status = elig ? 6u : 5u;
+            const uint32_t g = r0 + f;
+            lev[f] = (uint8_t)lv;
+            p.status[g] = (uint8_t)status;
+            if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
+            p.instance[g] = inst;
+            p.new_pin[g] = 0;
+            if (elig) {
+                flg[f] = (uint8_t)(fl | FL_ELIG);
+                const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
+                atomicAdd(&p.H[(size_t)r * Lv + lv], 1u);
+                atomicAdd(&s_rcnt[r], 1u);
+            }
+            if (pend && !doom) kp = wl << 6 | tyf;
+            if (ready && pinf < 0) kr = wl << 6 | tyf;
+        }
+        // first PENDING non-doomed / first ready unpinned row of each (w, t):
+        // the lowest lane of each (w, t) group carries the group's minimum row
+        const uint32_t mp = __match_any_sync(0xFFFFFFFFu, kp), mr = __match_any_sync(0xFFFFFFFFu, kr);
+        if (kp != 0xFFFFFFFFu && (__ffs(mp) - 1) == (int)lane) atomicMin(&s_wfp[wl * T + tyf], f);
+        if (kr != 0xFFFFFFFFu && (__ffs(mr) - 1) == (int)lane) atomicMin(&s_wfru[wl * T + tyf], f);
+    }
+    __syncthreads();
+
+    // ---- P4: the stateful fence and first placement
+    // make the per-(workflow, type) winner eligible
+    for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
+        const uint32_t wl = k / T, t = k - wl * T;
+        const uint32_t aff = s_aff[t];
+        uint32_t f = 0xFFFFFFFFu;
+        if (aff == 2u) {
+            const uint32_t c = s_wfp[k];
+            if (c != 0xFFFFFFFFu && !((s_winfl[wl] >> t) & 1ull) && (flg[c] & FL_READY)) f = c;
+        } else if (aff == 1u) {
+            f = s_wfru[k];
+        }
+        if (f != 0xFFFFFFFFu) {
+            flg[f] |= FL_ELIG;
+            p.status[r0 + f] = 6;
+            const int pinf = pn[f];
+            const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + t;
+            atomicAdd(&p.H[(size_t)r * Lv + lev[f]], 1u);
+            atomicAdd(&s_rcnt[r], 1u);
+        }
+    }
+    __syncthreads();
+
+    // ---- P5 (epilogue): loads, per-resource offsets, stable bucketing ---------
     for (uint32_t i = tid; i < I; i += kK1Threads)
         if (s_load[i]) atomicAdd(&p.load_part[i], s_load[i]);
     // exclusive scan of s_rcnt over R (serial per thread chunk + warp scan)
@@ -532,7 +551,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         n_elig += tot;
         __syncthreads();
     }
-    if (p.prof && tid == 0) p.prof[(size_t)p.n_wf * 2 + b * 4 + 2] = gtimer();
+    if (bprof && tid == 0) bprof[2] = gtimer();
     if (tid == 0) {
         atomicAdd(&p.counters[C_READY], s_cnt[0]);
         atomicAdd(&p.counters[C_ELIG], n_elig);

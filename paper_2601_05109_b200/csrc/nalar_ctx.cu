@@ -54,6 +54,7 @@ NcclApi g_nccl;
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
 constexpr uint32_t kMaxBlocks = 16384;
+constexpr uint32_t kMaxWfPerBlock = 4096;    // row -> workflow map is u16
 
 struct Key {
     uint32_t N, E, W, I, T, B, R, policy;
@@ -81,6 +82,7 @@ struct nalar_ctx {
     uint32_t *d_type_off = nullptr, *d_type_inst = nullptr;
     // outputs
     uint8_t *d_status = nullptr, *d_level = nullptr, *d_newpin = nullptr, *d_gflags = nullptr;
+    uint16_t* d_gwlm = nullptr;
     uint16_t* d_depth = nullptr;
     int16_t *d_inst = nullptr, *d_ainst = nullptr;
     uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
@@ -144,7 +146,7 @@ struct Layout {
 struct Plan {
     size_t wf_off, wf_prio, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, type_off, type_inst;
-    size_t status, level, newpin, gflags, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
+    size_t status, level, newpin, gflags, gwlm, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
     uint32_t Rmax, Bmax;
@@ -181,6 +183,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->level = L.take<uint8_t>(N);
     p->newpin = L.take<uint8_t>(N);
     p->gflags = L.take<uint8_t>(N);
+    p->gwlm = L.take<uint16_t>(N);
     p->depth = L.take<uint16_t>(N);
     p->inst = L.take<int16_t>(N);
     p->ainst = L.take<int16_t>(N);
@@ -227,15 +230,17 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* eoff, std::
             while (w < W) {
                 const uint32_t wr = wf_off[w + 1] - wf_off[w];
                 const uint32_t e_if = eoff[wf_off[w + 1]] - eoff[wf_off[ws]];
-                if (w > ws && k1_staged_smem(rows + wr, e_if, w - ws + 1) > kStageBudget) break;
+                if (w > ws && (k1_block_smem(rows + wr, e_if, w - ws + 1, c->T, true) > kStageBudget ||
+                               w - ws + 1 > kMaxWfPerBlock))
+                    break;
                 rows += wr;
                 ++w;
                 if (rows >= target) break;
             }
             const uint32_t ra = wf_off[ws], rb = wf_off[w];
-            const size_t need = k1_staged_smem(rb - ra, eoff[rb] - eoff[ra], w - ws);
-            const bool staged = need <= kStageBudget && !(c->cfg.flags & NALAR_F_FORCE_UNSTAGED);
-            if (staged) mx = std::max(mx, need);
+            const size_t need_st = k1_block_smem(rb - ra, eoff[rb] - eoff[ra], w - ws, c->T, true);
+            const bool staged = need_st <= kStageBudget && !(c->cfg.flags & NALAR_F_FORCE_UNSTAGED);
+            mx = std::max(mx, staged ? need_st : k1_block_smem(rb - ra, 0, w - ws, c->T, false));
             bw.push_back(ws); br.push_back(ra); be.push_back(eoff[ra]); bs.push_back(staged ? 1 : 0);
         }
         bw.push_back(W); br.push_back(wf_off[W]); be.push_back(eoff[wf_off[W]]);
@@ -255,6 +260,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
+    p.g_wlm = c->d_gwlm;
     p.prof = c->d_prof;
     p.n_wf = c->W;
     p.status = c->d_status; p.level = c->d_level; p.depth = c->d_depth; p.instance = c->d_inst;
@@ -406,6 +412,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_type_off = at<uint32_t>(a, p.type_off); c->d_type_inst = at<uint32_t>(a, p.type_inst);
     c->d_status = at<uint8_t>(a, p.status); c->d_level = at<uint8_t>(a, p.level);
     c->d_newpin = at<uint8_t>(a, p.newpin); c->d_gflags = at<uint8_t>(a, p.gflags);
+    c->d_gwlm = at<uint16_t>(a, p.gwlm);
     c->d_depth = at<uint16_t>(a, p.depth); c->d_inst = at<int16_t>(a, p.inst); c->d_ainst = at<int16_t>(a, p.ainst);
     c->d_wfagg = at<uint32_t>(a, p.wfagg); c->d_iload = at<uint32_t>(a, p.iload);
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
