@@ -10,13 +10,13 @@
 namespace nalar {
 
 constexpr int kK0Threads = 256;          // validate: warp per workflow
-constexpr int kK1Threads = 256;          // sweep: warp per workflow inside a block
+constexpr int kK1Threads = 512;          // sweep: warp per workflow inside a block
 constexpr int kK1Warps = kK1Threads / 32;
 constexpr int kK4Threads = 256;          // assign: one block per resource
 constexpr int kK4Warps = kK4Threads / 32;
 
 // per-row flags produced by the sweep
-enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8, FL_FAILP = 16 };
+enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8 };
 
 // indices into the per-epoch counters array (scratch)
 enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_NUM = 8 };
@@ -58,7 +58,6 @@ struct SweepParams {
     uint32_t B, n_types, n_inst, R, levels, policy;
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
-    uint16_t* g_wlm;            // [N] row -> local workflow scratch for unstaged blocks
     unsigned long long* prof;   // NALAR_F_PROFILE: [W][2] workflow start/end, [B][4] block phases
     uint32_t n_wf;
     // outputs

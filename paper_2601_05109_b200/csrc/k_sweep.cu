@@ -102,7 +102,7 @@ size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bo
     if (staged)
         b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
              align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
-             2 * align16(2 * (size_t)rows) + 2 * align16(rows);
+             align16(2 * (size_t)rows) + 2 * align16(rows);
     return b;
 }
 
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
     const uint32_t nr = r1 - r0, ne = e1 - e0, nw = w1 - w0;
     const bool staged = p.blk_staged[b] != 0;
-    unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 4 : nullptr;
+    unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;
     if (bprof && tid == 0) bprof[3] = gtimer();
 
     // ---- carve the fixed part --------------------------------------------
@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const uint32_t* wfo;  // absolute workflow row offsets, indexed by local workflow
     const int32_t* wpr;   // workflow priorities, indexed by local workflow
     uint16_t* dep;        // depth (work / output)
-    uint16_t* wlm;        // local workflow of each row
     uint8_t* flg;         // FL_* (work)
     uint8_t* lev;         // level (work / output)
     if (staged) {
@@ -177,7 +176,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         uint8_t* d_o = q;   q += align16(4 * ((size_t)nw + 1) + 32);
         uint8_t* d_q = q;   q += align16(4 * (size_t)nw + 32);
         dep = (uint16_t*)q; q += align16(2 * (size_t)nr);
-        wlm = (uint16_t*)q; q += align16(2 * (size_t)nr);
         flg = q;            q += align16(nr);
         lev = q;
         if (tid == 0) {
@@ -215,7 +213,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         wfo = p.wf_fut_off + w0;
         wpr = p.wf_prio + w0;
         dep = p.depth + r0;
-        wlm = p.g_wlm + r0;
         flg = p.g_flags + r0;
         lev = p.level + r0;
     }
@@ -234,32 +231,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     if (staged) mbar_wait(mbar, 0);
     if (bprof && tid == 0) bprof[0] = gtimer();
 
-    // ---- P1 (row-parallel): readiness inputs, workflow map, in-flight load ---
-    for (uint32_t f = tid; f < nr; f += kK1Threads) {
-        const uint32_t stf = st[f], tyf = ty[f];
-        const uint32_t eb = eo[f] - e0, ee = eo[f + 1] - e0;
-        bool allres = true, failp = false;
-        for (uint32_t e = eb; e < ee; ++e) {
-            const uint32_t v = ed[e];
-            if (v >> 31) continue;                      // CALL edges never gate (Q2)
-            const uint32_t ss = st[(v & 0x7FFFFFFFu) - r0];
-            allres &= ss == 3u;
-            failp |= ss == 4u;
-        }
-        uint32_t lo = 0, hi = nw - 1;                   // workflow of row f
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (wfo[mid] - r0 <= f) lo = mid;
-            else hi = mid - 1;
-        }
-        wlm[f] = (uint16_t)lo;
-        flg[f] = (allres ? FL_ALLRES : 0) | (failp ? FL_FAILP : 0);
-        if (stf == 1u || stf == 2u) {
-            atomicAdd(&s_load[ex[f]], 1u);
-            atomicOr(&s_winfl[lo], 1ull << tyf);
-        }
-    }
-    __syncthreads();
+    if (bprof && tid == 0) bprof[6] = gtimer();
 
     // ---- P2 (warp per workflow): depth + doom in creation order ---------------
     uint32_t n_ready = 0, n_doom = 0;
@@ -280,61 +252,66 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
             const uint32_t stf = valid ? st[f] : 3u;
-            const uint32_t fl0 = valid ? flg[f] : (uint32_t)FL_ALLRES;
             const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
             // predecessors before this step are final in smem; those inside the
             // step are kept as up to 4 lane slots (+ a mask for any extra ones)
             uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
             uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
-            bool dm = (fl0 & FL_FAILP) != 0;
-            auto take = [&](uint32_t v, uint32_t ds, uint32_t fs) {
+            bool dm = false, allres = true;
+            // one predecessor edge, branch-free (lanes differ in edge kinds)
+            auto take = [&](uint32_t v, uint32_t ds, uint32_t fs, uint32_t ss) {
                 const uint32_t s = (v & 0x7FFFFFFFu) - r0;
-                const bool call = (v >> 31) != 0;
-                if (s >= c0) {
-                    const uint32_t k = s - c0;
-                    if (np == 0) s0 = k;
-                    else if (np == 1) s1 = k;
-                    else if (np == 2) s2 = k;
-                    else if (np == 3) s3 = k;
-                    else extra |= 1u << k;
-                    ++np;
-                    if (!call) need_dep |= 1u << k;
-                } else {
-                    d = max(d, ds + 1u);
-                    if (!call) dm |= (fs & FL_DOOMED) != 0;
-                }
+                const bool dep_edge = (v >> 31) == 0u;
+                const bool in = s >= c0;
+                allres &= !dep_edge || ss == 3u;                 // CALL edges never gate (Q2)
+                dm |= dep_edge && ss == 4u;
+                const uint32_t k = (s - c0) & 31u;
+                s0 = (in && np == 0) ? k : s0;
+                s1 = (in && np == 1) ? k : s1;
+                s2 = (in && np == 2) ? k : s2;
+                s3 = (in && np == 3) ? k : s3;
+                extra |= (in && np >= 4) ? (1u << k) : 0u;
+                need_dep |= (in && dep_edge) ? (1u << k) : 0u;
+                np += in ? 1u : 0u;
+                d = in ? d : max(d, ds + 1u);
+                dm |= !in && dep_edge && (fs & FL_DOOMED);
             };
             uint32_t e = eb;
             for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
                 const uint32_t va = ed[e], vb = ed[e + 1];
                 const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
                 const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
-                take(va, dsa, fsa);
-                take(vb, dsb, fsb);
+                const uint32_t ssa = st[sa], ssb = st[sb];
+                take(va, dsa, fsa, ssa);
+                take(vb, dsb, fsb, ssb);
             }
             if (e < ee) {
                 const uint32_t va = ed[e];
                 const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
-                take(va, dep[sa], flg[sa]);
+                take(va, dep[sa], flg[sa], st[sa]);
             }
             if (ee > eb) d = max(d, 1u);
-            d = min(d, 65535u);
+            // unused in-step slots repeat slot 0 (a harmless duplicate)
+            s1 = np > 1 ? s1 : s0;
+            s2 = np > 2 ? s2 : s0;
+            s3 = np > 3 ? s3 : s0;
             const bool pend = stf == 0u;
             bool doom = pend && dm;
             if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
-            // in-step settling: Bellman-Ford rounds on registers -- depths move
-            // by shuffles, doom by ballots; two rounds per convergence vote
+            // in-step settling: Bellman-Ford rounds on registers, depths moving
+            // by shuffles (four rounds per convergence vote); then doom, a
+            // boolean closure over in-step DEP edges, by ballots
             if (__any_sync(0xFFFFFFFFu, np != 0u)) {
                 const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
-                const uint32_t m0 = np > 0 ? 0xFFFFFFFFu : 0u, m1 = np > 1 ? 0xFFFFFFFFu : 0u;
-                const uint32_t m2 = np > 2 ? 0xFFFFFFFFu : 0u, m3 = np > 3 ? 0xFFFFFFFFu : 0u;
-                auto round = [&]() -> bool {
+                const bool has = np != 0u;
+                // saturation is applied once after convergence: with D the
+                // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
+                auto round = [&]() {
                     const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
                     const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
                     const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
                     const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
-                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
-                    uint32_t nd = max(max(max(d, (x0 + 1u) & m0), (x1 + 1u) & m1), max((x2 + 1u) & m2, (x3 + 1u) & m3));
+                    uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
                     if (wide) {
 #pragma unroll 1
                         for (uint32_t k = 0; k < 32; ++k) {
@@ -342,24 +319,30 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                             if ((extra >> k) & 1u) nd = max(nd, x + 1u);
                         }
                     }
-                    nd = min(nd, 65535u);
-                    const bool ndm = doom || (pend && (need_dep & D) != 0u);
-                    const bool ch = (nd != d) | (ndm != doom);
-                    d = nd;
-                    doom = ndm;
-                    return ch;
+                    d = has ? max(d, nd) : d;
                 };
                 for (;;) {
                     round();
-                    const bool ch = round();
-                    if (!__any_sync(0xFFFFFFFFu, ch)) break;
+                    round();
+                    round();
+                    const uint32_t before = d;
+                    round();
+                    if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                }
+                if (__any_sync(0xFFFFFFFFu, doom)) {
+                    for (;;) {
+                        const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+                        doom = doom || (pend && (need_dep & D) != 0u);
+                        if (__ballot_sync(0xFFFFFFFFu, doom) == D) break;
+                    }
                 }
             }
+            d = min(d, 65535u);
             if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
-            const bool ready = pend && !doom && (fl0 & FL_ALLRES);
+            const bool ready = pend && !doom && allres;
             if (valid) {
                 dep[f] = (uint16_t)d;
-                flg[f] = (uint8_t)(fl0 | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
+                flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
                 m_dep = max(m_dep, d);
                 m_rnd = max(m_rnd, (uint32_t)rd[f]);
             }
@@ -394,7 +377,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         if (p.prof && lane == 0) {
             p.prof[(size_t)w * 2 + 1] = gtimer();
             cyc_rest += clock64() - cyc_t;
-            unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 4 + (size_t)p.R * 4 + (size_t)w * 3;
+            unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 4 + (size_t)w * 3;
             c[0] = cyc_edge; c[1] = cyc_round; c[2] = cyc_rest;
         }
         __syncwarp();
@@ -413,9 +396,21 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         const uint32_t f = f0 + tid;
         uint32_t kp = 0xFFFFFFFFu, kr = 0xFFFFFFFFu, wl = 0, tyf = 0;
         if (f < nr) {
-            wl = wlm[f];
+            {   // workflow of row f (binary search over the staged offsets)
+                uint32_t lo = 0, hi = nw - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    if (wfo[mid] - r0 <= f) lo = mid;
+                    else hi = mid - 1;
+                }
+                wl = lo;
+            }
             const uint32_t stf = st[f], fl = flg[f], d = dep[f];
             tyf = ty[f];
+            if (stf == 1u || stf == 2u) {       // in-flight: instance load, (w, t) fence
+                atomicAdd(&s_load[ex[f]], 1u);
+                atomicOr(&s_winfl[wl], 1ull << tyf);
+            }
             const int pinf = pn[f];
             const bool doom = fl & FL_DOOMED, ready = fl & FL_READY, pend = stf == 0u;
             const uint32_t aff = s_aff[tyf];
@@ -451,13 +446,13 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             if (pend && !doom) kp = wl << 6 | tyf;
             if (ready && pinf < 0) kr = wl << 6 | tyf;
         }
-        // first PENDING non-doomed / first ready unpinned row of each (w, t):
-        // the lowest lane of each (w, t) group carries the group's minimum row
-        const uint32_t mp = __match_any_sync(0xFFFFFFFFu, kp), mr = __match_any_sync(0xFFFFFFFFu, kr);
-        if (kp != 0xFFFFFFFFu && (__ffs(mp) - 1) == (int)lane) atomicMin(&s_wfp[wl * T + tyf], f);
-        if (kr != 0xFFFFFFFFu && (__ffs(mr) - 1) == (int)lane) atomicMin(&s_wfru[wl * T + tyf], f);
+        // first PENDING non-doomed / first ready unpinned row of each (w, t)
+        // (a minimum: order-independent, so plain shared-memory atomics)
+        if (kp != 0xFFFFFFFFu) atomicMin(&s_wfp[wl * T + tyf], f);
+        if (kr != 0xFFFFFFFFu) atomicMin(&s_wfru[wl * T + tyf], f);
     }
     __syncthreads();
+    if (bprof && tid == 0) bprof[4] = gtimer();
 
     // ---- P4: the stateful fence and first placement
     // make the per-(workflow, type) winner eligible
@@ -481,6 +476,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         }
     }
     __syncthreads();
+    if (bprof && tid == 0) bprof[5] = gtimer();
 
     // ---- P5 (epilogue): loads, per-resource offsets, stable bucketing ---------
     for (uint32_t i = tid; i < I; i += kK1Threads)

@@ -54,7 +54,7 @@ NcclApi g_nccl;
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
 constexpr uint32_t kMaxBlocks = 16384;
-constexpr uint32_t kMaxWfPerBlock = 4096;    // row -> workflow map is u16
+constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tables
 
 struct Key {
     uint32_t N, E, W, I, T, B, R, policy;
@@ -260,7 +260,6 @@ int run_k1(nalar_ctx* c, int policy) {
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
-    p.g_wlm = c->d_gwlm;
     p.prof = c->d_prof;
     p.n_wf = c->W;
     p.status = c->d_status; p.level = c->d_level; p.depth = c->d_depth; p.instance = c->d_inst;
@@ -294,7 +293,7 @@ int run_k4(nalar_ctx* c) {
     p.assign_row = c->d_arow; p.assign_inst = c->d_ainst;
     p.n_adm = c->d_scr + C_NUM;
     p.tot_loc = c->d_scr + C_NUM + c->Rmax;
-    p.prof = c->d_prof ? c->d_prof + 2ull * c->W + 4ull * c->B : nullptr;
+    p.prof = c->d_prof ? c->d_prof + 2ull * c->W + 8ull * c->B : nullptr;
     p.counters = c->d_scr;
     CK(launch_assign(p, c->stream));
     return NALAR_OK;
@@ -554,7 +553,7 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
         return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
     }
     if (k.flags & NALAR_F_PROFILE) {
-        const size_t need = 2ull * W + 4ull * c->B + 4ull * c->R + 3ull * W;
+        const size_t need = 2ull * W + 8ull * c->B + 4ull * c->R + 3ull * W;
         if (need > c->prof_words) {
             if (c->d_prof) cudaFree(c->d_prof);
             c->d_prof = nullptr;

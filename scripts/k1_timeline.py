@@ -33,7 +33,7 @@ wf = prof[:2 * W].reshape(W, 2)
 R = s.n_instances + s.n_types
 cyc = prof[len(prof) - 3 * W:].reshape(W, 3)              # edge loop, rounds, rest (SM cycles)
 prof = prof[:len(prof) - 3 * W]
-blk = prof[2 * W:len(prof) - 4 * R].reshape(-1, 4)        # staged, swept, bucketed, entered
+blk = prof[2 * W:len(prof) - 4 * R].reshape(-1, 8)        # staged, swept, bucketed, entered, P3 done, P4 done
 k4 = prof[len(prof) - 4 * R:].reshape(R, 4)              # start, published, based, done
 t0 = blk[:, 3].min()
 o = oracle_epoch(s, "srtf")
@@ -46,8 +46,12 @@ res = {
     "kernel_span_ns": int(blk[:, 2].max() - t0),
     "block_entry_spread_ns": int(blk[:, 3].max() - t0),
     "stage_ns_mean": float(np.mean(blk[:, 0] - blk[:, 3])), "stage_ns_max": int(np.max(blk[:, 0] - blk[:, 3])),
-    "sweep_ns_max": int(np.max(blk[:, 1] - blk[:, 0])), "sweep_ns_mean": float(np.mean(blk[:, 1] - blk[:, 0])),
+    "sweep_ns_max": int(np.max(blk[:, 1] - blk[:, 6])), "sweep_ns_mean": float(np.mean(blk[:, 1] - blk[:, 6])),
     "bucket_ns_max": int(np.max(blk[:, 2] - blk[:, 1])), "bucket_ns_mean": float(np.mean(blk[:, 2] - blk[:, 1])),
+    "p1_ns_max": int(np.max(blk[:, 6] - blk[:, 0])), "stage_to_p1_ns_max": int(np.max(blk[:, 0] - blk[:, 3])),
+    "p3_ns_max": int(np.max(blk[:, 4] - blk[:, 1])), "p3_ns_mean": float(np.mean(blk[:, 4] - blk[:, 1])),
+    "p4_ns_max": int(np.max(blk[:, 5] - blk[:, 4])), "p5_ns_max": int(np.max(blk[:, 2] - blk[:, 5])),
+    "p5_ns_mean": float(np.mean(blk[:, 2] - blk[:, 5])),
     "wf_dur_ns_max": int(dur.max()), "wf_dur_ns_mean": float(dur.mean()),
     "wf_end_ns_max": int(end.max()),
     "ns_per_row_mean": float(np.sum(dur) / np.sum(sizes)),

@@ -1,0 +1,59 @@
+// Latency of the warp-collective / shared-memory ops the sweep's critical path
+// uses, measured on one warp with dependent chains (SM cycles per op).
+#include <cstdio>
+#include <cstdint>
+#define N 2048
+__global__ void bench(unsigned long long* out, int seed) {
+    __shared__ uint32_t sm[1024];
+    const uint32_t lane = threadIdx.x;
+    for (int i = lane; i < 1024; i += 32) sm[i] = (i * 7 + 1) & 1023;
+    __syncwarp();
+    uint32_t x = lane + seed;
+    long long t0, t1;
+    // SHFL.IDX dependent chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x = __shfl_sync(0xFFFFFFFFu, x, (x + lane) & 31) + 1;
+    t1 = clock64(); if (lane == 0) out[0] = (t1 - t0);
+    // VOTE.ANY chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x += __any_sync(0xFFFFFFFFu, (x & 3) == lane);
+    t1 = clock64(); if (lane == 0) out[1] = (t1 - t0);
+    // BALLOT chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x += __ballot_sync(0xFFFFFFFFu, (x & 1)) & 1;
+    t1 = clock64(); if (lane == 0) out[2] = (t1 - t0);
+    // MATCH.ANY chain, 8 distinct keys
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x += __match_any_sync(0xFFFFFFFFu, (x + lane) & 7) & 1;
+    t1 = clock64(); if (lane == 0) out[3] = (t1 - t0);
+    // MATCH.ANY chain, 32 distinct keys
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x += __match_any_sync(0xFFFFFFFFu, (x & 0xFFFF0000u) + lane) & 1;
+    t1 = clock64(); if (lane == 0) out[4] = (t1 - t0);
+    // REDUX max chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x = __reduce_max_sync(0xFFFFFFFFu, x ^ lane) + 1;
+    t1 = clock64(); if (lane == 0) out[5] = (t1 - t0);
+    // LDS chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x = sm[(x + lane) & 1023];
+    t1 = clock64(); if (lane == 0) out[6] = (t1 - t0);
+    // IMNMX chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x = max(x + 1u, (uint32_t)lane);
+    t1 = clock64(); if (lane == 0) out[7] = (t1 - t0);
+    // smem atomicMin, 32 lanes same address
+    t0 = clock64();
+    for (int i = 0; i < N / 8; ++i) x += atomicMin(&sm[x & 1], lane + x) & 1;
+    t1 = clock64(); if (lane == 0) out[8] = (t1 - t0) * 8;
+    if (lane == 0) out[9] = x;
+}
+int main() {
+    unsigned long long* d; unsigned long long h[10];
+    cudaMalloc(&d, 80);
+    bench<<<1, 32>>>(d, 1); cudaDeviceSynchronize();
+    bench<<<1, 32>>>(d, 2); cudaMemcpy(h, d, 80, cudaMemcpyDeviceToHost);
+    const char* nm[] = {"shfl.idx", "vote.any", "ballot", "match.any(8 keys)", "match.any(32 keys)", "redux.max", "lds", "imnmx", "atom.shared.min(32-way)"};
+    for (int i = 0; i < 9; ++i) printf("%-26s %7.1f cycles/op\n", nm[i], (double)h[i] / N);
+    return 0;
+}
