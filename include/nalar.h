@@ -133,6 +133,56 @@ typedef struct {
     const uint8_t*  t_affinity;  /* [T] nalar_aff                            */
 } nalar_snapshot;
 
+/* Delta between two epochs of a dynamic workload (SURVEY §8(c) "Delta
+ * semantics"; the dynamic control flow of PAPER.md:45, 458-460: futures are
+ * created as the program runs, resolve, and whole workflows retire).  Applied
+ * by nalar_delta_apply in this order:
+ *  1. flags & NALAR_DELTA_APPLY_ASSIGNED: every future ASSIGNED by the last
+ *     epoch becomes QUEUED at its assigned instance;
+ *  2. per-future updates addressed by (workflow id, seq), seq = the future's
+ *     index inside its workflow in creation order; a field equal to
+ *     NALAR_KEEP_STATE / NALAR_KEEP_I16 is left unchanged;
+ *  3. retired workflows (by id) are removed whole;
+ *  4. appended futures are added at the END of their workflow in array order
+ *     (grouped by workflow id, ids ascending); an id not in the table opens a
+ *     new workflow with priority app_wf_prio[first row] and must exceed every
+ *     live id; an appended future's edges name EARLIER futures of the same
+ *     workflow by seq (bit 31 = NALAR_CALL_EDGE);
+ *  5. set_priority updates by workflow id, then instance cap / base-load
+ *     updates.
+ * All pointers are HOST pointers borrowed for the call. */
+#define NALAR_DELTA_APPLY_ASSIGNED 1u
+#define NALAR_KEEP_STATE 0xFFu
+#define NALAR_KEEP_I16   (-2)
+typedef struct {
+    uint32_t flags;
+    uint32_t n_updates;
+    const uint64_t* upd_wf_id;     /* [n_updates] */
+    const uint32_t* upd_seq;
+    const uint8_t*  upd_state;     /* nalar_state or NALAR_KEEP_STATE */
+    const int16_t*  upd_executor;  /* instance, -1, or NALAR_KEEP_I16 */
+    const int16_t*  upd_pin;       /* instance, -1, or NALAR_KEEP_I16 */
+    uint32_t n_retired;
+    const uint64_t* retired_wf_id; /* [n_retired] */
+    uint32_t n_append, n_append_edges;
+    const uint64_t* app_wf_id;     /* [n_append] */
+    const int32_t*  app_wf_prio;   /* [n_append] used when the row opens a workflow */
+    const uint8_t*  app_state;
+    const uint8_t*  app_type;
+    const uint8_t*  app_round;
+    const int16_t*  app_executor;
+    const int16_t*  app_pin;
+    const uint32_t* app_edge_off;  /* [n_append+1] */
+    const uint32_t* app_edges;     /* [n_append_edges] predecessor seq | CALL bit */
+    uint32_t n_prio;
+    const uint64_t* prio_wf_id;    /* [n_prio] */
+    const int32_t*  prio_value;
+    uint32_t n_inst;
+    const uint32_t* inst_id;       /* [n_inst] */
+    const uint32_t* inst_cap;
+    const uint32_t* inst_base_load;
+} nalar_delta;
+
 /* Caller-allocated HOST output buffers; any pointer may be NULL (skipped).
  * *_cap = capacity in elements.  On NALAR_E_SIZE the n_* fields hold the
  * required sizes and nothing is copied. */
@@ -187,6 +237,16 @@ int nalar_destroy(nalar_ctx* ctx);
  * the same workflow.  *err_row (may be NULL) = smallest offending row, or -1
  * when the error is not attributable to a row. */
 int nalar_snapshot_upload(nalar_ctx* ctx, const nalar_snapshot* snap, int64_t* err_row);
+
+/* Apply a delta to the resident table (see nalar_delta), on the device, then
+ * validate it like an upload (stream-ordered, synchronises).  E_STATE before
+ * any upload (or APPLY_ASSIGNED before any epoch); E_NOMEM if the table
+ * outgrows the reservation; E_INVAL on an unknown (workflow id, seq) or
+ * retired id, a new id not above the live ids, an appended edge not naming an
+ * earlier future of its workflow, or any row the upload contract rejects.
+ * *err_index (may be NULL): the offending update / retired / appended index
+ * (by the stage that failed), or the smallest offending row, or -1. */
+int nalar_delta_apply(nalar_ctx* ctx, const nalar_delta* delta, int64_t* err_index);
 
 /* One policy epoch over the uploaded table (nalar_policy).  Asynchronous on
  * the ctx stream; a collective over all ranks when world > 1 (NCCL mode).

@@ -107,7 +107,45 @@ struct AssignParams {
     unsigned long long* prof;   // NALAR_F_PROFILE: [R][4] start, bounded, based, done
 };
 
+struct RebuildPlan {             // one workflow of the table after a delta
+    uint64_t wf_id;
+    uint32_t src;                // its index in the old table, or ~0 (new workflow)
+    uint32_t n_old, n_old_edges; // rows / edges kept from the old table
+    uint32_t app_lo, app_n;      // appended futures [app_lo, app_lo + app_n)
+    uint32_t new_row0, new_edge0;
+    int32_t prio;                // for new workflows
+    uint32_t pad;
+};
+
+struct DeltaParams {
+    // old (current) table, updated in place by KD1 / KD2
+    uint32_t* wf_off; int32_t* wf_prio; uint64_t* wf_id;
+    uint8_t* state; uint8_t* type; uint8_t* round; int16_t* exec; int16_t* pin;
+    uint32_t* eoff; uint32_t* edges;
+    uint32_t n_wf;
+    // last epoch's assignment regions (KD1)
+    const uint32_t* tot_loc; const uint32_t* n_adm; const uint32_t* arow; const int16_t* ainst;
+    // updates (KD2)
+    uint32_t n_upd;
+    const uint64_t* upd_wf_id; const uint32_t* upd_seq; const uint8_t* upd_state;
+    const int16_t* upd_exec; const int16_t* upd_pin;
+    // rebuild (KD3) into the other buffer set
+    uint32_t n_wf_new;
+    const RebuildPlan* plan;
+    uint32_t* n_wf_off; int32_t* n_wf_prio; uint64_t* n_wf_id;
+    uint8_t* n_state; uint8_t* n_type; uint8_t* n_round; int16_t* n_exec; int16_t* n_pin;
+    uint32_t* n_eoff; uint32_t* n_edges;
+    const uint8_t* app_state; const uint8_t* app_type; const uint8_t* app_round;
+    const int16_t* app_exec; const int16_t* app_pin; const uint32_t* app_eoff; const uint32_t* app_edges;
+    // KD4
+    uint32_t n_prio; const uint64_t* prio_wf_id; const int32_t* prio_value;
+    uint32_t n_inst_upd, n_inst; const uint32_t* inst_id; const uint32_t* inst_cap; const uint32_t* inst_base;
+    uint32_t* i_cap; uint32_t* i_base;
+    unsigned long long* err;     // [0] bad update index, [1] bad prio / instance update index
+};
+
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);
+cudaError_t launch_delta(const DeltaParams& p, bool apply_assigned, uint32_t R, cudaStream_t s);
 cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 

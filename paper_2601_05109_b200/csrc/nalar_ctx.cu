@@ -59,7 +59,11 @@ constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tab
 struct Key {
     uint32_t N, E, W, I, T, B, R, policy;
     size_t smem;
-    bool operator==(const Key& o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
+    const void* table;   // current buffer set (deltas swap sets)
+    bool operator==(const Key& o) const {
+        return N == o.N && E == o.E && W == o.W && I == o.I && T == o.T && B == o.B && R == o.R &&
+               policy == o.policy && smem == o.smem && table == o.table;
+    }
 };
 
 }  // namespace
@@ -110,6 +114,23 @@ struct nalar_ctx {
     Key gkey[3]{};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ncclComm_t comm = nullptr;
+    // delta mode: device workflow ids, the second table buffer set, host mirror
+    uint64_t* d_wf_id = nullptr;
+    struct Alt {
+        uint32_t *wf_off = nullptr, *eoff = nullptr, *edges = nullptr;
+        int32_t* wf_prio = nullptr;
+        uint64_t* wf_id = nullptr;
+        uint8_t *state = nullptr, *type = nullptr, *round = nullptr;
+        int16_t *exec = nullptr, *pin = nullptr;
+        void* mem = nullptr;
+    } alt;
+    void* d_stage = nullptr;          // delta staging (device)
+    size_t stage_bytes = 0;
+    std::vector<uint64_t> m_wf_id;
+    std::vector<uint32_t> m_wf_off, m_wf_eoff;
+    bool assign_valid = false;        // last epoch's assignment regions match the table
+    Key last_key{};
+    bool last_key_set = false;
     unsigned long long* d_prof = nullptr;
     size_t prof_words = 0;
     std::string err;
@@ -144,7 +165,7 @@ struct Layout {
 };
 
 struct Plan {
-    size_t wf_off, wf_prio, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
+    size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t items, cnt_rb, off_rb, x, scr, err;
@@ -162,6 +183,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     Layout L;
     p->wf_off = L.take<uint32_t>(W + 1);
     p->wf_prio = L.take<int32_t>(W);
+    p->wf_id = L.take<uint64_t>(W);
     p->state = L.take<uint8_t>(N);
     p->type = L.take<uint8_t>(N);
     p->round = L.take<uint8_t>(N);
@@ -216,7 +238,8 @@ void destroy_graphs(nalar_ctx* c) {
 }
 
 // Greedy partition of whole workflows into K1 blocks, balanced by rows.
-void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* eoff, std::vector<uint32_t>& bw,
+// wf_off[W+1]: first row of each workflow; wf_eoff[W+1]: first edge of each workflow
+void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, std::vector<uint32_t>& bw,
                std::vector<uint32_t>& br, std::vector<uint32_t>& be, std::vector<uint8_t>& bs, size_t* max_smem) {
     const uint32_t W = c->W, N = c->N;
     uint32_t target = std::max<uint32_t>(64u, (N + kSmSplit - 1) / kSmSplit);
@@ -229,7 +252,7 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* eoff, std::
             uint32_t rows = 0;
             while (w < W) {
                 const uint32_t wr = wf_off[w + 1] - wf_off[w];
-                const uint32_t e_if = eoff[wf_off[w + 1]] - eoff[wf_off[ws]];
+                const uint32_t e_if = wf_eoff[w + 1] - wf_eoff[ws];
                 if (w > ws && (k1_block_smem(rows + wr, e_if, w - ws + 1, c->T, true) > kStageBudget ||
                                w - ws + 1 > kMaxWfPerBlock))
                     break;
@@ -238,12 +261,12 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* eoff, std::
                 if (rows >= target) break;
             }
             const uint32_t ra = wf_off[ws], rb = wf_off[w];
-            const size_t need_st = k1_block_smem(rb - ra, eoff[rb] - eoff[ra], w - ws, c->T, true);
+            const size_t need_st = k1_block_smem(rb - ra, wf_eoff[w] - wf_eoff[ws], w - ws, c->T, true);
             const bool staged = need_st <= kStageBudget && !(c->cfg.flags & NALAR_F_FORCE_UNSTAGED);
             mx = std::max(mx, staged ? need_st : k1_block_smem(rb - ra, 0, w - ws, c->T, false));
-            bw.push_back(ws); br.push_back(ra); be.push_back(eoff[ra]); bs.push_back(staged ? 1 : 0);
+            bw.push_back(ws); br.push_back(ra); be.push_back(wf_eoff[ws]); bs.push_back(staged ? 1 : 0);
         }
-        bw.push_back(W); br.push_back(wf_off[W]); be.push_back(eoff[wf_off[W]]);
+        bw.push_back(W); br.push_back(wf_off[W]); be.push_back(wf_eoff[W]);
         if (bw.size() - 1 <= c->Bmax) { *max_smem = mx; return; }
         target *= 2;
     }
@@ -316,7 +339,7 @@ int enqueue_first_half(nalar_ctx* c, int policy) {
 }
 
 int enqueue_collective(nalar_ctx* c) {
-    if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_NCCL) {
+    if (c->cfg.collective == NALAR_COLL_NCCL) {
         // NOTE: the full reservation-sized layout keeps slot offsets identical on all ranks
         const ncclResult_t r = g_nccl.allReduce(c->d_x, c->d_x, x_used_words(c), ncclUint32, ncclSum, c->comm,
                                                 c->stream);
@@ -339,6 +362,55 @@ int enqueue_epoch(nalar_ctx* c, int policy) {
     if (!rc) rc = enqueue_collective(c);
     if (!rc) rc = enqueue_second_half(c);
     return rc;
+}
+
+// K1 block table from the host mirror of the workflow layout; profile buffer
+int set_blocks(nalar_ctx* c) {
+    std::vector<uint32_t> bw, br, be;
+    std::vector<uint8_t> bs;
+    size_t mx = 0;
+    partition(c, c->m_wf_off.data(), c->m_wf_eoff.data(), bw, br, be, bs, &mx);
+    c->B = (uint32_t)bs.size();
+    c->fixed_smem = k1_fixed_smem(c->T, c->I, c->R);
+    c->smem = c->fixed_smem + mx;
+    cudaStream_t st = c->stream;
+    CK(cudaMemcpyAsync(c->d_blk_wf, bw.data(), 4ull * bw.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->d_blk_row0, br.data(), 4ull * br.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->d_blk_edge0, be.data(), 4ull * be.size(), cudaMemcpyHostToDevice, st));
+    if (!bs.empty()) CK(cudaMemcpyAsync(c->d_blk_staged, bs.data(), bs.size(), cudaMemcpyHostToDevice, st));
+    if (c->cfg.flags & NALAR_F_PROFILE) {
+        const size_t need = 2ull * c->W + 8ull * c->B + 4ull * c->R + 3ull * c->W;
+        if (need > c->prof_words) {
+            if (c->d_prof) cudaFree(c->d_prof);
+            c->d_prof = nullptr;
+            CK(cudaMalloc(&c->d_prof, 8 * std::max<size_t>(need, 1)));
+        }
+        c->prof_words = need;
+        CK(cudaMemsetAsync(c->d_prof, 0, 8 * std::max<size_t>(need, 1), st));
+    }
+    // block tables are synchronous host vectors: finish the copies before they die
+    CK(cudaStreamSynchronize(st));
+    return NALAR_OK;
+}
+
+// K0 over the current table; synchronises
+int validate_table(nalar_ctx* c, int64_t* err_row, const char*) {
+    cudaStream_t st = c->stream;
+    CK(cudaMemsetAsync(c->d_err, 0xFF, 8, st));
+    CK(cudaMemsetAsync(c->d_err + 1, 0, 8, st));
+    ValidateParams v{};
+    v.wf_fut_off = c->d_wf_off; v.f_state = c->d_state; v.f_type = c->d_type; v.f_exec = c->d_exec;
+    v.f_pin = c->d_pin; v.f_edge_off = c->d_eoff; v.edges = c->d_edges; v.i_type = c->d_itype;
+    v.n_wf = c->W; v.n_fut = c->N; v.n_edges = c->E; v.n_types = c->T; v.n_inst = c->I; v.err = c->d_err;
+    CK(launch_validate(v, st));
+    CK(cudaMemcpyAsync(c->h_err, c->d_err, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c->h_err[1]) return fail(c, NALAR_E_INVAL, "edge offsets not monotone");
+    if (c->h_err[0] != ~0ull) {
+        if (err_row) *err_row = (int64_t)c->h_err[0];
+        return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
+    }
+    return NALAR_OK;
 }
 
 }  // namespace
@@ -401,6 +473,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->arena_bytes = p.total;
     uint8_t* a = c->arena;
     c->d_wf_off = at<uint32_t>(a, p.wf_off); c->d_wf_prio = at<int32_t>(a, p.wf_prio);
+    c->d_wf_id = at<uint64_t>(a, p.wf_id);
     c->d_state = at<uint8_t>(a, p.state); c->d_type = at<uint8_t>(a, p.type); c->d_round = at<uint8_t>(a, p.round);
     c->d_exec = at<int16_t>(a, p.exec); c->d_pin = at<int16_t>(a, p.pin);
     c->d_eoff = at<uint32_t>(a, p.eoff); c->d_edges = at<uint32_t>(a, p.edges);
@@ -429,7 +502,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         return bail(NALAR_E_NOMEM);
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
-    if (cfg->world > 1 && cfg->collective == NALAR_COLL_NCCL) {
+    if (cfg->collective == NALAR_COLL_NCCL) {   // (world == 1 allowed: a 1-rank comm, for testing)
         if (!g_nccl.load(&c->err)) return bail(NALAR_E_COMM);
         ncclUniqueId id;
         memcpy(id.internal, cfg->nccl_id, 128);
@@ -448,6 +521,8 @@ int nalar_destroy(nalar_ctx* c) {
     if (c->comm) g_nccl.commDestroy(c->comm);
     if (c->own_arena && c->arena) cudaFree(c->arena);
     if (c->d_prof) cudaFree(c->d_prof);
+    if (c->alt.mem) cudaFree(c->alt.mem);
+    if (c->d_stage) cudaFree(c->d_stage);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
     if (c->h_err) cudaFreeHost(c->h_err);
@@ -499,13 +574,12 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     if (N && T == 0) return fail(c, NALAR_E_INVAL, "futures without types");
 
     c->N = N; c->E = E; c->W = W; c->I = I; c->T = T; c->R = I + T;
-    std::vector<uint32_t> bw, br, be;
-    std::vector<uint8_t> bs;
-    size_t mx = 0;
-    partition(c, s->wf_fut_off, s->f_edge_off, bw, br, be, bs, &mx);
-    c->B = (uint32_t)bs.size();
-    c->fixed_smem = k1_fixed_smem(T, I, c->R);
-    c->smem = c->fixed_smem + mx;
+    c->assign_valid = false;
+    // host mirror of the workflow layout (delta mode re-partitions from it)
+    c->m_wf_id.assign(s->wf_id, s->wf_id + W);
+    c->m_wf_off.assign(s->wf_fut_off, s->wf_fut_off + W + 1);
+    c->m_wf_eoff.resize(W + 1);
+    for (uint32_t w = 0; w <= W; ++w) c->m_wf_eoff[w] = s->f_edge_off[s->wf_fut_off[w]];
 
     cudaStream_t st = c->stream;
     auto h2d = [&](void* d, const void* h, size_t bytes) -> cudaError_t {
@@ -513,6 +587,7 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     };
     CK(h2d(c->d_wf_off, s->wf_fut_off, 4ull * (W + 1)));
     CK(h2d(c->d_wf_prio, s->wf_prio, 4ull * W));
+    CK(h2d(c->d_wf_id, s->wf_id, 8ull * W));
     CK(h2d(c->d_state, s->f_state, N));
     CK(h2d(c->d_type, s->f_type, N));
     CK(h2d(c->d_round, s->f_round, N));
@@ -524,10 +599,6 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     CK(h2d(c->d_icap, s->i_cap, 4ull * I));
     CK(h2d(c->d_ibase, s->i_base_load, 4ull * I));
     CK(h2d(c->d_taff, s->t_affinity, T));
-    CK(h2d(c->d_blk_wf, bw.data(), 4ull * bw.size()));
-    CK(h2d(c->d_blk_row0, br.data(), 4ull * br.size()));
-    CK(h2d(c->d_blk_edge0, be.data(), 4ull * be.size()));
-    CK(h2d(c->d_blk_staged, bs.data(), bs.size()));
     // instances grouped by type (ascending id), for the assignment pass
     std::vector<uint32_t> toff(T + 1, 0), tinst(I);
     for (uint32_t i = 0; i < I; ++i) toff[s->i_type[i] + 1]++;
@@ -538,31 +609,199 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     }
     CK(h2d(c->d_type_off, toff.data(), 4ull * (T + 1)));
     CK(h2d(c->d_type_inst, tinst.data(), 4ull * I));
-    CK(cudaMemsetAsync(c->d_err, 0xFF, 8, st));
-    CK(cudaMemsetAsync(c->d_err + 1, 0, 8, st));
-    ValidateParams v{};
-    v.wf_fut_off = c->d_wf_off; v.f_state = c->d_state; v.f_type = c->d_type; v.f_exec = c->d_exec;
-    v.f_pin = c->d_pin; v.f_edge_off = c->d_eoff; v.edges = c->d_edges; v.i_type = c->d_itype;
-    v.n_wf = W; v.n_fut = N; v.n_edges = E; v.n_types = T; v.n_inst = I; v.err = c->d_err;
-    CK(launch_validate(v, st));
+    int rc = set_blocks(c);
+    if (rc) return rc;
+    rc = validate_table(c, err_row, nullptr);
+    if (rc) return rc;
+    c->uploaded = true;
+    return NALAR_OK;
+}
+
+int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
+    if (err_index) *err_index = -1;
+    if (!c || !d) return NALAR_E_INVAL;
+    if (!c->uploaded) return fail(c, NALAR_E_STATE, "delta before upload");
+    const bool apply_asg = d->flags & NALAR_DELTA_APPLY_ASSIGNED;
+    if (apply_asg && !c->assign_valid) return fail(c, NALAR_E_STATE, "APPLY_ASSIGNED without a preceding epoch");
+    if ((d->n_updates && (!d->upd_wf_id || !d->upd_seq || !d->upd_state || !d->upd_executor || !d->upd_pin)) ||
+        (d->n_retired && !d->retired_wf_id) ||
+        (d->n_append && (!d->app_wf_id || !d->app_wf_prio || !d->app_state || !d->app_type || !d->app_round ||
+                         !d->app_executor || !d->app_pin || !d->app_edge_off)) ||
+        (d->n_append_edges && !d->app_edges) || (d->n_prio && (!d->prio_wf_id || !d->prio_value)) ||
+        (d->n_inst && (!d->inst_id || !d->inst_cap || !d->inst_base_load)))
+        return fail(c, NALAR_E_INVAL, "null delta array");
+    const uint32_t W = c->W;
+    // ---- host: the new workflow list (old minus retired, plus appended) ----
+    std::vector<uint8_t> retired(W, 0);
+    for (uint32_t k = 0; k < d->n_retired; ++k) {
+        const auto it = std::lower_bound(c->m_wf_id.begin(), c->m_wf_id.end(), d->retired_wf_id[k]);
+        if (it == c->m_wf_id.end() || *it != d->retired_wf_id[k]) {
+            if (err_index) *err_index = k;
+            return fail(c, NALAR_E_INVAL, "retired workflow id %llu not live", (unsigned long long)d->retired_wf_id[k]);
+        }
+        retired[it - c->m_wf_id.begin()] = 1;
+    }
+    if (d->n_append && (d->app_edge_off[0] != 0 || d->app_edge_off[d->n_append] != d->n_append_edges))
+        return fail(c, NALAR_E_INVAL, "app_edge_off bounds");
+    for (uint32_t j = 0; j < d->n_append; ++j)
+        if (d->app_edge_off[j + 1] < d->app_edge_off[j]) {
+            if (err_index) *err_index = j;
+            return fail(c, NALAR_E_INVAL, "app_edge_off not monotone");
+        }
+    // appended groups: (wf id, first index, count), ids ascending
+    struct Grp { uint64_t id; uint32_t lo, n; };
+    std::vector<Grp> groups;
+    for (uint32_t j = 0; j < d->n_append; ++j) {
+        if (!groups.empty() && groups.back().id == d->app_wf_id[j]) { groups.back().n++; continue; }
+        if (!groups.empty() && d->app_wf_id[j] < groups.back().id) {
+            if (err_index) *err_index = j;
+            return fail(c, NALAR_E_INVAL, "appended futures not grouped by ascending workflow id");
+        }
+        groups.push_back({d->app_wf_id[j], j, 1});
+    }
+    std::vector<RebuildPlan> plan;
+    plan.reserve(W + groups.size());
+    const uint64_t max_live = W ? c->m_wf_id.back() : 0;
+    size_t g = 0;
+    uint32_t row = 0, edge = 0;
+    auto app_edges = [&](const Grp& gr) { return d->app_edge_off[gr.lo + gr.n] - d->app_edge_off[gr.lo]; };
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint64_t id = c->m_wf_id[w];
+        while (g < groups.size() && groups[g].id < id) {   // an id between live ids is not new
+            if (err_index) *err_index = groups[g].lo;
+            return fail(c, NALAR_E_INVAL, "appended workflow id %llu is neither live nor new",
+                        (unsigned long long)groups[g].id);
+        }
+        const bool has_app = g < groups.size() && groups[g].id == id;
+        if (retired[w]) {
+            if (has_app) {
+                if (err_index) *err_index = groups[g].lo;
+                return fail(c, NALAR_E_INVAL, "append to a retired workflow");
+            }
+            continue;
+        }
+        RebuildPlan pl{};
+        pl.wf_id = id; pl.src = w;
+        pl.n_old = c->m_wf_off[w + 1] - c->m_wf_off[w];
+        pl.n_old_edges = c->m_wf_eoff[w + 1] - c->m_wf_eoff[w];
+        pl.app_lo = has_app ? groups[g].lo : 0; pl.app_n = has_app ? groups[g].n : 0;
+        pl.new_row0 = row; pl.new_edge0 = edge;
+        row += pl.n_old + pl.app_n;
+        edge += pl.n_old_edges + (has_app ? app_edges(groups[g]) : 0);
+        if (has_app) ++g;
+        plan.push_back(pl);
+    }
+    for (; g < groups.size(); ++g) {
+        if (groups[g].id <= max_live && W) {
+            if (err_index) *err_index = groups[g].lo;
+            return fail(c, NALAR_E_INVAL, "new workflow id %llu not above the live ids", (unsigned long long)groups[g].id);
+        }
+        RebuildPlan pl{};
+        pl.wf_id = groups[g].id; pl.src = 0xFFFFFFFFu;
+        pl.app_lo = groups[g].lo; pl.app_n = groups[g].n;
+        pl.prio = d->app_wf_prio[groups[g].lo];
+        pl.new_row0 = row; pl.new_edge0 = edge;
+        row += pl.app_n;
+        edge += app_edges(groups[g]);
+        plan.push_back(pl);
+    }
+    const uint32_t W2 = (uint32_t)plan.size(), N2 = row, E2 = edge;
+    if (N2 > c->cfg.max_futures || E2 > c->cfg.max_edges || W2 > c->cfg.max_workflows)
+        return fail(c, NALAR_E_NOMEM, "delta outgrows the reservation");
+    // ---- device: second buffer set, staging ----------------------------------
+    if (!c->alt.mem) {
+        Layout L;
+        const size_t N = c->cfg.max_futures, E = c->cfg.max_edges, Wm = c->cfg.max_workflows;
+        const size_t o_wo = L.take<uint32_t>(Wm + 1), o_wp = L.take<int32_t>(Wm), o_wi = L.take<uint64_t>(Wm);
+        const size_t o_st = L.take<uint8_t>(N), o_ty = L.take<uint8_t>(N), o_rd = L.take<uint8_t>(N);
+        const size_t o_ex = L.take<int16_t>(N), o_pn = L.take<int16_t>(N), o_eo = L.take<uint32_t>(N + 1);
+        const size_t o_ed = L.take<uint32_t>(E);
+        if (cudaMalloc(&c->alt.mem, L.off + 256) != cudaSuccess) { c->alt.mem = nullptr; return fail(c, NALAR_E_NOMEM, "delta buffers"); }
+        uint8_t* m = (uint8_t*)c->alt.mem;
+        c->alt.wf_off = at<uint32_t>(m, o_wo); c->alt.wf_prio = at<int32_t>(m, o_wp); c->alt.wf_id = at<uint64_t>(m, o_wi);
+        c->alt.state = at<uint8_t>(m, o_st); c->alt.type = at<uint8_t>(m, o_ty); c->alt.round = at<uint8_t>(m, o_rd);
+        c->alt.exec = at<int16_t>(m, o_ex); c->alt.pin = at<int16_t>(m, o_pn); c->alt.eoff = at<uint32_t>(m, o_eo);
+        c->alt.edges = at<uint32_t>(m, o_ed);
+    }
+    Layout S;
+    const uint32_t nu = d->n_updates, na = d->n_append, nae = d->n_append_edges, np = d->n_prio, ni = d->n_inst;
+    const size_t s_uid = S.take<uint64_t>(nu), s_useq = S.take<uint32_t>(nu), s_ust = S.take<uint8_t>(nu);
+    const size_t s_uex = S.take<int16_t>(nu), s_upn = S.take<int16_t>(nu);
+    const size_t s_plan = S.take<RebuildPlan>(W2);
+    const size_t s_ast = S.take<uint8_t>(na), s_aty = S.take<uint8_t>(na), s_ard = S.take<uint8_t>(na);
+    const size_t s_aex = S.take<int16_t>(na), s_apn = S.take<int16_t>(na), s_aeo = S.take<uint32_t>(na + 1);
+    const size_t s_aed = S.take<uint32_t>(nae);
+    const size_t s_pid = S.take<uint64_t>(np), s_pvl = S.take<int32_t>(np);
+    const size_t s_iid = S.take<uint32_t>(ni), s_icp = S.take<uint32_t>(ni), s_ibl = S.take<uint32_t>(ni);
+    if (S.off > c->stage_bytes) {
+        if (c->d_stage) cudaFree(c->d_stage);
+        c->d_stage = nullptr;
+        c->stage_bytes = 0;
+        if (cudaMalloc(&c->d_stage, 2 * S.off + 4096) != cudaSuccess) return fail(c, NALAR_E_NOMEM, "delta staging");
+        c->stage_bytes = 2 * S.off + 4096;
+    }
+    uint8_t* sb = (uint8_t*)c->d_stage;
+    cudaStream_t st = c->stream;
+    auto h2d = [&](size_t off, const void* h, size_t bytes) -> cudaError_t {
+        return bytes ? cudaMemcpyAsync(sb + off, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    };
+    CK(h2d(s_uid, d->upd_wf_id, 8ull * nu)); CK(h2d(s_useq, d->upd_seq, 4ull * nu));
+    CK(h2d(s_ust, d->upd_state, nu)); CK(h2d(s_uex, d->upd_executor, 2ull * nu)); CK(h2d(s_upn, d->upd_pin, 2ull * nu));
+    CK(h2d(s_plan, plan.data(), sizeof(RebuildPlan) * W2));
+    CK(h2d(s_ast, d->app_state, na)); CK(h2d(s_aty, d->app_type, na)); CK(h2d(s_ard, d->app_round, na));
+    CK(h2d(s_aex, d->app_executor, 2ull * na)); CK(h2d(s_apn, d->app_pin, 2ull * na));
+    if (na) { CK(h2d(s_aeo, d->app_edge_off, 4ull * (na + 1))); } else { static const uint32_t z = 0; CK(h2d(s_aeo, &z, 4)); }
+    CK(h2d(s_aed, d->app_edges, 4ull * nae));
+    CK(h2d(s_pid, d->prio_wf_id, 8ull * np)); CK(h2d(s_pvl, d->prio_value, 4ull * np));
+    CK(h2d(s_iid, d->inst_id, 4ull * ni)); CK(h2d(s_icp, d->inst_cap, 4ull * ni)); CK(h2d(s_ibl, d->inst_base_load, 4ull * ni));
+    CK(cudaMemsetAsync(c->d_err, 0xFF, 16, st));
+    DeltaParams p{};
+    p.wf_off = c->d_wf_off; p.wf_prio = c->d_wf_prio; p.wf_id = c->d_wf_id;
+    p.state = c->d_state; p.type = c->d_type; p.round = c->d_round; p.exec = c->d_exec; p.pin = c->d_pin;
+    p.eoff = c->d_eoff; p.edges = c->d_edges; p.n_wf = W;
+    p.tot_loc = c->d_scr + C_NUM + c->Rmax; p.n_adm = c->d_scr + C_NUM; p.arow = c->d_arow; p.ainst = c->d_ainst;
+    p.n_upd = nu; p.upd_wf_id = at<uint64_t>(sb, s_uid); p.upd_seq = at<uint32_t>(sb, s_useq);
+    p.upd_state = at<uint8_t>(sb, s_ust); p.upd_exec = at<int16_t>(sb, s_uex); p.upd_pin = at<int16_t>(sb, s_upn);
+    p.n_wf_new = W2; p.plan = at<RebuildPlan>(sb, s_plan);
+    p.n_wf_off = c->alt.wf_off; p.n_wf_prio = c->alt.wf_prio; p.n_wf_id = c->alt.wf_id;
+    p.n_state = c->alt.state; p.n_type = c->alt.type; p.n_round = c->alt.round; p.n_exec = c->alt.exec;
+    p.n_pin = c->alt.pin; p.n_eoff = c->alt.eoff; p.n_edges = c->alt.edges;
+    p.app_state = at<uint8_t>(sb, s_ast); p.app_type = at<uint8_t>(sb, s_aty); p.app_round = at<uint8_t>(sb, s_ard);
+    p.app_exec = at<int16_t>(sb, s_aex); p.app_pin = at<int16_t>(sb, s_apn); p.app_eoff = at<uint32_t>(sb, s_aeo);
+    p.app_edges = at<uint32_t>(sb, s_aed);
+    p.n_prio = np; p.prio_wf_id = at<uint64_t>(sb, s_pid); p.prio_value = at<int32_t>(sb, s_pvl);
+    p.n_inst_upd = ni; p.n_inst = c->I; p.inst_id = at<uint32_t>(sb, s_iid); p.inst_cap = at<uint32_t>(sb, s_icp);
+    p.inst_base = at<uint32_t>(sb, s_ibl); p.i_cap = c->d_icap; p.i_base = c->d_ibase;
+    p.err = c->d_err;
+    CK(launch_delta(p, apply_asg, c->R, st));
+    // tails of the new offset arrays
+    const uint32_t tails[2] = {N2, E2};
+    CK(cudaMemcpyAsync(c->alt.wf_off + W2, &tails[0], 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->alt.eoff + N2, &tails[1], 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(c->h_err, c->d_err, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (c->h_err[1]) return fail(c, NALAR_E_INVAL, "edge offsets not monotone");
-    if (c->h_err[0] != ~0ull) {
-        if (err_row) *err_row = (int64_t)c->h_err[0];
-        return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
+    c->assign_valid = false;
+    if (c->h_err[0] != ~0ull || c->h_err[1] != ~0ull) {
+        c->uploaded = false;          // the table was partly updated in place
+        const unsigned long long bad = c->h_err[0] != ~0ull ? c->h_err[0] : c->h_err[1];
+        if (err_index) *err_index = (int64_t)bad;
+        return fail(c, NALAR_E_INVAL, "delta update %llu names no live future / workflow / instance", bad);
     }
-    if (k.flags & NALAR_F_PROFILE) {
-        const size_t need = 2ull * W + 8ull * c->B + 4ull * c->R + 3ull * W;
-        if (need > c->prof_words) {
-            if (c->d_prof) cudaFree(c->d_prof);
-            c->d_prof = nullptr;
-            CK(cudaMalloc(&c->d_prof, 8 * std::max<size_t>(need, 1)));
-        }
-        c->prof_words = need;
-        CK(cudaMemset(c->d_prof, 0, 8 * std::max<size_t>(need, 1)));
-    }
-    c->uploaded = true;
+    // ---- swap in the new table, re-partition, validate ------------------------
+    std::swap(c->d_wf_off, c->alt.wf_off); std::swap(c->d_wf_prio, c->alt.wf_prio); std::swap(c->d_wf_id, c->alt.wf_id);
+    std::swap(c->d_state, c->alt.state); std::swap(c->d_type, c->alt.type); std::swap(c->d_round, c->alt.round);
+    std::swap(c->d_exec, c->alt.exec); std::swap(c->d_pin, c->alt.pin); std::swap(c->d_eoff, c->alt.eoff);
+    std::swap(c->d_edges, c->alt.edges);
+    std::vector<uint64_t> nid(W2);
+    std::vector<uint32_t> noff(W2 + 1), neoff(W2 + 1);
+    for (uint32_t w = 0; w < W2; ++w) { nid[w] = plan[w].wf_id; noff[w] = plan[w].new_row0; neoff[w] = plan[w].new_edge0; }
+    noff[W2] = N2; neoff[W2] = E2;
+    c->m_wf_id.swap(nid); c->m_wf_off.swap(noff); c->m_wf_eoff.swap(neoff);
+    c->N = N2; c->E = E2; c->W = W2;
+    int rc = set_blocks(c);
+    if (!rc) rc = validate_table(c, err_index, nullptr);
+    if (rc) { c->uploaded = false; return rc; }
+    c->epoch_done = false;
     return NALAR_OK;
 }
 
@@ -573,10 +812,15 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
     if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
         return fail(c, NALAR_E_STATE, "external collective: use nalar_epoch_begin/finish");
     int rc;
-    if (c->cfg.flags & NALAR_F_NO_GRAPH) {
+    Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->smem, c->d_state};
+    // a graph pays off only for a shape that repeats (not after every delta)
+    const bool repeat = c->last_key_set && c->last_key == key;
+    const bool cached = c->gexec[policy] && c->gkey[policy] == key;
+    c->last_key = key;
+    c->last_key_set = true;
+    if ((c->cfg.flags & NALAR_F_NO_GRAPH) || (!repeat && !cached)) {
         rc = enqueue_epoch(c, policy);
     } else {
-        Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->smem};
         cudaGraphExec_t& ge = c->gexec[policy];
         if (!ge || !(c->gkey[policy] == key)) {
             if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
@@ -594,7 +838,7 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
         CK(cudaGraphLaunch(ge, c->stream));
         rc = NALAR_OK;
     }
-    if (!rc) { c->epoch_done = true; c->last_policy = policy; }
+    if (!rc) { c->epoch_done = true; c->last_policy = policy; c->assign_valid = true; }
     return rc;
 }
 
@@ -619,7 +863,7 @@ int nalar_epoch_finish(nalar_ctx* c) {
     if (!c->in_epoch) return fail(c, NALAR_E_STATE, "finish without begin");
     c->in_epoch = false;
     int rc = enqueue_second_half(c);
-    if (!rc) c->epoch_done = true;
+    if (!rc) { c->epoch_done = true; c->assign_valid = true; }
     return rc;
 }
 

@@ -29,7 +29,9 @@ WF_AGG_FIELDS = ("total", "pending", "ready", "inflight", "resolved", "failed", 
 EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id", "nalar_create",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
-           "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile")
+           "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile",
+           "nalar_delta_apply")
+NALAR_DELTA_APPLY_ASSIGNED = 1
 
 
 class nalar_config(C.Structure):
@@ -63,6 +65,20 @@ class nalar_decisions(C.Structure):
                 ("n_assigned", C.c_uint32)]
 
 
+class nalar_delta(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("n_updates", C.c_uint32),
+                ("upd_wf_id", C.c_void_p), ("upd_seq", C.c_void_p), ("upd_state", C.c_void_p),
+                ("upd_executor", C.c_void_p), ("upd_pin", C.c_void_p),
+                ("n_retired", C.c_uint32), ("retired_wf_id", C.c_void_p),
+                ("n_append", C.c_uint32), ("n_append_edges", C.c_uint32),
+                ("app_wf_id", C.c_void_p), ("app_wf_prio", C.c_void_p), ("app_state", C.c_void_p),
+                ("app_type", C.c_void_p), ("app_round", C.c_void_p), ("app_executor", C.c_void_p),
+                ("app_pin", C.c_void_p), ("app_edge_off", C.c_void_p), ("app_edges", C.c_void_p),
+                ("n_prio", C.c_uint32), ("prio_wf_id", C.c_void_p), ("prio_value", C.c_void_p),
+                ("n_inst", C.c_uint32), ("inst_id", C.c_void_p), ("inst_cap", C.c_void_p),
+                ("inst_base_load", C.c_void_p)]
+
+
 class nalar_epoch_stats(C.Structure):
     _fields_ = [("epoch_us", C.c_float), ("k1_us", C.c_float), ("coll_us", C.c_float),
                 ("k4_us", C.c_float), ("n_futures", C.c_uint32), ("n_ready", C.c_uint32),
@@ -91,6 +107,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_epoch_stats_get.argtypes = [C.c_void_p, P(nalar_epoch_stats)]
     lib.nalar_debug_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]
     lib.nalar_debug_profile.restype = C.c_int
+    lib.nalar_delta_apply.argtypes = [C.c_void_p, P(nalar_delta), P(C.c_int64)]
+    lib.nalar_delta_apply.restype = C.c_int
     lib.nalar_stream.argtypes = [C.c_void_p]
     lib.nalar_stream.restype = C.c_void_p
     lib.nalar_last_error.argtypes = [C.c_void_p]
@@ -212,6 +230,37 @@ def nalar_debug_profile(h) -> np.ndarray:
     return buf[:n.value]
 
 
+_DELTA_ARRAYS = {"upd_wf_id": np.uint64, "upd_seq": np.uint32, "upd_state": np.uint8,
+                 "upd_executor": np.int16, "upd_pin": np.int16, "retired_wf_id": np.uint64,
+                 "app_wf_id": np.uint64, "app_wf_prio": np.int32, "app_state": np.uint8,
+                 "app_type": np.uint8, "app_round": np.uint8, "app_executor": np.int16,
+                 "app_pin": np.int16, "app_edge_off": np.uint32, "app_edges": np.uint32,
+                 "prio_wf_id": np.uint64, "prio_value": np.int32, "inst_id": np.uint32,
+                 "inst_cap": np.uint32, "inst_base_load": np.uint32}
+
+
+def delta_struct(dl) -> tuple:
+    """nalar_delta over a nalar_gen.Delta-like object (numpy arrays)."""
+    keep = {k: np.ascontiguousarray(getattr(dl, k), dtype=dt) for k, dt in _DELTA_ARRAYS.items()}
+    d = nalar_delta()
+    d.flags = int(dl.flags)
+    d.n_updates = len(keep["upd_seq"])
+    d.n_retired = len(keep["retired_wf_id"])
+    d.n_append = len(keep["app_wf_id"])
+    d.n_append_edges = len(keep["app_edges"])
+    d.n_prio = len(keep["prio_wf_id"])
+    d.n_inst = len(keep["inst_id"])
+    for k, a in keep.items():
+        setattr(d, k, _ptr(a))
+    return d, keep
+
+
+def nalar_delta_apply(h, d: nalar_delta) -> tuple[int, int]:
+    err = C.c_int64(-1)
+    rc = _lib.nalar_delta_apply(h, C.byref(d), C.byref(err))
+    return rc, err.value
+
+
 def nalar_stream(h) -> int:
     return _lib.nalar_stream(h) or 0
 
@@ -270,6 +319,17 @@ class Context:
             e.err_row = row
             raise e
         self.n = (s.n_futures, s.n_workflows, s.n_instances)
+
+    def apply_delta(self, dl) -> None:
+        d, keep = delta_struct(dl)
+        rc, idx = nalar_delta_apply(self.h, d)
+        if rc:
+            e = NalarError(rc, f"delta_apply: {nalar_last_error(self.h)}")
+            e.err_index = idx
+            raise e
+        # sizes for fetch: the library tracks them; mirror N / W here
+        self.n = (int(getattr(dl, "n_futures_after", self.n[0])),
+                  int(getattr(dl, "n_workflows_after", self.n[1])), self.n[2])
 
     def epoch(self, policy="srtf") -> None:
         pol = POLICIES[policy] if isinstance(policy, str) else int(policy)

@@ -242,3 +242,19 @@ def test_sharded_equals_single(G, which):
         m = (o["assign_row"] >= r0) & (o["assign_row"] < r1)
         assert np.array_equal(g["assign_row"].astype(np.int64), o["assign_row"][m].astype(np.int64) - r0)
         assert np.array_equal(g["assign_inst"], o["assign_inst"][m])
+
+
+def test_nccl_collective_in_graph_single_rank():
+    """The library-owned NCCL communicator and the in-graph allreduce of the
+    exchange buffer (world = 1: a one-rank communicator; the sum is the identity)."""
+    nalar = _nalar()
+    uid = nalar.nalar_nccl_unique_id()
+    for s in (c2(3), c4(1)):
+        ctx = nalar.Context.for_snapshot(s, world=1, rank=0, collective=nalar.NALAR_COLL_NCCL,
+                                         nccl_id=uid, flags=nalar.NALAR_F_TIMING)
+        ctx.upload(s)
+        for _ in range(3):                      # graph captured on the repeat, then replayed
+            ctx.epoch("srtf")
+        assert_same(s, oracle_epoch(s, "srtf"), ctx.fetch(), "nccl")
+        assert ctx.stats().coll_us > 0
+        ctx.close()
