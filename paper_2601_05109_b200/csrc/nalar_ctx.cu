@@ -327,14 +327,23 @@ size_t x_used_words(nalar_ctx* c) {
     return (size_t)G * c->R * c->Lv + c->I + c->R;
 }
 
+// an event inside a captured graph must be an external event-record node
+cudaError_t record_ev(nalar_ctx* c, int k) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(c->stream, &cs);
+    if (e != cudaSuccess) return e;
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(c->ev[k], c->stream, cudaEventRecordExternal)
+                                               : cudaEventRecord(c->ev[k], c->stream);
+}
+
 int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
     // clear exchange buffer (used part) + counters + adm_pub; contiguous region
     CK(cudaMemsetAsync(c->d_x, 0, c->x_words * 4 + (C_NUM + 2 * (size_t)c->Rmax) * 4, c->stream));
-    if (timing) CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
+    if (timing) CK(record_ev(c, 0));
     int rc = run_k1(c, policy);
     if (rc) return rc;
-    if (timing) CK(cudaEventRecordWithFlags(c->ev[1], c->stream, cudaEventRecordExternal));
+    if (timing) CK(record_ev(c, 1));
     return NALAR_OK;
 }
 
@@ -350,10 +359,10 @@ int enqueue_collective(nalar_ctx* c) {
 
 int enqueue_second_half(nalar_ctx* c) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
-    if (timing) CK(cudaEventRecordWithFlags(c->ev[2], c->stream, cudaEventRecordExternal));
+    if (timing) CK(record_ev(c, 2));
     int rc = run_k4(c);
     if (rc) return rc;
-    if (timing) CK(cudaEventRecordWithFlags(c->ev[3], c->stream, cudaEventRecordExternal));
+    if (timing) CK(record_ev(c, 3));
     return NALAR_OK;
 }
 
