@@ -159,6 +159,41 @@ def load_traffic(kernel):
         return None
 
 
+def c3_dynamic(nalar, device, epochs, warm=450, seed=1):
+    """BASELINE config 3: the router workflow at 80 RPS (nalar_gen.dynamic), one
+    epoch every 100 ms of simulated time.  Per epoch through the public API:
+    the epoch, the fetch of the decisions the simulator needs, and the delta
+    (apply-assigned, updates, retirements, appends) applied on the device.
+    The simulator's own Python step is excluded from the timed region."""
+    from nalar_gen import RouterSim
+    sim = RouterSim(seed)
+    sim.warmup(warm)
+    s = sim.snapshot()
+    ctx = nalar.Context(200000, 400000, 20000, 32, 4, device=device)
+    ctx.upload(s)
+    lat, live, app, upd, ret = [], [], [], [], []
+    for k in range(epochs):
+        t0 = time.perf_counter()
+        ctx.epoch("srtf")
+        r = ctx.fetch(("new_pin", "assign"))
+        t1 = time.perf_counter()
+        d = sim.step(r["assign_row"], r["assign_inst"], r["new_pin"])
+        t2 = time.perf_counter()
+        ctx.apply_delta(d)
+        t3 = time.perf_counter()
+        lat.append((t1 - t0) + (t3 - t2))
+        live.append(d.n_futures_after); app.append(len(d.app_wf_id))
+        upd.append(len(d.upd_seq)); ret.append(len(d.retired_wf_id))
+    ctx.close()
+    ms = [x * 1e3 for x in lat]
+    return {"workload": "C3 router workflow, 80 RPS Poisson arrivals, 100 ms epochs, dynamic control flow",
+            "epochs": epochs, "live_futures_mean": float(np.mean(live)),
+            "appended_per_epoch": float(np.mean(app)), "updates_per_epoch": float(np.mean(upd)),
+            "retired_workflows_per_epoch": float(np.mean(ret)),
+            "epoch_fetch_delta_ms_p50": nearest_rank(ms, 50), "epoch_fetch_delta_ms_p99": nearest_rank(ms, 99),
+            "futures_per_s": float(np.mean(live)) / (nearest_rank(ms, 50) / 1e3)}
+
+
 def run_reference(args, world, rank):
     """--impl reference: the oracle (this tier's reference arm) on host cores."""
     if rank != 0:
@@ -195,6 +230,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--c3-epochs", type=int, default=60)
     args = ap.parse_args()
     world, rank, local = dist_env()
     if world == 1:
@@ -203,6 +239,7 @@ def main():
         run_reference(args, world, rank)
         return
 
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")       # one node: bootstrap over loopback
     import torch
     import torch.distributed as dist
     from paper_2601_05109_b200 import nalar
@@ -350,6 +387,8 @@ def main():
             "clocks": clk.summary(),
             "paper_context": "464 ms per global-control-loop at 131K futures, Python+gRPC+Redis on "
                              "64 emulated CPU nodes (PAPER.md:715); context, not the target"}
+    if rank == 0 and world == 1 and args.c3_epochs:
+        line["c3_dynamic"] = c3_dynamic(nalar, local, args.c3_epochs)
     if rank == 0 and world == 1:
         from oracle import build_oracle
         build_oracle()

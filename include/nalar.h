@@ -277,6 +277,7 @@ int nalar_debug_profile(nalar_ctx* ctx, uint64_t* host, size_t cap_words, size_t
 /* Device stream the ctx runs on (cudaStream_t). */
 void* nalar_stream(nalar_ctx* ctx);
 
+/* ctx == NULL: why the calling thread's last nalar_create failed. */
 const char* nalar_last_error(const nalar_ctx* ctx);
 int nalar_abi_version(void);
 

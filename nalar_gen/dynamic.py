@@ -249,6 +249,7 @@ class RouterSim:
         self._new_rows.clear()
         self._changed.clear()
         self._retire.clear()
+        self.refresh_keys()
 
     def step(self, assign_row, assign_inst, new_pin) -> Delta:
         """Push one epoch's decisions (rows of the CURRENT snapshot), advance one
@@ -301,4 +302,9 @@ class RouterSim:
         self._retire.clear()
         d.n_futures_after = self.n_live
         d.n_workflows_after = len(self.wfs)
+        self.refresh_keys()
         return d
+
+    def refresh_keys(self) -> None:
+        """(workflow id, seq) of every row of the current table, in row order."""
+        self.row_key = [(wid, j) for wid in sorted(self.wfs) for j in range(len(self.wfs[wid].rows))]

@@ -50,6 +50,7 @@ struct NcclApi {
     }
 };
 NcclApi g_nccl;
+thread_local std::string g_create_err;   // nalar_last_error(NULL) after a failed nalar_create
 
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
@@ -449,6 +450,7 @@ int nalar_nccl_unique_id(unsigned char out[128]) {
 int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     if (!out || !cfg) return NALAR_E_INVAL;
     *out = nullptr;
+    g_create_err.clear();
     nalar_ctx* c = new (std::nothrow) nalar_ctx();
     if (!c) return NALAR_E_NOMEM;
     c->cfg = *cfg;
@@ -512,10 +514,15 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
     if (cfg->collective == NALAR_COLL_NCCL) {   // (world == 1 allowed: a 1-rank comm, for testing)
-        if (!g_nccl.load(&c->err)) return bail(NALAR_E_COMM);
+        if (!g_nccl.load(&c->err)) { g_create_err = c->err; return bail(NALAR_E_COMM); }
         ncclUniqueId id;
         memcpy(id.internal, cfg->nccl_id, 128);
-        if (g_nccl.commInitRank(&c->comm, cfg->world, id, cfg->rank) != ncclSuccess) return bail(NALAR_E_COMM);
+        const ncclResult_t r = g_nccl.commInitRank(&c->comm, cfg->world, id, cfg->rank);
+        if (r != ncclSuccess) {
+            g_create_err = std::string("ncclCommInitRank: ") + g_nccl.getErrorString(r);
+            c->comm = nullptr;
+            return bail(NALAR_E_COMM);
+        }
     }
     *out = c;
     return NALAR_OK;
@@ -553,7 +560,7 @@ int nalar_debug_profile(nalar_ctx* c, uint64_t* host, size_t cap, size_t* n_word
 
 void* nalar_stream(nalar_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
-const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row) {
     if (err_row) *err_row = -1;

@@ -158,7 +158,9 @@ def nalar_create(cfg: nalar_config) -> C.c_void_p:
     h = C.c_void_p()
     rc = _lib.nalar_create(C.byref(h), C.byref(cfg))
     if rc:
-        raise NalarError(rc, "nalar_create failed (no sm_100 device, bad limits or NCCL init)")
+        why = (_lib.nalar_last_error(None) or b"").decode()
+        raise NalarError(rc, "nalar_create failed (no sm_100 device, bad limits or NCCL init)"
+                         + (f": {why}" if why else ""))
     return h
 
 

@@ -247,6 +247,8 @@ def test_sharded_equals_single(G, which):
 def test_nccl_collective_in_graph_single_rank():
     """The library-owned NCCL communicator and the in-graph allreduce of the
     exchange buffer (world = 1: a one-rank communicator; the sum is the identity)."""
+    import os
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")      # single-node bootstrap over loopback
     nalar = _nalar()
     uid = nalar.nalar_nccl_unique_id()
     for s in (c2(3), c4(1)):
