@@ -27,6 +27,7 @@ struct NcclApi {
     void* h = nullptr;
     ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
@@ -39,10 +40,11 @@ struct NcclApi {
         if (!h) { *err = std::string("dlopen libnccl failed: ") + dlerror(); return false; }
         getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
         commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        commInitAll = (decltype(commInitAll))dlsym(h, "ncclCommInitAll");
         allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
         commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
         getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
-        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !getErrorString) {
+        if (!getUniqueId || !commInitRank || !commInitAll || !allReduce || !commDestroy || !getErrorString) {
             *err = "libnccl: missing symbols";
             return false;
         }
@@ -517,7 +519,9 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         if (!g_nccl.load(&c->err)) { g_create_err = c->err; return bail(NALAR_E_COMM); }
         ncclUniqueId id;
         memcpy(id.internal, cfg->nccl_id, 128);
-        const ncclResult_t r = g_nccl.commInitRank(&c->comm, cfg->world, id, cfg->rank);
+        // one rank needs no bootstrap: a single-device communicator
+        const ncclResult_t r = cfg->world == 1 ? g_nccl.commInitAll(&c->comm, 1, &cfg->device)
+                                               : g_nccl.commInitRank(&c->comm, cfg->world, id, cfg->rank);
         if (r != ncclSuccess) {
             g_create_err = std::string("ncclCommInitRank: ") + g_nccl.getErrorString(r);
             c->comm = nullptr;
