@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     const uint32_t r = blockIdx.x;
+    // launched as a programmatic dependent of the sweep (PDL): everything
+    // below reads the sweep's results, so wait for its completion here
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     unsigned long long* prof = p.prof ? p.prof + (size_t)r * 4 : nullptr;
     if (prof && tid == 0) prof[0] = gtimer();
     const bool is_type = r >= I;
@@ -373,8 +376,17 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
 
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
     if (p.R == 0) return cudaSuccess;
-    k4_assign<<<p.R, kK4Threads, 0, s>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.R);
+    cfg.blockDim = dim3(kK4Threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k4_assign, p);
 }
 
 }  // namespace nalar

@@ -119,6 +119,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const bool staged = p.blk_staged[b] != 0;
     unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;
     if (bprof && tid == 0) bprof[3] = gtimer();
+    // let the assignment kernel launch now (PDL); it waits for this grid's
+    // completion before reading anything the sweep writes
+    asm volatile("griddepcontrol.launch_dependents;");
 
     // ---- carve the fixed part --------------------------------------------
     uint8_t* sp = smem;
