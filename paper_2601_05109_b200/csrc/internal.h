@@ -146,6 +146,7 @@ struct DeltaParams {
 
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);
 cudaError_t launch_delta(const DeltaParams& p, bool apply_assigned, uint32_t R, cudaStream_t s);
+cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s);
 cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 

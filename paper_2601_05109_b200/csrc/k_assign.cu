@@ -106,36 +106,45 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     const uint32_t r = blockIdx.x;
-    // launched as a programmatic dependent of the sweep (PDL): everything
-    // below reads the sweep's results, so wait for its completion here
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     unsigned long long* prof = p.prof ? p.prof + (size_t)r * 4 : nullptr;
     if (prof && tid == 0) prof[0] = gtimer();
     const bool is_type = r >= I;
+    // ---- static data first: this kernel is a programmatic dependent of the
+    // sweep (PDL) and runs this part while the sweep is still working --------
     const uint32_t t = is_type ? r - I : p.i_type[r];
-
-    // ---- instances of type t: load, spare, phase-A admissions (all ranks) ----
-    // (per-type instance lists in ascending id are built on the host at upload)
-    uint32_t ni = 0;
+    uint32_t ni = 0, k0 = 0;
     if (is_type) {
-        const uint32_t k0 = p.type_off[t];
+        k0 = p.type_off[t];
         ni = p.type_off[t + 1] - k0;
         for (uint32_t k = tid; k < ni; k += kK4Threads) {
             const uint32_t i = p.type_inst[k0 + k];
-            const uint64_t load = (uint64_t)p.i_base[i] + p.load_sum[i];
-            const uint64_t cap = p.i_cap[i];
+            s_inst[k] = i;
+            s_spare[k] = p.i_cap[i];          // capacity for now
+            s_sp2[k] = p.i_base[i];           // base load for now
+        }
+    }
+    const uint32_t cap_r = is_type ? 0u : p.i_cap[r], base_r = is_type ? 0u : p.i_base[r];
+    const uint8_t aff = is_type ? p.t_aff[t] : 0;
+    const uint32_t blk0 = tid < B ? p.blk_row0[tid] : 0u;
+    // everything below reads the sweep's results
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    // ---- instances of type t: load, spare, phase-A admissions (all ranks) ----
+    if (is_type) {
+        for (uint32_t k = tid; k < ni; k += kK4Threads) {
+            const uint32_t i = s_inst[k];
+            const uint64_t load = (uint64_t)s_sp2[k] + p.load_sum[i];
+            const uint64_t cap = s_spare[k];
             const uint32_t spare = (uint32_t)(cap > load ? cap - load : 0ull);
             const uint32_t ha = p.tot[i];
-            s_inst[k] = i;
             s_spare[k] = spare;
             s_sp2[k] = spare - (ha < spare ? ha : spare);
             p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
             p.i_spare[i] = spare;
         }
     } else if (tid == 0) {
-        const uint64_t load = (uint64_t)p.i_base[r] + p.load_sum[r];
-        const uint64_t cap = p.i_cap[r];
-        s_bound = cap > load ? cap - load : 0ull;
+        const uint64_t load = (uint64_t)base_r + p.load_sum[r];
+        s_bound = cap_r > load ? cap_r - load : 0ull;
     }
     // offset of this resource's region of the assignment list
     uint32_t base_part = 0;
@@ -267,7 +276,6 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
 
     // ---- walk this rank's futures of r in row order --------------------------
     // pass 1 compacts the live ones (level not yet full), pass 2 ranks them
-    const uint8_t aff = is_type ? p.t_aff[t] : 0;
     uint32_t found = 0;
     for (uint32_t b0 = 0; b0 < B && found < n_adm; b0 += kK4Threads) {
         // prefix of per-K1-block counts and item bases for blocks [b0, b0 + 256)
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         uint32_t c = 0;
         if (bb < B) {
             c = p.cnt_rb[(size_t)r * B + bb];
-            s_base[tid] = p.blk_row0[bb] + p.off_rb[(size_t)r * B + bb];
+            s_base[tid] = (b0 == 0 ? blk0 : p.blk_row0[bb]) + p.off_rb[(size_t)r * B + bb];
         }
         uint32_t incl = c;
 #pragma unroll

@@ -25,6 +25,8 @@
 // in row order -- a stable counting sort whose positions come from scans, never
 // from atomics -- and adds them to the (resource, level) histogram that the
 // assignment pass (and, for G > 1, the allreduce) consumes.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace nalar {
@@ -250,156 +252,113 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         uint32_t m_dep = 0, m_rnd = 0;
         long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = p.prof ? clock64() : 0;
 
-        // 64 rows per step: lane owns rows c0 + 2*lane and c0 + 2*lane + 1, so
-        // a row whose predecessor is the row just before it in the same lane
-        // settles in the same round (chains of consecutive rows advance up to
-        // two levels per shuffle round)
-        for (uint32_t c0 = fa; c0 < fb; c0 += 64) {
+        for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
             if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
-            const uint32_t fr0 = c0 + 2 * lane, fr1 = fr0 + 1;
-            const bool v0 = fr0 < fb, v1 = fr1 < fb;
-            const uint32_t st0 = v0 ? st[fr0] : 3u, st1 = v1 ? st[fr1] : 3u;
+            const uint32_t f = c0 + lane;
+            const bool valid = f < fb;
+            const uint32_t stf = valid ? st[f] : 3u;
+            const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
             // predecessors before this step are final in smem; those inside the
-            // step are kept as up to 3 slots per row (local index k in [0, 64):
-            // lane k >> 1, row k & 1), extra ones in a 64-bit mask
-            uint32_t d0 = 0, d1 = 0, np0 = 0, np1 = 0;
-            uint32_t a0 = 0, a1 = 0, a2 = 0, b0 = 0, b1 = 0, b2 = 0;   // slots of row 0 / row 1
-            uint64_t nd_0 = 0, nd_1 = 0, ex0 = 0, ex1 = 0;               // DEP masks, extras
-            bool dm0 = false, dm1 = false, ar0 = true, ar1 = true, in1 = false;
-            auto edges_of = [&](uint32_t f, bool valid, uint32_t self_k, uint32_t& d, uint32_t& np,
-                                uint32_t& q0, uint32_t& q1, uint32_t& q2, uint64_t& need_dep, uint64_t& ex,
-                                bool& dm, bool& allres, bool* in_lane) {
-                const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
-                auto take = [&](uint32_t v, uint32_t ds, uint32_t fs, uint32_t ss) {
-                    const uint32_t s = (v & 0x7FFFFFFFu) - r0;
-                    const bool dep_edge = (v >> 31) == 0u;
-                    const bool in = s >= c0;
-                    allres &= !dep_edge || ss == 3u;             // CALL edges never gate (Q2)
-                    dm |= dep_edge && ss == 4u;
-                    const uint32_t k = (s - c0) & 63u;
-                    need_dep |= (in && dep_edge) ? (1ull << k) : 0ull;
-                    const bool own = in && in_lane && k + 1 == self_k;   // the row just before, same lane
-                    if (own) *in_lane = true;
-                    const bool slot = in && !own;
-                    q0 = (slot && np == 0) ? k : q0;
-                    q1 = (slot && np == 1) ? k : q1;
-                    q2 = (slot && np == 2) ? k : q2;
-                    ex |= (slot && np >= 3) ? (1ull << k) : 0ull;
-                    np += slot ? 1u : 0u;
-                    d = in ? d : max(d, ds + 1u);
-                    dm |= !in && dep_edge && (fs & FL_DOOMED);
-                };
-                uint32_t e = eb;
-                for (; e + 1 < ee; e += 2) {        // two edges per step: loads overlap
-                    const uint32_t va = ed[e], vb = ed[e + 1];
-                    const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
-                    const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
-                    const uint32_t ssa = st[sa], ssb = st[sb];
-                    take(va, dsa, fsa, ssa);
-                    take(vb, dsb, fsb, ssb);
-                }
-                if (e < ee) {
-                    const uint32_t va = ed[e];
-                    const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
-                    take(va, dep[sa], flg[sa], st[sa]);
-                }
-                if (ee > eb) d = max(d, 1u);
-                // unused slots repeat slot 0 (a harmless duplicate)
-                q1 = np > 1 ? q1 : q0;
-                q2 = np > 2 ? q2 : q0;
+            // step are kept as up to 4 lane slots (+ a mask for any extra ones)
+            uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
+            uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
+            bool dm = false, allres = true;
+            // one predecessor edge, branch-free (lanes differ in edge kinds)
+            auto take = [&](uint32_t v, uint32_t ds, uint32_t fs, uint32_t ss) {
+                const uint32_t s = (v & 0x7FFFFFFFu) - r0;
+                const bool dep_edge = (v >> 31) == 0u;
+                const bool in = s >= c0;
+                allres &= !dep_edge || ss == 3u;                 // CALL edges never gate (Q2)
+                dm |= dep_edge && ss == 4u;
+                const uint32_t k = (s - c0) & 31u;
+                s0 = (in && np == 0) ? k : s0;
+                s1 = (in && np == 1) ? k : s1;
+                s2 = (in && np == 2) ? k : s2;
+                s3 = (in && np == 3) ? k : s3;
+                extra |= (in && np >= 4) ? (1u << k) : 0u;
+                need_dep |= (in && dep_edge) ? (1u << k) : 0u;
+                np += in ? 1u : 0u;
+                d = in ? d : max(d, ds + 1u);
+                dm |= !in && dep_edge && (fs & FL_DOOMED);
             };
-            edges_of(fr0, v0, 2 * lane, d0, np0, a0, a1, a2, nd_0, ex0, dm0, ar0, nullptr);
-            edges_of(fr1, v1, 2 * lane + 1, d1, np1, b0, b1, b2, nd_1, ex1, dm1, ar1, &in1);
-            d0 = min(d0, 65535u);
-            d1 = min(d1, 65535u);
-            const bool pe0 = st0 == 0u, pe1 = st1 == 0u;
-            bool dom0 = pe0 && dm0, dom1 = pe1 && dm1;
+            uint32_t e = eb;
+            for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
+                const uint32_t va = ed[e], vb = ed[e + 1];
+                const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
+                const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
+                const uint32_t ssa = st[sa], ssb = st[sb];
+                take(va, dsa, fsa, ssa);
+                take(vb, dsb, fsb, ssb);
+            }
+            if (e < ee) {
+                const uint32_t va = ed[e];
+                const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
+                take(va, dep[sa], flg[sa], st[sa]);
+            }
+            if (ee > eb) d = max(d, 1u);
+            // unused in-step slots repeat slot 0 (a harmless duplicate)
+            s1 = np > 1 ? s1 : s0;
+            s2 = np > 2 ? s2 : s0;
+            s3 = np > 3 ? s3 : s0;
+            const bool pend = stf == 0u;
+            bool doom = pend && dm;
             if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
-            // in-step settling: Bellman-Ford rounds on registers (packed pairs of
-            // 16-bit depths move by shuffles), a vote every four rounds; then
-            // doom, a boolean closure over in-step DEP edges, by ballots
-            if (__any_sync(0xFFFFFFFFu, (np0 | np1) != 0u || in1)) {
-                const bool wide = __any_sync(0xFFFFFFFFu, (ex0 | ex1) != 0ull);
-                const bool h0 = np0 != 0u, h1 = np1 != 0u;
-                auto val = [](uint32_t x, uint32_t k) { return (k & 1u) ? (x >> 16) : (x & 0xFFFFu); };
+            // in-step settling: Bellman-Ford rounds on registers, depths moving
+            // by shuffles (four rounds per convergence vote); then doom, a
+            // boolean closure over in-step DEP edges, by ballots
+            if (__any_sync(0xFFFFFFFFu, np != 0u)) {
+                const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
+                const bool has = np != 0u;
+                // saturation is applied once after convergence: with D the
+                // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
                 auto round = [&]() {
-                    const uint32_t pk = d0 | (d1 << 16);
-                    const uint32_t xa0 = __shfl_sync(0xFFFFFFFFu, pk, a0 >> 1);
-                    const uint32_t xa1 = __shfl_sync(0xFFFFFFFFu, pk, a1 >> 1);
-                    const uint32_t xa2 = __shfl_sync(0xFFFFFFFFu, pk, a2 >> 1);
-                    const uint32_t xb0 = __shfl_sync(0xFFFFFFFFu, pk, b0 >> 1);
-                    const uint32_t xb1 = __shfl_sync(0xFFFFFFFFu, pk, b1 >> 1);
-                    const uint32_t xb2 = __shfl_sync(0xFFFFFFFFu, pk, b2 >> 1);
-                    uint32_t n0 = max(max(val(xa0, a0), val(xa1, a1)), val(xa2, a2)) + 1u;
-                    uint32_t n1 = max(max(val(xb0, b0), val(xb1, b1)), val(xb2, b2)) + 1u;
+                    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
+                    const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
+                    const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
+                    const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
+                    uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
                     if (wide) {
 #pragma unroll 1
                         for (uint32_t k = 0; k < 32; ++k) {
-                            const uint32_t x = __shfl_sync(0xFFFFFFFFu, pk, k);
-                            const uint32_t lo = x & 0xFFFFu, hi = x >> 16;
-                            if ((ex0 >> (2 * k)) & 1ull) n0 = max(n0, lo + 1u);
-                            if ((ex0 >> (2 * k + 1)) & 1ull) n0 = max(n0, hi + 1u);
-                            if ((ex1 >> (2 * k)) & 1ull) n1 = max(n1, lo + 1u);
-                            if ((ex1 >> (2 * k + 1)) & 1ull) n1 = max(n1, hi + 1u);
+                            const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
+                            if ((extra >> k) & 1u) nd = max(nd, x + 1u);
                         }
                     }
-                    d0 = h0 ? min(max(d0, n0), 65535u) : d0;
-                    n1 = h1 ? max(d1, n1) : d1;
-                    n1 = in1 ? max(n1, d0 + 1u) : n1;            // same-lane predecessor, this round
-                    d1 = min(n1, 65535u);
+                    d = has ? max(d, nd) : d;
                 };
                 for (;;) {
                     round();
                     round();
                     round();
-                    const uint32_t before = d0 | (d1 << 16);
+                    const uint32_t before = d;
                     round();
-                    if (!__any_sync(0xFFFFFFFFu, (d0 | (d1 << 16)) != before)) break;
+                    if (!__any_sync(0xFFFFFFFFu, d != before)) break;
                 }
-                if (__any_sync(0xFFFFFFFFu, dom0 || dom1)) {
-                    auto spread = [](uint32_t x) {
-                        uint64_t v = x;
-                        v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
-                        v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
-                        v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
-                        v = (v | (v << 2)) & 0x3333333333333333ull;
-                        v = (v | (v << 1)) & 0x5555555555555555ull;
-                        return v;
-                    };
+                if (__any_sync(0xFFFFFFFFu, doom)) {
                     for (;;) {
-                        const uint32_t B0 = __ballot_sync(0xFFFFFFFFu, dom0), B1 = __ballot_sync(0xFFFFFFFFu, dom1);
-                        const uint64_t D = spread(B0) | (spread(B1) << 1);
-                        dom0 = dom0 || (pe0 && (nd_0 & D) != 0ull);
-                        dom1 = dom1 || (pe1 && (nd_1 & D) != 0ull);
-                        if (__ballot_sync(0xFFFFFFFFu, dom0) == B0 && __ballot_sync(0xFFFFFFFFu, dom1) == B1) break;
+                        const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+                        doom = doom || (pend && (need_dep & D) != 0u);
+                        if (__ballot_sync(0xFFFFFFFFu, doom) == D) break;
                     }
                 }
             }
+            d = min(d, 65535u);
             if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
-            const bool rd0 = pe0 && !dom0 && ar0, rd1 = pe1 && !dom1 && ar1;
-            if (v0) {
-                dep[fr0] = (uint16_t)d0;
-                flg[fr0] = (uint8_t)((ar0 ? FL_ALLRES : 0) | (dom0 ? FL_DOOMED : 0) | (rd0 ? FL_READY : 0));
-                m_dep = max(m_dep, d0);
-                m_rnd = max(m_rnd, (uint32_t)rd[fr0]);
-            }
-            if (v1) {
-                dep[fr1] = (uint16_t)d1;
-                flg[fr1] = (uint8_t)((ar1 ? FL_ALLRES : 0) | (dom1 ? FL_DOOMED : 0) | (rd1 ? FL_READY : 0));
-                m_dep = max(m_dep, d1);
-                m_rnd = max(m_rnd, (uint32_t)rd[fr1]);
+            const bool ready = pend && !doom && allres;
+            if (valid) {
+                dep[f] = (uint16_t)d;
+                flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
+                m_dep = max(m_dep, d);
+                m_rnd = max(m_rnd, (uint32_t)rd[f]);
             }
             // per-workflow aggregates by ballots ("aggregating")
-            auto cnt = [](bool x, bool y) {
-                return (uint32_t)(__popc(__ballot_sync(0xFFFFFFFFu, x)) + __popc(__ballot_sync(0xFFFFFFFFu, y)));
-            };
-            c_pend += cnt(v0 && pe0, v1 && pe1);
-            c_ready += cnt(rd0, rd1);
-            c_infl += cnt(v0 && (st0 == 1u || st0 == 2u), v1 && (st1 == 1u || st1 == 2u));
-            c_res += cnt(v0 && st0 == 3u, v1 && st1 == 3u);
-            c_fail += cnt(v0 && st0 == 4u, v1 && st1 == 4u);
-            c_doom += cnt(dom0, dom1);
-            c_pinp += cnt(v0 && pe0 && pn[fr0] >= 0, v1 && pe1 && pn[fr1] >= 0);
+            c_pend += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend));
+            c_ready += __popc(__ballot_sync(0xFFFFFFFFu, ready));
+            c_infl += __popc(__ballot_sync(0xFFFFFFFFu, valid && (stf == 1u || stf == 2u)));
+            c_res += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 3u));
+            c_fail += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 4u));
+            c_doom += __popc(__ballot_sync(0xFFFFFFFFu, doom));
+            c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pn[f] >= 0));
             __syncwarp();
         }
         m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
@@ -434,6 +393,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     }
     __syncthreads();
     if (bprof && tid == 0) bprof[1] = gtimer();
+
+    // the exchange buffer / counters this kernel accumulates into are cleared by
+    // the zero kernel this one depends on programmatically (PDL): everything
+    // above only staged inputs and wrote shared memory and plain outputs
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ---- P3 (row-parallel): level, status, outputs, histogram, minima --------
     const uint32_t pol = p.policy;
@@ -601,6 +565,19 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     }
 }
 
+// clears the per-epoch exchange buffer and counters; lets the sweep launch at once
+__global__ void k_zero(uint32_t* __restrict__ x, size_t n) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        x[i] = 0u;
+}
+
+cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s) {
+    const uint32_t grid = (uint32_t)std::min<size_t>(148, (n_words + 255) / 256 + 1);
+    k_zero<<<grid, 256, 0, s>>>(x, n_words);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s) {
     if (p.B == 0) return cudaSuccess;
     static size_t configured = 0;
@@ -609,8 +586,17 @@ cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    k1_sweep<<<p.B, kK1Threads, smem, s>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.B);
+    cfg.blockDim = dim3(kK1Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k1_sweep, p);
 }
 
 }  // namespace nalar

@@ -342,7 +342,7 @@ cudaError_t record_ev(nalar_ctx* c, int k) {
 int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
     // clear exchange buffer (used part) + counters + adm_pub; contiguous region
-    CK(cudaMemsetAsync(c->d_x, 0, c->x_words * 4 + (C_NUM + 2 * (size_t)c->Rmax) * 4, c->stream));
+    CK(launch_zero(c->d_x, c->x_words + C_NUM + 2 * (size_t)c->Rmax, c->stream));
     if (timing) CK(record_ev(c, 0));
     int rc = run_k1(c, policy);
     if (rc) return rc;
