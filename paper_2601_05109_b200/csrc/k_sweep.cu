@@ -311,28 +311,49 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 const bool has = np != 0u;
                 // saturation is applied once after convergence: with D the
                 // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
-                auto round = [&]() {
-                    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
-                    const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
-                    const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
-                    const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
-                    uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
-                    if (wide) {
+                if (!wide) {
+                    // the common case: 4 slots; shuffles as plain shfl.sync (the
+                    // warp is converged here) so nothing sits between them and
+                    // the max chain
+                    auto round = [&]() {
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile(
+                            "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                            : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                            : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+                        const uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
+                        d = has ? max(d, nd) : d;
+                    };
+                    for (;;) {
+                        round();
+                        round();
+                        round();
+                        const uint32_t before = d;
+                        round();
+                        if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                    }
+                } else {
+                    auto round = [&]() {
+                        const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
+                        const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
+                        const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
+                        const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
+                        uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
 #pragma unroll 1
                         for (uint32_t k = 0; k < 32; ++k) {
                             const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
                             if ((extra >> k) & 1u) nd = max(nd, x + 1u);
                         }
+                        d = has ? max(d, nd) : d;
+                    };
+                    for (;;) {
+                        const uint32_t before = d;
+                        round();
+                        if (!__any_sync(0xFFFFFFFFu, d != before)) break;
                     }
-                    d = has ? max(d, nd) : d;
-                };
-                for (;;) {
-                    round();
-                    round();
-                    round();
-                    const uint32_t before = d;
-                    round();
-                    if (!__any_sync(0xFFFFFFFFu, d != before)) break;
                 }
                 if (__any_sync(0xFFFFFFFFu, doom)) {
                     for (;;) {
