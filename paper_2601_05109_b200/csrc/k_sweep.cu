@@ -252,15 +252,33 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         uint32_t m_dep = 0, m_rnd = 0;
         long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = p.prof ? clock64() : 0;
 
+        // the next step's row inputs and first two edge words are loaded one
+        // step ahead, so their shared-memory latency hides behind this step
+        uint32_t q_st = 3u, q_eb = 0u, q_ee = 0u, q_va = 0u, q_vb = 0u, q_rd = 0u;
+        int q_pn = -1;
+        auto prefetch = [&](uint32_t c) {
+            const uint32_t g = c + lane;
+            const bool ok = g < fb;
+            q_st = ok ? st[g] : 3u;
+            q_eb = ok ? eo[g] - e0 : 0u;
+            q_ee = ok ? eo[g + 1] - e0 : 0u;
+            q_rd = ok ? rd[g] : 0u;
+            q_pn = ok ? pn[g] : -1;
+            q_va = q_eb < q_ee ? ed[q_eb] : 0u;
+            q_vb = q_eb + 1 < q_ee ? ed[q_eb + 1] : 0u;
+        };
+        prefetch(fa);
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
             if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
-            const uint32_t stf = valid ? st[f] : 3u;
-            const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
+            const uint32_t stf = q_st, eb = q_eb, ee = q_ee, rdf = q_rd;
+            const int pnf = q_pn;
+            const uint32_t pva = q_va, pvb = q_vb;
+            if (c0 + 32 < fb) prefetch(c0 + 32);
             // predecessors before this step are final in smem; those inside the
             // step are kept as up to 4 lane slots (+ a mask for any extra ones)
-            uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
+            uint32_t d = 0, need_dep = 0, need_all = 0, extra = 0, np = 0;
             uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
             bool dm = false, allres = true;
             // one predecessor edge, branch-free (lanes differ in edge kinds)
@@ -277,13 +295,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 s3 = (in && np == 3) ? k : s3;
                 extra |= (in && np >= 4) ? (1u << k) : 0u;
                 need_dep |= (in && dep_edge) ? (1u << k) : 0u;
+                need_all |= in ? (1u << k) : 0u;
                 np += in ? 1u : 0u;
                 d = in ? d : max(d, ds + 1u);
                 dm |= !in && dep_edge && (fs & FL_DOOMED);
             };
             uint32_t e = eb;
             for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
-                const uint32_t va = ed[e], vb = ed[e + 1];
+                const uint32_t va = e == eb ? pva : ed[e], vb = e == eb ? pvb : ed[e + 1];
                 const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
                 const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
                 const uint32_t ssa = st[sa], ssb = st[sb];
@@ -291,7 +310,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 take(vb, dsb, fsb, ssb);
             }
             if (e < ee) {
-                const uint32_t va = ed[e];
+                const uint32_t va = e == eb ? pva : ed[e];
                 const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
                 take(va, dep[sa], flg[sa], st[sa]);
             }
@@ -300,6 +319,39 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             s1 = np > 1 ? s1 : s0;
             s2 = np > 2 ? s2 : s0;
             s3 = np > 3 ? s3 : s0;
+            // exact reduction: an in-step predecessor p that is itself a direct
+            // predecessor of another in-step predecessor q can never win the max
+            // (d[q] >= d[p] + 1), and every dropped p still reaches f through kept
+            // edges, so the least fixpoint is unchanged.  Fewer slots, fewer
+            // shuffles per settling round.
+            {
+                uint32_t m0, m1, m2, m3;
+                asm volatile(
+                    "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                    : "=r"(m0), "=r"(m1), "=r"(m2), "=r"(m3)
+                    : "r"(need_all), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+                const uint32_t feeds = np == 0u ? 0u : (m0 | m1 | m2 | m3);   // predecessors of my predecessors
+                if (extra == 0u && np > 1u) {
+                    uint32_t t[4] = {s0, s1, s2, s3}, nk = 0, o0 = s0, o1 = s0, o2 = s0, o3 = s0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool keep = (uint32_t)i < np && !((feeds >> t[i]) & 1u);
+                        o0 = (keep && nk == 0) ? t[i] : o0;
+                        o1 = (keep && nk == 1) ? t[i] : o1;
+                        o2 = (keep && nk == 2) ? t[i] : o2;
+                        o3 = (keep && nk == 3) ? t[i] : o3;
+                        nk += keep ? 1u : 0u;
+                    }
+                    s0 = o0;
+                    s1 = nk > 1 ? o1 : o0;
+                    s2 = nk > 2 ? o2 : o0;
+                    s3 = nk > 3 ? o3 : o0;
+                    np = nk;
+                }
+            }
             const bool pend = stf == 0u;
             bool doom = pend && dm;
             if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
@@ -312,28 +364,57 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 // saturation is applied once after convergence: with D the
                 // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
                 if (!wide) {
-                    // the common case: 4 slots; shuffles as plain shfl.sync (the
-                    // warp is converged here) so nothing sits between them and
-                    // the max chain
-                    auto round = [&]() {
-                        uint32_t x0, x1, x2, x3;
-                        asm volatile(
-                            "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
-                            "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
-                            "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
-                            "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
-                            : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
-                            : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
-                        const uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
-                        d = has ? max(d, nd) : d;
+                    // the common case: at most 4 slots, and only as many shuffles
+                    // per round as the step's widest row needs; shuffles as plain
+                    // shfl.sync (the warp is converged here)
+                    const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
+                    auto settle = [&](auto round) {
+                        for (;;) {
+                            round();
+                            round();
+                            round();
+                            const uint32_t before = d;
+                            round();
+                            if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                        }
                     };
-                    for (;;) {
-                        round();
-                        round();
-                        round();
-                        const uint32_t before = d;
-                        round();
-                        if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                    if (K <= 1) {
+                        settle([&]() {
+                            uint32_t x0;
+                            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(x0) : "r"(d), "r"(s0));
+                            d = has ? max(d, x0 + 1u) : d;
+                        });
+                    } else if (K == 2) {
+                        settle([&]() {
+                            uint32_t x0, x1;
+                            asm volatile(
+                                "shfl.sync.idx.b32 %0, %2, %3, 31, -1;\n\t"
+                                "shfl.sync.idx.b32 %1, %2, %4, 31, -1;"
+                                : "=r"(x0), "=r"(x1) : "r"(d), "r"(s0), "r"(s1));
+                            d = has ? max(d, max(x0, x1) + 1u) : d;
+                        });
+                    } else if (K == 3) {
+                        settle([&]() {
+                            uint32_t x0, x1, x2;
+                            asm volatile(
+                                "shfl.sync.idx.b32 %0, %3, %4, 31, -1;\n\t"
+                                "shfl.sync.idx.b32 %1, %3, %5, 31, -1;\n\t"
+                                "shfl.sync.idx.b32 %2, %3, %6, 31, -1;"
+                                : "=r"(x0), "=r"(x1), "=r"(x2) : "r"(d), "r"(s0), "r"(s1), "r"(s2));
+                            d = has ? max(d, max(max(x0, x1), x2) + 1u) : d;
+                        });
+                    } else {
+                        settle([&]() {
+                            uint32_t x0, x1, x2, x3;
+                            asm volatile(
+                                "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
+                                "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                                "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
+                                "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                                : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+                            d = has ? max(d, max(max(x0, x1), max(x2, x3)) + 1u) : d;
+                        });
                     }
                 } else {
                     auto round = [&]() {
@@ -370,7 +451,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 dep[f] = (uint16_t)d;
                 flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
                 m_dep = max(m_dep, d);
-                m_rnd = max(m_rnd, (uint32_t)rd[f]);
+                m_rnd = max(m_rnd, rdf);
             }
             // per-workflow aggregates by ballots ("aggregating")
             c_pend += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend));
@@ -379,7 +460,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             c_res += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 3u));
             c_fail += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 4u));
             c_doom += __popc(__ballot_sync(0xFFFFFFFFu, doom));
-            c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pn[f] >= 0));
+            c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pnf >= 0));
             __syncwarp();
         }
         m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
