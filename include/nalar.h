@@ -268,10 +268,12 @@ int nalar_epoch_stats_get(nalar_ctx* ctx, nalar_epoch_stats* stats);
 
 /* Diagnostics (NALAR_F_PROFILE): copy the last epoch's K1 timeline to host:
  * words [0, 2W): start/end ns of each workflow's sweep; then per K1 block b
- * 8 words: staged, swept, bucketed, entered, finished, fenced, prepped, 0; then per resource r 4 words of
- * K4: start, admitted count known, slot tables built, done; then per workflow 3 words of
- * SM cycles spent in the sweep's edge loop / settling rounds / the rest.
- * *n_words = 2W + 8B + 4R + 3W. */
+ * 8 words: staged, swept, bucketed, entered, finished, fenced, prepped, 0; then per resource r 8 words of
+ * K4: start, admitted count known, slot tables built, done, sweep complete, walk prefix, first
+ * live compaction, 0; then per workflow 4 words:
+ * SM cycles in the sweep's edge loop / settling rounds / the rest, and the
+ * settling-round count (bits 0-15) with steps by slot width (12 bits each).
+ * *n_words = 2W + 8B + 8R + 4W. */
 int nalar_debug_profile(nalar_ctx* ctx, uint64_t* host, size_t cap_words, size_t* n_words);
 
 /* Device stream the ctx runs on (cudaStream_t). */

@@ -12,6 +12,8 @@ namespace nalar {
 constexpr int kK0Threads = 256;          // validate: warp per workflow
 constexpr int kK1Threads = 512;          // sweep: warp per workflow inside a block
 constexpr int kK1Warps = kK1Threads / 32;
+constexpr uint32_t kLongSteps = 6;      // workflows of >= 6 steps use the transfer decomposition
+constexpr uint32_t kMaxIface = 7;       // interface rows per step in a transfer
 constexpr int kK4Threads = 256;          // assign: one block per resource
 constexpr int kK4Warps = kK4Threads / 32;
 
@@ -58,6 +60,8 @@ struct SweepParams {
     uint32_t B, n_types, n_inst, R, levels, policy;
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
+    uint32_t *g_tlo, *g_thi, *g_ifc, *g_ndp;   // [N] step-transfer scratch for unstaged blocks
+    uint16_t* g_aux;
     unsigned long long* prof;   // NALAR_F_PROFILE: [W][2] workflow start/end, [B][4] block phases
     uint32_t n_wf;
     // outputs

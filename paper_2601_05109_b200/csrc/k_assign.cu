@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     const uint32_t r = blockIdx.x;
-    unsigned long long* prof = p.prof ? p.prof + (size_t)r * 4 : nullptr;
+    unsigned long long* prof = p.prof ? p.prof + (size_t)r * 8 : nullptr;
     if (prof && tid == 0) prof[0] = gtimer();
     const bool is_type = r >= I;
     // ---- static data first: this kernel is a programmatic dependent of the
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     const uint32_t blk0 = tid < B ? p.blk_row0[tid] : 0u;
     // everything below reads the sweep's results
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (prof && tid == 0) prof[4] = gtimer();
 
     // ---- instances of type t: load, spare, phase-A admissions (all ranks) ----
     if (is_type) {
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         __syncthreads();
         const uint32_t total = s_pref[kK4Threads];
         const uint32_t nb = min((uint32_t)kK4Threads, B - b0);
+        if (prof && tid == 0 && b0 == 0) prof[5] = gtimer();
         for (uint32_t q0 = 0; q0 < total && found < n_adm; q0 += 4 * kK4Threads) {
             // pass 1: four consecutive items per thread
             uint2 it[4];
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             lb += li - nl;
             for (uint32_t j = 0; j < nl; ++j) s_live[lb + j] = it[j];
             __syncthreads();
+            if (prof && tid == 0 && q0 == 0 && b0 == 0) prof[6] = gtimer() + 0 * n_live;
             // pass 2: stable rank of each live item inside its level
             for (uint32_t j0 = 0; j0 < n_live; j0 += kK4Threads) {
                 const uint32_t j = j0 + tid;

@@ -100,11 +100,13 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
 }
 
 size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
-    size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs);   // per-workflow tables
+    size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs) +
+               align16(4 * ((size_t)wfs + 1));                                           // per-workflow tables
     if (staged)
         b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
              align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
-             align16(2 * (size_t)rows) + 2 * align16(rows);
+             align16(2 * (size_t)rows) + 2 * align16(rows) +
+             4 * align16(4 * (size_t)rows) + align16(2 * (size_t)rows);                // step transfers
     return b;
 }
 
@@ -151,6 +153,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     q += align16((size_t)nw * (8 * (size_t)T + 8));
     uint32_t* s_wrnd = (uint32_t*)q;                         // [nw] max retry round
     q += align16(4 * (size_t)nw);
+    uint32_t* s_lpref = (uint32_t*)q;                        // [nw+1] long-workflow step tasks
+    q += align16(4 * ((size_t)nw + 1));
+    uint32_t* s_ticket2 = (uint32_t*)(smem + 32);
 
     // ---- the block's slice of the table: staged in smem by TMA, or in place --
     const uint8_t* st;    // state, type, round, pin, executor: indexed by local row
@@ -165,6 +170,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     uint16_t* dep;        // depth (work / output)
     uint8_t* flg;         // FL_* (work)
     uint8_t* lev;         // level (work / output)
+    uint32_t* tlo;        // step transfer bytes (long workflows): inputs 0..3
+    uint32_t* thi;        //   inputs 4..6, root path in byte 7
+    uint32_t* ifc;        //   interface rows of the step starting at this row
+    uint32_t* ndp;        //   in-step DEP predecessors (lane mask)
+    uint16_t* aux;        //   DEP-from-interface mask, FAILED pred, all-resolved, k, ok
     if (staged) {
         const Win ws = window(p.f_state, 1, r0, r1), wt = window(p.f_type, 1, r0, r1);
         const Win wr = window(p.f_round, 1, r0, r1);
@@ -182,7 +192,12 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         uint8_t* d_q = q;   q += align16(4 * (size_t)nw + 32);
         dep = (uint16_t*)q; q += align16(2 * (size_t)nr);
         flg = q;            q += align16(nr);
-        lev = q;
+        lev = q;            q += align16(nr);
+        tlo = (uint32_t*)q; q += align16(4 * (size_t)nr);
+        thi = (uint32_t*)q; q += align16(4 * (size_t)nr);
+        ifc = (uint32_t*)q; q += align16(4 * (size_t)nr);
+        ndp = (uint32_t*)q; q += align16(4 * (size_t)nr);
+        aux = (uint16_t*)q;
         if (tid == 0) {
             mbar_init(mbar, 1);
             const uint32_t total = ws.bytes + wt.bytes + wr.bytes + wp.bytes + wx.bytes + we.bytes +
@@ -220,6 +235,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         dep = p.depth + r0;
         flg = p.g_flags + r0;
         lev = p.level + r0;
+        tlo = p.g_tlo + r0;
+        thi = p.g_thi + r0;
+        ifc = p.g_ifc + r0;
+        ndp = p.g_ndp + r0;
+        aux = p.g_aux + r0;
     }
 
     // ---- zero block state while the copies are in flight ------------------
@@ -238,20 +258,251 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
 
     if (bprof && tid == 0) bprof[6] = gtimer();
 
-    // ---- P2 (warp per workflow): depth + doom in creation order ---------------
+    // ---- P2: depth + doom in creation order ------------------------------------
+    // Short workflows: one warp sweeps all steps (32 rows each) in order.
+    // Long workflows (>= kLongSteps steps): depth is linear in the (max,+)
+    // semiring, so each step has a transfer function from its interface (the
+    // <= 7 distinct predecessors outside the step) to its rows:
+    //   d[f] = max(c_f, max_i D[x_i] + t_f(i)),
+    // doom likewise over (or, and).  P2a computes every step's transfer in
+    // parallel across warps (no step waits for another); P2b then composes the
+    // steps in order on one warp with a cheap evaluation per step.  Steps that
+    // do not fit (wide interface / fan-in) fall back to the ordinary sweep step
+    // in P2b.
     uint32_t n_ready = 0, n_doom = 0;
-    for (;;) {
-        uint32_t wi = 0;
-        if (lane == 0) wi = atomicAdd(s_ticket, 1u);
-        wi = __shfl_sync(0xFFFFFFFFu, wi, 0);
-        if (wi >= nw) break;
-        const uint32_t w = w0 + wi;
-        const uint32_t fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
-        if (p.prof && lane == 0) p.prof[(size_t)w * 2] = gtimer();
-        uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
-        uint32_t m_dep = 0, m_rnd = 0;
-        long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = p.prof ? clock64() : 0;
+    auto is_long = [&](uint32_t wi) { return wfo[wi + 1] - wfo[wi] >= 32u * kLongSteps; };
+    // long-step task prefix over workflows (warp 0), s_lpref[nw] = total
+    if (warp == 0) {
+        uint32_t carry = 0;
+        for (uint32_t b0 = 0; b0 < nw; b0 += 32) {
+            const uint32_t wi = b0 + lane;
+            const uint32_t n = (wi < nw && is_long(wi)) ? (wfo[wi + 1] - wfo[wi] + 31u) / 32u : 0u;
+            uint32_t incl = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            if (wi < nw) s_lpref[wi] = carry + incl - n;
+            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        if (lane == 0) { s_lpref[nw] = carry; *s_ticket2 = 0; }
+    }
+    __syncthreads();
+    const uint32_t n_long_tasks = s_lpref[nw];
 
+    uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
+    uint32_t m_dep = 0, m_rnd = 0;
+    long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = 0;
+    uint32_t n_rounds = 0, n_k[5] = {0, 0, 0, 0, 0};
+    auto wf_begin = [&](uint32_t wi) {
+        c_pend = c_ready = c_infl = c_res = c_fail = c_doom = c_pinp = 0;
+        m_dep = m_rnd = 0;
+        cyc_edge = cyc_round = cyc_rest = 0;
+        cyc_t = p.prof ? clock64() : 0;
+        n_rounds = 0;
+        n_k[0] = n_k[1] = n_k[2] = n_k[3] = n_k[4] = 0;
+        if (p.prof && lane == 0) p.prof[(size_t)(w0 + wi) * 2] = gtimer();
+    };
+    auto wf_end = [&](uint32_t wi) {
+        const uint32_t w = w0 + wi, fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
+        m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
+        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
+        n_ready += c_ready;
+        n_doom += c_doom;
+        if (lane < 10) {
+            uint32_t v = fb - fa;
+            v = lane == 1 ? c_pend : v;
+            v = lane == 2 ? c_ready : v;
+            v = lane == 3 ? c_infl : v;
+            v = lane == 4 ? c_res : v;
+            v = lane == 5 ? c_fail : v;
+            v = lane == 6 ? c_doom : v;
+            v = lane == 7 ? c_pinp : v;
+            v = lane == 8 ? m_dep : v;
+            v = lane == 9 ? m_rnd : v;
+            p.wf_agg[(size_t)w * 10 + lane] = v;
+        }
+        if (lane == 0) s_wrnd[wi] = m_rnd;
+        if (p.prof && lane == 0) {
+            p.prof[(size_t)w * 2 + 1] = gtimer();
+            cyc_rest += clock64() - cyc_t;
+            unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)w * 4;
+            c[0] = cyc_edge; c[1] = cyc_round; c[2] = cyc_rest;
+            c[3] = n_rounds | ((unsigned long long)n_k[1] << 16) | ((unsigned long long)n_k[2] << 28) |
+                   ((unsigned long long)n_k[3] << 40) | ((unsigned long long)n_k[4] << 52);
+        }
+        __syncwarp();
+    };
+    // final depth / doom of a step's rows -> smem, flags, per-workflow aggregates
+    auto finish_step = [&](uint32_t f, bool valid, uint32_t stf, uint32_t d, bool doom, bool allres, uint32_t rdf,
+                           int pnf) {
+        const bool pend = stf == 0u;
+        const bool ready = pend && !doom && allres;
+        if (valid) {
+            dep[f] = (uint16_t)d;
+            flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
+            m_dep = max(m_dep, d);
+            m_rnd = max(m_rnd, rdf);
+        }
+        // per-workflow aggregates by ballots ("aggregating")
+        c_pend += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend));
+        c_ready += __popc(__ballot_sync(0xFFFFFFFFu, ready));
+        c_infl += __popc(__ballot_sync(0xFFFFFFFFu, valid && (stf == 1u || stf == 2u)));
+        c_res += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 3u));
+        c_fail += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 4u));
+        c_doom += __popc(__ballot_sync(0xFFFFFFFFu, doom));
+        c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pnf >= 0));
+        __syncwarp();
+    };
+    // the ordinary sweep step: predecessors before the step are final in smem;
+    // those inside it settle by Bellman-Ford rounds
+    auto regular_step = [&](uint32_t c0, uint32_t stf, uint32_t eb, uint32_t ee, uint32_t pva, uint32_t pvb,
+                            uint32_t& d_out, bool& doom_out, bool& allres_out) {
+        // predecessors before this step are final in smem; those inside the
+        // step are kept as up to 4 lane slots (+ a mask for any extra ones)
+        uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
+        uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
+        bool dm = false, allres = true;
+        // one predecessor edge, branch-free (lanes differ in edge kinds)
+        auto take = [&](uint32_t v, uint32_t ds, uint32_t fs, uint32_t ss) {
+            const uint32_t s = (v & 0x7FFFFFFFu) - r0;
+            const bool dep_edge = (v >> 31) == 0u;
+            const bool in = s >= c0;
+            allres &= !dep_edge || ss == 3u;                 // CALL edges never gate (Q2)
+            dm |= dep_edge && ss == 4u;
+            const uint32_t k = (s - c0) & 31u;
+            s0 = (in && np == 0) ? k : s0;
+            s1 = (in && np == 1) ? k : s1;
+            s2 = (in && np == 2) ? k : s2;
+            s3 = (in && np == 3) ? k : s3;
+            extra |= (in && np >= 4) ? (1u << k) : 0u;
+            need_dep |= (in && dep_edge) ? (1u << k) : 0u;
+            np += in ? 1u : 0u;
+            d = in ? d : max(d, ds + 1u);
+            dm |= !in && dep_edge && (fs & FL_DOOMED);
+        };
+        uint32_t e = eb;
+        for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
+            const uint32_t va = e == eb ? pva : ed[e], vb = e == eb ? pvb : ed[e + 1];
+            const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
+            const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
+            const uint32_t ssa = st[sa], ssb = st[sb];
+            take(va, dsa, fsa, ssa);
+            take(vb, dsb, fsb, ssb);
+        }
+        if (e < ee) {
+            const uint32_t va = e == eb ? pva : ed[e];
+            const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
+            take(va, dep[sa], flg[sa], st[sa]);
+        }
+        if (ee > eb) d = max(d, 1u);
+        // unused in-step slots repeat slot 0 (a harmless duplicate)
+        s1 = np > 1 ? s1 : s0;
+        s2 = np > 2 ? s2 : s0;
+        s3 = np > 3 ? s3 : s0;
+        const bool pend = stf == 0u;
+        bool doom = pend && dm;
+        if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
+        // in-step settling: Bellman-Ford rounds on registers, depths moving
+        // by shuffles (four rounds per convergence vote); then doom, a
+        // boolean closure over in-step DEP edges, by ballots
+        if (__any_sync(0xFFFFFFFFu, np != 0u)) {
+            const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
+            const bool has = np != 0u;
+            // saturation is applied once after convergence: with D the
+            // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
+            if (!wide) {
+                // the common case: at most 4 slots, and only as many shuffles
+                // per round as the step's widest row needs
+                const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
+                n_k[K < 4 ? K : 4]++;
+                auto settle = [&](auto round) {
+                    for (;;) {
+                        round();
+                        round();
+                        round();
+                        const uint32_t before = d;
+                        round();
+                        n_rounds += 4;
+                        if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                    }
+                };
+                if (K <= 1) {
+                    settle([&]() {
+                        uint32_t x0;
+                        asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(x0) : "r"(d), "r"(s0));
+                        d = has ? max(d, x0 + 1u) : d;
+                    });
+                } else if (K == 2) {
+                    settle([&]() {
+                        uint32_t x0, x1;
+                        asm volatile(
+                            "shfl.sync.idx.b32 %0, %2, %3, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %1, %2, %4, 31, -1;"
+                            : "=r"(x0), "=r"(x1) : "r"(d), "r"(s0), "r"(s1));
+                        d = has ? max(d, max(x0, x1) + 1u) : d;
+                    });
+                } else if (K == 3) {
+                    settle([&]() {
+                        uint32_t x0, x1, x2;
+                        asm volatile(
+                            "shfl.sync.idx.b32 %0, %3, %4, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %1, %3, %5, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %2, %3, %6, 31, -1;"
+                            : "=r"(x0), "=r"(x1), "=r"(x2) : "r"(d), "r"(s0), "r"(s1), "r"(s2));
+                        d = has ? max(d, max(max(x0, x1), x2) + 1u) : d;
+                    });
+                } else {
+                    settle([&]() {
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile(
+                            "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                            : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                            : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+                        d = has ? max(d, max(max(x0, x1), max(x2, x3)) + 1u) : d;
+                    });
+                }
+            } else {
+                auto round = [&]() {
+                    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
+                    const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
+                    const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
+                    const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
+                    uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
+#pragma unroll 1
+                    for (uint32_t k = 0; k < 32; ++k) {
+                        const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
+                        if ((extra >> k) & 1u) nd = max(nd, x + 1u);
+                    }
+                    d = has ? max(d, nd) : d;
+                };
+                for (;;) {
+                    const uint32_t before = d;
+                    round();
+                    if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                }
+            }
+            if (__any_sync(0xFFFFFFFFu, doom)) {
+                for (;;) {
+                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+                    doom = doom || (pend && (need_dep & D) != 0u);
+                    if (__ballot_sync(0xFFFFFFFFu, doom) == D) break;
+                }
+            }
+        }
+        d_out = min(d, 65535u);
+        doom_out = doom;
+        allres_out = allres;
+        if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
+    };
+    // a whole short workflow, step by step
+    auto sweep_workflow = [&](uint32_t wi) {
+        const uint32_t fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
+        wf_begin(wi);
         // the next step's row inputs and first two edge words are loaded one
         // step ahead, so their shared-memory latency hides behind this step
         uint32_t q_st = 3u, q_eb = 0u, q_ee = 0u, q_va = 0u, q_vb = 0u, q_rd = 0u;
@@ -276,218 +527,206 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
             const int pnf = q_pn;
             const uint32_t pva = q_va, pvb = q_vb;
             if (c0 + 32 < fb) prefetch(c0 + 32);
-            // predecessors before this step are final in smem; those inside the
-            // step are kept as up to 4 lane slots (+ a mask for any extra ones)
-            uint32_t d = 0, need_dep = 0, need_all = 0, extra = 0, np = 0;
-            uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane;
-            bool dm = false, allres = true;
-            // one predecessor edge, branch-free (lanes differ in edge kinds)
-            auto take = [&](uint32_t v, uint32_t ds, uint32_t fs, uint32_t ss) {
-                const uint32_t s = (v & 0x7FFFFFFFu) - r0;
-                const bool dep_edge = (v >> 31) == 0u;
-                const bool in = s >= c0;
-                allres &= !dep_edge || ss == 3u;                 // CALL edges never gate (Q2)
-                dm |= dep_edge && ss == 4u;
-                const uint32_t k = (s - c0) & 31u;
-                s0 = (in && np == 0) ? k : s0;
-                s1 = (in && np == 1) ? k : s1;
-                s2 = (in && np == 2) ? k : s2;
-                s3 = (in && np == 3) ? k : s3;
-                extra |= (in && np >= 4) ? (1u << k) : 0u;
-                need_dep |= (in && dep_edge) ? (1u << k) : 0u;
-                need_all |= in ? (1u << k) : 0u;
-                np += in ? 1u : 0u;
-                d = in ? d : max(d, ds + 1u);
-                dm |= !in && dep_edge && (fs & FL_DOOMED);
-            };
-            uint32_t e = eb;
-            for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
-                const uint32_t va = e == eb ? pva : ed[e], vb = e == eb ? pvb : ed[e + 1];
-                const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
-                const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
-                const uint32_t ssa = st[sa], ssb = st[sb];
-                take(va, dsa, fsa, ssa);
-                take(vb, dsb, fsb, ssb);
-            }
-            if (e < ee) {
-                const uint32_t va = e == eb ? pva : ed[e];
-                const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
-                take(va, dep[sa], flg[sa], st[sa]);
-            }
-            if (ee > eb) d = max(d, 1u);
-            // unused in-step slots repeat slot 0 (a harmless duplicate)
-            s1 = np > 1 ? s1 : s0;
-            s2 = np > 2 ? s2 : s0;
-            s3 = np > 3 ? s3 : s0;
-            // exact reduction: an in-step predecessor p that is itself a direct
-            // predecessor of another in-step predecessor q can never win the max
-            // (d[q] >= d[p] + 1), and every dropped p still reaches f through kept
-            // edges, so the least fixpoint is unchanged.  Fewer slots, fewer
-            // shuffles per settling round.
-            {
-                uint32_t m0, m1, m2, m3;
-                asm volatile(
-                    "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
-                    : "=r"(m0), "=r"(m1), "=r"(m2), "=r"(m3)
-                    : "r"(need_all), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
-                const uint32_t feeds = np == 0u ? 0u : (m0 | m1 | m2 | m3);   // predecessors of my predecessors
-                if (extra == 0u && np > 1u) {
-                    uint32_t t[4] = {s0, s1, s2, s3}, nk = 0, o0 = s0, o1 = s0, o2 = s0, o3 = s0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const bool keep = (uint32_t)i < np && !((feeds >> t[i]) & 1u);
-                        o0 = (keep && nk == 0) ? t[i] : o0;
-                        o1 = (keep && nk == 1) ? t[i] : o1;
-                        o2 = (keep && nk == 2) ? t[i] : o2;
-                        o3 = (keep && nk == 3) ? t[i] : o3;
-                        nk += keep ? 1u : 0u;
-                    }
-                    s0 = o0;
-                    s1 = nk > 1 ? o1 : o0;
-                    s2 = nk > 2 ? o2 : o0;
-                    s3 = nk > 3 ? o3 : o0;
-                    np = nk;
-                }
-            }
-            const bool pend = stf == 0u;
-            bool doom = pend && dm;
-            if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
-            // in-step settling: Bellman-Ford rounds on registers, depths moving
-            // by shuffles (four rounds per convergence vote); then doom, a
-            // boolean closure over in-step DEP edges, by ballots
-            if (__any_sync(0xFFFFFFFFu, np != 0u)) {
-                const bool wide = __any_sync(0xFFFFFFFFu, extra != 0u);
-                const bool has = np != 0u;
-                // saturation is applied once after convergence: with D the
-                // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
-                if (!wide) {
-                    // the common case: at most 4 slots, and only as many shuffles
-                    // per round as the step's widest row needs; shuffles as plain
-                    // shfl.sync (the warp is converged here)
-                    const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
-                    auto settle = [&](auto round) {
-                        for (;;) {
-                            round();
-                            round();
-                            round();
-                            const uint32_t before = d;
-                            round();
-                            if (!__any_sync(0xFFFFFFFFu, d != before)) break;
-                        }
-                    };
-                    if (K <= 1) {
-                        settle([&]() {
-                            uint32_t x0;
-                            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(x0) : "r"(d), "r"(s0));
-                            d = has ? max(d, x0 + 1u) : d;
-                        });
-                    } else if (K == 2) {
-                        settle([&]() {
-                            uint32_t x0, x1;
-                            asm volatile(
-                                "shfl.sync.idx.b32 %0, %2, %3, 31, -1;\n\t"
-                                "shfl.sync.idx.b32 %1, %2, %4, 31, -1;"
-                                : "=r"(x0), "=r"(x1) : "r"(d), "r"(s0), "r"(s1));
-                            d = has ? max(d, max(x0, x1) + 1u) : d;
-                        });
-                    } else if (K == 3) {
-                        settle([&]() {
-                            uint32_t x0, x1, x2;
-                            asm volatile(
-                                "shfl.sync.idx.b32 %0, %3, %4, 31, -1;\n\t"
-                                "shfl.sync.idx.b32 %1, %3, %5, 31, -1;\n\t"
-                                "shfl.sync.idx.b32 %2, %3, %6, 31, -1;"
-                                : "=r"(x0), "=r"(x1), "=r"(x2) : "r"(d), "r"(s0), "r"(s1), "r"(s2));
-                            d = has ? max(d, max(max(x0, x1), x2) + 1u) : d;
-                        });
-                    } else {
-                        settle([&]() {
-                            uint32_t x0, x1, x2, x3;
-                            asm volatile(
-                                "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
-                                "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
-                                "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
-                                "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
-                                : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
-                                : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
-                            d = has ? max(d, max(max(x0, x1), max(x2, x3)) + 1u) : d;
-                        });
-                    }
+            uint32_t d;
+            bool doom, allres;
+            regular_step(c0, stf, eb, ee, pva, pvb, d, doom, allres);
+            finish_step(f, valid, stf, d, doom, allres, rdf, pnf);
+        }
+        wf_end(wi);
+    };
+    // P2a: the transfer function of one step of a long workflow
+    auto transfer_step = [&](uint32_t c0, uint32_t fb) {
+        const uint32_t f = c0 + lane;
+        const bool valid = f < fb;
+        const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
+        uint32_t o0 = ~0u, o1 = ~0u, o2 = ~0u, o3 = ~0u, no = 0, odep = 0;     // out-of-step preds
+        uint32_t s0 = lane, s1 = lane, s2 = lane, s3 = lane, np = 0, need_dep = 0;
+        bool ovf = false, failp = false, allres = true;
+        for (uint32_t e = eb; e < ee; ++e) {
+            const uint32_t v = ed[e];
+            const uint32_t s = (v & 0x7FFFFFFFu) - r0;
+            const bool dep_edge = (v >> 31) == 0u;
+            const uint32_t ss = st[s];
+            allres &= !dep_edge || ss == 3u;
+            failp |= dep_edge && ss == 4u;
+            if (s >= c0) {
+                const uint32_t k = s - c0;
+                s0 = np == 0 ? k : s0;
+                s1 = np == 1 ? k : s1;
+                s2 = np == 2 ? k : s2;
+                s3 = np == 3 ? k : s3;
+                ovf |= np >= 4;
+                ++np;
+                need_dep |= dep_edge ? (1u << k) : 0u;
+            } else {
+                const int q = s == o0 ? 0 : s == o1 ? 1 : s == o2 ? 2 : s == o3 ? 3 : -1;
+                if (q >= 0) {
+                    odep |= dep_edge ? (1u << q) : 0u;
                 } else {
-                    auto round = [&]() {
-                        const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
-                        const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
-                        const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
-                        const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
-                        uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
-#pragma unroll 1
-                        for (uint32_t k = 0; k < 32; ++k) {
-                            const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
-                            if ((extra >> k) & 1u) nd = max(nd, x + 1u);
-                        }
-                        d = has ? max(d, nd) : d;
-                    };
-                    for (;;) {
-                        const uint32_t before = d;
-                        round();
-                        if (!__any_sync(0xFFFFFFFFu, d != before)) break;
-                    }
+                    o0 = no == 0 ? s : o0;
+                    o1 = no == 1 ? s : o1;
+                    o2 = no == 2 ? s : o2;
+                    o3 = no == 3 ? s : o3;
+                    ovf |= no >= 4;
+                    odep |= (dep_edge && no < 4) ? (1u << no) : 0u;
+                    ++no;
                 }
+            }
+        }
+        s1 = np > 1 ? s1 : s0;
+        s2 = np > 2 ? s2 : s0;
+        s3 = np > 3 ? s3 : s0;
+        // the step's interface: distinct out-of-step rows, ascending, <= 7
+        uint32_t k = 0, myx = 0, i0 = 0, i1 = 0, i2 = 0, i3 = 0, taken = 0;
+        for (;;) {
+            uint32_t cand = ~0u;
+            cand = (!(taken & 1u) && no > 0) ? min(cand, o0) : cand;
+            cand = (!(taken & 2u) && no > 1) ? min(cand, o1) : cand;
+            cand = (!(taken & 4u) && no > 2) ? min(cand, o2) : cand;
+            cand = (!(taken & 8u) && no > 3) ? min(cand, o3) : cand;
+            const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, cand);
+            if (m == ~0u) break;
+            if (k == kMaxIface) { ovf = true; break; }
+            if (lane == k) myx = m;
+            if (no > 0 && o0 == m) { i0 = k; taken |= 1u; }
+            if (no > 1 && o1 == m) { i1 = k; taken |= 2u; }
+            if (no > 2 && o2 == m) { i2 = k; taken |= 4u; }
+            if (no > 3 && o3 == m) { i3 = k; taken |= 8u; }
+            ++k;
+        }
+        const bool ok = !__any_sync(0xFFFFFFFFu, ovf);
+        // transfer bytes: byte i < k = 1 + longest path from x_i into this row,
+        // byte 7 = 1 + longest path from a root of the step (0 = none)
+        auto setb = [](uint32_t& lo, uint32_t& hi, uint32_t i, uint32_t v) {
+            if (i < 4) lo = __vmaxu4(lo, v << (8 * i));
+            else hi = __vmaxu4(hi, v << (8 * (i - 4)));
+        };
+        uint32_t tlo_v = 0, thi_v = 0, edm = 0;
+        if (ok && valid) {
+            if (no > 0) { setb(tlo_v, thi_v, i0, 2u); edm |= (odep & 1u) ? (1u << i0) : 0u; }
+            if (no > 1) { setb(tlo_v, thi_v, i1, 2u); edm |= (odep & 2u) ? (1u << i1) : 0u; }
+            if (no > 2) { setb(tlo_v, thi_v, i2, 2u); edm |= (odep & 4u) ? (1u << i2) : 0u; }
+            if (no > 3) { setb(tlo_v, thi_v, i3, 2u); edm |= (odep & 8u) ? (1u << i3) : 0u; }
+            if (ee == eb) thi_v |= 1u << 24;         // a root: c = 0
+        }
+        if (ok && __any_sync(0xFFFFFFFFu, np != 0u)) {
+            const bool has = np != 0u;
+            auto inc = [](uint32_t x) { return x + (__vcmpne4(x, 0u) & 0x01010101u); };
+            auto round = [&]() {
+                uint32_t l0, l1, l2, l3, h0, h1, h2, h3;
+                asm volatile(
+                    "shfl.sync.idx.b32 %0, %8, %10, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %1, %8, %11, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %2, %8, %12, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %3, %8, %13, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %4, %9, %10, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %5, %9, %11, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %6, %9, %12, 31, -1;\n\t"
+                    "shfl.sync.idx.b32 %7, %9, %13, 31, -1;"
+                    : "=r"(l0), "=r"(l1), "=r"(l2), "=r"(l3), "=r"(h0), "=r"(h1), "=r"(h2), "=r"(h3)
+                    : "r"(tlo_v), "r"(thi_v), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+                const uint32_t nl = __vmaxu4(__vmaxu4(inc(l0), inc(l1)), __vmaxu4(inc(l2), inc(l3)));
+                const uint32_t nh = __vmaxu4(__vmaxu4(inc(h0), inc(h1)), __vmaxu4(inc(h2), inc(h3)));
+                tlo_v = has ? __vmaxu4(tlo_v, nl) : tlo_v;
+                thi_v = has ? __vmaxu4(thi_v, nh) : thi_v;
+            };
+            for (;;) {
+                round();
+                round();
+                round();
+                const uint32_t bl = tlo_v, bh = thi_v;
+                round();
+                if (!__any_sync(0xFFFFFFFFu, tlo_v != bl || thi_v != bh)) break;
+            }
+        }
+        if (valid) {
+            tlo[f] = tlo_v;
+            thi[f] = thi_v;
+            ndp[f] = need_dep;
+            aux[f] = (uint16_t)(edm | (failp ? 0x80u : 0u) | (allres ? 0x100u : 0u) |
+                                (lane == 0 ? ((k << 9) | (ok ? 0x2000u : 0u)) : 0u));
+        }
+        if (lane < k && ok) ifc[c0 + lane] = myx;
+    };
+    // P2b: compose the steps of a long workflow in order
+    auto compose_workflow = [&](uint32_t wi) {
+        const uint32_t fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
+        wf_begin(wi);
+        for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
+            if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
+            const uint32_t f = c0 + lane;
+            const bool valid = f < fb;
+            const uint32_t stf = valid ? st[f] : 3u, rdf = valid ? rd[f] : 0u;
+            const int pnf = valid ? pn[f] : -1;
+            const uint32_t a0 = aux[c0];
+            uint32_t d;
+            bool doom, allres;
+            if (a0 & 0x2000u) {
+                const uint32_t k = (a0 >> 9) & 15u;
+                const uint32_t tl = valid ? tlo[f] : 0u, th = valid ? thi[f] : 0u;
+                const uint32_t a = valid ? aux[f] : 0x100u;
+                const uint32_t nd = valid ? ndp[f] : 0u;
+                uint32_t best = 0;
+                bool dmb = (a & 0x80u) != 0;
+                for (uint32_t i = 0; i < k; ++i) {
+                    const uint32_t x = ifc[c0 + i];
+                    const uint32_t by = i < 4 ? (tl >> (8 * i)) & 0xFFu : (th >> (8 * (i - 4))) & 0xFFu;
+                    best = by ? max(best, (uint32_t)dep[x] + by - 1u) : best;
+                    dmb |= ((a >> i) & 1u) && (flg[x] & FL_DOOMED);
+                }
+                const uint32_t c7 = th >> 24;
+                best = c7 ? max(best, c7 - 1u) : best;
+                d = min(best, 65535u);
+                allres = (a & 0x100u) != 0;
+                const bool pend = stf == 0u;
+                doom = pend && dmb;
                 if (__any_sync(0xFFFFFFFFu, doom)) {
                     for (;;) {
                         const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
-                        doom = doom || (pend && (need_dep & D) != 0u);
+                        doom = doom || (pend && (nd & D) != 0u);
                         if (__ballot_sync(0xFFFFFFFFu, doom) == D) break;
                     }
                 }
+                if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
+            } else {
+                const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
+                const uint32_t pva = eb < ee ? ed[eb] : 0u, pvb = eb + 1 < ee ? ed[eb + 1] : 0u;
+                regular_step(c0, stf, eb, ee, pva, pvb, d, doom, allres);
             }
-            d = min(d, 65535u);
-            if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
-            const bool ready = pend && !doom && allres;
-            if (valid) {
-                dep[f] = (uint16_t)d;
-                flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
-                m_dep = max(m_dep, d);
-                m_rnd = max(m_rnd, rdf);
+            finish_step(f, valid, stf, d, doom, allres, rdf, pnf);
+        }
+        wf_end(wi);
+    };
+
+    // P2a: long-workflow steps and whole short workflows, by ticket
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(s_ticket, 1u);
+        t = __shfl_sync(0xFFFFFFFFu, t, 0);
+        if (t < n_long_tasks) {
+            uint32_t lo = 0, hi = nw - 1;            // last workflow with s_lpref <= t
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (s_lpref[mid] <= t) lo = mid;
+                else hi = mid - 1;
             }
-            // per-workflow aggregates by ballots ("aggregating")
-            c_pend += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend));
-            c_ready += __popc(__ballot_sync(0xFFFFFFFFu, ready));
-            c_infl += __popc(__ballot_sync(0xFFFFFFFFu, valid && (stf == 1u || stf == 2u)));
-            c_res += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 3u));
-            c_fail += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 4u));
-            c_doom += __popc(__ballot_sync(0xFFFFFFFFu, doom));
-            c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pnf >= 0));
-            __syncwarp();
+            transfer_step(wfo[lo] - r0 + 32u * (t - s_lpref[lo]), wfo[lo + 1] - r0);
+            continue;
         }
-        m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
-        m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
-        n_ready += c_ready;
-        n_doom += c_doom;
-        if (lane < 10) {
-            uint32_t v = fb - fa;
-            v = lane == 1 ? c_pend : v;
-            v = lane == 2 ? c_ready : v;
-            v = lane == 3 ? c_infl : v;
-            v = lane == 4 ? c_res : v;
-            v = lane == 5 ? c_fail : v;
-            v = lane == 6 ? c_doom : v;
-            v = lane == 7 ? c_pinp : v;
-            v = lane == 8 ? m_dep : v;
-            v = lane == 9 ? m_rnd : v;
-            p.wf_agg[(size_t)w * 10 + lane] = v;
+        const uint32_t wi = t - n_long_tasks;
+        if (wi >= nw) break;
+        if (!is_long(wi)) sweep_workflow(wi);
+    }
+    if (n_long_tasks) {
+        __syncthreads();
+        // P2b: each long workflow composed by one warp
+        for (;;) {
+            uint32_t wi = 0;
+            if (lane == 0) wi = atomicAdd(s_ticket2, 1u);
+            wi = __shfl_sync(0xFFFFFFFFu, wi, 0);
+            if (wi >= nw) break;
+            if (is_long(wi)) compose_workflow(wi);
         }
-        if (lane == 0) s_wrnd[wi] = m_rnd;
-        if (p.prof && lane == 0) {
-            p.prof[(size_t)w * 2 + 1] = gtimer();
-            cyc_rest += clock64() - cyc_t;
-            unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 4 + (size_t)w * 3;
-            c[0] = cyc_edge; c[1] = cyc_round; c[2] = cyc_rest;
-        }
-        __syncwarp();
     }
     if (lane == 0) {
         atomicAdd(&s_cnt[0], n_ready);

@@ -90,6 +90,8 @@ struct nalar_ctx {
     // outputs
     uint8_t *d_status = nullptr, *d_level = nullptr, *d_newpin = nullptr, *d_gflags = nullptr;
     uint16_t* d_gwlm = nullptr;
+    uint32_t *d_gtlo = nullptr, *d_gthi = nullptr, *d_gifc = nullptr, *d_gndp = nullptr;
+    uint16_t* d_gaux = nullptr;
     uint16_t* d_depth = nullptr;
     int16_t *d_inst = nullptr, *d_ainst = nullptr;
     uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
@@ -170,7 +172,7 @@ struct Layout {
 struct Plan {
     size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, type_off, type_inst;
-    size_t status, level, newpin, gflags, gwlm, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
+    size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
     uint32_t Rmax, Bmax;
@@ -209,6 +211,11 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->newpin = L.take<uint8_t>(N);
     p->gflags = L.take<uint8_t>(N);
     p->gwlm = L.take<uint16_t>(N);
+    p->gtlo = L.take<uint32_t>(N);
+    p->gthi = L.take<uint32_t>(N);
+    p->gifc = L.take<uint32_t>(N);
+    p->gndp = L.take<uint32_t>(N);
+    p->gaux = L.take<uint16_t>(N);
     p->depth = L.take<uint16_t>(N);
     p->inst = L.take<int16_t>(N);
     p->ainst = L.take<int16_t>(N);
@@ -286,6 +293,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
+    p.g_tlo = c->d_gtlo; p.g_thi = c->d_gthi; p.g_ifc = c->d_gifc; p.g_ndp = c->d_gndp; p.g_aux = c->d_gaux;
     p.prof = c->d_prof;
     p.n_wf = c->W;
     p.status = c->d_status; p.level = c->d_level; p.depth = c->d_depth; p.instance = c->d_inst;
@@ -391,7 +399,7 @@ int set_blocks(nalar_ctx* c) {
     CK(cudaMemcpyAsync(c->d_blk_edge0, be.data(), 4ull * be.size(), cudaMemcpyHostToDevice, st));
     if (!bs.empty()) CK(cudaMemcpyAsync(c->d_blk_staged, bs.data(), bs.size(), cudaMemcpyHostToDevice, st));
     if (c->cfg.flags & NALAR_F_PROFILE) {
-        const size_t need = 2ull * c->W + 8ull * c->B + 4ull * c->R + 3ull * c->W;
+        const size_t need = 2ull * c->W + 8ull * c->B + 8ull * c->R + 4ull * c->W;
         if (need > c->prof_words) {
             if (c->d_prof) cudaFree(c->d_prof);
             c->d_prof = nullptr;
@@ -498,6 +506,8 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_status = at<uint8_t>(a, p.status); c->d_level = at<uint8_t>(a, p.level);
     c->d_newpin = at<uint8_t>(a, p.newpin); c->d_gflags = at<uint8_t>(a, p.gflags);
     c->d_gwlm = at<uint16_t>(a, p.gwlm);
+    c->d_gtlo = at<uint32_t>(a, p.gtlo); c->d_gthi = at<uint32_t>(a, p.gthi);
+    c->d_gifc = at<uint32_t>(a, p.gifc); c->d_gndp = at<uint32_t>(a, p.gndp); c->d_gaux = at<uint16_t>(a, p.gaux);
     c->d_depth = at<uint16_t>(a, p.depth); c->d_inst = at<int16_t>(a, p.inst); c->d_ainst = at<int16_t>(a, p.ainst);
     c->d_wfagg = at<uint32_t>(a, p.wfagg); c->d_iload = at<uint32_t>(a, p.iload);
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);

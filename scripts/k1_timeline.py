@@ -31,10 +31,10 @@ prof = nalar.nalar_debug_profile(ctx.h).astype(np.int64)
 W = s.n_workflows
 wf = prof[:2 * W].reshape(W, 2)
 R = s.n_instances + s.n_types
-cyc = prof[len(prof) - 3 * W:].reshape(W, 3)              # edge loop, rounds, rest (SM cycles)
-prof = prof[:len(prof) - 3 * W]
-blk = prof[2 * W:len(prof) - 4 * R].reshape(-1, 8)        # staged, swept, bucketed, entered, P3 done, P4 done
-k4 = prof[len(prof) - 4 * R:].reshape(R, 4)              # start, published, based, done
+cyc = prof[len(prof) - 4 * W:].reshape(W, 4)              # edge loop, rounds, rest (SM cycles), round counts
+prof = prof[:len(prof) - 4 * W]
+blk = prof[2 * W:len(prof) - 8 * R].reshape(-1, 8)        # staged, swept, bucketed, entered, P3 done, P4 done
+k4 = prof[len(prof) - 8 * R:].reshape(R, 8)              # start, n_adm, tables, done, waited, prefix, pass1
 t0 = blk[:, 3].min()
 o = oracle_epoch(s, "srtf")
 sizes = np.diff(s.wf_fut_off.astype(np.int64))
@@ -62,10 +62,18 @@ res["k4"] = {"start_after_k1_ns": int(k4[:, 0].min() - blk[:, 2].max()),
              "tables_ns_max": int((k4[:, 2] - k4[:, 1]).max()),
              "walk_ns_max": int((k4[:, 3] - k4[:, 2]).max()),
              "start_spread_ns": int(k4[:, 0].max() - k4[:, 0].min()),
-             "slowest_walk_r": int(np.argmax(k4[:, 3] - k4[:, 2]))}
+             "slowest_walk_r": int(np.argmax(k4[:, 3] - k4[:, 2])),
+             "k1_end_to_k4_end_ns": int(k4[:, 3].max() - blk[:, 2].max()),
+             "after_wait_to_nadm_ns_max": int((k4[:, 1] - k4[:, 4]).max()),
+             "prefix_ns_max": int(np.max(np.where(k4[:, 5] > 0, k4[:, 5] - k4[:, 2], 0))),
+             "pass1_ns_max": int(np.max(np.where(k4[:, 6] > 0, k4[:, 6] - k4[:, 5], 0))),
+             "rest_of_walk_ns_max": int(np.max(np.where(k4[:, 6] > 0, k4[:, 3] - k4[:, 6], 0))),
+             "wait_release_spread_ns": int(k4[:, 4].max() - k4[:, 4].min())}
 top = np.argsort(-dur)[:10]
 res["slowest"] = [{"w": int(w), "rows": int(sizes[w]), "max_depth": int(maxd[w]), "dur_ns": int(dur[w]),
-                   "start_ns": int(start[w]), "cyc_edge_round_rest": [int(x) for x in cyc[w]]}
+                   "start_ns": int(start[w]), "cyc_edge_round_rest": [int(x) for x in cyc[w, :3]],
+                   "rounds": int(cyc[w, 3] & 0xFFFF),
+                   "steps_by_K": [int((cyc[w, 3] >> sh) & 0xFFF) for sh in (16, 28, 40, 52)]}
                   for w in top]
 chunks = np.ceil(sizes / 32.0)
 res["cycles_per_chunk"] = {"edge": float(cyc[:, 0].sum() / chunks.sum()),

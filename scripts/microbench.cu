@@ -46,14 +46,37 @@ __global__ void bench(unsigned long long* out, int seed) {
     t0 = clock64();
     for (int i = 0; i < N / 8; ++i) x += atomicMin(&sm[x & 1], lane + x) & 1;
     t1 = clock64(); if (lane == 0) out[8] = (t1 - t0) * 8;
+    // a settling round: K independent shuffles of the same value, max chain
+    {
+        uint32_t d = lane, s0 = (lane + 1) & 31, s1 = (lane + 5) & 31, s2 = (lane + 9) & 31, s3 = (lane + 17) & 31;
+        t0 = clock64();
+        for (int i = 0; i < N; ++i) {
+            uint32_t a, b, c, e;
+            asm volatile("shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\tshfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                         "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\tshfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+            d = max(d, max(max(a, b), max(c, e)) + 1u) & 0xFFFFF;
+        }
+        t1 = clock64(); if (lane == 0) out[10] = (t1 - t0);
+        t0 = clock64();
+        for (int i = 0; i < N; ++i) {
+            uint32_t a;
+            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(a) : "r"(d), "r"(s0));
+            d = max(d, a + 1u) & 0xFFFFF;
+        }
+        t1 = clock64(); if (lane == 0) out[11] = (t1 - t0);
+        x += d;
+    }
     if (lane == 0) out[9] = x;
 }
 int main() {
-    unsigned long long* d; unsigned long long h[10];
-    cudaMalloc(&d, 80);
+    unsigned long long* d; unsigned long long h[12];
+    cudaMalloc(&d, 96);
     bench<<<1, 32>>>(d, 1); cudaDeviceSynchronize();
-    bench<<<1, 32>>>(d, 2); cudaMemcpy(h, d, 80, cudaMemcpyDeviceToHost);
+    bench<<<1, 32>>>(d, 2); cudaMemcpy(h, d, 96, cudaMemcpyDeviceToHost);
     const char* nm[] = {"shfl.idx", "vote.any", "ballot", "match.any(8 keys)", "match.any(32 keys)", "redux.max", "lds", "imnmx", "atom.shared.min(32-way)"};
     for (int i = 0; i < 9; ++i) printf("%-26s %7.1f cycles/op\n", nm[i], (double)h[i] / N);
+    printf("%-26s %7.1f cycles/round\n", "round: 4 shfl + max chain", (double)h[10] / N);
+    printf("%-26s %7.1f cycles/round\n", "round: 1 shfl + max", (double)h[11] / N);
     return 0;
 }
