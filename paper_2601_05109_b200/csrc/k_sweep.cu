@@ -110,8 +110,11 @@ size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bo
     return b;
 }
 
-__global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
+// The body is instantiated twice: for a staged block every table pointer
+// derives from the shared-memory window, so the compiler emits LDS/STS; for an
+// unstaged (oversized) block they point into global memory.
+template <bool kStaged>
+__device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t b = blockIdx.x;
     const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Lv = p.levels;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
     const uint32_t r0 = p.blk_row0[b], r1 = p.blk_row0[b + 1];
     const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
     const uint32_t nr = r1 - r0, ne = e1 - e0, nw = w1 - w0;
-    const bool staged = p.blk_staged[b] != 0;
+    constexpr bool staged = kStaged;
     unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;
     if (bprof && tid == 0) bprof[3] = gtimer();
     // let the assignment kernel launch now (PDL); it waits for this grid's
@@ -596,49 +599,98 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         }
         const bool ok = !__any_sync(0xFFFFFFFFu, ovf);
         // transfer bytes: byte i < k = 1 + longest path from x_i into this row,
-        // byte 7 = 1 + longest path from a root of the step (0 = none)
-        auto setb = [](uint32_t& lo, uint32_t& hi, uint32_t i, uint32_t v) {
-            if (i < 4) lo = __vmaxu4(lo, v << (8 * i));
-            else hi = __vmaxu4(hi, v << (8 * (i - 4)));
+        // byte 7 = 1 + longest path from a root of the step (0 = none).
+        // While settling, slot i lives in 16-bit half (i & 1) of h[i >> 1]
+        // (slot 7 = the root path) with a bias: a valid value b is 0x8000 + b,
+        // "no path" is anything below 0x8000.  Then the step "1 + longest
+        // path over in-step predecessors" is one native u16x2 max tree plus a
+        // plain add of 1 per half (invalid halves stay far below the bias),
+        // and since +1 is monotone it is applied once after the max.
+        uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, edm = 0;
+        auto seth = [&](uint32_t i, uint32_t v) {
+            const uint32_t x = (0x8000u + v) << (16 * (i & 1u));
+            h0 = (i >> 1) == 0 ? (h0 | x) : h0;
+            h1 = (i >> 1) == 1 ? (h1 | x) : h1;
+            h2 = (i >> 1) == 2 ? (h2 | x) : h2;
+            h3 = (i >> 1) == 3 ? (h3 | x) : h3;
         };
-        uint32_t tlo_v = 0, thi_v = 0, edm = 0;
         if (ok && valid) {
-            if (no > 0) { setb(tlo_v, thi_v, i0, 2u); edm |= (odep & 1u) ? (1u << i0) : 0u; }
-            if (no > 1) { setb(tlo_v, thi_v, i1, 2u); edm |= (odep & 2u) ? (1u << i1) : 0u; }
-            if (no > 2) { setb(tlo_v, thi_v, i2, 2u); edm |= (odep & 4u) ? (1u << i2) : 0u; }
-            if (no > 3) { setb(tlo_v, thi_v, i3, 2u); edm |= (odep & 8u) ? (1u << i3) : 0u; }
-            if (ee == eb) thi_v |= 1u << 24;         // a root: c = 0
+            if (no > 0) { seth(i0, 2u); edm |= (odep & 1u) ? (1u << i0) : 0u; }
+            if (no > 1) { seth(i1, 2u); edm |= (odep & 2u) ? (1u << i1) : 0u; }
+            if (no > 2) { seth(i2, 2u); edm |= (odep & 4u) ? (1u << i2) : 0u; }
+            if (no > 3) { seth(i3, 2u); edm |= (odep & 8u) ? (1u << i3) : 0u; }
+            if (ee == eb) seth(7u, 1u);              // a root: c = 0
         }
+        auto vmax2 = [](uint32_t x, uint32_t y) {
+            uint32_t r;
+            asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+            return r;
+        };
+        // one settling round on a pair of slots (4 shuffles, 3 + 1 maxes, 1 add)
+        auto pair_round = [&](uint32_t& h, bool has) {
+            uint32_t l0, l1, l2, l3;
+            asm volatile(
+                "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
+                "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
+                "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                : "=r"(l0), "=r"(l1), "=r"(l2), "=r"(l3)
+                : "r"(h), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+            const uint32_t nl = vmax2(vmax2(l0, l1), vmax2(l2, l3)) + 0x00010001u;
+            h = has ? vmax2(h, nl) : h;
+        };
         if (ok && __any_sync(0xFFFFFFFFu, np != 0u)) {
             const bool has = np != 0u;
-            auto inc = [](uint32_t x) { return x + (__vcmpne4(x, 0u) & 0x01010101u); };
-            auto round = [&]() {
-                uint32_t l0, l1, l2, l3, h0, h1, h2, h3;
-                asm volatile(
-                    "shfl.sync.idx.b32 %0, %8, %10, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %1, %8, %11, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %2, %8, %12, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %3, %8, %13, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %4, %9, %10, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %5, %9, %11, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %6, %9, %12, 31, -1;\n\t"
-                    "shfl.sync.idx.b32 %7, %9, %13, 31, -1;"
-                    : "=r"(l0), "=r"(l1), "=r"(l2), "=r"(l3), "=r"(h0), "=r"(h1), "=r"(h2), "=r"(h3)
-                    : "r"(tlo_v), "r"(thi_v), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
-                const uint32_t nl = __vmaxu4(__vmaxu4(inc(l0), inc(l1)), __vmaxu4(inc(l2), inc(l3)));
-                const uint32_t nh = __vmaxu4(__vmaxu4(inc(h0), inc(h1)), __vmaxu4(inc(h2), inc(h3)));
-                tlo_v = has ? __vmaxu4(tlo_v, nl) : tlo_v;
-                thi_v = has ? __vmaxu4(thi_v, nh) : thi_v;
-            };
-            for (;;) {
-                round();
-                round();
-                round();
-                const uint32_t bl = tlo_v, bh = thi_v;
-                round();
-                if (!__any_sync(0xFFFFFFFFu, tlo_v != bl || thi_v != bh)) break;
+            if (k <= 1) {
+                // the root path rides in slot 1 of h0 while settling
+                h0 = (h0 & 0xFFFFu) | (h3 & 0xFFFF0000u);
+                for (;;) {
+                    pair_round(h0, has);
+                    pair_round(h0, has);
+                    pair_round(h0, has);
+                    const uint32_t b0 = h0;
+                    pair_round(h0, has);
+                    if (!__any_sync(0xFFFFFFFFu, h0 != b0)) break;
+                }
+                h3 = h0 & 0xFFFF0000u;
+                h0 &= 0xFFFFu;
+            } else if (k <= 3) {
+                h1 = (h1 & 0xFFFFu) | (h3 & 0xFFFF0000u);
+                for (;;) {
+                    pair_round(h0, has);
+                    pair_round(h1, has);
+                    pair_round(h0, has);
+                    pair_round(h1, has);
+                    const uint32_t b0 = h0, b1 = h1;
+                    pair_round(h0, has);
+                    pair_round(h1, has);
+                    if (!__any_sync(0xFFFFFFFFu, h0 != b0 || h1 != b1)) break;
+                }
+                h3 = h1 & 0xFFFF0000u;
+                h1 &= 0xFFFFu;
+            } else {
+                for (;;) {
+                    pair_round(h0, has);
+                    pair_round(h1, has);
+                    pair_round(h2, has);
+                    pair_round(h3, has);
+                    const uint32_t b0 = h0, b1 = h1, b2 = h2, b3 = h3;
+                    pair_round(h0, has);
+                    pair_round(h1, has);
+                    pair_round(h2, has);
+                    pair_round(h3, has);
+                    if (!__any_sync(0xFFFFFFFFu, h0 != b0 || h1 != b1 || h2 != b2 || h3 != b3)) break;
+                }
             }
         }
+        // back to bytes: a valid half 0x8000 + b gives b (<= 34), else 0
+        auto unbias = [](uint32_t h) {
+            const uint32_t lo = (h & 0x8000u) ? (h & 0xFFu) : 0u;
+            const uint32_t hi = (h & 0x80000000u) ? ((h >> 16) & 0xFFu) : 0u;
+            return lo | (hi << 8);
+        };
+        const uint32_t tlo_v = unbias(h0) | (unbias(h1) << 16);
+        const uint32_t thi_v = unbias(h2) | (unbias(h3) << 16);
         if (valid) {
             tlo[f] = tlo_v;
             thi[f] = thi_v;
@@ -668,11 +720,16 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 const uint32_t nd = valid ? ndp[f] : 0u;
                 uint32_t best = 0;
                 bool dmb = (a & 0x80u) != 0;
-                for (uint32_t i = 0; i < k; ++i) {
-                    const uint32_t x = ifc[c0 + i];
+                // interface values: all gathers issued together (broadcast loads)
+                uint32_t xs[kMaxIface];
+#pragma unroll
+                for (uint32_t i = 0; i < kMaxIface; ++i) xs[i] = i < k ? ifc[c0 + i] : (uint32_t)f;
+#pragma unroll
+                for (uint32_t i = 0; i < kMaxIface; ++i) {
+                    const uint32_t dx = dep[xs[i]], fx = flg[xs[i]];
                     const uint32_t by = i < 4 ? (tl >> (8 * i)) & 0xFFu : (th >> (8 * (i - 4))) & 0xFFu;
-                    best = by ? max(best, (uint32_t)dep[x] + by - 1u) : best;
-                    dmb |= ((a >> i) & 1u) && (flg[x] & FL_DOOMED);
+                    best = (i < k && by) ? max(best, dx + by - 1u) : best;
+                    dmb |= i < k && ((a >> i) & 1u) && (fx & FL_DOOMED);
                 }
                 const uint32_t c7 = th >> 24;
                 best = c7 ? max(best, c7 - 1u) : best;
@@ -680,6 +737,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
                 allres = (a & 0x100u) != 0;
                 const bool pend = stf == 0u;
                 doom = pend && dmb;
+                if (p.prof) { const long long t = clock64() + (long long)(d + doom); cyc_edge += t - cyc_t; cyc_t = t; }
                 if (__any_sync(0xFFFFFFFFu, doom)) {
                     for (;;) {
                         const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
@@ -904,6 +962,12 @@ __global__ void __launch_bounds__(kK1Threads) k1_sweep(SweepParams p) {
         atomicAdd(&p.counters[C_ELIG], n_elig);
         atomicAdd(&p.counters[C_DOOMED], s_cnt[2]);
     }
+}
+
+__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    if (p.blk_staged[blockIdx.x]) k1_body<true>(p, smem);
+    else k1_body<false>(p, smem);
 }
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once

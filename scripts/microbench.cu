@@ -69,6 +69,28 @@ __global__ void bench(unsigned long long* out, int seed) {
     }
     if (lane == 0) out[9] = x;
 }
+// the 4-shuffle settling round with W warps on one SM (all busy): cycles per round per warp
+__global__ void contention(unsigned long long* out, int nshfl) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t d = lane, s0 = (lane + 1) & 31, s1 = (lane + 5) & 31, s2 = (lane + 9) & 31, s3 = (lane + 17) & 31;
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int i = 0; i < N; ++i) {
+        uint32_t a, b, c, e;
+        asm volatile("shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\tshfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                     "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\tshfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                     : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+        d = max(d, max(max(a, b), max(c, e)) + 1u) & 0xFFFFF;
+        if (nshfl == 8) {
+            asm volatile("shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\tshfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                         "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\tshfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "r"(d ^ 1u), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+            d = max(d, max(max(a, b), max(c, e))) & 0xFFFFF;
+        }
+    }
+    const long long t1 = clock64();
+    if (lane == 0) out[warp] = (t1 - t0) + (d == 12345u);
+}
 int main() {
     unsigned long long* d; unsigned long long h[12];
     cudaMalloc(&d, 96);
@@ -78,5 +100,14 @@ int main() {
     for (int i = 0; i < 9; ++i) printf("%-26s %7.1f cycles/op\n", nm[i], (double)h[i] / N);
     printf("%-26s %7.1f cycles/round\n", "round: 4 shfl + max chain", (double)h[10] / N);
     printf("%-26s %7.1f cycles/round\n", "round: 1 shfl + max", (double)h[11] / N);
+    unsigned long long* c; cudaMalloc(&c, 32 * 8);
+    for (int ns = 4; ns <= 8; ns += 4)
+        for (int W = 1; W <= 32; W *= 2) {
+            contention<<<1, 32 * W>>>(c, ns); cudaDeviceSynchronize();
+            contention<<<1, 32 * W>>>(c, ns);
+            unsigned long long hc[32]; cudaMemcpy(hc, c, 8 * W, cudaMemcpyDeviceToHost);
+            unsigned long long mx = 0; for (int w = 0; w < W; ++w) mx = hc[w] > mx ? hc[w] : mx;
+            printf("contention: %d shfl/round, %2d warps: %7.1f cycles/round (slowest warp)\n", ns, W, (double)mx / N);
+        }
     return 0;
 }
