@@ -13,9 +13,13 @@ HEADER = os.path.join(ROOT, "include", "nalar.h")
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2601_05109_b200.build import build_lib
-    path = build_lib()
-    return path
+    # loaded by path: importing the package would load libnalar.so before it exists
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_nalar_build", os.path.join(ROOT, "paper_2601_05109_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build_lib()
 
 
 def _declared():
