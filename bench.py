@@ -383,7 +383,8 @@ def main():
                          "algorithmic_bytes": dom_b, "peak_source": peak_src},
             "e2e": {"value": total_fut / e2e_mean, "unit": "futures/s", "ms_per_step": e2e_mean * 1e3,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": 2 * args.steps,
+            # per epoch: k_zero (exchange buffer + counters), k1_sweep, k4_assign
+            "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
             "paper_context": "464 ms per global-control-loop at 131K futures, Python+gRPC+Redis on "
                              "64 emulated CPU nodes (PAPER.md:715); context, not the target"}
