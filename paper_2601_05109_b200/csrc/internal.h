@@ -57,6 +57,7 @@ struct SweepParams {
     const uint32_t* blk_row0;   // [B+1] first row of each block
     const uint32_t* blk_edge0;  // [B+1] first edge of each block
     const uint8_t* blk_staged;  // [B]   1 = rows staged in shared memory by TMA
+    const uint32_t* wf_perm;    // [W]   per block: local workflow indices, largest first (task order)
     uint32_t B, n_types, n_inst, R, levels, policy;
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks

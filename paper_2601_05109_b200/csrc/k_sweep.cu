@@ -65,6 +65,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+// step-done flag of a long workflow's transfer (P2a -> P2b hand-off inside the
+// block): the producer warp publishes with release, the composing warp acquires
+__device__ __forceinline__ void st_release_u16(uint16_t* p, uint16_t v) {
+    asm volatile("st.release.cta.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u16(const uint16_t* p) {
+    uint16_t v;
+    asm volatile("ld.acquire.cta.b16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+    return v;
+}
+constexpr uint32_t kStepDone = 0x4000u;   // aux[c0] bit: the step's transfer is written
+
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -88,6 +100,62 @@ __device__ __forceinline__ Win window(const void* base, size_t elem, size_t lo, 
     return w;
 }
 
+// Settling of a step transfer (see transfer_step): slots are biased u16
+// halves of NP packed words; a round is K shuffles per word (K = the widest
+// row's in-step predecessors) and a native u16x2 max tree.  Issue slots, not
+// the shuffle pipe, bound P2a (all 16 warps settle at once), so the round is
+// kept to K + (K - 1) + 3 instructions per word.
+template <int K, int NP>
+__device__ __forceinline__ uint32_t settle_pairs(uint32_t& h0, uint32_t& h1, uint32_t& h2, uint32_t& h3, bool has,
+                                                 uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
+    auto vmax2 = [](uint32_t x, uint32_t y) {
+        uint32_t r;
+        asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+        return r;
+    };
+    auto round = [&](uint32_t& x) {
+        uint32_t m = __shfl_sync(0xFFFFFFFFu, x, s0);
+        if (K > 1) m = vmax2(m, __shfl_sync(0xFFFFFFFFu, x, s1));
+        if (K > 2) m = vmax2(m, __shfl_sync(0xFFFFFFFFu, x, s2));
+        if (K > 3) m = vmax2(m, __shfl_sync(0xFFFFFFFFu, x, s3));
+        x = has ? vmax2(x, m + 0x00010001u) : x;
+    };
+    auto all = [&]() {
+        round(h0);
+        if (NP > 1) round(h1);
+        if (NP > 2) { round(h2); round(h3); }
+    };
+    uint32_t it = 0;
+    for (;;) {
+        all();
+        all();
+        all();
+        const uint32_t b0 = h0, b1 = h1, b2 = h2, b3 = h3;
+        all();
+        ++it;
+        if (!__any_sync(0xFFFFFFFFu, h0 != b0 || h1 != b1 || h2 != b2 || h3 != b3)) break;
+    }
+    return it;
+}
+
+// In-step doom closure (doom reaches a PENDING row through a DEP edge from a
+// doomed / FAILED row; Q3).  Rows of a step are in topological order, so one
+// ascending walk over the lanes settles it: every lane's DEP-predecessor mask
+// is fetched by 32 independent shuffles issued back to back, then the walk is
+// a chain of three ALU ops per lane (instead of one ballot per link of the
+// longest in-step chain).
+__device__ __forceinline__ bool doom_closure(bool doom, bool pend, uint32_t need_dep) {
+    uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
+    if (D == 0u) return false;
+    const uint32_t mine = pend ? need_dep : 0u;       // only PENDING rows become doomed
+    uint32_t nj[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) nj[j] = __shfl_sync(0xFFFFFFFFu, mine, j);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) D |= (nj[j] & D) ? 1u << j : 0u;
+    return (D >> (threadIdx.x & 31u)) & 1u;
+}
+
 }  // namespace
 
 size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
@@ -101,7 +169,8 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
 
 size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
     size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs) +
-               align16(4 * ((size_t)wfs + 1));                                           // per-workflow tables
+               align16(4 * ((size_t)wfs + 1)) + align16(4 * (size_t)wfs) +
+               align16(32 * (size_t)wfs);                                                // per-workflow tables
     if (staged)
         b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
              align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
@@ -134,7 +203,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     uint8_t* sp = smem;
     uint64_t* mbar = (uint64_t*)sp;
     uint32_t* s_ticket = (uint32_t*)(sp + 8);
-    uint32_t* s_cnt = (uint32_t*)(sp + 16);      // [0] ready [1] elig [2] doomed
+    uint32_t* s_cnt = (uint32_t*)(sp + 16);      // [0] ready [1] elig [2] doomed [3] long workflows
     sp += 64;
     uint32_t* s_load = (uint32_t*)sp;
     sp += 4 * (size_t)I;
@@ -150,7 +219,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
 
     // ---- per-workflow tables (always in smem) -------------------------------
     uint8_t* q = smem + p.fixed_smem;
-    unsigned long long* s_winfl = (unsigned long long*)q;   // [nw] types with futures in flight
+    uint32_t* s_winfl = (uint32_t*)q;                        // [nw][2] types with futures in flight (bitset)
     uint32_t* s_wfp = (uint32_t*)(q + 8 * (size_t)nw);       // [nw][T] first PENDING non-doomed row
     uint32_t* s_wfru = s_wfp + (size_t)nw * T;               // [nw][T] first ready unpinned row
     q += align16((size_t)nw * (8 * (size_t)T + 8));
@@ -158,7 +227,10 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     q += align16(4 * (size_t)nw);
     uint32_t* s_lpref = (uint32_t*)q;                        // [nw+1] long-workflow step tasks
     q += align16(4 * ((size_t)nw + 1));
-    uint32_t* s_ticket2 = (uint32_t*)(smem + 32);
+    uint32_t* s_perm = (uint32_t*)q;                         // [nw] task order, largest first
+    q += align16(4 * (size_t)nw);
+    uint32_t* s_agg = (uint32_t*)q;                          // [nw][8] counts (P3), max depth (sweep)
+    q += align16(32 * (size_t)nw);
 
     // ---- the block's slice of the table: staged in smem by TMA, or in place --
     const uint8_t* st;    // state, type, round, pin, executor: indexed by local row
@@ -250,7 +322,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     for (uint32_t r = tid; r < R; r += kK1Threads) s_rcnt[r] = 0;
     for (uint32_t t = tid; t < T; t += kK1Threads) s_aff[t] = p.t_aff[t];
     for (uint32_t k = tid; k < nw * T; k += kK1Threads) { s_wfp[k] = 0xFFFFFFFFu; s_wfru[k] = 0xFFFFFFFFu; }
-    for (uint32_t k = tid; k < nw; k += kK1Threads) s_winfl[k] = 0ull;
+    for (uint32_t k = tid; k < nw; k += kK1Threads) { s_winfl[2 * k] = 0u; s_winfl[2 * k + 1] = 0u; s_perm[k] = p.wf_perm[w0 + k]; }
+    for (uint32_t k = tid; k < 8 * nw; k += kK1Threads) s_agg[k] = 0;
+    for (uint32_t k = tid; k < nr; k += kK1Threads) aux[k] = 0;   // step-done flags
     if (tid == 0) {
         *s_ticket = 0;
         s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
@@ -272,14 +346,14 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     // steps in order on one warp with a cheap evaluation per step.  Steps that
     // do not fit (wide interface / fan-in) fall back to the ordinary sweep step
     // in P2b.
-    uint32_t n_ready = 0, n_doom = 0;
     auto is_long = [&](uint32_t wi) { return wfo[wi + 1] - wfo[wi] >= 32u * kLongSteps; };
     // long-step task prefix over workflows (warp 0), s_lpref[nw] = total
     if (warp == 0) {
-        uint32_t carry = 0;
+        uint32_t carry = 0, nlong = 0;
         for (uint32_t b0 = 0; b0 < nw; b0 += 32) {
             const uint32_t wi = b0 + lane;
             const uint32_t n = (wi < nw && is_long(wi)) ? (wfo[wi + 1] - wfo[wi] + 31u) / 32u : 0u;
+            nlong += __popc(__ballot_sync(0xFFFFFFFFu, n != 0u));
             uint32_t incl = n;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -289,79 +363,56 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             if (wi < nw) s_lpref[wi] = carry + incl - n;
             carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        if (lane == 0) { s_lpref[nw] = carry; *s_ticket2 = 0; }
+        if (lane == 0) { s_lpref[nw] = carry; s_cnt[3] = nlong; }
     }
     __syncthreads();
     const uint32_t n_long_tasks = s_lpref[nw];
+    // The largest long workflows (at most two) are composed from the start by
+    // warps 0 / 1: the compose chain is the block's critical path, so it
+    // follows the transfers step by step instead of starting behind them.
+    const uint32_t n_early = min(s_cnt[3], 2u);
 
-    uint32_t c_pend = 0, c_ready = 0, c_infl = 0, c_res = 0, c_fail = 0, c_doom = 0, c_pinp = 0;
     uint32_t m_dep = 0, m_rnd = 0;
-    long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = 0;
-    uint32_t n_rounds = 0, n_k[5] = {0, 0, 0, 0, 0};
+    long long cyc_edge = 0, cyc_round = 0, cyc_rest = 0, cyc_t = 0, cyc_wait = 0;
+    uint32_t n_rounds = 0;
+    unsigned long long n_kp = 0;   // profile: steps by widest in-step fan-in K (12-bit fields)
     auto wf_begin = [&](uint32_t wi) {
-        c_pend = c_ready = c_infl = c_res = c_fail = c_doom = c_pinp = 0;
         m_dep = m_rnd = 0;
-        cyc_edge = cyc_round = cyc_rest = 0;
+        cyc_edge = cyc_round = cyc_rest = cyc_wait = 0;
         cyc_t = p.prof ? clock64() : 0;
         n_rounds = 0;
-        n_k[0] = n_k[1] = n_k[2] = n_k[3] = n_k[4] = 0;
+        n_kp = 0;
         if (p.prof && lane == 0) p.prof[(size_t)(w0 + wi) * 2] = gtimer();
     };
     auto wf_end = [&](uint32_t wi) {
-        const uint32_t w = w0 + wi, fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
+        const uint32_t w = w0 + wi;
         m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
         m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
-        n_ready += c_ready;
-        n_doom += c_doom;
-        if (lane < 10) {
-            uint32_t v = fb - fa;
-            v = lane == 1 ? c_pend : v;
-            v = lane == 2 ? c_ready : v;
-            v = lane == 3 ? c_infl : v;
-            v = lane == 4 ? c_res : v;
-            v = lane == 5 ? c_fail : v;
-            v = lane == 6 ? c_doom : v;
-            v = lane == 7 ? c_pinp : v;
-            v = lane == 8 ? m_dep : v;
-            v = lane == 9 ? m_rnd : v;
-            p.wf_agg[(size_t)w * 10 + lane] = v;
-        }
-        if (lane == 0) s_wrnd[wi] = m_rnd;
+        if (lane == 0) { s_wrnd[wi] = m_rnd; s_agg[wi * 8 + 7] = m_dep; }
         if (p.prof && lane == 0) {
             p.prof[(size_t)w * 2 + 1] = gtimer();
             cyc_rest += clock64() - cyc_t;
             unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)w * 4;
             c[0] = cyc_edge; c[1] = cyc_round; c[2] = cyc_rest;
-            c[3] = n_rounds | ((unsigned long long)n_k[1] << 16) | ((unsigned long long)n_k[2] << 28) |
-                   ((unsigned long long)n_k[3] << 40) | ((unsigned long long)n_k[4] << 52);
+            c[3] = cyc_wait ? (unsigned long long)cyc_wait << 32 : (n_rounds | n_kp);
         }
         __syncwarp();
     };
-    // final depth / doom of a step's rows -> smem, flags, per-workflow aggregates
-    auto finish_step = [&](uint32_t f, bool valid, uint32_t stf, uint32_t d, bool doom, bool allres, uint32_t rdf,
-                           int pnf) {
-        const bool pend = stf == 0u;
-        const bool ready = pend && !doom && allres;
+    // final depth / doom of a step's rows -> smem (the per-workflow counts are
+    // taken row-parallel in P3; the maxima ride along here)
+    auto finish_step = [&](uint32_t f, bool valid, uint32_t d, bool doom, bool allres, uint32_t rdf) {
         if (valid) {
             dep[f] = (uint16_t)d;
-            flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0) | (ready ? FL_READY : 0));
+            flg[f] = (uint8_t)((allres ? FL_ALLRES : 0) | (doom ? FL_DOOMED : 0));
             m_dep = max(m_dep, d);
             m_rnd = max(m_rnd, rdf);
         }
-        // per-workflow aggregates by ballots ("aggregating")
-        c_pend += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend));
-        c_ready += __popc(__ballot_sync(0xFFFFFFFFu, ready));
-        c_infl += __popc(__ballot_sync(0xFFFFFFFFu, valid && (stf == 1u || stf == 2u)));
-        c_res += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 3u));
-        c_fail += __popc(__ballot_sync(0xFFFFFFFFu, valid && stf == 4u));
-        c_doom += __popc(__ballot_sync(0xFFFFFFFFu, doom));
-        c_pinp += __popc(__ballot_sync(0xFFFFFFFFu, valid && pend && pnf >= 0));
         __syncwarp();
     };
     // the ordinary sweep step: predecessors before the step are final in smem;
     // those inside it settle by Bellman-Ford rounds
-    auto regular_step = [&](uint32_t c0, uint32_t stf, uint32_t eb, uint32_t ee, uint32_t pva, uint32_t pvb,
-                            uint32_t& d_out, bool& doom_out, bool& allres_out) {
+    auto regular_step = [&](uint32_t c0, bool valid, uint32_t stf, uint32_t eb, uint32_t ee, uint32_t pva,
+                            uint32_t pvb, uint32_t& d_out, bool& doom_out, bool& allres_out) {
         // predecessors before this step are final in smem; those inside the
         // step are kept as up to 4 lane slots (+ a mask for any extra ones)
         uint32_t d = 0, need_dep = 0, extra = 0, np = 0;
@@ -419,7 +470,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                 // the common case: at most 4 slots, and only as many shuffles
                 // per round as the step's widest row needs
                 const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
-                n_k[K < 4 ? K : 4]++;
+                if (p.prof) n_kp += 1ull << (16 + 12 * ((K < 4 ? K : 4) - 1));
                 auto settle = [&](auto round) {
                     for (;;) {
                         round();
@@ -470,17 +521,22 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                     });
                 }
             } else {
+                // a row with more than four in-step predecessors (a fan-in,
+                // e.g. the aggregate of many subtasks) reads the extra ones
+                // from shared memory: every round the lanes publish their
+                // current depth in their own row's slot (clamped -- exact,
+                // the final saturation absorbs it) and only the wide lanes
+                // loop over their extra bits
                 auto round = [&]() {
                     const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, d, s0);
                     const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, d, s1);
                     const uint32_t x2 = __shfl_sync(0xFFFFFFFFu, d, s2);
                     const uint32_t x3 = __shfl_sync(0xFFFFFFFFu, d, s3);
                     uint32_t nd = max(max(x0, x1), max(x2, x3)) + 1u;
-#pragma unroll 1
-                    for (uint32_t k = 0; k < 32; ++k) {
-                        const uint32_t x = __shfl_sync(0xFFFFFFFFu, d, k);
-                        if ((extra >> k) & 1u) nd = max(nd, x + 1u);
-                    }
+                    if (valid) dep[c0 + lane] = (uint16_t)min(d, 65535u);
+                    __syncwarp();
+                    for (uint32_t e = extra; e; e &= e - 1u) nd = max(nd, (uint32_t)dep[c0 + __ffs(e) - 1u] + 1u);
+                    __syncwarp();
                     d = has ? max(d, nd) : d;
                 };
                 for (;;) {
@@ -489,14 +545,8 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                     if (!__any_sync(0xFFFFFFFFu, d != before)) break;
                 }
             }
-            if (__any_sync(0xFFFFFFFFu, doom)) {
-                for (;;) {
-                    const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
-                    doom = doom || (pend && (need_dep & D) != 0u);
-                    if (__ballot_sync(0xFFFFFFFFu, doom) == D) break;
-                }
-            }
         }
+        doom = doom_closure(doom, pend, need_dep);
         d_out = min(d, 65535u);
         doom_out = doom;
         allres_out = allres;
@@ -509,7 +559,6 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         // the next step's row inputs and first two edge words are loaded one
         // step ahead, so their shared-memory latency hides behind this step
         uint32_t q_st = 3u, q_eb = 0u, q_ee = 0u, q_va = 0u, q_vb = 0u, q_rd = 0u;
-        int q_pn = -1;
         auto prefetch = [&](uint32_t c) {
             const uint32_t g = c + lane;
             const bool ok = g < fb;
@@ -517,7 +566,6 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             q_eb = ok ? eo[g] - e0 : 0u;
             q_ee = ok ? eo[g + 1] - e0 : 0u;
             q_rd = ok ? rd[g] : 0u;
-            q_pn = ok ? pn[g] : -1;
             q_va = q_eb < q_ee ? ed[q_eb] : 0u;
             q_vb = q_eb + 1 < q_ee ? ed[q_eb + 1] : 0u;
         };
@@ -527,18 +575,29 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
             const uint32_t stf = q_st, eb = q_eb, ee = q_ee, rdf = q_rd;
-            const int pnf = q_pn;
             const uint32_t pva = q_va, pvb = q_vb;
             if (c0 + 32 < fb) prefetch(c0 + 32);
             uint32_t d;
             bool doom, allres;
-            regular_step(c0, stf, eb, ee, pva, pvb, d, doom, allres);
-            finish_step(f, valid, stf, d, doom, allres, rdf, pnf);
+            regular_step(c0, valid, stf, eb, ee, pva, pvb, d, doom, allres);
+            finish_step(f, valid, d, doom, allres, rdf);
         }
         wf_end(wi);
     };
     // P2a: the transfer function of one step of a long workflow
+    // NALAR_F_PROFILE: per-block cycle sums of the transfer phases
+    unsigned long long* tprof =
+        p.prof ? p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)p.n_wf * 4 + b * 8 : nullptr;
+    long long tt = 0;
+    auto tstamp = [&](int j) {
+        if (tprof) {
+            const long long t = clock64();
+            if (lane == 0 && j > 0) atomicAdd(&tprof[j - 1], (unsigned long long)(t - tt));
+            tt = t;
+        }
+    };
     auto transfer_step = [&](uint32_t c0, uint32_t fb) {
+        tstamp(0);
         const uint32_t f = c0 + lane;
         const bool valid = f < fb;
         const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
@@ -579,6 +638,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         s1 = np > 1 ? s1 : s0;
         s2 = np > 2 ? s2 : s0;
         s3 = np > 3 ? s3 : s0;
+        tstamp(1);
         // the step's interface: distinct out-of-step rows, ascending, <= 7
         uint32_t k = 0, myx = 0, i0 = 0, i1 = 0, i2 = 0, i3 = 0, taken = 0;
         for (;;) {
@@ -601,18 +661,23 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         // transfer bytes: byte i < k = 1 + longest path from x_i into this row,
         // byte 7 = 1 + longest path from a root of the step (0 = none).
         // While settling, slot i lives in 16-bit half (i & 1) of h[i >> 1]
-        // (slot 7 = the root path) with a bias: a valid value b is 0x8000 + b,
-        // "no path" is anything below 0x8000.  Then the step "1 + longest
-        // path over in-step predecessors" is one native u16x2 max tree plus a
-        // plain add of 1 per half (invalid halves stay far below the bias),
-        // and since +1 is monotone it is applied once after the max.
+        // (slot 7 = the root path; with k <= 1 it rides in the free half of
+        // h[0], with k <= 3 in that of h[1]) with a bias: a valid value b is
+        // 0x8000 + b, "no path" is anything below 0x8000.  A settling round is
+        // then a native u16x2 max tree plus a plain add of 1 per half (invalid
+        // halves stay far below the bias); +1 is monotone, so it is applied
+        // once after the max.
+        const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
+        const uint32_t NPw = k <= 1 ? 1u : (k <= 3 ? 2u : 4u);
+        const uint32_t root_slot = k <= 1 ? 1u : (k <= 3 ? 3u : 7u);
         uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, edm = 0;
         auto seth = [&](uint32_t i, uint32_t v) {
-            const uint32_t x = (0x8000u + v) << (16 * (i & 1u));
-            h0 = (i >> 1) == 0 ? (h0 | x) : h0;
-            h1 = (i >> 1) == 1 ? (h1 | x) : h1;
-            h2 = (i >> 1) == 2 ? (h2 | x) : h2;
-            h3 = (i >> 1) == 3 ? (h3 | x) : h3;
+            const uint32_t sl = i == 7u ? root_slot : i;
+            const uint32_t x = (0x8000u + v) << (16 * (sl & 1u));
+            h0 = (sl >> 1) == 0 ? (h0 | x) : h0;
+            h1 = (sl >> 1) == 1 ? (h1 | x) : h1;
+            h2 = (sl >> 1) == 2 ? (h2 | x) : h2;
+            h3 = (sl >> 1) == 3 ? (h3 | x) : h3;
         };
         if (ok && valid) {
             if (no > 0) { seth(i0, 2u); edm |= (odep & 1u) ? (1u << i0) : 0u; }
@@ -621,86 +686,56 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             if (no > 3) { seth(i3, 2u); edm |= (odep & 8u) ? (1u << i3) : 0u; }
             if (ee == eb) seth(7u, 1u);              // a root: c = 0
         }
-        auto vmax2 = [](uint32_t x, uint32_t y) {
-            uint32_t r;
-            asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
-            return r;
-        };
-        // one settling round on a pair of slots (4 shuffles, 3 + 1 maxes, 1 add)
-        auto pair_round = [&](uint32_t& h, bool has) {
-            uint32_t l0, l1, l2, l3;
-            asm volatile(
-                "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
-                "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
-                "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
-                "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
-                : "=r"(l0), "=r"(l1), "=r"(l2), "=r"(l3)
-                : "r"(h), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
-            const uint32_t nl = vmax2(vmax2(l0, l1), vmax2(l2, l3)) + 0x00010001u;
-            h = has ? vmax2(h, nl) : h;
-        };
-        if (ok && __any_sync(0xFFFFFFFFu, np != 0u)) {
+        tstamp(2);
+        uint32_t nit = 0;
+        if (ok && K != 0u) {
             const bool has = np != 0u;
-            if (k <= 1) {
-                // the root path rides in slot 1 of h0 while settling
-                h0 = (h0 & 0xFFFFu) | (h3 & 0xFFFF0000u);
-                for (;;) {
-                    pair_round(h0, has);
-                    pair_round(h0, has);
-                    pair_round(h0, has);
-                    const uint32_t b0 = h0;
-                    pair_round(h0, has);
-                    if (!__any_sync(0xFFFFFFFFu, h0 != b0)) break;
-                }
-                h3 = h0 & 0xFFFF0000u;
-                h0 &= 0xFFFFu;
-            } else if (k <= 3) {
-                h1 = (h1 & 0xFFFFu) | (h3 & 0xFFFF0000u);
-                for (;;) {
-                    pair_round(h0, has);
-                    pair_round(h1, has);
-                    pair_round(h0, has);
-                    pair_round(h1, has);
-                    const uint32_t b0 = h0, b1 = h1;
-                    pair_round(h0, has);
-                    pair_round(h1, has);
-                    if (!__any_sync(0xFFFFFFFFu, h0 != b0 || h1 != b1)) break;
-                }
-                h3 = h1 & 0xFFFF0000u;
-                h1 &= 0xFFFFu;
-            } else {
-                for (;;) {
-                    pair_round(h0, has);
-                    pair_round(h1, has);
-                    pair_round(h2, has);
-                    pair_round(h3, has);
-                    const uint32_t b0 = h0, b1 = h1, b2 = h2, b3 = h3;
-                    pair_round(h0, has);
-                    pair_round(h1, has);
-                    pair_round(h2, has);
-                    pair_round(h3, has);
-                    if (!__any_sync(0xFFFFFFFFu, h0 != b0 || h1 != b1 || h2 != b2 || h3 != b3)) break;
-                }
+#define NALAR_SETTLE(NP_)                                                             \
+            switch (K) {                                                              \
+                case 1: nit = settle_pairs<1, NP_>(h0, h1, h2, h3, has, s0, s1, s2, s3); break;    \
+                case 2: nit = settle_pairs<2, NP_>(h0, h1, h2, h3, has, s0, s1, s2, s3); break;    \
+                case 3: nit = settle_pairs<3, NP_>(h0, h1, h2, h3, has, s0, s1, s2, s3); break;    \
+                default: nit = settle_pairs<4, NP_>(h0, h1, h2, h3, has, s0, s1, s2, s3); break;   \
             }
+            if (NPw == 1u) { NALAR_SETTLE(1) }
+            else if (NPw == 2u) { NALAR_SETTLE(2) }
+            else { NALAR_SETTLE(4) }
+#undef NALAR_SETTLE
         }
-        // back to bytes: a valid half 0x8000 + b gives b (<= 34), else 0
-        auto unbias = [](uint32_t h) {
-            const uint32_t lo = (h & 0x8000u) ? (h & 0xFFu) : 0u;
-            const uint32_t hi = (h & 0x80000000u) ? ((h >> 16) & 0xFFu) : 0u;
+        tstamp(3);
+        if (tprof && lane == 0) { atomicAdd(&tprof[5], 1ull); atomicAdd(&tprof[6], (unsigned long long)K); atomicAdd(&tprof[7], (unsigned long long)k); atomicAdd(&tprof[4], (unsigned long long)nit); }
+        // move the root path to slot 7 (half 1 of h[3]) and unbias to bytes:
+        // a valid half 0x8000 + b gives b (<= 34), else 0
+        if (root_slot == 1u) {
+            h3 = h0 & 0xFFFF0000u;
+            h0 &= 0xFFFFu;
+        } else if (root_slot == 3u) {
+            h3 = h1 & 0xFFFF0000u;
+            h1 &= 0xFFFFu;
+        }
+        auto unbias = [](uint32_t x) {
+            const uint32_t lo = (x & 0x8000u) ? (x & 0xFFu) : 0u;
+            const uint32_t hi = (x & 0x80000000u) ? ((x >> 16) & 0xFFu) : 0u;
             return lo | (hi << 8);
         };
         const uint32_t tlo_v = unbias(h0) | (unbias(h1) << 16);
         const uint32_t thi_v = unbias(h2) | (unbias(h3) << 16);
+        const uint32_t av = edm | (failp ? 0x80u : 0u) | (allres ? 0x100u : 0u);
+
         if (valid) {
             tlo[f] = tlo_v;
             thi[f] = thi_v;
             ndp[f] = need_dep;
-            aux[f] = (uint16_t)(edm | (failp ? 0x80u : 0u) | (allres ? 0x100u : 0u) |
-                                (lane == 0 ? ((k << 9) | (ok ? 0x2000u : 0u)) : 0u));
+            if (lane != 0) aux[f] = (uint16_t)av;
         }
         if (lane < k && ok) ifc[c0 + lane] = myx;
+        // publish: lane 0's aux word (k, ok) doubles as the step-done flag
+        __syncwarp();
+        if (lane == 0) st_release_u16(&aux[c0], (uint16_t)(av | (k << 9) | (ok ? 0x2000u : 0u) | kStepDone));
+        tstamp(4);
     };
-    // P2b: compose the steps of a long workflow in order
+    // P2b: compose the steps of a long workflow in order: a step needs the
+    // depths / doom flags of its <= 7 interface rows, all in earlier steps
     auto compose_workflow = [&](uint32_t wi) {
         const uint32_t fa = wfo[wi] - r0, fb = wfo[wi + 1] - r0;
         wf_begin(wi);
@@ -708,9 +743,18 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
-            const uint32_t stf = valid ? st[f] : 3u, rdf = valid ? rd[f] : 0u;
-            const int pnf = valid ? pn[f] : -1;
-            const uint32_t a0 = aux[c0];
+            const uint32_t rdf = valid ? rd[f] : 0u;
+            const uint32_t stf = valid ? st[f] : 3u;
+            // the step's transfer comes from another warp (P2a); wait for it
+            uint32_t a0 = ld_acquire_u16(&aux[c0]);
+            if (!(a0 & kStepDone)) {
+                const long long tw = p.prof ? clock64() : 0;
+                do {
+                    __nanosleep(20);
+                    a0 = ld_acquire_u16(&aux[c0]);
+                } while (!(a0 & kStepDone));
+                if (p.prof) cyc_wait += clock64() - tw;
+            }
             uint32_t d;
             bool doom, allres;
             if (a0 & 0x2000u) {
@@ -719,44 +763,43 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                 const uint32_t a = valid ? aux[f] : 0x100u;
                 const uint32_t nd = valid ? ndp[f] : 0u;
                 uint32_t best = 0;
-                bool dmb = (a & 0x80u) != 0;
-                // interface values: all gathers issued together (broadcast loads)
+                bool dm = (a & 0x80u) != 0;
+                // interface depths / flags: all gathers issued together (broadcast loads)
                 uint32_t xs[kMaxIface];
 #pragma unroll
-                for (uint32_t i = 0; i < kMaxIface; ++i) xs[i] = i < k ? ifc[c0 + i] : (uint32_t)f;
+                for (uint32_t i = 0; i < kMaxIface; ++i) xs[i] = i < k ? ifc[c0 + i] : c0;
 #pragma unroll
                 for (uint32_t i = 0; i < kMaxIface; ++i) {
                     const uint32_t dx = dep[xs[i]], fx = flg[xs[i]];
                     const uint32_t by = i < 4 ? (tl >> (8 * i)) & 0xFFu : (th >> (8 * (i - 4))) & 0xFFu;
                     best = (i < k && by) ? max(best, dx + by - 1u) : best;
-                    dmb |= i < k && ((a >> i) & 1u) && (fx & FL_DOOMED);
+                    dm |= i < k && ((a >> i) & 1u) && (fx & FL_DOOMED);
                 }
                 const uint32_t c7 = th >> 24;
                 best = c7 ? max(best, c7 - 1u) : best;
                 d = min(best, 65535u);
                 allres = (a & 0x100u) != 0;
-                const bool pend = stf == 0u;
-                doom = pend && dmb;
-                if (p.prof) { const long long t = clock64() + (long long)(d + doom); cyc_edge += t - cyc_t; cyc_t = t; }
-                if (__any_sync(0xFFFFFFFFu, doom)) {
-                    for (;;) {
-                        const uint32_t D = __ballot_sync(0xFFFFFFFFu, doom);
-                        doom = doom || (pend && (nd & D) != 0u);
-                        if (__ballot_sync(0xFFFFFFFFu, doom) == D) break;
-                    }
-                }
+                if (p.prof) { const long long t = clock64() + (long long)d; cyc_edge += t - cyc_t; cyc_t = t; }
+                doom = doom_closure(stf == 0u && dm, stf == 0u, nd);
                 if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
             } else {
                 const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
                 const uint32_t pva = eb < ee ? ed[eb] : 0u, pvb = eb + 1 < ee ? ed[eb + 1] : 0u;
-                regular_step(c0, stf, eb, ee, pva, pvb, d, doom, allres);
+                regular_step(c0, valid, stf, eb, ee, pva, pvb, d, doom, allres);
             }
-            finish_step(f, valid, stf, d, doom, allres, rdf, pnf);
+            finish_step(f, valid, d, doom, allres, rdf);
         }
         wf_end(wi);
     };
 
-    // P2a: long-workflow steps and whole short workflows, by ticket
+    // Tasks by ticket (after the early composes above): every step transfer of
+    // the block's long workflows (P2a), then the remaining workflows largest
+    // first -- a long one is composed, a short one swept.  A composing warp
+    // follows its transfers step by step, waiting on the producer's release
+    // flag.  Deadlock-free: a compose only ever waits on transfers, and every
+    // transfer is claimed by one of the >= 14 warps not composing early, none
+    // of which waits before finishing it.
+    if (warp < n_early) compose_workflow(s_perm[warp]);
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(s_ticket, 1u);
@@ -771,24 +814,10 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             transfer_step(wfo[lo] - r0 + 32u * (t - s_lpref[lo]), wfo[lo + 1] - r0);
             continue;
         }
-        const uint32_t wi = t - n_long_tasks;
-        if (wi >= nw) break;
-        if (!is_long(wi)) sweep_workflow(wi);
-    }
-    if (n_long_tasks) {
-        __syncthreads();
-        // P2b: each long workflow composed by one warp
-        for (;;) {
-            uint32_t wi = 0;
-            if (lane == 0) wi = atomicAdd(s_ticket2, 1u);
-            wi = __shfl_sync(0xFFFFFFFFu, wi, 0);
-            if (wi >= nw) break;
-            if (is_long(wi)) compose_workflow(wi);
-        }
-    }
-    if (lane == 0) {
-        atomicAdd(&s_cnt[0], n_ready);
-        atomicAdd(&s_cnt[2], n_doom);
+        if (t - n_long_tasks + n_early >= nw) break;
+        const uint32_t wi = s_perm[t - n_long_tasks + n_early];
+        if (is_long(wi)) compose_workflow(wi);
+        else sweep_workflow(wi);
     }
     __syncthreads();
     if (bprof && tid == 0) bprof[1] = gtimer();
@@ -803,8 +832,11 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     const int64_t lmax = (int64_t)Lv - 1;
     for (uint32_t f0 = 0; f0 < nr; f0 += kK1Threads) {
         const uint32_t f = f0 + tid;
-        uint32_t kp = 0xFFFFFFFFu, kr = 0xFFFFFFFFu, wl = 0, tyf = 0;
-        if (f < nr) {
+        const bool valid = f < nr;
+        uint32_t kp = 0xFFFFFFFFu, kr = 0xFFFFFFFFu, wl = 0xFFFFFFFFu, tyf = 0;
+        bool pend = false, ready = false, doom = false, infl_row = false, pinp = false;
+        uint32_t stf = 3u;
+        if (valid) {
             {   // workflow of row f (binary search over the staged offsets)
                 uint32_t lo = 0, hi = nw - 1;
                 while (lo < hi) {
@@ -814,16 +846,20 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                 }
                 wl = lo;
             }
-            const uint32_t stf = st[f], fl = flg[f], d = dep[f];
+            stf = st[f];
+            const uint32_t fl = flg[f], d = dep[f];
             tyf = ty[f];
-            if (stf == 1u || stf == 2u) {       // in-flight: instance load, (w, t) fence
+            infl_row = stf == 1u || stf == 2u;
+            if (infl_row) {                     // in-flight: instance load, (w, t) fence
                 atomicAdd(&s_load[ex[f]], 1u);
-                atomicOr(&s_winfl[wl], 1ull << tyf);
+                atomicOr(&s_winfl[2 * wl + (tyf >> 5)], 1u << (tyf & 31u));   // native 32-bit ATOMS.OR
             }
             const int pinf = pn[f];
-            const bool doom = fl & FL_DOOMED, ready = fl & FL_READY, pend = stf == 0u;
+            pend = stf == 0u;
+            doom = fl & FL_DOOMED;
+            ready = pend && !doom && (fl & FL_ALLRES);      // PAPER.md:463, Q2
+            pinp = pend && pinf >= 0;
             const uint32_t aff = s_aff[tyf];
-            const bool infl_row = stf == 1u || stf == 2u;
             // eligibility known now unless decided per (workflow, type) in P4
             const bool elig = ready && (aff == 0u || (aff == 1u && pinf >= 0));
             uint32_t lv = 0;
@@ -842,18 +878,52 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             else status = elig ? 6u : 5u;
             const uint32_t g = r0 + f;
             lev[f] = (uint8_t)lv;
+            flg[f] = (uint8_t)(fl | (ready ? FL_READY : 0) | (elig ? FL_ELIG : 0));
             p.status[g] = (uint8_t)status;
             if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
             p.instance[g] = inst;
             p.new_pin[g] = 0;
             if (elig) {
-                flg[f] = (uint8_t)(fl | FL_ELIG);
                 const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
                 atomicAdd(&p.H[(size_t)r * Lv + lv], 1u);
                 atomicAdd(&s_rcnt[r], 1u);
             }
             if (pend && !doom) kp = wl << 6 | tyf;
             if (ready && pinf < 0) kr = wl << 6 | tyf;
+        }
+        // per-workflow counts ("aggregating metrics and metadata"):
+        // rows are in workflow order, so a warp's lanes form contiguous
+        // workflow segments; the segment head adds its segment's popcounts
+        {
+            const uint32_t wup = __shfl_up_sync(0xFFFFFFFFu, wl, 1);
+            const bool head = valid && (lane == 0 || wup != wl);
+            const uint32_t hm = __ballot_sync(0xFFFFFFFFu, head | !valid);
+            const uint32_t above = lane == 31 ? 0u : hm & (0xFFFFFFFEu << lane);
+            const uint32_t seg = (above ? (above & (0u - above)) - 1u : 0xFFFFFFFFu) & (0xFFFFFFFFu << lane);
+            const uint32_t b_pend = __ballot_sync(0xFFFFFFFFu, pend);
+            const uint32_t b_ready = __ballot_sync(0xFFFFFFFFu, ready);
+            const uint32_t b_infl = __ballot_sync(0xFFFFFFFFu, infl_row);
+            const uint32_t b_res = __ballot_sync(0xFFFFFFFFu, stf == 3u && valid);
+            const uint32_t b_fail = __ballot_sync(0xFFFFFFFFu, stf == 4u);
+            const uint32_t b_doom = __ballot_sync(0xFFFFFFFFu, doom);
+            const uint32_t b_pinp = __ballot_sync(0xFFFFFFFFu, pinp);
+            if (head) {
+                uint32_t* a = s_agg + (size_t)wl * 8;
+                const uint32_t v0 = __popc(b_pend & seg), v1 = __popc(b_ready & seg), v2 = __popc(b_infl & seg);
+                const uint32_t v3 = __popc(b_res & seg), v4 = __popc(b_fail & seg), v5 = __popc(b_doom & seg);
+                const uint32_t v6 = __popc(b_pinp & seg);
+                if (v0) atomicAdd(a + 0, v0);
+                if (v1) atomicAdd(a + 1, v1);
+                if (v2) atomicAdd(a + 2, v2);
+                if (v3) atomicAdd(a + 3, v3);
+                if (v4) atomicAdd(a + 4, v4);
+                if (v5) atomicAdd(a + 5, v5);
+                if (v6) atomicAdd(a + 6, v6);
+            }
+            if (lane == 0) {
+                if (b_ready) atomicAdd(&s_cnt[0], __popc(b_ready));
+                if (b_doom) atomicAdd(&s_cnt[2], __popc(b_doom));
+            }
         }
         // first PENDING non-doomed / first ready unpinned row of each (w, t)
         // (a minimum: order-independent, so plain shared-memory atomics)
@@ -863,6 +933,18 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     __syncthreads();
     if (bprof && tid == 0) bprof[4] = gtimer();
 
+    // per-workflow aggregates out (coalesced): total, pending, ready, inflight,
+    // resolved, failed, doomed, pinned_pending, max_depth, max_round
+    for (uint32_t k = tid; k < nw * 10; k += kK1Threads) {
+        const uint32_t wl = k / 10, j = k - wl * 10;
+        uint32_t v;
+        if (j == 0) v = wfo[wl + 1] - wfo[wl];
+        else if (j <= 7) v = s_agg[wl * 8 + j - 1];
+        else if (j == 8) v = s_agg[wl * 8 + 7];
+        else v = s_wrnd[wl];
+        p.wf_agg[(size_t)w0 * 10 + k] = v;
+    }
+
     // ---- P4: the stateful fence and first placement
     // make the per-(workflow, type) winner eligible
     for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
@@ -871,7 +953,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         uint32_t f = 0xFFFFFFFFu;
         if (aff == 2u) {
             const uint32_t c = s_wfp[k];
-            if (c != 0xFFFFFFFFu && !((s_winfl[wl] >> t) & 1ull) && (flg[c] & FL_READY)) f = c;
+            if (c != 0xFFFFFFFFu && !((s_winfl[2 * wl + (t >> 5)] >> (t & 31u)) & 1u) && (flg[c] & FL_READY)) f = c;
         } else if (aff == 1u) {
             f = s_wfru[k];
         }

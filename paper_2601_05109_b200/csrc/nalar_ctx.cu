@@ -86,6 +86,7 @@ struct nalar_ctx {
     int16_t *d_exec = nullptr, *d_pin = nullptr;
     uint32_t *d_blk_wf = nullptr, *d_blk_row0 = nullptr, *d_blk_edge0 = nullptr;
     uint8_t* d_blk_staged = nullptr;
+    uint32_t* d_wf_perm = nullptr;
     uint32_t *d_type_off = nullptr, *d_type_inst = nullptr;
     // outputs
     uint8_t *d_status = nullptr, *d_level = nullptr, *d_newpin = nullptr, *d_gflags = nullptr;
@@ -133,6 +134,7 @@ struct nalar_ctx {
     size_t stage_bytes = 0;
     std::vector<uint64_t> m_wf_id;
     std::vector<uint32_t> m_wf_off, m_wf_eoff;
+    std::vector<uint32_t> m_perm;          // per-block task order (set_blocks)
     bool assign_valid = false;        // last epoch's assignment regions match the table
     Key last_key{};
     bool last_key_set = false;
@@ -171,7 +173,7 @@ struct Layout {
 
 struct Plan {
     size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
-    size_t blk_wf, blk_row0, blk_edge0, blk_staged, type_off, type_inst;
+    size_t blk_wf, blk_row0, blk_edge0, blk_staged, wf_perm, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
@@ -204,6 +206,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->blk_row0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_edge0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_staged = L.take<uint8_t>(p->Bmax);
+    p->wf_perm = L.take<uint32_t>(W);
     p->type_off = L.take<uint32_t>(T + 1);
     p->type_inst = L.take<uint32_t>(I);
     p->status = L.take<uint8_t>(N);
@@ -290,6 +293,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.t_aff = c->d_taff;
     p.blk_wf = c->d_blk_wf; p.blk_row0 = c->d_blk_row0; p.blk_edge0 = c->d_blk_edge0;
     p.blk_staged = c->d_blk_staged;
+    p.wf_perm = c->d_wf_perm;
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
@@ -398,8 +402,21 @@ int set_blocks(nalar_ctx* c) {
     CK(cudaMemcpyAsync(c->d_blk_row0, br.data(), 4ull * br.size(), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(c->d_blk_edge0, be.data(), 4ull * be.size(), cudaMemcpyHostToDevice, st));
     if (!bs.empty()) CK(cudaMemcpyAsync(c->d_blk_staged, bs.data(), bs.size(), cudaMemcpyHostToDevice, st));
+    // task order inside each block: largest workflow first (longest-processing-
+    // time-first list scheduling of workflows onto the block's warps)
+    c->m_perm.resize(c->W);
+    for (size_t b = 0; b + 1 < bw.size(); ++b) {
+        const uint32_t ws = bw[b], we = bw[b + 1];
+        uint32_t* o = c->m_perm.data() + ws;
+        for (uint32_t k = 0; k < we - ws; ++k) o[k] = k;
+        const uint32_t* off = c->m_wf_off.data() + ws;
+        std::stable_sort(o, o + (we - ws), [off](uint32_t x, uint32_t y) {
+            return off[x + 1] - off[x] > off[y + 1] - off[y];
+        });
+    }
+    if (c->W) CK(cudaMemcpyAsync(c->d_wf_perm, c->m_perm.data(), 4ull * c->W, cudaMemcpyHostToDevice, st));
     if (c->cfg.flags & NALAR_F_PROFILE) {
-        const size_t need = 2ull * c->W + 8ull * c->B + 8ull * c->R + 4ull * c->W;
+        const size_t need = 2ull * c->W + 8ull * c->B + 8ull * c->R + 4ull * c->W + 8ull * c->B;
         if (need > c->prof_words) {
             if (c->d_prof) cudaFree(c->d_prof);
             c->d_prof = nullptr;
@@ -502,6 +519,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_taff = at<uint8_t>(a, p.taff);
     c->d_blk_wf = at<uint32_t>(a, p.blk_wf); c->d_blk_row0 = at<uint32_t>(a, p.blk_row0);
     c->d_blk_edge0 = at<uint32_t>(a, p.blk_edge0); c->d_blk_staged = at<uint8_t>(a, p.blk_staged);
+    c->d_wf_perm = at<uint32_t>(a, p.wf_perm);
     c->d_type_off = at<uint32_t>(a, p.type_off); c->d_type_inst = at<uint32_t>(a, p.type_inst);
     c->d_status = at<uint8_t>(a, p.status); c->d_level = at<uint8_t>(a, p.level);
     c->d_newpin = at<uint8_t>(a, p.newpin); c->d_gflags = at<uint8_t>(a, p.gflags);

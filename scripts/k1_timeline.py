@@ -29,12 +29,15 @@ for _ in range(5):
 torch.cuda.synchronize()
 prof = nalar.nalar_debug_profile(ctx.h).astype(np.int64)
 W = s.n_workflows
-wf = prof[:2 * W].reshape(W, 2)
 R = s.n_instances + s.n_types
-cyc = prof[len(prof) - 4 * W:].reshape(W, 4)              # edge loop, rounds, rest (SM cycles), round counts
-prof = prof[:len(prof) - 4 * W]
-blk = prof[2 * W:len(prof) - 8 * R].reshape(-1, 8)        # staged, swept, bucketed, entered, P3 done, P4 done
-k4 = prof[len(prof) - 8 * R:].reshape(R, 8)              # start, n_adm, tables, done, waited, prefix, pass1
+B_ = (len(prof) - 2 * W - 8 * R - 4 * W) // 16     # layout: [W][2] [B][8] [R][8] [W][4] [B][8]
+o1, o2 = 2 * W, 2 * W + 8 * B_
+o3, o4 = o2 + 8 * R, o2 + 8 * R + 4 * W
+wf = prof[:o1].reshape(W, 2)
+blk = prof[o1:o2].reshape(B_, 8)        # staged, swept, bucketed, entered, P3 done, P4 done
+k4 = prof[o2:o3].reshape(R, 8)          # start, n_adm, tables, done, waited, prefix, pass1
+cyc = prof[o3:o4].reshape(W, 4)         # edge loop, rounds, rest (SM cycles), round counts
+tx = prof[o4:o4 + 8 * B_].reshape(B_, 8)  # transfer phases: edge, iface, settle, end, iters, n, K, k
 t0 = blk[:, 3].min()
 o = oracle_epoch(s, "srtf")
 sizes = np.diff(s.wf_fut_off.astype(np.int64))
@@ -83,6 +86,12 @@ res["cycles_per_chunk"] = {"edge": float(cyc[:, 0].sum() / chunks.sum()),
 A = np.stack([sizes, maxd, np.ones_like(sizes)], 1).astype(np.float64)
 coef, *_ = np.linalg.lstsq(A, dur.astype(np.float64), rcond=None)
 res["fit_ns"] = {"per_row": coef[0], "per_depth": coef[1], "const": coef[2]}
+nt = max(int(tx[:, 5].sum()), 1)
+res["transfer_steps"] = {"n": int(tx[:, 5].sum()),
+                         "cycles_per_step": {k: float(tx[:, j].sum() / nt) for j, k in
+                                             enumerate(("edges", "iface", "settle", "store"))},
+                         "settle_iters_mean": float(tx[:, 4].sum() / nt), "K_mean": float(tx[:, 6].sum() / nt),
+                         "k_mean": float(tx[:, 7].sum() / nt)}
 print(json.dumps(res, indent=1))
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"), indent=1)
