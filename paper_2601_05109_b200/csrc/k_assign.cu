@@ -84,7 +84,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
+__global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     __shared__ uint32_t s_inst[NALAR_MAX_INSTANCES_DEV];
     __shared__ uint32_t s_spare[NALAR_MAX_INSTANCES_DEV];   // spare before phase A
     __shared__ uint32_t s_sp2[NALAR_MAX_INSTANCES_DEV];     // spare after phase A
@@ -130,38 +130,48 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (prof && tid == 0) prof[4] = gtimer();
 
+    // ---- every load of the sweep's results this block needs first, issued
+    // together (one L2 round trip instead of a chain of dependent ones) -----
+    const uint32_t lv = tid;
+    uint32_t hg = 0, hb = 0, hl = 0;
+    if (lv < Lv) {
+        for (uint32_t s = 0; s < G; ++s) {
+            const uint32_t h = p.H[((size_t)s * R + r) * Lv + lv];
+            hg += h;
+            if (s < p.slot) hb += h;
+            if (s == p.slot) hl = h;
+        }
+    }
+    uint32_t base_part = 0;                  // offset of r's region of the assignment list
+    for (uint32_t q = tid; q < r; q += kK4Threads) base_part += p.tot_loc[q];
+    const uint32_t cnt0 = tid < B ? p.cnt_rb[(size_t)r * B + tid] : 0u;   // first 256 K1 blocks
+    const uint32_t off0 = tid < B ? p.off_rb[(size_t)r * B + tid] : 0u;
+    uint32_t ls0 = 0, ha0 = 0;
+    if (is_type) {
+        if (tid < ni) { ls0 = p.load_sum[s_inst[tid]]; ha0 = p.tot[s_inst[tid]]; }
+    } else if (tid == 0) {
+        ls0 = p.load_sum[r];
+    }
+
     // ---- instances of type t: load, spare, phase-A admissions (all ranks) ----
     if (is_type) {
         for (uint32_t k = tid; k < ni; k += kK4Threads) {
             const uint32_t i = s_inst[k];
-            const uint64_t load = (uint64_t)s_sp2[k] + p.load_sum[i];
+            const uint64_t load = (uint64_t)s_sp2[k] + (k < kK4Threads ? ls0 : p.load_sum[i]);
             const uint64_t cap = s_spare[k];
             const uint32_t spare = (uint32_t)(cap > load ? cap - load : 0ull);
-            const uint32_t ha = p.tot[i];
+            const uint32_t ha = k < kK4Threads ? ha0 : p.tot[i];
             s_spare[k] = spare;
             s_sp2[k] = spare - (ha < spare ? ha : spare);
             p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
             p.i_spare[i] = spare;
         }
     } else if (tid == 0) {
-        const uint64_t load = (uint64_t)base_r + p.load_sum[r];
+        const uint64_t load = (uint64_t)base_r + ls0;
         s_bound = cap_r > load ? cap_r - load : 0ull;
     }
-    // offset of this resource's region of the assignment list
-    uint32_t base_part = 0;
-    for (uint32_t q = tid; q < r; q += kK4Threads) base_part += p.tot_loc[q];
     // ---- level histogram of r: global, lower-ranks, local ------------------
     {
-        const uint32_t lv = tid;
-        uint32_t hg = 0, hb = 0, hl = 0;
-        if (lv < Lv) {
-            for (uint32_t s = 0; s < G; ++s) {
-                const uint32_t h = p.H[((size_t)s * R + r) * Lv + lv];
-                hg += h;
-                if (s < p.slot) hb += h;
-                if (s == p.slot) hl = h;
-            }
-        }
         s_Hg[lv] = hg;
         s_Hl[lv] = hl;
         s_before[lv] = hb;
@@ -254,7 +264,22 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
             }
             p.i_assigned[s_inst[k]] = (uint32_t)asg;
         }
-        if (table && n_adm && warp == 0) {
+        if (table && n_adm && ni <= 16u) {
+            // slots in (level desc, instance asc) order, all at once: slot
+            // (s, k) sits after every slot of a higher level and after the
+            // level-s slots of lower instances
+            for (uint32_t k = 0; k < ni; ++k) {
+                const uint32_t sp = s_sp2[k];
+                for (uint32_t sv = 1 + tid; sv <= sp; sv += kK4Threads) {
+                    uint32_t pos = 0;
+                    for (uint32_t j = 0; j < ni; ++j) {
+                        const uint32_t x = s_sp2[j];
+                        pos += (x > sv ? x - sv : 0u) + (j < k && x >= sv ? 1u : 0u);
+                    }
+                    s_slot[pos] = (uint16_t)s_inst[k];
+                }
+            }
+        } else if (table && n_adm && warp == 0) {
             // slots in (level desc, instance asc) order, one level per step
             uint32_t pos = 0;
             for (uint64_t sv = maxs; sv >= 1; --sv) {
@@ -283,8 +308,8 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         const uint32_t bb = b0 + tid;
         uint32_t c = 0;
         if (bb < B) {
-            c = p.cnt_rb[(size_t)r * B + bb];
-            s_base[tid] = (b0 == 0 ? blk0 : p.blk_row0[bb]) + p.off_rb[(size_t)r * B + bb];
+            c = b0 == 0 ? cnt0 : p.cnt_rb[(size_t)r * B + bb];
+            s_base[tid] = b0 == 0 ? blk0 + off0 : p.blk_row0[bb] + p.off_rb[(size_t)r * B + bb];
         }
         uint32_t incl = c;
 #pragma unroll
@@ -306,7 +331,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
         for (uint32_t q0 = 0; q0 < total && found < n_adm; q0 += 4 * kK4Threads) {
             // pass 1: four consecutive items per thread
             uint2 it[4];
-            uint32_t nl = 0;
+            uint32_t live = 0;                // bit j: item j is live (register-resident, no local memory)
             const uint32_t qa = q0 + 4 * tid;
             if (qa < total) {
                 uint32_t lo = 0, hi = nb - 1;
@@ -318,13 +343,17 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t q = qa + j;
+                    it[j] = make_uint2(0u, 0u);
                     if (q < total) {
                         while (lo + 1 < nb && s_pref[lo + 1] <= q) ++lo;
-                        const uint2 x = p.items[s_base[lo] + (q - s_pref[lo])];
-                        if ((uint64_t)s_A[x.y] + s_before[x.y] < bound) it[nl++] = x;
+                        it[j] = p.items[s_base[lo] + (q - s_pref[lo])];
                     }
                 }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (qa + j < total && (uint64_t)s_A[it[j].y] + s_before[it[j].y] < bound) live |= 1u << j;
             }
+            const uint32_t nl = __popc(live);
             uint32_t li = nl;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -339,7 +368,12 @@ __global__ void __launch_bounds__(kK4Threads) k4_assign(AssignParams p) {
                 n_live += s_red32[k];
             }
             lb += li - nl;
-            for (uint32_t j = 0; j < nl; ++j) s_live[lb + j] = it[j];
+            {
+                uint32_t o = lb;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if ((live >> j) & 1u) s_live[o++] = it[j];
+            }
             __syncthreads();
             if (prof && tid == 0 && q0 == 0 && b0 == 0) prof[6] = gtimer() + 0 * n_live;
             // pass 2: stable rank of each live item inside its level

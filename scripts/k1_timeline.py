@@ -92,6 +92,12 @@ res["transfer_steps"] = {"n": int(tx[:, 5].sum()),
                                              enumerate(("edges", "iface", "settle", "store"))},
                          "settle_iters_mean": float(tx[:, 4].sum() / nt), "K_mean": float(tx[:, 6].sum() / nt),
                          "k_mean": float(tx[:, 7].sum() / nt)}
+k1_end = blk[:, 2].max()
+res["k4"]["wait_release_after_k1_end_ns"] = int(k4[:, 4].min() - k1_end)
+slow = np.argsort(-(k4[:, 3] - k1_end))[:6]
+res["k4"]["slowest_ctas"] = [{"r": int(r), **{n: (int(k4[r, j] - k1_end) if k4[r, j] > 0 else None) for n, j in
+                                             (("start", 0), ("released", 4), ("n_adm", 1), ("tables", 2),
+                                              ("prefix", 5), ("pass1", 6), ("done", 3))}} for r in slow]
 print(json.dumps(res, indent=1))
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"), indent=1)
