@@ -149,6 +149,33 @@ struct DeltaParams {
     unsigned long long* err;     // [0] bad update index, [1] bad prio / instance update index
 };
 
+// host <-> device segment copies (k_io.cu): src / dst are device-accessible
+// pointers (device memory or mapped pinned host memory)
+constexpr int kMaxSegs = 24;
+struct CopySeg {
+    const void* src;
+    void* dst;
+    uint64_t bytes;
+};
+struct CopyParams {
+    CopySeg seg[kMaxSegs];
+    uint64_t chunk_off[kMaxSegs + 1];   // prefix of 16-byte chunk counts
+    uint32_t n;
+};
+struct FetchParams {
+    const uint32_t* n_adm;      // [R] this rank's admitted futures per resource
+    const uint32_t* tot_loc;    // [R] region sizes of the device assignment list
+    const uint32_t* arow;
+    const int16_t* ainst;
+    const uint32_t* counters;   // C_*
+    uint32_t* out_row;          // mapped host (or null)
+    int16_t* out_inst;
+    uint32_t* out_counters;     // mapped host [C_NUM]
+    uint32_t R, a_cap;
+};
+
+cudaError_t launch_copy_segs(const CopyParams& p, cudaStream_t s);
+cudaError_t launch_fetch(const FetchParams& f, const CopyParams& p, cudaStream_t s);
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);
 cudaError_t launch_delta(const DeltaParams& p, bool apply_assigned, uint32_t R, cudaStream_t s);
 cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s);

@@ -5,46 +5,47 @@
 // futures carry an executor of their type (PAPER.md:479 executor metadata);
 // pins name an instance of the future's type (state placement).
 //
-// One warp per workflow; each lane checks one row per step.  The smallest
-// offending row wins (atomicMin), so the reported row is deterministic.
+// Row-parallel: one thread per row (the workflow of a row by binary search
+// over the workflow offsets, which the host has checked to be monotone), so a
+// deep workflow costs no more than any other -- the check is a few dependent
+// loads deep, not one round trip per 32 rows of the longest workflow.  The
+// smallest offending row wins (atomicMin), so the reported row is
+// deterministic.
 #include "internal.h"
 
 namespace nalar {
 
 __global__ void __launch_bounds__(kK0Threads) k0_validate(ValidateParams p) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (w >= p.n_wf) return;
-    const uint32_t a = p.wf_fut_off[w], b = p.wf_fut_off[w + 1];
-    if (b < a || b > p.n_fut) {            // structural: offsets not monotone
-        if (lane == 0) atomicOr(&p.err[1], 1ull);
+    const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= p.n_fut) return;
+    const uint32_t st = p.f_state[f], ty = p.f_type[f];
+    const int pin = p.f_pin[f], ex = p.f_exec[f];
+    const uint32_t e0 = p.f_edge_off[f], e1 = p.f_edge_off[f + 1];
+    // first row of f's workflow: the last w with wf_fut_off[w] <= f
+    uint32_t lo = 0, hi = p.n_wf - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (p.wf_fut_off[mid] <= f) lo = mid;
+        else hi = mid - 1;
+    }
+    const uint32_t a = p.wf_fut_off[lo];
+    if (e1 < e0 || e1 > p.n_edges) {       // structural: CSR offsets not monotone
+        atomicOr(&p.err[1], 1ull);
         return;
     }
-    for (uint32_t f = a + lane; f < b; f += 32) {
-        bool ok = true;
-        const uint32_t st = p.f_state[f], ty = p.f_type[f];
-        const int pin = p.f_pin[f], ex = p.f_exec[f];
-        const uint32_t e0 = p.f_edge_off[f], e1 = p.f_edge_off[f + 1];
-        if (e1 < e0 || e1 > p.n_edges) {   // structural: CSR offsets not monotone
-            atomicOr(&p.err[1], 1ull);
-            continue;
-        }
-        if (st > 4u || ty >= p.n_types) ok = false;
-        if (ok && pin != -1 && (pin < 0 || (uint32_t)pin >= p.n_inst || p.i_type[pin] != ty)) ok = false;
-        if (ok && (st == 1u || st == 2u) && (ex < 0 || (uint32_t)ex >= p.n_inst || p.i_type[ex] != ty))
-            ok = false;
-        for (uint32_t e = e0; ok && e < e1; ++e) {
-            const uint32_t s = p.edges[e] & 0x7FFFFFFFu;
-            if (s < a || s >= f) ok = false;
-        }
-        if (!ok) atomicMin(&p.err[0], (unsigned long long)f);
+    bool ok = st <= 4u && ty < p.n_types;
+    if (ok && pin != -1 && (pin < 0 || (uint32_t)pin >= p.n_inst || p.i_type[pin] != ty)) ok = false;
+    if (ok && (st == 1u || st == 2u) && (ex < 0 || (uint32_t)ex >= p.n_inst || p.i_type[ex] != ty)) ok = false;
+    for (uint32_t e = e0; ok && e < e1; ++e) {
+        const uint32_t s = p.edges[e] & 0x7FFFFFFFu;
+        if (s < a || s >= f) ok = false;
     }
+    if (!ok) atomicMin(&p.err[0], (unsigned long long)f);
 }
 
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s) {
-    if (p.n_wf == 0) return cudaSuccess;
-    const uint64_t threads = (uint64_t)p.n_wf * 32u;
-    const uint32_t grid = (uint32_t)((threads + kK0Threads - 1) / kK0Threads);
+    if (p.n_fut == 0 || p.n_wf == 0) return cudaSuccess;
+    const uint32_t grid = (uint32_t)((p.n_fut + kK0Threads - 1) / kK0Threads);
     k0_validate<<<grid, kK0Threads, 0, s>>>(p);
     return cudaGetLastError();
 }

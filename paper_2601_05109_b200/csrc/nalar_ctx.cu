@@ -7,6 +7,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -110,6 +112,12 @@ struct nalar_ctx {
     void* h_list = nullptr;
     size_t h_list_cap = 0;
     unsigned long long* h_err = nullptr;
+    uint32_t* h_cnt_dev = nullptr;     // device view of h_cnt (mapped)
+    // pinned staging of the host-built tables (type lists, K1 block tables,
+    // task order) so they travel in the upload's single copy kernel
+    uint8_t* h_tab = nullptr;
+    uint8_t* h_tab_dev = nullptr;
+    size_t tab_off[7] = {0, 0, 0, 0, 0, 0, 0};   // type_off, type_inst, blk_wf, blk_row0, blk_edge0, blk_staged, perm
     // current table
     uint32_t N = 0, E = 0, W = 0, I = 0, T = 0, B = 0, R = 0;
     size_t smem = 0, fixed_smem = 0;
@@ -244,6 +252,49 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
 
 template <typename T>
 T* at(uint8_t* base, size_t off) { return reinterpret_cast<T*>(base + off); }
+
+// Device-accessible address of a host pointer (pinned memory is mapped under
+// UVA), or nullptr for pageable memory.
+void* mapped_view(const void* h) {
+    if (!h) return nullptr;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type == cudaMemoryTypeHost && a.devicePointer) return a.devicePointer;
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return const_cast<void*>(h);
+    return nullptr;
+}
+
+// A batch of copies issued as one kernel (k_io.cu) when both sides are
+// device-accessible; a pageable host side falls back to cudaMemcpyAsync.
+struct CopyBatch {
+    cudaStream_t st;
+    CopyParams p{};
+    explicit CopyBatch(cudaStream_t s) : st(s) {}
+    cudaError_t add_dev(const void* src, void* dst, size_t bytes) {
+        if (!bytes) return cudaSuccess;
+        p.seg[p.n++] = CopySeg{src, dst, (uint64_t)bytes};
+        return p.n == (uint32_t)kMaxSegs ? flush() : cudaSuccess;
+    }
+    cudaError_t h2d(void* d, const void* h, size_t bytes) {
+        if (!bytes) return cudaSuccess;
+        const void* v = mapped_view(h);
+        return v ? add_dev(v, d, bytes) : cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);
+    }
+    void chunk_offsets() {
+        p.chunk_off[0] = 0;
+        for (uint32_t i = 0; i < p.n; ++i) p.chunk_off[i + 1] = p.chunk_off[i] + (p.seg[i].bytes + 15) / 16;
+    }
+    cudaError_t flush() {
+        if (!p.n) return cudaSuccess;
+        chunk_offsets();
+        const cudaError_t e = launch_copy_segs(p, st);
+        p.n = 0;
+        return e;
+    }
+};
 
 void destroy_graphs(nalar_ctx* c) {
     for (auto& g : c->gexec)
@@ -389,7 +440,7 @@ int enqueue_epoch(nalar_ctx* c, int policy) {
 }
 
 // K1 block table from the host mirror of the workflow layout; profile buffer
-int set_blocks(nalar_ctx* c) {
+int set_blocks(nalar_ctx* c, CopyBatch* batch) {
     std::vector<uint32_t> bw, br, be;
     std::vector<uint8_t> bs;
     size_t mx = 0;
@@ -398,10 +449,6 @@ int set_blocks(nalar_ctx* c) {
     c->fixed_smem = k1_fixed_smem(c->T, c->I, c->R);
     c->smem = c->fixed_smem + mx;
     cudaStream_t st = c->stream;
-    CK(cudaMemcpyAsync(c->d_blk_wf, bw.data(), 4ull * bw.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->d_blk_row0, br.data(), 4ull * br.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->d_blk_edge0, be.data(), 4ull * be.size(), cudaMemcpyHostToDevice, st));
-    if (!bs.empty()) CK(cudaMemcpyAsync(c->d_blk_staged, bs.data(), bs.size(), cudaMemcpyHostToDevice, st));
     // task order inside each block: largest workflow first (longest-processing-
     // time-first list scheduling of workflows onto the block's warps)
     c->m_perm.resize(c->W);
@@ -414,7 +461,19 @@ int set_blocks(nalar_ctx* c) {
             return off[x + 1] - off[x] > off[y + 1] - off[y];
         });
     }
-    if (c->W) CK(cudaMemcpyAsync(c->d_wf_perm, c->m_perm.data(), 4ull * c->W, cudaMemcpyHostToDevice, st));
+    // into the pinned staging, then one copy kernel with the caller's batch
+    CopyBatch own(st);
+    CopyBatch& cb = batch ? *batch : own;
+    struct Part { int slot; const void* src; size_t bytes; void* dst; };
+    const Part parts[5] = {
+        {2, bw.data(), 4ull * bw.size(), c->d_blk_wf}, {3, br.data(), 4ull * br.size(), c->d_blk_row0},
+        {4, be.data(), 4ull * be.size(), c->d_blk_edge0}, {5, bs.data(), bs.size(), c->d_blk_staged},
+        {6, c->m_perm.data(), 4ull * c->W, c->d_wf_perm}};
+    for (const Part& q : parts) {
+        if (!q.bytes) continue;
+        memcpy(c->h_tab + c->tab_off[q.slot], q.src, q.bytes);
+        CK(cb.add_dev(c->h_tab_dev + c->tab_off[q.slot], q.dst, q.bytes));
+    }
     if (c->cfg.flags & NALAR_F_PROFILE) {
         const size_t need = 2ull * c->W + 8ull * c->B + 8ull * c->R + 4ull * c->W + 8ull * c->B;
         if (need > c->prof_words) {
@@ -425,8 +484,7 @@ int set_blocks(nalar_ctx* c) {
         c->prof_words = need;
         CK(cudaMemsetAsync(c->d_prof, 0, 8 * std::max<size_t>(need, 1), st));
     }
-    // block tables are synchronous host vectors: finish the copies before they die
-    CK(cudaStreamSynchronize(st));
+    if (!batch) CK(own.flush());
     return NALAR_OK;
 }
 
@@ -541,6 +599,16 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     if (cudaMallocHost(&c->h_cnt, 64) != cudaSuccess || cudaMallocHost(&c->h_err, 64) != cudaSuccess ||
         cudaMallocHost(&c->h_reg, 8ull * std::max<uint32_t>(c->Rmax, 1)) != cudaSuccess)
         return bail(NALAR_E_NOMEM);
+    {
+        const size_t Tm = cfg->max_types, Im = cfg->max_instances, Wm = cfg->max_workflows, Bm = c->Bmax;
+        const size_t sz[7] = {4 * (Tm + 1), 4 * Im, 4 * (Bm + 1), 4 * (Bm + 1), 4 * (Bm + 1), Bm, 4 * Wm};
+        size_t o = 0;
+        for (int k = 0; k < 7; ++k) { c->tab_off[k] = o; o += (sz[k] + 15) & ~(size_t)15; }
+        if (cudaMallocHost(&c->h_tab, std::max<size_t>(o, 16)) != cudaSuccess) return bail(NALAR_E_NOMEM);
+        c->h_tab_dev = (uint8_t*)mapped_view(c->h_tab);
+        c->h_cnt_dev = (uint32_t*)mapped_view(c->h_cnt);
+        if (!c->h_tab_dev || !c->h_cnt_dev) return bail(NALAR_E_CUDA);
+    }
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
     if (cfg->collective == NALAR_COLL_NCCL) {   // (world == 1 allowed: a 1-rank comm, for testing)
@@ -576,6 +644,7 @@ int nalar_destroy(nalar_ctx* c) {
     if (c->h_err) cudaFreeHost(c->h_err);
     if (c->h_reg) cudaFreeHost(c->h_reg);
     if (c->h_list) cudaFreeHost(c->h_list);
+    if (c->h_tab) cudaFreeHost(c->h_tab);
     delete c;
     return NALAR_OK;
 }
@@ -595,6 +664,11 @@ void* nalar_stream(nalar_ctx* c) { return c ? (void*)c->stream : nullptr; }
 const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row) {
+    // NALAR_TRACE_UPLOAD=1: host-side phase times of this call on stderr
+    static const bool trace = getenv("NALAR_TRACE_UPLOAD") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double tt[6] = {trace ? now() : 0, 0, 0, 0, 0, 0};
     if (err_row) *err_row = -1;
     if (!c || !s) return NALAR_E_INVAL;
     c->uploaded = false;
@@ -629,10 +703,11 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     c->m_wf_eoff.resize(W + 1);
     for (uint32_t w = 0; w <= W; ++w) c->m_wf_eoff[w] = s->f_edge_off[s->wf_fut_off[w]];
 
+    if (trace) tt[1] = now();
     cudaStream_t st = c->stream;
-    auto h2d = [&](void* d, const void* h, size_t bytes) -> cudaError_t {
-        return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
-    };
+    // every array in one copy kernel when the caller's buffers are pinned
+    CopyBatch cb(st);
+    auto h2d = [&](void* d, const void* h, size_t bytes) -> cudaError_t { return cb.h2d(d, h, bytes); };
     CK(h2d(c->d_wf_off, s->wf_fut_off, 4ull * (W + 1)));
     CK(h2d(c->d_wf_prio, s->wf_prio, 4ull * W));
     CK(h2d(c->d_wf_id, s->wf_id, 8ull * W));
@@ -648,18 +723,29 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     CK(h2d(c->d_ibase, s->i_base_load, 4ull * I));
     CK(h2d(c->d_taff, s->t_affinity, T));
     // instances grouped by type (ascending id), for the assignment pass
-    std::vector<uint32_t> toff(T + 1, 0), tinst(I);
+    if (trace) tt[2] = now();
+    uint32_t* toff = (uint32_t*)(c->h_tab + c->tab_off[0]);
+    uint32_t* tinst = (uint32_t*)(c->h_tab + c->tab_off[1]);
+    std::fill(toff, toff + T + 1, 0u);
     for (uint32_t i = 0; i < I; ++i) toff[s->i_type[i] + 1]++;
     for (uint32_t t = 0; t < T; ++t) toff[t + 1] += toff[t];
     {
-        std::vector<uint32_t> cur(toff.begin(), toff.end() - 1);
+        std::vector<uint32_t> cur(toff, toff + T);
         for (uint32_t i = 0; i < I; ++i) tinst[cur[s->i_type[i]]++] = i;
     }
-    CK(h2d(c->d_type_off, toff.data(), 4ull * (T + 1)));
-    CK(h2d(c->d_type_inst, tinst.data(), 4ull * I));
-    int rc = set_blocks(c);
+    CK(cb.add_dev(c->h_tab_dev + c->tab_off[0], c->d_type_off, 4ull * (T + 1)));
+    CK(cb.add_dev(c->h_tab_dev + c->tab_off[1], c->d_type_inst, 4ull * I));
+    int rc = set_blocks(c, &cb);
     if (rc) return rc;
+    CK(cb.flush());
+    if (trace) tt[3] = now();
     rc = validate_table(c, err_row, nullptr);
+    if (trace) {
+        tt[4] = now();
+        fprintf(stderr, "[nalar upload] checks+mirror %.1f us, array copies issued %.1f, tables+partition+kernel %.1f, "
+                "validate+sync %.1f, total %.1f\n", tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3],
+                tt[4] - tt[0]);
+    }
     if (rc) return rc;
     c->uploaded = true;
     return NALAR_OK;
@@ -846,7 +932,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     noff[W2] = N2; neoff[W2] = E2;
     c->m_wf_id.swap(nid); c->m_wf_off.swap(noff); c->m_wf_eoff.swap(neoff);
     c->N = N2; c->E = E2; c->W = W2;
-    int rc = set_blocks(c);
+    int rc = set_blocks(c, nullptr);
     if (!rc) rc = validate_table(c, err_index, nullptr);
     if (rc) { c->uploaded = false; return rc; }
     c->epoch_done = false;
@@ -919,6 +1005,53 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     if (!c || !o) return NALAR_E_INVAL;
     if (!c->epoch_done) return fail(c, NALAR_E_STATE, "fetch before epoch");
     cudaStream_t st = c->stream;
+    // Fast path: every requested output buffer is pinned (device-mapped) host
+    // memory -> one kernel writes them all, compacting the assignment list on
+    // the way, and one synchronisation.
+    {
+        struct Out { void* h; const void* d; size_t bytes; };
+        const Out outs[9] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
+                             {o->depth, c->d_depth, 2ull * c->N}, {o->instance, c->d_inst, 2ull * c->N},
+                             {o->new_pin, c->d_newpin, c->N},
+                             {o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W},
+                             {o->i_load, c->d_iload, 4ull * c->I}, {o->i_spare, c->d_ispare, 4ull * c->I},
+                             {o->i_assigned, c->d_iasg, 4ull * c->I}};
+        const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
+        const bool wbad = o->wf_agg && o->wf_cap < c->W;
+        const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
+        bool mapped = !(fbad || wbad || ibad);
+        CopyBatch cb(st);
+        for (const Out& q : outs) {
+            if (!mapped || !q.h || !q.bytes) continue;
+            void* v = mapped_view(q.h);
+            if (!v) mapped = false;
+            else cb.p.seg[cb.p.n++] = CopySeg{q.d, v, (uint64_t)q.bytes};
+        }
+        void* v_row = o->assign_row ? mapped_view(o->assign_row) : nullptr;
+        void* v_inst = o->assign_inst ? mapped_view(o->assign_inst) : nullptr;
+        if ((o->assign_row && !v_row) || (o->assign_inst && !v_inst)) mapped = false;
+        if (mapped) {
+            cb.chunk_offsets();
+            FetchParams f{};
+            f.n_adm = c->d_scr + C_NUM;
+            f.tot_loc = c->d_scr + C_NUM + c->Rmax;
+            f.arow = c->d_arow;
+            f.ainst = c->d_ainst;
+            f.counters = c->d_scr;
+            f.out_row = (uint32_t*)v_row;
+            f.out_inst = (int16_t*)v_inst;
+            f.out_counters = c->h_cnt_dev;
+            f.R = c->assign_valid ? c->R : 0u;
+            f.a_cap = o->a_cap;
+            CK(launch_fetch(f, cb.p, st));
+            CK(cudaStreamSynchronize(st));
+            const uint32_t na = c->h_cnt[C_ASSIGNED];
+            o->n_f = c->N; o->n_w = c->W; o->n_i = c->I; o->n_assigned = na;
+            if ((o->assign_row || o->assign_inst) && o->a_cap < na)
+                return fail(c, NALAR_E_SIZE, "output buffer too small");
+            return NALAR_OK;
+        }
+    }
     CK(cudaMemcpyAsync(c->h_cnt, c->d_scr, C_NUM * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const uint32_t na = c->h_cnt[C_ASSIGNED];
