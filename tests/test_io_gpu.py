@@ -1,0 +1,137 @@
+"""The public API's kernel I/O paths (k_io.cu) against the oracle.
+
+nalar_snapshot_upload moves pinned (device-mapped) host arrays with one
+segment-copy kernel and falls back to cudaMemcpyAsync for pageable ones;
+nalar_fetch_decisions writes pinned output buffers (and compacts the
+assignment list) in one kernel.  Every combination must give bit-identical
+results to the CPU oracle, and the size errors must still be reported.
+"""
+import numpy as np
+import pytest
+
+from nalar_gen import Snapshot, c1, c2, c4, random_table, swe_table
+from oracle import oracle_epoch
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load", "i_spare",
+        "i_assigned", "assign_row", "assign_inst")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def pinned_like(a, keep):
+    torch = _torch()
+    t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    keep.append(t)
+    v = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+    v[...] = a
+    return v
+
+
+def pinned_snapshot(s, keep, only=None):
+    arrs = {k: (pinned_like(a, keep) if only is None or k in only else a) for k, a in s.arrays().items()}
+    return Snapshot(global_row_base=s.global_row_base, name=s.name, **arrs)
+
+
+def same(o, g, tag):
+    for k in KEYS:
+        a, b = np.asarray(o[k]), np.asarray(g[k])
+        assert a.shape == b.shape and np.array_equal(a, b), f"{tag}: {k}"
+
+
+@pytest.mark.parametrize("mk", [c1, lambda: c2(1), lambda: swe_table(3000, seed=5),
+                                lambda: random_table(7, n_workflows=5, max_rows=30, consistent=True)])
+@pytest.mark.parametrize("pin_in,pin_out", [(True, True), (True, False), (False, True)])
+def test_pinned_paths_bit_exact(mk, pin_in, pin_out):
+    from paper_2601_05109_b200 import nalar
+    keep = []
+    s = mk()
+    o = oracle_epoch(s, "srtf")
+    sp = pinned_snapshot(s, keep) if pin_in else s
+    ctx = nalar.Context.for_snapshot(s)
+    for _ in range(2):                       # re-upload into the same context
+        ctx.upload(sp)
+        ctx.epoch("srtf")
+        alloc = (lambda n, dt: pinned_like(np.zeros(n, dt), keep)) if pin_out else None
+        g = ctx.fetch(out=ctx.output_buffers(alloc=alloc))
+        same(o, g, f"{s.name} in={pin_in} out={pin_out}")
+    ctx.close()
+
+
+def test_partially_pinned_snapshot():
+    from paper_2601_05109_b200 import nalar
+    keep = []
+    s = swe_table(5000, seed=9)
+    o = oracle_epoch(s, "lpt")
+    sp = pinned_snapshot(s, keep, only={"f_state", "edges", "wf_prio", "i_cap"})
+    ctx = nalar.Context.for_snapshot(s)
+    ctx.upload(sp)
+    ctx.epoch("lpt")
+    g = ctx.fetch(out=ctx.output_buffers(alloc=lambda n, dt: pinned_like(np.zeros(n, dt), keep)))
+    same(o, g, "partial")
+    ctx.close()
+
+
+def test_pinned_fetch_list_too_small():
+    from paper_2601_05109_b200 import nalar
+    keep = []
+    s = c2(2)
+    o = oracle_epoch(s, "srtf")
+    n_asg = len(o["assign_row"])
+    assert n_asg > 1
+    ctx = nalar.Context.for_snapshot(s)
+    ctx.upload(pinned_snapshot(s, keep))
+    ctx.epoch("srtf")
+    out = ctx.output_buffers(("status", "assign"), alloc=lambda n, dt: pinned_like(np.zeros(n, dt), keep))
+    out["assign_row"] = out["assign_row"][:n_asg - 1]
+    out["assign_inst"] = out["assign_inst"][:n_asg - 1]
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.fetch(("status", "assign"), out=out)
+    assert e.value.code == nalar.NALAR_E_SIZE
+    # exactly enough room works, through the same fast path
+    out["assign_row"] = pinned_like(np.zeros(n_asg, np.uint32), keep)
+    out["assign_inst"] = pinned_like(np.zeros(n_asg, np.int16), keep)
+    g = ctx.fetch(("status", "assign"), out=out)
+    assert np.array_equal(g["assign_row"], o["assign_row"])
+    assert np.array_equal(g["assign_inst"], o["assign_inst"])
+    assert np.array_equal(g["status"], o["status"])
+    ctx.close()
+
+
+def test_pinned_invalid_upload_reports_row():
+    from paper_2601_05109_b200 import nalar
+    keep = []
+    s = c1()
+    arrs = s.arrays()
+    edges = arrs["edges"].copy()
+    # an edge of row 5 pointing forward (row 9): the first offending row is 5
+    e0 = int(arrs["f_edge_off"][5])
+    edges[e0] = 9
+    bad = Snapshot(global_row_base=0, name="bad", **{**arrs, "edges": edges})
+    ctx = nalar.Context.for_snapshot(bad)
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.upload(pinned_snapshot(bad, keep))
+    assert e.value.err_row == 5
+    ctx.close()
+
+
+def test_c4_pinned_e2e_matches_oracle():
+    """The configuration bench.py's e2e leg times: pinned C4 in and out."""
+    from paper_2601_05109_b200 import nalar
+    keep = []
+    s = c4()
+    o = oracle_epoch(s, "srtf")
+    sp = pinned_snapshot(s, keep)
+    ctx = nalar.Context.for_snapshot(s)
+    ctx.upload(sp)
+    ctx.epoch("srtf")
+    outb = ctx.output_buffers(("status", "instance", "assign"),
+                              alloc=lambda n, dt: pinned_like(np.zeros(n, dt), keep))
+    g = ctx.fetch(("status", "instance", "assign"), out=outb)
+    for k in ("status", "instance", "assign_row", "assign_inst"):
+        assert np.array_equal(np.asarray(o[k]), np.asarray(g[k])), k
+    ctx.close()
