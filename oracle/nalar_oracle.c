@@ -2,7 +2,8 @@
  *
  * Plain, slow, single-threaded CPU oracle of the Nalar global controller's
  * policy epoch (arXiv 2601.05109).  Written step by step in the order of the
- * epoch definition (readings Q1-Q22 listed in
+ * epoch definition (plus O9 for the NEXT-3 K,V
+ * retention hints; readings Q1-Q22 and Q-kv listed in
  * DESIGN.md "Readings of the paper").  No blocking, fusion or reordering; the
  * only library routine used is qsort (O6/O7 sort by the total order of O4).
  *
@@ -268,6 +269,51 @@ int oracle_epoch(const oracle_table* t, int policy, oracle_out* o) {
             o->assign_row[na] = f;
             o->assign_inst[na] = (int16_t)best;
             na++;
+        }
+    }
+
+    /* O9 K,V-cache retention hints (DESIGN.md Q-kv).
+     * "Because Nalar tracks futures and knows which requests are pending or
+     * likely to arrive next, it can supply the LLM serving layer with explicit
+     * hints about which K,V caches should be retained" P:527 [§4.3]; whether a
+     * cache "remains on the GPU, is offloaded to far memory" P:528, "that a
+     * session has ended" P:525; SPEC kv_hint retain | offload | drop S:542.
+     * A session is (workflow w, SESSION-affinity type t) (Q13); its cache is at
+     * its home = the lowest instance any of its futures is pinned to in the
+     * input table (no pin: no cache, no hint).  A future is live if QUEUED,
+     * RUNNING, or PENDING and not doomed.
+     *   retain  (1): the session has a live future;
+     *   offload (2): it has none, but its workflow still has one (it may recur);
+     *   drop    (3): its workflow has no live future (the session has ended).
+     * kv_level = the highest O4 level among the session's live futures (the
+     * retention urgency), 0 when none. */
+    for (uint32_t w = 0; w < W; ++w) {
+        uint32_t wf_live = 0;
+        for (uint32_t f = t->wf_fut_off[w]; f < t->wf_fut_off[w + 1]; ++f) {
+            uint8_t st = t->f_state[f];
+            if (st == S_QUEUED || st == S_RUNNING || (st == S_PENDING && !doomed[f])) wf_live++;
+        }
+        for (uint32_t ty = 0; ty < T; ++ty) {
+            size_t k = (size_t)w * T + ty;
+            int home = -1;
+            uint32_t live = 0, lv = 0;
+            if (t->t_affinity[ty] == A_SESSION) {
+                for (uint32_t f = t->wf_fut_off[w]; f < t->wf_fut_off[w + 1]; ++f) {
+                    if (t->f_type[f] != ty) continue;
+                    int pin = t->f_pin[f];
+                    if (pin >= 0 && (home < 0 || pin < home)) home = pin;
+                    uint8_t st = t->f_state[f];
+                    if (st == S_QUEUED || st == S_RUNNING || (st == S_PENDING && !doomed[f])) {
+                        live++;
+                        if (o->level[f] > lv) lv = o->level[f];
+                    }
+                }
+            }
+            uint8_t hint = 0;
+            if (home >= 0) hint = live > 0 ? 1 : (wf_live > 0 ? 2 : 3);
+            if (o->kv_hint) o->kv_hint[k] = hint;
+            if (o->kv_level) o->kv_level[k] = (uint8_t)lv;
+            if (o->kv_home) o->kv_home[k] = (int16_t)home;
         }
     }
 

@@ -44,6 +44,9 @@ typedef struct {
     uint32_t* i_assigned; /* [I] */
     uint32_t* assign_row; /* [N] capacity; (resource, global rank) order */
     int16_t*  assign_inst;/* [N] */
+    uint8_t*  kv_hint;    /* [W*T] O9: 0 none, 1 retain, 2 offload, 3 drop (SESSION types) */
+    uint8_t*  kv_level;   /* [W*T] O9: max level of the session's live futures */
+    int16_t*  kv_home;    /* [W*T] O9: the session's home instance, or -1 */
     uint32_t  n_assigned; /* out */
     uint32_t  n_ready, n_eligible, n_doomed; /* out */
 } oracle_out;

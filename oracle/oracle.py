@@ -33,6 +33,7 @@ class _Out(C.Structure):
                 ("instance", C.c_void_p), ("new_pin", C.c_void_p), ("wf_agg", C.c_void_p),
                 ("i_load", C.c_void_p), ("i_spare", C.c_void_p), ("i_assigned", C.c_void_p),
                 ("assign_row", C.c_void_p), ("assign_inst", C.c_void_p),
+                ("kv_hint", C.c_void_p), ("kv_level", C.c_void_p), ("kv_home", C.c_void_p),
                 ("n_assigned", C.c_uint32), ("n_ready", C.c_uint32), ("n_eligible", C.c_uint32),
                 ("n_doomed", C.c_uint32)]
 
@@ -91,10 +92,12 @@ def oracle_epoch(s, policy="srtf", levels: int = 256) -> dict:
         "i_load": np.zeros(I, np.uint32), "i_spare": np.zeros(I, np.uint32),
         "i_assigned": np.zeros(I, np.uint32), "assign_row": np.zeros(max(N, 1), np.uint32),
         "assign_inst": np.zeros(max(N, 1), np.int16),
+        "kv_hint": np.zeros((W, s.n_types), np.uint8), "kv_level": np.zeros((W, s.n_types), np.uint8),
+        "kv_home": np.zeros((W, s.n_types), np.int16),
     }
     o = _Out(*[_ptr(out[k]) for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg",
                                       "i_load", "i_spare", "i_assigned", "assign_row",
-                                      "assign_inst")], 0, 0, 0, 0)
+                                      "assign_inst", "kv_hint", "kv_level", "kv_home")], 0, 0, 0, 0)
     rc = lib.oracle_epoch(C.byref(t), pol, C.byref(o))
     if rc != 0:
         raise ValueError("oracle: invalid table")

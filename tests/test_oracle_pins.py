@@ -377,3 +377,88 @@ def test_validation():
     assert oracle_validate(s)[0] == -1 and oracle_validate(s)[1] == 29
     s = c2(seed=1, n_workflows=3); s.wf_id[2] = s.wf_id[1]
     assert oracle_validate(s) == (-1, -1)
+
+
+# --------------------------------------------------------------------------
+# O9 K,V-cache retention hints (NEXT-3, SPEC kv_hint S:542)
+# --------------------------------------------------------------------------
+KV_NONE, KV_RETAIN, KV_OFFLOAD, KV_DROP = range(4)
+
+
+def test_kv_hints_hand_derived():
+    """Every hint class, derived by hand.  Types: 0 LLM (SESSION), 1 TOOL
+    (NONE), 2 CODER (SESSION); instances 0,1 LLM; 2 TOOL; 3,4 CODER."""
+    tb = TableBuilder(i_type=[0, 0, 1, 2, 2], i_cap=[4, 4, 4, 4, 4], i_base_load=[0] * 5,
+                      t_affinity=[AFF_SESSION, AFF_NONE, AFF_SESSION])
+    # w0: LLM session homed at min(1, 0) = 0 with a live PENDING future (level =
+    # prio 5 + SRTF depth 1 = 6) -> retain@0, level 6.  CODER session homed at 4,
+    # only RESOLVED -> offload (the workflow is still live).
+    tb.add_workflow(1, 5, [(RESOLVED, 0, 0, -1, 1, []),            # r0 LLM pinned 1
+                           (PENDING, 0, 0, -1, 0, [(0, False)]),    # r1 LLM pinned 0, ready, depth 1
+                           (RESOLVED, 2, 0, -1, 4, [(0, False)]),   # r2 CODER pinned 4
+                           (PENDING, 1, 0, -1, -1, [(2, False)])])  # r3 TOOL
+    # w1: everything terminal -> its LLM session (home 1) is dropped; its CODER
+    # session has no pin -> no hint.
+    tb.add_workflow(2, 0, [(RESOLVED, 0, 0, -1, 1, []),
+                           (FAILED, 2, 0, -1, -1, [(0, False)])])
+    # w2: LLM session homed at 1 whose only PENDING future is doomed (a FAILED DEP
+    # predecessor); the TOOL future is RUNNING -> offload.  CODER session pinned
+    # at 3 with a QUEUED future at 3 (level = prio 0 + depth 0) -> retain@3.
+    tb.add_workflow(3, 0, [(FAILED, 1, 0, -1, -1, []),
+                           (PENDING, 0, 0, -1, 1, [(0, False)]),
+                           (RUNNING, 1, 0, 2, -1, []),
+                           (QUEUED, 2, 0, 3, 3, [])])
+    s = tb.build()
+    o = oracle_epoch(s, "srtf")
+    assert o["kv_hint"].tolist() == [[KV_RETAIN, KV_NONE, KV_OFFLOAD],
+                                     [KV_DROP, KV_NONE, KV_NONE],
+                                     [KV_OFFLOAD, KV_NONE, KV_RETAIN]]
+    assert o["kv_home"].tolist() == [[0, -1, 4], [1, -1, -1], [1, -1, 3]]
+    assert o["kv_level"].tolist() == [[6, 0, 0], [0, 0, 0], [0, 0, 0]]
+    assert o["status"][[1, 7]].tolist() == [S_ASG, S_DOOM]
+
+
+def _kv_from_statuses(s, o):
+    """O9 by another route: live futures are read off the O8 statuses (INFLIGHT,
+    WAITING, INELIGIBLE, DEFERRED, ASSIGNED -- not DOOMED), homes by a vectorised
+    grouped minimum, levels by a grouped maximum."""
+    W, T = s.n_workflows, s.n_types
+    wf = np.repeat(np.arange(W), np.diff(s.wf_fut_off.astype(np.int64)))
+    ty = s.f_type.astype(np.int64)
+    live = np.isin(o["status"], [S_INF, S_WAIT, S_INEL, S_DEF, S_ASG])
+    key = wf * T + ty
+    home = np.full(W * T, 1 << 30, np.int64)
+    pinned = s.f_pin >= 0
+    np.minimum.at(home, key[pinned], s.f_pin[pinned].astype(np.int64))
+    n_live = np.bincount(key[live], minlength=W * T)
+    lev = np.zeros(W * T, np.int64)
+    np.maximum.at(lev, key[live], o["level"][live].astype(np.int64))
+    wf_live = np.bincount(wf[live], minlength=W)[np.arange(W * T) // T]
+    sess = (s.t_affinity[np.arange(W * T) % T] == AFF_SESSION)
+    has_home = sess & (home < (1 << 30))
+    hint = np.where(~has_home, KV_NONE,
+                    np.where(n_live > 0, KV_RETAIN, np.where(wf_live > 0, KV_OFFLOAD, KV_DROP)))
+    lev = np.where(sess, lev, 0)
+    home = np.where(has_home, home, -1)
+    return hint.reshape(W, T), lev.reshape(W, T), home.reshape(W, T)
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_kv_hints_grouped_route(seed):
+    s = random_table(seed, n_workflows=1 + seed % 6, max_rows=2 + seed % 25, n_types=1 + seed % 4,
+                     inst_per_type=(0, 1 + seed % 3), consistent=seed % 2 == 0, p_pin=0.5)
+    o = oracle_epoch(s, ["fcfs", "srtf", "lpt"][seed % 3])
+    h, lv, home = _kv_from_statuses(s, o)
+    assert o["kv_hint"].tolist() == h.tolist()
+    assert o["kv_level"].tolist() == lv.tolist()
+    assert o["kv_home"].tolist() == home.tolist()
+
+
+def test_kv_hints_c2_c4_grouped_route():
+    for s in (c2(1), c4()):
+        o = oracle_epoch(s, "srtf")
+        h, lv, home = _kv_from_statuses(s, o)
+        assert np.array_equal(o["kv_hint"], h) and np.array_equal(o["kv_level"], lv)
+        assert np.array_equal(o["kv_home"], home)
+        if s.n_futures == 1 << 17:
+            assert set(np.unique(h)) == {KV_NONE, KV_RETAIN, KV_OFFLOAD, KV_DROP}
