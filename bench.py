@@ -142,8 +142,10 @@ def k1_algorithmic_bytes(s, n_elig):
     """SURVEY §8(d) byte model recomputed for this layout:
     per future 11 B read (state, type, round, executor, pin, edge_off) + 7 B
     written (status, level, depth, instance, new_pin); 4 B per edge; per
-    workflow 48 B (offset, prio, 10 aggregates); 8 B per eligible item."""
-    return 18 * s.n_futures + 4 * s.n_edges + 48 * s.n_workflows + 8 * n_elig
+    workflow 48 B (offset, prio, 10 aggregates) + 4 B per (workflow, type) of
+    K,V hints (hint, level, home); 8 B per eligible item."""
+    return (18 * s.n_futures + 4 * s.n_edges + 48 * s.n_workflows + 4 * s.n_workflows * s.n_types +
+            8 * n_elig)
 
 
 def k4_algorithmic_bytes(R, levels, G, n_elig, n_asg):

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define NALAR_ABI_VERSION 1
+#define NALAR_ABI_VERSION 2
 
 /* limits (DESIGN.md §3 "Data layout") */
 #define NALAR_MAX_LEVELS     256      /* level is u8                          */
@@ -206,6 +206,18 @@ typedef struct {
     int16_t*  assign_inst;/* [n_assigned] their instances                      */
     uint32_t  a_cap;
     uint32_t  n_f, n_w, n_i, n_assigned;  /* out */
+    /* K,V-cache retention hints ("explicit
+     * hints about which K,V caches should be retained", SPEC kv_hint S:542),
+     * one entry per (workflow w, type t), row-major [W][T].  A session is a
+     * workflow's SESSION-affinity type; its home is the lowest instance any of
+     * its futures is pinned to in the uploaded table.  With a home:
+     * 1 retain (a live -- QUEUED, RUNNING or non-doomed PENDING -- future of the
+     * session exists), 2 offload (none, but the workflow has a live future),
+     * 3 drop (the workflow has none: the session ended); 0 otherwise.        */
+    uint8_t*  kv_hint;    /* [W][T]                                            */
+    uint8_t*  kv_level;   /* [W][T] max level of the session's live futures    */
+    int16_t*  kv_home;    /* [W][T] home instance or -1                        */
+    uint32_t  kv_cap;     /* elements (>= W * T)                               */
 } nalar_decisions;
 
 /* TickReport analog. */

@@ -72,6 +72,9 @@ struct SweepParams {
     int16_t* instance;
     uint8_t* new_pin;
     uint32_t* wf_agg;           // [W][10]
+    uint8_t* kv_hint;           // [W][T] K,V retention hint (NEXT-3): 0 none, 1 retain, 2 offload, 3 drop
+    uint8_t* kv_level;          // [W][T] retention urgency: max level of the session's live futures
+    int16_t* kv_home;           // [W][T] the session's home instance, or -1
     uint32_t* H;                // this rank's histogram slot [R][Lv]
     uint32_t* load_part;        // [I] in-flight counts of this rank's rows
     uint32_t* tot;              // [R] eligible futures per resource (this rank; summed by the allreduce)

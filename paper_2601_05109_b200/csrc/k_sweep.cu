@@ -170,7 +170,7 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
 size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
     size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs) +
                align16(4 * ((size_t)wfs + 1)) + align16(4 * (size_t)wfs) +
-               align16(32 * (size_t)wfs);                                                // per-workflow tables
+               align16(32 * (size_t)wfs) + align16(8 * (size_t)wfs * T);                 // per-workflow tables
     if (staged)
         b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
              align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
@@ -231,6 +231,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     q += align16(4 * (size_t)nw);
     uint32_t* s_agg = (uint32_t*)q;                          // [nw][8] counts (P3), max depth (sweep)
     q += align16(32 * (size_t)nw);
+    uint32_t* s_khome = (uint32_t*)q;                        // [nw][T] session home (min pin) -- NEXT-3
+    uint32_t* s_klev = s_khome + (size_t)nw * T;             // [nw][T] 1 + max level of live futures
+    q += align16(8 * (size_t)nw * T);
 
     // ---- the block's slice of the table: staged in smem by TMA, or in place --
     const uint8_t* st;    // state, type, round, pin, executor: indexed by local row
@@ -321,7 +324,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     for (uint32_t i = tid; i < I; i += kK1Threads) s_load[i] = 0;
     for (uint32_t r = tid; r < R; r += kK1Threads) s_rcnt[r] = 0;
     for (uint32_t t = tid; t < T; t += kK1Threads) s_aff[t] = p.t_aff[t];
-    for (uint32_t k = tid; k < nw * T; k += kK1Threads) { s_wfp[k] = 0xFFFFFFFFu; s_wfru[k] = 0xFFFFFFFFu; }
+    for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
+        s_wfp[k] = 0xFFFFFFFFu; s_wfru[k] = 0xFFFFFFFFu; s_khome[k] = 0xFFFFFFFFu; s_klev[k] = 0u;
+    }
     for (uint32_t k = tid; k < nw; k += kK1Threads) { s_winfl[2 * k] = 0u; s_winfl[2 * k + 1] = 0u; s_perm[k] = p.wf_perm[w0 + k]; }
     for (uint32_t k = tid; k < 8 * nw; k += kK1Threads) s_agg[k] = 0;
     for (uint32_t k = tid; k < nr; k += kK1Threads) aux[k] = 0;   // step-done flags
@@ -890,6 +895,10 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             }
             if (pend && !doom) kp = wl << 6 | tyf;
             if (ready && pinf < 0) kr = wl << 6 | tyf;
+            if (aff == 1u) {                // K,V retention hints (NEXT-3): home, urgency
+                if (pinf >= 0) atomicMin(&s_khome[wl * T + tyf], (uint32_t)pinf);
+                if (infl_row || (pend && !doom)) atomicMax(&s_klev[wl * T + tyf], lv + 1u);
+            }
         }
         // per-workflow counts ("aggregating metrics and metadata"):
         // rows are in workflow order, so a warp's lanes form contiguous
@@ -943,6 +952,20 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         else if (j == 8) v = s_agg[wl * 8 + 7];
         else v = s_wrnd[wl];
         p.wf_agg[(size_t)w0 * 10 + k] = v;
+    }
+    // K,V-cache retention hints per (workflow, SESSION type) (PAPER.md:524-529,
+    // SPEC kv_hint S:542; DESIGN.md Q-kv): retain while the session has a live
+    // future, offload when only its workflow does, drop when neither
+    for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
+        const uint32_t wl = k / T, t = k - wl * T;
+        const bool sess = s_aff[t] == 1u;
+        const uint32_t home = s_khome[k], kl = s_klev[k];
+        const uint32_t* a = s_agg + (size_t)wl * 8;
+        const uint32_t wf_live = a[0] - a[5] + a[2];      // pending - doomed + in flight
+        const bool has = sess && home != 0xFFFFFFFFu;
+        p.kv_hint[(size_t)w0 * T + k] = (uint8_t)(has ? (kl ? 1u : (wf_live ? 2u : 3u)) : 0u);
+        p.kv_level[(size_t)w0 * T + k] = (uint8_t)(sess && kl ? kl - 1u : 0u);
+        p.kv_home[(size_t)w0 * T + k] = (int16_t)(has ? (int)home : -1);
     }
 
     // ---- P4: the stateful fence and first placement

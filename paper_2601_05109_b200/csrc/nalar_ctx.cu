@@ -97,6 +97,8 @@ struct nalar_ctx {
     uint16_t* d_gaux = nullptr;
     uint16_t* d_depth = nullptr;
     int16_t *d_inst = nullptr, *d_ainst = nullptr;
+    uint8_t *d_kvh = nullptr, *d_kvl = nullptr;
+    int16_t* d_kvhome = nullptr;
     uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
     // intermediates
     uint2* d_items = nullptr;
@@ -183,6 +185,7 @@ struct Plan {
     size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, wf_perm, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
+    size_t kvh, kvl, kvhome;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
     uint32_t Rmax, Bmax;
@@ -231,6 +234,9 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->inst = L.take<int16_t>(N);
     p->ainst = L.take<int16_t>(N);
     p->wfagg = L.take<uint32_t>(W * NALAR_WF_AGG_FIELDS);
+    p->kvh = L.take<uint8_t>(W * T);
+    p->kvl = L.take<uint8_t>(W * T);
+    p->kvhome = L.take<int16_t>(W * T);
     p->iload = L.take<uint32_t>(I);
     p->ispare = L.take<uint32_t>(I);
     p->iasg = L.take<uint32_t>(I);
@@ -353,6 +359,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.n_wf = c->W;
     p.status = c->d_status; p.level = c->d_level; p.depth = c->d_depth; p.instance = c->d_inst;
     p.new_pin = c->d_newpin; p.wf_agg = c->d_wfagg;
+    p.kv_hint = c->d_kvh; p.kv_level = c->d_kvl; p.kv_home = c->d_kvhome;
     const uint32_t slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
     p.H = c->d_x + (size_t)slot * c->R * c->Lv;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
@@ -586,6 +593,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_gifc = at<uint32_t>(a, p.gifc); c->d_gndp = at<uint32_t>(a, p.gndp); c->d_gaux = at<uint16_t>(a, p.gaux);
     c->d_depth = at<uint16_t>(a, p.depth); c->d_inst = at<int16_t>(a, p.inst); c->d_ainst = at<int16_t>(a, p.ainst);
     c->d_wfagg = at<uint32_t>(a, p.wfagg); c->d_iload = at<uint32_t>(a, p.iload);
+    c->d_kvh = at<uint8_t>(a, p.kvh); c->d_kvl = at<uint8_t>(a, p.kvl); c->d_kvhome = at<int16_t>(a, p.kvhome);
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
     c->d_items = at<uint2>(a, p.items); c->d_cnt_rb = at<uint32_t>(a, p.cnt_rb); c->d_off_rb = at<uint32_t>(a, p.off_rb);
     c->d_x = at<uint32_t>(a, p.x); c->d_scr = at<uint32_t>(a, p.scr);
@@ -1010,16 +1018,20 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     // the way, and one synchronisation.
     {
         struct Out { void* h; const void* d; size_t bytes; };
-        const Out outs[9] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
+        const Out outs[12] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
                              {o->depth, c->d_depth, 2ull * c->N}, {o->instance, c->d_inst, 2ull * c->N},
                              {o->new_pin, c->d_newpin, c->N},
                              {o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W},
                              {o->i_load, c->d_iload, 4ull * c->I}, {o->i_spare, c->d_ispare, 4ull * c->I},
-                             {o->i_assigned, c->d_iasg, 4ull * c->I}};
+                             {o->i_assigned, c->d_iasg, 4ull * c->I},
+                             {o->kv_hint, c->d_kvh, (size_t)c->W * c->T},
+                             {o->kv_level, c->d_kvl, (size_t)c->W * c->T},
+                             {o->kv_home, c->d_kvhome, 2ull * c->W * c->T}};
         const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
         const bool wbad = o->wf_agg && o->wf_cap < c->W;
         const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
-        bool mapped = !(fbad || wbad || ibad);
+        const bool kbad = (o->kv_hint || o->kv_level || o->kv_home) && o->kv_cap < (size_t)c->W * c->T;
+        bool mapped = !(fbad || wbad || ibad || kbad);
         CopyBatch cb(st);
         for (const Out& q : outs) {
             if (!mapped || !q.h || !q.bytes) continue;
@@ -1060,7 +1072,8 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     const bool wbad = o->wf_agg && o->wf_cap < c->W;
     const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
     const bool abad = (o->assign_row || o->assign_inst) && o->a_cap < na;
-    if (fbad || wbad || ibad || abad) return fail(c, NALAR_E_SIZE, "output buffer too small");
+    const bool kbad = (o->kv_hint || o->kv_level || o->kv_home) && o->kv_cap < (size_t)c->W * c->T;
+    if (fbad || wbad || ibad || abad || kbad) return fail(c, NALAR_E_SIZE, "output buffer too small");
     auto d2h = [&](void* h, const void* d, size_t bytes) -> cudaError_t {
         return (h && bytes) ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
     };
@@ -1070,6 +1083,9 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     CK(d2h(o->instance, c->d_inst, 2ull * c->N));
     CK(d2h(o->new_pin, c->d_newpin, c->N));
     CK(d2h(o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W));
+    CK(d2h(o->kv_hint, c->d_kvh, (size_t)c->W * c->T));
+    CK(d2h(o->kv_level, c->d_kvl, (size_t)c->W * c->T));
+    CK(d2h(o->kv_home, c->d_kvhome, 2ull * c->W * c->T));
     CK(d2h(o->i_load, c->d_iload, 4ull * c->I));
     CK(d2h(o->i_spare, c->d_ispare, 4ull * c->I));
     CK(d2h(o->i_assigned, c->d_iasg, 4ull * c->I));

@@ -62,7 +62,9 @@ class nalar_decisions(C.Structure):
                 ("i_cap", C.c_uint32),
                 ("assign_row", C.c_void_p), ("assign_inst", C.c_void_p), ("a_cap", C.c_uint32),
                 ("n_f", C.c_uint32), ("n_w", C.c_uint32), ("n_i", C.c_uint32),
-                ("n_assigned", C.c_uint32)]
+                ("n_assigned", C.c_uint32),
+                ("kv_hint", C.c_void_p), ("kv_level", C.c_void_p), ("kv_home", C.c_void_p),
+                ("kv_cap", C.c_uint32)]
 
 
 class nalar_delta(C.Structure):
@@ -296,6 +298,7 @@ class Context:
         self.cfg = cfg
         self.h = nalar_create(cfg)
         self.n = None
+        self.n_types = 0
 
     @classmethod
     def for_snapshot(cls, s, **kw):
@@ -321,6 +324,7 @@ class Context:
             e.err_row = row
             raise e
         self.n = (s.n_futures, s.n_workflows, s.n_instances)
+        self.n_types = s.n_types
 
     def apply_delta(self, dl) -> None:
         d, keep = delta_struct(dl)
@@ -351,7 +355,7 @@ class Context:
         return nalar_epoch_stats_get(self.h)
 
     def output_buffers(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg",
-                                     "i_load", "i_spare", "i_assigned", "assign"), alloc=None):
+                                     "i_load", "i_spare", "i_assigned", "assign", "kv"), alloc=None):
         """Host buffers for fetch(); ``alloc(n, dtype)`` may return pinned memory."""
         N, W, I = self.n
         alloc = alloc or (lambda n, dt: np.zeros(n, dt))
@@ -360,20 +364,28 @@ class Context:
                 "wf_agg": (W * 10, np.uint32), "i_load": (I, np.uint32),
                 "i_spare": (I, np.uint32), "i_assigned": (I, np.uint32)}
         out = {k: alloc(n, dt) for k, (n, dt) in spec.items() if k in fields}
+        if "kv" in fields:
+            T = self.n_types
+            out["kv_hint"] = alloc(W * T, np.uint8)
+            out["kv_level"] = alloc(W * T, np.uint8)
+            out["kv_home"] = alloc(W * T, np.int16)
         if "assign" in fields:
             out["assign_row"] = alloc(max(N, 1), np.uint32)
             out["assign_inst"] = alloc(max(N, 1), np.int16)
         return out
 
     def fetch(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
-                            "i_spare", "i_assigned", "assign"), out=None) -> dict:
+                            "i_spare", "i_assigned", "assign", "kv"), out=None) -> dict:
         N, W, I = self.n
         bufs = out if out is not None else self.output_buffers(fields)
         d = nalar_decisions()
         for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
-                  "i_spare", "i_assigned", "assign_row", "assign_inst"):
+                  "i_spare", "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home"):
             if k in bufs:
                 setattr(d, k, _ptr(bufs[k]))
+        if "kv_hint" in bufs:
+            d.kv_cap = min(len(bufs["kv_hint"]), len(bufs.get("kv_level", bufs["kv_hint"])),
+                           len(bufs.get("kv_home", bufs["kv_hint"])))
         d.f_cap, d.wf_cap, d.i_cap = N, W, I
         if "assign_row" in bufs:
             d.a_cap = min(len(bufs["assign_row"]), len(bufs["assign_inst"]))
@@ -381,6 +393,9 @@ class Context:
         res = dict(bufs)
         if "wf_agg" in res:
             res["wf_agg"] = res["wf_agg"].reshape(W, 10)
+        for k in ("kv_hint", "kv_level", "kv_home"):
+            if k in res:
+                res[k] = res[k][:W * self.n_types].reshape(W, self.n_types)
         if "assign_row" in res:
             res["assign_row"] = res["assign_row"][:d.n_assigned]
             res["assign_inst"] = res["assign_inst"][:d.n_assigned]

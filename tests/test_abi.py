@@ -80,7 +80,7 @@ int main(void){
 def test_no_cpu_fallback_without_gpu(lib):
     import torch
     from paper_2601_05109_b200 import nalar
-    assert nalar.nalar_abi_version() == 1
+    assert nalar.nalar_abi_version() == 2
     cfg = nalar.nalar_config()
     cfg.world, cfg.max_futures, cfg.max_edges, cfg.max_workflows = 1, 10, 10, 2
     cfg.max_instances, cfg.max_types = 2, 1

@@ -15,7 +15,7 @@ from oracle import oracle_epoch
 pytestmark = pytest.mark.gpu
 
 KEYS = ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load", "i_spare",
-        "i_assigned", "assign_row", "assign_inst")
+        "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home")
 
 
 def _torch():

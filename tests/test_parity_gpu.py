@@ -16,7 +16,7 @@ from oracle import oracle_epoch, oracle_validate
 pytestmark = pytest.mark.gpu
 
 KEYS = ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load", "i_spare",
-        "i_assigned", "assign_row", "assign_inst")
+        "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home")
 
 
 def _nalar():
@@ -235,6 +235,8 @@ def test_sharded_equals_single(G, which):
         got = np.concatenate([g[k] for g, _ in outs])
         assert np.array_equal(got, o[k]), (k, G)
     assert np.array_equal(np.concatenate([g["wf_agg"] for g, _ in outs]), o["wf_agg"])
+    for k in ("kv_hint", "kv_level", "kv_home"):
+        assert np.array_equal(np.concatenate([g[k] for g, _ in outs]), o[k]), (k, G)
     for g, sh in outs:
         for k in ("i_load", "i_spare", "i_assigned"):
             assert np.array_equal(g[k], o[k]), (k, G)
