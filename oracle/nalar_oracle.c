@@ -325,3 +325,90 @@ int oracle_epoch(const oracle_table* t, int policy, oracle_out* o) {
     free(doomed); free(ready); free(eligible); free(wf_of);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O10 resource reassignment (DESIGN.md Q-ra).           */
+/* "resource reassignment from low-load agents to high-load agents" P:663,   */
+/* P:672, P:676 [§6.1]; kill / provision primitives P:393-394 [§4.2];        */
+/* max_instances / min_instances directives P:252-253 (Table 1); SPEC        */
+/* resource_reassign S:448-456: if type A's utilisation > u_hi and B's <     */
+/* u_lo, B above min_instances and A below max_instances, emit Kill(one B     */
+/* instance) + Provision(A).                                                  */
+/*   busy_t = sum over t's instances of (load + assigned this epoch)          */
+/*            + t's DEFERRED futures (unmet demand);  cap_t = sum of caps;    */
+/*   util_t = busy_t / cap_t, compared exactly: 100 busy vs pct * cap;        */
+/*   hot:  n_t < max_t and 100 busy_t > u_hi cap_t;                           */
+/*   cold: n_t > min_t and 100 busy_t < u_lo cap_t;                            */
+/*   hot types by util desc, cold by util asc (ties: lower type id); the k-th */
+/*   hot is paired with the k-th cold: kill the cold type's instance with the */
+/*   least (load + assigned) (ties: the highest id), provision the hot type.  */
+/* ------------------------------------------------------------------------ */
+static const uint64_t* g_busy;
+static const uint64_t* g_cap;
+/* util(a) > util(b) as exact fractions; cap 0 with busy > 0 is infinite */
+static int util_gt(uint32_t a, uint32_t b) {
+    uint64_t ba = g_busy[a], ca = g_cap[a], bb = g_busy[b], cb = g_cap[b];
+    int ia = ca == 0 && ba > 0, ib = cb == 0 && bb > 0;
+    if (ia || ib) return ia && !ib;
+    if (ca == 0 && cb == 0) return 0;                        /* both 0/0: equal */
+    if (ca == 0) return 0;                                   /* 0/0 = 0 */
+    if (cb == 0) return ba > 0;
+    return (unsigned __int128)ba * cb > (unsigned __int128)bb * ca;
+}
+static int cmp_hot(const void* x, const void* y) {
+    uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
+    if (util_gt(a, b)) return -1;
+    if (util_gt(b, a)) return 1;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+static int cmp_cold(const void* x, const void* y) {
+    uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
+    if (util_gt(b, a)) return -1;
+    if (util_gt(a, b)) return 1;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+int oracle_reassign(const oracle_table* t, const oracle_out* o, const oracle_ra_params* p, oracle_ra_out* r) {
+    uint32_t N = t->n_futures, I = t->n_instances, T = t->n_types;
+    uint64_t* busy = (uint64_t*)calloc(T ? T : 1, sizeof(uint64_t));
+    uint64_t* cap = (uint64_t*)calloc(T ? T : 1, sizeof(uint64_t));
+    uint32_t* cnt = (uint32_t*)calloc(T ? T : 1, sizeof(uint32_t));
+    uint32_t* hot = (uint32_t*)malloc(sizeof(uint32_t) * (T ? T : 1));
+    uint32_t* cold = (uint32_t*)malloc(sizeof(uint32_t) * (T ? T : 1));
+    for (uint32_t i = 0; i < I; ++i) {
+        uint32_t ty = t->i_type[i];
+        busy[ty] += (uint64_t)o->i_load[i] + o->i_assigned[i];
+        cap[ty] += t->i_cap[i];
+        cnt[ty] += 1;
+    }
+    for (uint32_t f = 0; f < N; ++f)
+        if (o->status[f] == O_DEFERRED) busy[t->f_type[f]] += 1;
+    uint32_t nh = 0, nc = 0;
+    for (uint32_t ty = 0; ty < T; ++ty) {
+        r->t_busy[ty] = (uint32_t)(busy[ty] > 0xFFFFFFFFull ? 0xFFFFFFFFull : busy[ty]);
+        r->t_cap[ty] = (uint32_t)(cap[ty] > 0xFFFFFFFFull ? 0xFFFFFFFFull : cap[ty]);
+        uint32_t mn = p->t_min_inst ? p->t_min_inst[ty] : 0u;
+        uint32_t mx = p->t_max_inst ? p->t_max_inst[ty] : 0xFFFFu;
+        if (cnt[ty] < mx && 100ull * busy[ty] > (uint64_t)p->u_hi_pct * cap[ty]) hot[nh++] = ty;
+        else if (cnt[ty] > mn && 100ull * busy[ty] < (uint64_t)p->u_lo_pct * cap[ty]) cold[nc++] = ty;
+    }
+    g_busy = busy;
+    g_cap = cap;
+    qsort(hot, nh, sizeof(uint32_t), cmp_hot);
+    qsort(cold, nc, sizeof(uint32_t), cmp_cold);
+    uint32_t np = nh < nc ? nh : nc;
+    for (uint32_t k = 0; k < np; ++k) {
+        int64_t best = -1;
+        uint64_t best_b = 0;
+        for (uint32_t i = 0; i < I; ++i) {
+            if (t->i_type[i] != cold[k]) continue;
+            uint64_t b = (uint64_t)o->i_load[i] + o->i_assigned[i];
+            if (best < 0 || b <= best_b) { best = i; best_b = b; }     /* ties: the highest id */
+        }
+        r->kill_inst[k] = (int16_t)best;
+        r->prov_type[k] = (int16_t)hot[k];
+    }
+    r->n_pairs = np;
+    free(busy); free(cap); free(cnt); free(hot); free(cold);
+    return 0;
+}

@@ -51,6 +51,26 @@ typedef struct {
     uint32_t  n_ready, n_eligible, n_doomed; /* out */
 } oracle_out;
 
+/* O10 resource reassignment parameters (NEXT-2): per-type directives
+ * min_instances / max_instances (Table 1) and the
+ * utilisation thresholds in percent (SPEC S:452 defaults u_hi 80, u_lo 30). */
+typedef struct {
+    const uint16_t* t_min_inst; /* [T] */
+    const uint16_t* t_max_inst; /* [T] */
+    uint32_t u_hi_pct, u_lo_pct;
+} oracle_ra_params;
+
+typedef struct {
+    uint32_t* t_busy;     /* [T] sum(load + assigned) over the type's instances + its DEFERRED futures */
+    uint32_t* t_cap;      /* [T] sum of the type's capacities */
+    int16_t*  kill_inst;  /* [T] pair k: the instance to kill */
+    int16_t*  prov_type;  /* [T] pair k: the type to provision */
+    uint32_t  n_pairs;    /* out */
+} oracle_ra_out;
+
+/* O10 from a finished epoch (o from oracle_epoch on the same table). */
+int oracle_reassign(const oracle_table* t, const oracle_out* o, const oracle_ra_params* p, oracle_ra_out* r);
+
 /* 0 = valid, -1 = invalid; *err_row = smallest offending future row, or -1
  * when the violation is not attributable to a row. */
 int oracle_validate(const oracle_table* t, int64_t* err_row);

@@ -38,6 +38,16 @@ class _Out(C.Structure):
                 ("n_doomed", C.c_uint32)]
 
 
+class _RaParams(C.Structure):
+    _fields_ = [("t_min_inst", C.c_void_p), ("t_max_inst", C.c_void_p),
+                ("u_hi_pct", C.c_uint32), ("u_lo_pct", C.c_uint32)]
+
+
+class _RaOut(C.Structure):
+    _fields_ = [("t_busy", C.c_void_p), ("t_cap", C.c_void_p), ("kill_inst", C.c_void_p),
+                ("prov_type", C.c_void_p), ("n_pairs", C.c_uint32)]
+
+
 _lib = None
 
 
@@ -56,6 +66,8 @@ def _load():
         _lib = C.CDLL(ORACLE_SO)
         _lib.oracle_validate.argtypes = [C.POINTER(_Table), C.POINTER(C.c_int64)]
         _lib.oracle_epoch.argtypes = [C.POINTER(_Table), C.c_int, C.POINTER(_Out)]
+        _lib.oracle_reassign.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_RaParams),
+                                         C.POINTER(_RaOut)]
     return _lib
 
 
@@ -80,7 +92,9 @@ def oracle_validate(s, levels: int = 256):
     return rc, err.value
 
 
-def oracle_epoch(s, policy="srtf", levels: int = 256) -> dict:
+def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None) -> dict:
+    """One epoch; ``reassign`` = dict(t_min_inst, t_max_inst, u_hi_pct, u_lo_pct)
+    also runs O10 (resource reassignment) on the result."""
     lib = _load()
     pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
     t, keep = _table(s, levels)
@@ -101,6 +115,19 @@ def oracle_epoch(s, policy="srtf", levels: int = 256) -> dict:
     rc = lib.oracle_epoch(C.byref(t), pol, C.byref(o))
     if rc != 0:
         raise ValueError("oracle: invalid table")
+    if reassign is not None:            # O10 (NEXT-2) on the finished epoch
+        T = s.n_types
+        mn = np.ascontiguousarray(reassign.get("t_min_inst", np.zeros(T)), np.uint16)
+        mx = np.ascontiguousarray(reassign.get("t_max_inst", np.full(T, 0xFFFF)), np.uint16)
+        ra = {"t_busy": np.zeros(T, np.uint32), "t_cap": np.zeros(T, np.uint32),
+              "kill_inst": np.zeros(max(T, 1), np.int16), "prov_type": np.zeros(max(T, 1), np.int16)}
+        prm = _RaParams(_ptr(mn), _ptr(mx), int(reassign.get("u_hi_pct", 80)),
+                        int(reassign.get("u_lo_pct", 30)))
+        ro = _RaOut(*[_ptr(ra[k]) for k in ("t_busy", "t_cap", "kill_inst", "prov_type")], 0)
+        lib.oracle_reassign(C.byref(t), C.byref(o), C.byref(prm), C.byref(ro))
+        out["t_busy"], out["t_cap"] = ra["t_busy"], ra["t_cap"]
+        out["ra_kill"] = ra["kill_inst"][:ro.n_pairs].copy()
+        out["ra_prov"] = ra["prov_type"][:ro.n_pairs].copy()
     na = o.n_assigned
     out["assign_row"] = out["assign_row"][:na].copy()
     out["assign_inst"] = out["assign_inst"][:na].copy()

@@ -462,3 +462,85 @@ def test_kv_hints_c2_c4_grouped_route():
         assert np.array_equal(o["kv_home"], home)
         if s.n_futures == 1 << 17:
             assert set(np.unique(h)) == {KV_NONE, KV_RETAIN, KV_OFFLOAD, KV_DROP}
+
+
+# --------------------------------------------------------------------------
+# O10 resource reassignment (NEXT-2)
+# --------------------------------------------------------------------------
+def test_reassign_hand_derived():
+    """Types 0, 1, 2 with two instances each (cap 4).  Type 0: loads (4, 3)
+    plus two deferred futures -> busy 9 / cap 8 (112%) hot.  Type 1: loads
+    (1, 0) -> 12.5% cold; kill its least-loaded instance 3.  Type 2: loads
+    (2, 2) -> 50% neither."""
+    tb = TableBuilder(i_type=[0, 0, 1, 1, 2, 2], i_cap=[4] * 6, i_base_load=[4, 3, 1, 0, 2, 2],
+                      t_affinity=[AFF_NONE, AFF_NONE, AFF_NONE])
+    tb.add_workflow(1, 0, [(PENDING, 0, 0, -1, -1, []), (PENDING, 0, 0, -1, -1, [])])
+    s = tb.build()
+    o = oracle_epoch(s, "fcfs", reassign={"u_hi_pct": 80, "u_lo_pct": 30})
+    assert o["status"].tolist() == [S_ASG, S_DEF]          # instance 1 has one slot left
+    assert o["t_busy"].tolist() == [9, 1, 4] and o["t_cap"].tolist() == [8, 8, 8]
+    assert o["ra_kill"].tolist() == [3] and o["ra_prov"].tolist() == [0]
+    # directives: type 1 at its floor, or type 0 at its ceiling -> nothing
+    o = oracle_epoch(s, "fcfs", reassign={"t_min_inst": [0, 2, 0], "u_hi_pct": 80, "u_lo_pct": 30})
+    assert o["ra_kill"].tolist() == []
+    o = oracle_epoch(s, "fcfs", reassign={"t_max_inst": [2, 9, 9], "u_hi_pct": 80, "u_lo_pct": 30})
+    assert o["ra_kill"].tolist() == []
+    # balanced thresholds -> no commands (SPEC S:454 "balanced utilization")
+    o = oracle_epoch(s, "fcfs", reassign={"u_hi_pct": 200, "u_lo_pct": 0})
+    assert o["ra_kill"].tolist() == []
+
+
+def _reassign_fraction_route(s, o, mn, mx, hi, lo):
+    """O10 by another route: exact Fractions and Python sorting."""
+    from fractions import Fraction
+    T, I = s.n_types, s.n_instances
+    busy = [0] * T
+    cap = [0] * T
+    cnt = [0] * T
+    for i in range(I):
+        t = int(s.i_type[i])
+        busy[t] += int(o["i_load"][i]) + int(o["i_assigned"][i])
+        cap[t] += int(s.i_cap[i])
+        cnt[t] += 1
+    for f in np.nonzero(o["status"] == S_DEF)[0]:
+        busy[int(s.f_type[f])] += 1
+    inf = Fraction(10 ** 30)
+    util = [(Fraction(busy[t], cap[t]) if cap[t] else (inf if busy[t] else Fraction(0))) for t in range(T)]
+    hot = [t for t in range(T) if cnt[t] < mx[t] and util[t] > Fraction(hi, 100)]
+    cold = [t for t in range(T) if t not in hot and cnt[t] > mn[t] and util[t] < Fraction(lo, 100)]
+    hot.sort(key=lambda t: (-util[t], t))
+    cold.sort(key=lambda t: (util[t], t))
+    kill, prov = [], []
+    for a, b in zip(hot, cold):
+        cands = [i for i in range(I) if s.i_type[i] == b]
+        kill.append(min(cands, key=lambda i: (int(o["i_load"][i]) + int(o["i_assigned"][i]), -i)))
+        prov.append(a)
+    return busy, cap, kill, prov
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_reassign_fraction_route(seed):
+    rng = np.random.default_rng(seed)
+    s = random_table(seed, n_workflows=2 + seed % 5, max_rows=4 + seed % 20, n_types=1 + seed % 5,
+                     inst_per_type=(0, 1 + seed % 4), consistent=seed % 2 == 1, max_cap=1 + seed % 7,
+                     max_base=seed % 9)
+    T = s.n_types
+    mn = rng.integers(0, 3, T).tolist()
+    mx = rng.integers(1, 6, T).tolist()
+    hi, lo = int(rng.integers(30, 120)), int(rng.integers(0, 50))
+    lo = min(lo, hi)
+    o = oracle_epoch(s, "srtf", reassign={"t_min_inst": mn, "t_max_inst": mx, "u_hi_pct": hi,
+                                          "u_lo_pct": lo})
+    busy, cap, kill, prov = _reassign_fraction_route(s, o, mn, mx, hi, lo)
+    assert o["t_busy"].tolist() == busy and o["t_cap"].tolist() == cap
+    assert o["ra_kill"].tolist() == kill and o["ra_prov"].tolist() == prov
+
+
+def test_reassign_c4_shifts_toward_hot_types():
+    """with skewed demand the commands move instances toward the hot type."""
+    s = c4()
+    o = oracle_epoch(s, "srtf", reassign={"u_hi_pct": 80, "u_lo_pct": 30})
+    busy, cap, kill, prov = _reassign_fraction_route(s, o, [0] * 8, [0xFFFF] * 8, 80, 30)
+    assert o["ra_kill"].tolist() == kill and o["ra_prov"].tolist() == prov and len(kill) >= 1
+    for k, p in zip(kill, prov):
+        assert busy[p] * cap[s.i_type[k]] > busy[s.i_type[k]] * cap[p]    # from colder to hotter
