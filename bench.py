@@ -304,6 +304,18 @@ def main():
     total_fut = table.n_futures
     value = total_fut / (mean_ms / 1e3)
 
+    # NEXT rows in the same timed configuration: resource
+    # reassignment (NEXT-2) switched on; K,V hints (NEXT-3) are always computed
+    ctx.set_policy_params(reassign=True, u_hi_pct=80, u_lo_pct=30)
+    timed_epochs(args.warmup, True)
+    ms_ra = timed_epochs(max(args.steps // 4, 10), True)
+    ra_out = ctx.fetch(("reassign", "kv"))
+    ctx.set_policy_params(reassign=False)
+    next_rows = {"reassign_on_epoch_us": float(np.mean(ms_ra)) * 1e3,
+                 "reassign_commands": int(ra_out["n_reassign"]),
+                 "kv_hints": {k: int(v) for k, v in zip(("none", "retain", "offload", "drop"),
+                                                       np.bincount(ra_out["kv_hint"].ravel(), minlength=4))}}
+
     # per-kernel device times (CUDA events captured inside the epoch graph)
     tctx = new_ctx(flags=nalar.NALAR_F_TIMING)
     tctx.upload(s)
@@ -387,6 +399,7 @@ def main():
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             # per epoch: k_zero (exchange buffer + counters), k1_sweep, k4_assign
             "gpu_launches": 3 * args.steps,
+            "next_rows": next_rows,
             "clocks": clk.summary(),
             "paper_context": "464 ms per global-control-loop at 131K futures, Python+gRPC+Redis on "
                              "64 emulated CPU nodes (PAPER.md:715); context, not the target"}

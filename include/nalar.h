@@ -218,7 +218,41 @@ typedef struct {
     uint8_t*  kv_level;   /* [W][T] max level of the session's live futures    */
     int16_t*  kv_home;    /* [W][T] home instance or -1                        */
     uint32_t  kv_cap;     /* elements (>= W * T)                               */
+    /* Resource reassignment (only with
+     * nalar_policy_params.reassign): per type t, busy_t = sum over t's
+     * instances of (load + assigned this epoch) + t's deferred futures, and
+     * cap_t = sum of capacities; and the commands, pair k = Kill(ra_kill[k])
+     * + Provision(type ra_prov[k]), hottest type with the
+     * coldest.  Identical on every rank.                                     */
+    uint32_t* t_busy;     /* [T]                                               */
+    uint32_t* t_capsum;   /* [T]                                               */
+    int16_t*  ra_kill;    /* [T] (n_reassign used)                             */
+    int16_t*  ra_prov;    /* [T]                                               */
+    uint32_t  t_cap;      /* elements of the four arrays above (>= T)          */
+    uint32_t  n_reassign; /* out                                               */
 } nalar_decisions;
+
+/* Policy parameters beyond the per-epoch policy (persist on the context;
+ * take effect from the next epoch). */
+typedef struct {
+    /* resource reassignment (NEXT-2; "resource reassignment from
+     * low-load agents to high-load agents"): type A with
+     * 100 busy_A > u_hi_pct cap_A and fewer than max_instances[A] instances is
+     * hot, type B with 100 busy_B < u_lo_pct cap_B and more than
+     * min_instances[B] is cold (max/min_instances: the Table 1 directives,
+     * PAPER.md:252-253).  Hot types by utilisation desc are paired with cold
+     * ones by utilisation asc (ties: lower type id); the killed instance is
+     * the cold type's least-loaded (load + assigned; ties: highest id). */
+    uint32_t reassign;             /* 0 off, 1 on                                  */
+    uint32_t u_hi_pct, u_lo_pct;   /* percent, u_lo_pct <= u_hi_pct (SPEC: 80 / 30) */
+    const uint16_t* t_min_inst;    /* [n_types] or NULL (all 0)                    */
+    const uint16_t* t_max_inst;    /* [n_types] or NULL (all 65535)                */
+    uint32_t n_types;              /* <= max_types                                 */
+} nalar_policy_params;
+
+/* Copies p (host arrays borrowed for the call).  E_INVAL on u_lo > u_hi or
+ * n_types > max_types. */
+int nalar_set_policy_params(nalar_ctx* ctx, const nalar_policy_params* p);
 
 /* TickReport analog. */
 typedef struct {

@@ -21,7 +21,16 @@ constexpr int kK4Warps = kK4Threads / 32;
 enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8 };
 
 // indices into the per-epoch counters array (scratch)
-enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_NUM = 8 };
+enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_RA_TICKET = 4, C_RA_PAIRS = 5, C_NUM = 8 };
+
+// per-type statistics of resource reassignment (NEXT-2), written by K4's type
+// blocks; the last K4 block pairs hot with cold types
+struct TypeStat {
+    unsigned long long busy;    // sum(load) + eligible futures of the type (= load + assigned + deferred)
+    unsigned long long cap;     // sum of capacities
+    uint32_t n_inst;
+    int32_t kill;               // least (load + assigned) instance, ties the highest id; -1 none
+};
 
 // bytes of K1 shared memory that do not scale with the block's rows
 size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
@@ -113,6 +122,15 @@ struct AssignParams {
     uint32_t* n_adm;            // [R] this rank's admitted futures per resource
     uint32_t* counters;
     unsigned long long* prof;   // NALAR_F_PROFILE: [R][4] start, bounded, based, done
+    // resource reassignment (NEXT-2), active when ra_on
+    uint32_t ra_on, u_hi_pct, u_lo_pct;
+    const uint16_t* t_min_inst; // [T]
+    const uint16_t* t_max_inst; // [T]
+    TypeStat* tstat;            // [T] scratch
+    uint32_t* t_busy;           // [T] out (saturated u32)
+    uint32_t* t_capsum;         // [T] out
+    int16_t* ra_kill;           // [T] out: pair k's instance to kill
+    int16_t* ra_prov;           // [T] out: pair k's type to provision
 };
 
 struct RebuildPlan {             // one workflow of the table after a delta

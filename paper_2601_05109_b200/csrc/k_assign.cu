@@ -76,6 +76,142 @@ __device__ __forceinline__ uint32_t slot_instance(const uint32_t* sp2, const uin
     return 0xFFFFFFFFu;
 }
 
+// ---- resource reassignment (DESIGN.md Q-ra) -----------
+// Type block t: busy_t = sum(load) + eligible futures of t (= load + assigned +
+// deferred: every eligible future is assigned or deferred), cap_t, and the kill
+// candidate (least load + assigned, ties the highest id).  Global inputs only
+// (allreduced loads / totals), so every rank computes the same commands.
+__device__ void reassign_stats(const AssignParams& p, bool is_type, uint32_t t, uint32_t ni, uint32_t ha_unp,
+                               unsigned long long busy, unsigned long long cap, uint64_t best,
+                               unsigned long long* s_rb, unsigned long long* s_rc, uint64_t* s_rbest) {
+    // per-thread partials (busy = load + eligible, cap, the kill key) come from
+    // the instance loops this block already ran -- no loads here
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        busy += __shfl_xor_sync(0xFFFFFFFFu, busy, o);
+        cap += __shfl_xor_sync(0xFFFFFFFFu, cap, o);
+        const uint64_t b2 = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+        best = b2 < best ? b2 : best;
+    }
+    if (lane == 0) { s_rb[warp] = busy; s_rc[warp] = cap; s_rbest[warp] = best; }
+    __syncthreads();
+    if (!is_type || tid != 0) return;
+    unsigned long long B = ha_unp, Cc = 0;          // + unpinned eligible futures of t
+    uint64_t bk = ~0ull;
+    for (int w = 0; w < kK4Warps; ++w) {
+        B += s_rb[w];
+        Cc += s_rc[w];
+        bk = s_rbest[w] < bk ? s_rbest[w] : bk;
+    }
+    TypeStat ts;
+    ts.busy = B;
+    ts.cap = Cc;
+    ts.n_inst = ni;
+    ts.kill = bk == ~0ull ? -1 : (int32_t)(0xFFFFu - (uint32_t)(bk & 0xFFFFull));
+    p.tstat[t] = ts;
+    p.t_busy[t] = B > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)B;
+    p.t_capsum[t] = Cc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)Cc;
+}
+
+// another block's TypeStat, read past L1 (written before its ticket)
+__device__ __forceinline__ TypeStat load_ts(const TypeStat* a, uint32_t t) {
+    TypeStat x;
+    x.busy = __ldcg(&a[t].busy);
+    x.cap = __ldcg(&a[t].cap);
+    x.n_inst = __ldcg(&a[t].n_inst);
+    x.kill = __ldcg(&a[t].kill);
+    return x;
+}
+
+// util(a) > util(b) as exact fractions (cap 0 with busy > 0 is infinite)
+__device__ __forceinline__ bool util_gt(const TypeStat& a, const TypeStat& b) {
+    const bool ia = a.cap == 0 && a.busy > 0, ib = b.cap == 0 && b.busy > 0;
+    if (ia || ib) return ia && !ib;
+    if (a.cap == 0) return false;
+    if (b.cap == 0) return a.busy > 0;
+    const unsigned long long xh = __umul64hi(a.busy, b.cap), xl = a.busy * b.cap;
+    const unsigned long long yh = __umul64hi(b.busy, a.cap), yl = b.busy * a.cap;
+    return xh > yh || (xh == yh && xl > yl);
+}
+
+// the last K4 block (ticket) pairs the k-th hottest with the k-th coldest type
+__device__ __forceinline__ uint64_t gtimer2() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ void reassign_finish(const AssignParams& p, uint32_t* s_last, TypeStat* s_ts, const uint16_t* s_tmin,
+                                const uint16_t* s_tmax) {
+    unsigned long long* prof = p.prof ? p.prof + (size_t)blockIdx.x * 8 : nullptr;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // acq_rel ticket: releases this block's TypeStat (written by this same
+        // thread) and, for the last block, acquires every other block's -- a
+        // full fence.sc would stall each block for microseconds
+        uint32_t old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&p.counters[C_RA_TICKET])
+                     : "memory");
+        *s_last = old == p.R - 1u;
+    }
+    __syncthreads();
+    if (prof && threadIdx.x == 0) prof[7] = gtimer2();
+    if (!*s_last) return;
+    const uint32_t T = p.n_types < 64u ? p.n_types : 64u;
+    // every input of the pairing staged in parallel (a serial thread-0 walk over
+    // global memory would pay one L2 round trip per type)
+    __shared__ uint8_t s_cls[64];         // 1 hot, 2 cold
+    __shared__ uint8_t s_hot[64], s_cold[64];
+    __shared__ uint32_t s_nh, s_nc;
+    if (threadIdx.x == 0) { s_nh = 0; s_nc = 0; }
+    for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const TypeStat tt = load_ts(p.tstat, t);
+        s_ts[t] = tt;
+        const uint32_t mn = s_tmin[t], mx = s_tmax[t];
+        uint8_t cl = 0;
+        if (tt.n_inst < mx && 100ull * tt.busy > (unsigned long long)p.u_hi_pct * tt.cap) cl = 1;
+        else if (tt.n_inst > mn && 100ull * tt.busy < (unsigned long long)p.u_lo_pct * tt.cap) cl = 2;
+        s_cls[t] = cl;
+    }
+    __syncthreads();
+    // rank every hot type by utilisation desc and every cold one by
+    // utilisation asc (ties: lower id): all T x T exact comparisons in
+    // parallel into bitmasks, then one popcount per type
+    __shared__ uint32_t s_gt[64][2], s_eq[64][2];   // bit u of row t: util(u) > util(t) / ==
+    for (uint32_t k = threadIdx.x; k < 2 * T; k += blockDim.x) { s_gt[k >> 1][k & 1] = 0; s_eq[k >> 1][k & 1] = 0; }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < T * T; k += blockDim.x) {
+        const uint32_t t = k / T, u = k - t * T;
+        if (s_cls[t] == 0 || s_cls[u] != s_cls[t] || u == t) continue;
+        if (util_gt(s_ts[u], s_ts[t])) atomicOr(&s_gt[t][u >> 5], 1u << (u & 31u));
+        else if (!util_gt(s_ts[t], s_ts[u])) atomicOr(&s_eq[t][u >> 5], 1u << (u & 31u));
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint8_t cl = s_cls[t];
+        if (!cl) continue;
+        const unsigned long long gt = s_gt[t][0] | ((unsigned long long)s_gt[t][1] << 32);
+        const unsigned long long eq = s_eq[t][0] | ((unsigned long long)s_eq[t][1] << 32);
+        unsigned long long same = 0;     // the other types of t's class
+        for (uint32_t u = 0; u < T; ++u) same |= (s_cls[u] == cl && u != t) ? 1ull << u : 0ull;
+        const unsigned long long lower = t ? (~0ull >> (64 - t)) : 0ull;
+        const unsigned long long lt = same & ~gt & ~eq;
+        const uint32_t rank = cl == 1 ? __popcll(gt) + __popcll(eq & lower)      // hot: util desc
+                                      : __popcll(lt) + __popcll(eq & lower);     // cold: util asc
+        if (cl == 1) { s_hot[rank] = (uint8_t)t; atomicAdd(&s_nh, 1u); }
+        else { s_cold[rank] = (uint8_t)t; atomicAdd(&s_nc, 1u); }
+    }
+    __syncthreads();
+    const uint32_t np = s_nh < s_nc ? s_nh : s_nc;
+    for (uint32_t k = threadIdx.x; k < np; k += blockDim.x) {
+        p.ra_kill[k] = (int16_t)s_ts[s_cold[k]].kill;
+        p.ra_prov[k] = (int16_t)s_hot[k];
+    }
+    if (threadIdx.x != 0) return;
+    p.counters[C_RA_PAIRS] = np;
+    if (prof) prof[7] = gtimer2() | (1ull << 63);
+}
+
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -102,6 +238,13 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     __shared__ uint2 s_live[4 * kK4Threads];
     __shared__ uint16_t s_slot[kSlotCap];
     __shared__ uint64_t s_bound;
+    __shared__ unsigned long long s_rb[kK4Warps], s_rc[kK4Warps];
+    __shared__ uint64_t s_rbest[kK4Warps];
+    __shared__ uint32_t s_last;
+    __shared__ TypeStat s_ts[64];
+    __shared__ uint16_t s_tmin[64], s_tmax[64];
+    unsigned long long ra_busy = 0, ra_cap = 0;      // NEXT-2 partials of this thread's instances
+    uint64_t ra_best = ~0ull;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
@@ -126,6 +269,10 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     const uint32_t cap_r = is_type ? 0u : p.i_cap[r], base_r = is_type ? 0u : p.i_base[r];
     const uint8_t aff = is_type ? p.t_aff[t] : 0;
     const uint32_t blk0 = tid < B ? p.blk_row0[tid] : 0u;
+    if (p.ra_on && tid < 64u && tid < p.n_types) {       // NEXT-2 directives (static)
+        s_tmin[tid] = p.t_min_inst ? p.t_min_inst[tid] : 0u;
+        s_tmax[tid] = p.t_max_inst ? p.t_max_inst[tid] : 0xFFFFu;
+    }
     // everything below reads the sweep's results
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (prof && tid == 0) prof[4] = gtimer();
@@ -147,6 +294,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     const uint32_t cnt0 = tid < B ? p.cnt_rb[(size_t)r * B + tid] : 0u;   // first 256 K1 blocks
     const uint32_t off0 = tid < B ? p.off_rb[(size_t)r * B + tid] : 0u;
     uint32_t ls0 = 0, ha0 = 0;
+    const uint32_t ha_unp = (is_type && p.ra_on && tid == 0) ? p.tot[r] : 0u;   // unpinned eligible of t
     if (is_type) {
         if (tid < ni) { ls0 = p.load_sum[s_inst[tid]]; ha0 = p.tot[s_inst[tid]]; }
     } else if (tid == 0) {
@@ -164,6 +312,8 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
             s_spare[k] = spare;
             s_sp2[k] = spare - (ha < spare ? ha : spare);
             p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
+            ra_busy += load + ha;
+            ra_cap += cap;
             p.i_spare[i] = spare;
         }
     } else if (tid == 0) {
@@ -263,6 +413,11 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
                 }
             }
             p.i_assigned[s_inst[k]] = (uint32_t)asg;
+            {   // NEXT-2 kill key: least load + assigned, ties the highest id
+                const uint64_t la = asg + p.i_load[s_inst[k]];
+                const uint64_t key = ((la > 0xFFFFFFFFull ? 0xFFFFFFFFull : la) << 32) | (0xFFFFu - s_inst[k]);
+                ra_best = key < ra_best ? key : ra_best;
+            }
         }
         if (table && n_adm && ni <= 16u) {
             // slots in (level desc, instance asc) order, all at once: slot
@@ -294,8 +449,10 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
         }
     }
     if (prof && tid == 0) prof[2] = gtimer();
+    if (p.ra_on) reassign_stats(p, is_type, t, ni, ha_unp, ra_busy, ra_cap, ra_best, s_rb, s_rc, s_rbest);
     if (n_adm == 0) {
         if (prof && tid == 0) prof[3] = gtimer();
+        if (p.ra_on) reassign_finish(p, &s_last, s_ts, s_tmin, s_tmax);
         return;
     }
     __syncthreads();
@@ -417,6 +574,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
         }
     }
     if (prof && tid == 0) prof[3] = gtimer();
+    if (p.ra_on) reassign_finish(p, &s_last, s_ts, s_tmin, s_tmax);
 }
 
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {

@@ -62,12 +62,12 @@ constexpr uint32_t kMaxBlocks = 16384;
 constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tables
 
 struct Key {
-    uint32_t N, E, W, I, T, B, R, policy;
+    uint32_t N, E, W, I, T, B, R, policy, params_gen;
     size_t smem;
     const void* table;   // current buffer set (deltas swap sets)
     bool operator==(const Key& o) const {
         return N == o.N && E == o.E && W == o.W && I == o.I && T == o.T && B == o.B && R == o.R &&
-               policy == o.policy && smem == o.smem && table == o.table;
+               policy == o.policy && params_gen == o.params_gen && smem == o.smem && table == o.table;
     }
 };
 
@@ -97,6 +97,12 @@ struct nalar_ctx {
     uint16_t* d_gaux = nullptr;
     uint16_t* d_depth = nullptr;
     int16_t *d_inst = nullptr, *d_ainst = nullptr;
+    // resource reassignment (NEXT-2)
+    uint16_t *d_tmin = nullptr, *d_tmax = nullptr;
+    TypeStat* d_tstat = nullptr;
+    uint32_t *d_tbusy = nullptr, *d_tcap = nullptr;
+    int16_t *d_rakill = nullptr, *d_raprov = nullptr;
+    uint32_t ra_on = 0, u_hi = 80, u_lo = 30, params_gen = 0;
     uint8_t *d_kvh = nullptr, *d_kvl = nullptr;
     int16_t* d_kvhome = nullptr;
     uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
@@ -185,7 +191,7 @@ struct Plan {
     size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, wf_perm, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
-    size_t kvh, kvl, kvhome;
+    size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
     uint32_t Rmax, Bmax;
@@ -237,6 +243,13 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->kvh = L.take<uint8_t>(W * T);
     p->kvl = L.take<uint8_t>(W * T);
     p->kvhome = L.take<int16_t>(W * T);
+    p->tmin = L.take<uint16_t>(T);
+    p->tmax = L.take<uint16_t>(T);
+    p->tstat = L.take<TypeStat>(T);
+    p->tbusy = L.take<uint32_t>(T);
+    p->tcap = L.take<uint32_t>(T);
+    p->rakill = L.take<int16_t>(T);
+    p->raprov = L.take<int16_t>(T);
     p->iload = L.take<uint32_t>(I);
     p->ispare = L.take<uint32_t>(I);
     p->iasg = L.take<uint32_t>(I);
@@ -391,6 +404,9 @@ int run_k4(nalar_ctx* c) {
     p.tot_loc = c->d_scr + C_NUM + c->Rmax;
     p.prof = c->d_prof ? c->d_prof + 2ull * c->W + 8ull * c->B : nullptr;
     p.counters = c->d_scr;
+    p.ra_on = c->ra_on; p.u_hi_pct = c->u_hi; p.u_lo_pct = c->u_lo;
+    p.t_min_inst = c->d_tmin; p.t_max_inst = c->d_tmax; p.tstat = c->d_tstat;
+    p.t_busy = c->d_tbusy; p.t_capsum = c->d_tcap; p.ra_kill = c->d_rakill; p.ra_prov = c->d_raprov;
     CK(launch_assign(p, c->stream));
     return NALAR_OK;
 }
@@ -594,6 +610,9 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_depth = at<uint16_t>(a, p.depth); c->d_inst = at<int16_t>(a, p.inst); c->d_ainst = at<int16_t>(a, p.ainst);
     c->d_wfagg = at<uint32_t>(a, p.wfagg); c->d_iload = at<uint32_t>(a, p.iload);
     c->d_kvh = at<uint8_t>(a, p.kvh); c->d_kvl = at<uint8_t>(a, p.kvl); c->d_kvhome = at<int16_t>(a, p.kvhome);
+    c->d_tmin = at<uint16_t>(a, p.tmin); c->d_tmax = at<uint16_t>(a, p.tmax); c->d_tstat = at<TypeStat>(a, p.tstat);
+    c->d_tbusy = at<uint32_t>(a, p.tbusy); c->d_tcap = at<uint32_t>(a, p.tcap);
+    c->d_rakill = at<int16_t>(a, p.rakill); c->d_raprov = at<int16_t>(a, p.raprov);
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
     c->d_items = at<uint2>(a, p.items); c->d_cnt_rb = at<uint32_t>(a, p.cnt_rb); c->d_off_rb = at<uint32_t>(a, p.off_rb);
     c->d_x = at<uint32_t>(a, p.x); c->d_scr = at<uint32_t>(a, p.scr);
@@ -954,7 +973,7 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
     if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
         return fail(c, NALAR_E_STATE, "external collective: use nalar_epoch_begin/finish");
     int rc;
-    Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->smem, c->d_state};
+    Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->params_gen, c->smem, c->d_state};
     // a graph pays off only for a shape that repeats (not after every delta)
     const bool repeat = c->last_key_set && c->last_key == key;
     const bool cached = c->gexec[policy] && c->gkey[policy] == key;
@@ -1018,7 +1037,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     // the way, and one synchronisation.
     {
         struct Out { void* h; const void* d; size_t bytes; };
-        const Out outs[12] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
+        const Out outs[16] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
                              {o->depth, c->d_depth, 2ull * c->N}, {o->instance, c->d_inst, 2ull * c->N},
                              {o->new_pin, c->d_newpin, c->N},
                              {o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W},
@@ -1026,12 +1045,15 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
                              {o->i_assigned, c->d_iasg, 4ull * c->I},
                              {o->kv_hint, c->d_kvh, (size_t)c->W * c->T},
                              {o->kv_level, c->d_kvl, (size_t)c->W * c->T},
-                             {o->kv_home, c->d_kvhome, 2ull * c->W * c->T}};
+                             {o->kv_home, c->d_kvhome, 2ull * c->W * c->T},
+                             {o->t_busy, c->d_tbusy, 4ull * c->T}, {o->t_capsum, c->d_tcap, 4ull * c->T},
+                             {o->ra_kill, c->d_rakill, 2ull * c->T}, {o->ra_prov, c->d_raprov, 2ull * c->T}};
         const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
         const bool wbad = o->wf_agg && o->wf_cap < c->W;
         const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
         const bool kbad = (o->kv_hint || o->kv_level || o->kv_home) && o->kv_cap < (size_t)c->W * c->T;
-        bool mapped = !(fbad || wbad || ibad || kbad);
+        const bool tbad = (o->t_busy || o->t_capsum || o->ra_kill || o->ra_prov) && o->t_cap < c->T;
+        bool mapped = !(fbad || wbad || ibad || kbad || tbad);
         CopyBatch cb(st);
         for (const Out& q : outs) {
             if (!mapped || !q.h || !q.bytes) continue;
@@ -1059,6 +1081,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
             CK(cudaStreamSynchronize(st));
             const uint32_t na = c->h_cnt[C_ASSIGNED];
             o->n_f = c->N; o->n_w = c->W; o->n_i = c->I; o->n_assigned = na;
+            o->n_reassign = c->ra_on ? c->h_cnt[C_RA_PAIRS] : 0u;
             if ((o->assign_row || o->assign_inst) && o->a_cap < na)
                 return fail(c, NALAR_E_SIZE, "output buffer too small");
             return NALAR_OK;
@@ -1073,7 +1096,9 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
     const bool abad = (o->assign_row || o->assign_inst) && o->a_cap < na;
     const bool kbad = (o->kv_hint || o->kv_level || o->kv_home) && o->kv_cap < (size_t)c->W * c->T;
-    if (fbad || wbad || ibad || abad || kbad) return fail(c, NALAR_E_SIZE, "output buffer too small");
+    const bool tbad = (o->t_busy || o->t_capsum || o->ra_kill || o->ra_prov) && o->t_cap < c->T;
+    if (fbad || wbad || ibad || abad || kbad || tbad) return fail(c, NALAR_E_SIZE, "output buffer too small");
+    o->n_reassign = c->ra_on ? c->h_cnt[C_RA_PAIRS] : 0u;
     auto d2h = [&](void* h, const void* d, size_t bytes) -> cudaError_t {
         return (h && bytes) ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
     };
@@ -1086,6 +1111,10 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     CK(d2h(o->kv_hint, c->d_kvh, (size_t)c->W * c->T));
     CK(d2h(o->kv_level, c->d_kvl, (size_t)c->W * c->T));
     CK(d2h(o->kv_home, c->d_kvhome, 2ull * c->W * c->T));
+    CK(d2h(o->t_busy, c->d_tbusy, 4ull * c->T));
+    CK(d2h(o->t_capsum, c->d_tcap, 4ull * c->T));
+    CK(d2h(o->ra_kill, c->d_rakill, 2ull * c->T));
+    CK(d2h(o->ra_prov, c->d_raprov, 2ull * c->T));
     CK(d2h(o->i_load, c->d_iload, 4ull * c->I));
     CK(d2h(o->i_spare, c->d_ispare, 4ull * c->I));
     CK(d2h(o->i_assigned, c->d_iasg, 4ull * c->I));
@@ -1122,6 +1151,25 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
             at += tot_loc[r];
         }
     }
+    return NALAR_OK;
+}
+
+int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
+    if (!c || !p) return NALAR_E_INVAL;
+    if (p->u_lo_pct > p->u_hi_pct) return fail(c, NALAR_E_INVAL, "u_lo_pct > u_hi_pct");
+    if (p->n_types > c->cfg.max_types) return fail(c, NALAR_E_INVAL, "n_types > max_types");
+    std::vector<uint16_t> mn(c->cfg.max_types, 0), mx(c->cfg.max_types, 0xFFFF);
+    for (uint32_t t = 0; t < p->n_types; ++t) {
+        if (p->t_min_inst) mn[t] = p->t_min_inst[t];
+        if (p->t_max_inst) mx[t] = p->t_max_inst[t];
+    }
+    CK(cudaMemcpyAsync(c->d_tmin, mn.data(), 2ull * mn.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_tmax, mx.data(), 2ull * mx.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->ra_on = p->reassign ? 1u : 0u;
+    c->u_hi = p->u_hi_pct;
+    c->u_lo = p->u_lo_pct;
+    c->params_gen++;                      // epoch graphs bake the parameters in
     return NALAR_OK;
 }
 

@@ -30,7 +30,7 @@ EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
            "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile",
-           "nalar_delta_apply")
+           "nalar_delta_apply", "nalar_set_policy_params")
 NALAR_DELTA_APPLY_ASSIGNED = 1
 
 
@@ -64,7 +64,14 @@ class nalar_decisions(C.Structure):
                 ("n_f", C.c_uint32), ("n_w", C.c_uint32), ("n_i", C.c_uint32),
                 ("n_assigned", C.c_uint32),
                 ("kv_hint", C.c_void_p), ("kv_level", C.c_void_p), ("kv_home", C.c_void_p),
-                ("kv_cap", C.c_uint32)]
+                ("kv_cap", C.c_uint32),
+                ("t_busy", C.c_void_p), ("t_capsum", C.c_void_p), ("ra_kill", C.c_void_p),
+                ("ra_prov", C.c_void_p), ("t_cap", C.c_uint32), ("n_reassign", C.c_uint32)]
+
+
+class nalar_policy_params(C.Structure):
+    _fields_ = [("reassign", C.c_uint32), ("u_hi_pct", C.c_uint32), ("u_lo_pct", C.c_uint32),
+                ("t_min_inst", C.c_void_p), ("t_max_inst", C.c_void_p), ("n_types", C.c_uint32)]
 
 
 class nalar_delta(C.Structure):
@@ -111,6 +118,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_debug_profile.restype = C.c_int
     lib.nalar_delta_apply.argtypes = [C.c_void_p, P(nalar_delta), P(C.c_int64)]
     lib.nalar_delta_apply.restype = C.c_int
+    lib.nalar_set_policy_params.argtypes = [C.c_void_p, P(nalar_policy_params)]
+    lib.nalar_set_policy_params.restype = C.c_int
     lib.nalar_stream.argtypes = [C.c_void_p]
     lib.nalar_stream.restype = C.c_void_p
     lib.nalar_last_error.argtypes = [C.c_void_p]
@@ -354,8 +363,21 @@ class Context:
     def stats(self) -> nalar_epoch_stats:
         return nalar_epoch_stats_get(self.h)
 
+    def set_policy_params(self, reassign=True, u_hi_pct=80, u_lo_pct=30, t_min_inst=None,
+                          t_max_inst=None, n_types=None) -> None:
+        """Resource-reassignment parameters (NEXT-2); SPEC defaults u_hi 80 %, u_lo 30 %."""
+        mn = None if t_min_inst is None else np.ascontiguousarray(t_min_inst, np.uint16)
+        mx = None if t_max_inst is None else np.ascontiguousarray(t_max_inst, np.uint16)
+        nt = n_types if n_types is not None else (len(mn) if mn is not None else
+                                                  (len(mx) if mx is not None else 0))
+        p = nalar_policy_params(int(bool(reassign)), int(u_hi_pct), int(u_lo_pct),
+                                _ptr(mn) if mn is not None else None,
+                                _ptr(mx) if mx is not None else None, int(nt))
+        _check(self.h, _lib.nalar_set_policy_params(self.h, C.byref(p)), "set_policy_params")
+
     def output_buffers(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg",
-                                     "i_load", "i_spare", "i_assigned", "assign", "kv"), alloc=None):
+                                     "i_load", "i_spare", "i_assigned", "assign", "kv", "reassign"),
+                       alloc=None):
         """Host buffers for fetch(); ``alloc(n, dtype)`` may return pinned memory."""
         N, W, I = self.n
         alloc = alloc or (lambda n, dt: np.zeros(n, dt))
@@ -369,20 +391,29 @@ class Context:
             out["kv_hint"] = alloc(W * T, np.uint8)
             out["kv_level"] = alloc(W * T, np.uint8)
             out["kv_home"] = alloc(W * T, np.int16)
+        if "reassign" in fields:
+            T = max(self.n_types, 1)
+            out["t_busy"] = alloc(T, np.uint32)
+            out["t_capsum"] = alloc(T, np.uint32)
+            out["ra_kill"] = alloc(T, np.int16)
+            out["ra_prov"] = alloc(T, np.int16)
         if "assign" in fields:
             out["assign_row"] = alloc(max(N, 1), np.uint32)
             out["assign_inst"] = alloc(max(N, 1), np.int16)
         return out
 
     def fetch(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
-                            "i_spare", "i_assigned", "assign", "kv"), out=None) -> dict:
+                            "i_spare", "i_assigned", "assign", "kv", "reassign"), out=None) -> dict:
         N, W, I = self.n
         bufs = out if out is not None else self.output_buffers(fields)
         d = nalar_decisions()
         for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
-                  "i_spare", "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home"):
+                  "i_spare", "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home",
+                  "t_busy", "t_capsum", "ra_kill", "ra_prov"):
             if k in bufs:
                 setattr(d, k, _ptr(bufs[k]))
+        if "t_busy" in bufs:
+            d.t_cap = min(len(bufs[k]) for k in ("t_busy", "t_capsum", "ra_kill", "ra_prov") if k in bufs)
         if "kv_hint" in bufs:
             d.kv_cap = min(len(bufs["kv_hint"]), len(bufs.get("kv_level", bufs["kv_hint"])),
                            len(bufs.get("kv_home", bufs["kv_hint"])))
@@ -396,6 +427,13 @@ class Context:
         for k in ("kv_hint", "kv_level", "kv_home"):
             if k in res:
                 res[k] = res[k][:W * self.n_types].reshape(W, self.n_types)
+        for k in ("t_busy", "t_capsum"):
+            if k in res:
+                res[k] = res[k][:self.n_types]
+        for k in ("ra_kill", "ra_prov"):
+            if k in res:
+                res[k] = res[k][:d.n_reassign]
+        res["n_reassign"] = d.n_reassign
         if "assign_row" in res:
             res["assign_row"] = res["assign_row"][:d.n_assigned]
             res["assign_inst"] = res["assign_inst"][:d.n_assigned]

@@ -20,9 +20,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1 << 17)
 ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--out", default="gpurun_out/k1_timeline.json")
+ap.add_argument("--reassign", action="store_true")
 a = ap.parse_args()
 s = swe_table(a.n, seed=a.seed)
 ctx = nalar.Context.for_snapshot(s, flags=nalar.NALAR_F_PROFILE | nalar.NALAR_F_NO_GRAPH)
+if a.reassign:
+    ctx.set_policy_params(reassign=True, u_hi_pct=80, u_lo_pct=30)
 ctx.upload(s)
 for _ in range(5):
     ctx.epoch("srtf")
@@ -93,6 +96,12 @@ res["transfer_steps"] = {"n": int(tx[:, 5].sum()),
                          "settle_iters_mean": float(tx[:, 4].sum() / nt), "K_mean": float(tx[:, 6].sum() / nt),
                          "k_mean": float(tx[:, 7].sum() / nt)}
 k1_end = blk[:, 2].max()
+last = np.nonzero(k4[:, 7] < 0)[0]
+if len(last):
+    res["k4"]["ra_last_block"] = int(last[0])
+    res["k4"]["ra_pairing_end_ns"] = int((k4[last[0], 7] & ((1 << 62) - 1)) - k1_end)
+    tick = np.where(k4[:, 7] > 0, k4[:, 7], 0)
+    res["k4"]["ra_ticket_last_ns"] = int(tick.max() - k1_end) if tick.max() > 0 else None
 res["k4"]["wait_release_after_k1_end_ns"] = int(k4[:, 4].min() - k1_end)
 slow = np.argsort(-(k4[:, 3] - k1_end))[:6]
 res["k4"]["slowest_ctas"] = [{"r": int(r), **{n: (int(k4[r, j] - k1_end) if k4[r, j] > 0 else None) for n, j in
