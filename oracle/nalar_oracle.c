@@ -412,3 +412,85 @@ int oracle_reassign(const oracle_table* t, const oracle_out* o, const oracle_ra_
     free(busy); free(cap); free(cnt); free(hot); free(cold);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O11 head-of-line-blocking migration (DESIGN.md Q-mig). */
+/* "migrates a job if it's waiting in the queue and observing head-of-line   */
+/* blocking" P:663 [§6.1]; the migrate primitive P:391 and its protocol      */
+/* (Fig 5); SPEC hol_migration S:441: for each Queued future whose */
+/* wait age > theta_wait and whose instance's head job has predicted          */
+/* remaining time > theta_head, Migrate to the instance with the smallest     */
+/* (queue_len + running), provided its backlog is below the source's by      */
+/* margin delta; managed-state agents move whole sessions.    */
+/*   blocked(i) = head_rem[i] > theta_head; sources are blocked instances,    */
+/*   destinations unblocked ones of the same type (no capacity test: a moved  */
+/*   future queues there, SPEC compares backlogs only; the margin guards);    */
+/*   backlog = load + assigned this epoch (O5-O7).                            */
+/*   A QUEUED future f at a blocked executor s with age > theta_wait is a     */
+/*   candidate unless its type is STATEFUL (in-order per session:     */
+/*   never moves); a SESSION future only if it is its session's only QUEUED   */
+/*   future and the session has nothing RUNNING (moving it moves the whole    */
+/*   session; a running session defers).                          */
+/*   Per type, candidates in the O4 order, literal sequential greedy:         */
+/*   d = argmin backlog over unblocked instances of the type (ties: lowest    */
+/*   id); migrate iff d exists and backlog[d] + delta <=                      */
+/*   backlog[s]; then backlog[s] -= 1, backlog[d] += 1.                       */
+/* ------------------------------------------------------------------------ */
+int oracle_migrate(const oracle_table* t, const oracle_out* o, const oracle_mig_params* p, oracle_mig_out* r) {
+    uint32_t N = t->n_futures, W = t->n_workflows, I = t->n_instances, T = t->n_types;
+    int64_t* backlog = (int64_t*)calloc(I ? I : 1, sizeof(int64_t));
+    uint8_t* blocked = (uint8_t*)calloc(I ? I : 1, 1);
+    uint8_t* cand = (uint8_t*)calloc(N ? N : 1, 1);
+    uint32_t* buf = (uint32_t*)malloc(sizeof(uint32_t) * (N ? N : 1));
+    for (uint32_t i = 0; i < I; ++i) {
+        backlog[i] = (int64_t)o->i_load[i] + o->i_assigned[i];
+        blocked[i] = (uint8_t)(p->i_head_rem[i] > p->theta_head);
+        r->i_mig_in[i] = 0;
+        r->i_mig_out[i] = 0;
+    }
+    for (uint32_t f = 0; f < N; ++f) r->migrate_to[f] = -1;
+    /* candidates */
+    for (uint32_t w = 0; w < W; ++w) {
+        for (uint32_t f = t->wf_fut_off[w]; f < t->wf_fut_off[w + 1]; ++f) {
+            if (t->f_state[f] != S_QUEUED) continue;
+            int s = t->f_executor[f];
+            uint8_t ty = t->f_type[f], aff = t->t_affinity[ty];
+            if (!blocked[s] || p->f_age[f] <= p->theta_wait || aff == A_STATEFUL) continue;
+            if (aff == A_SESSION) {
+                uint32_t nq = 0, nr = 0;
+                for (uint32_t g = t->wf_fut_off[w]; g < t->wf_fut_off[w + 1]; ++g) {
+                    if (t->f_type[g] != ty) continue;
+                    if (t->f_state[g] == S_QUEUED) nq++;
+                    if (t->f_state[g] == S_RUNNING) nr++;
+                }
+                if (nq != 1 || nr != 0) continue;
+            }
+            cand[f] = 1;
+        }
+    }
+    g_level = o->level;
+    uint32_t nm = 0;
+    for (uint32_t ty = 0; ty < T; ++ty) {
+        uint32_t n = 0;
+        for (uint32_t f = 0; f < N; ++f)
+            if (cand[f] && t->f_type[f] == ty) buf[n++] = f;
+        qsort(buf, n, sizeof(uint32_t), cmp_order);
+        for (uint32_t k = 0; k < n; ++k) {
+            uint32_t f = buf[k];
+            int s = t->f_executor[f];
+            int64_t d = -1;
+            for (uint32_t i = 0; i < I; ++i)
+                if (t->i_type[i] == ty && !blocked[i] && (d < 0 || backlog[i] < backlog[d])) d = i;
+            if (d < 0 || backlog[d] + (int64_t)p->delta > backlog[s]) continue;
+            backlog[s] -= 1;
+            backlog[d] += 1;
+            r->migrate_to[f] = (int16_t)d;
+            r->i_mig_out[s] += 1;
+            r->i_mig_in[d] += 1;
+            nm++;
+        }
+    }
+    r->n_migrated = nm;
+    free(backlog); free(blocked); free(cand); free(buf);
+    return 0;
+}

@@ -68,6 +68,25 @@ typedef struct {
     uint32_t  n_pairs;    /* out */
 } oracle_ra_out;
 
+/* O11 head-of-line-blocking migration (NEXT-1): per QUEUED future its wait
+ * age, per instance the predicted remaining time of its head job (same unit),
+ * thresholds theta_wait / theta_head and the anti-thrash margin delta (SPEC
+ * S:441 and its defaults). */
+typedef struct {
+    const uint32_t* f_age;       /* [N] */
+    const uint32_t* i_head_rem;  /* [I] */
+    uint32_t theta_wait, theta_head, delta;
+} oracle_mig_params;
+
+typedef struct {
+    int16_t*  migrate_to;  /* [N] destination instance, -1 none */
+    uint32_t* i_mig_in;    /* [I] */
+    uint32_t* i_mig_out;   /* [I] */
+    uint32_t  n_migrated;  /* out */
+} oracle_mig_out;
+
+int oracle_migrate(const oracle_table* t, const oracle_out* o, const oracle_mig_params* p, oracle_mig_out* r);
+
 /* O10 from a finished epoch (o from oracle_epoch on the same table). */
 int oracle_reassign(const oracle_table* t, const oracle_out* o, const oracle_ra_params* p, oracle_ra_out* r);
 

@@ -48,6 +48,16 @@ class _RaOut(C.Structure):
                 ("prov_type", C.c_void_p), ("n_pairs", C.c_uint32)]
 
 
+class _MigParams(C.Structure):
+    _fields_ = [("f_age", C.c_void_p), ("i_head_rem", C.c_void_p), ("theta_wait", C.c_uint32),
+                ("theta_head", C.c_uint32), ("delta", C.c_uint32)]
+
+
+class _MigOut(C.Structure):
+    _fields_ = [("migrate_to", C.c_void_p), ("i_mig_in", C.c_void_p), ("i_mig_out", C.c_void_p),
+                ("n_migrated", C.c_uint32)]
+
+
 _lib = None
 
 
@@ -68,6 +78,8 @@ def _load():
         _lib.oracle_epoch.argtypes = [C.POINTER(_Table), C.c_int, C.POINTER(_Out)]
         _lib.oracle_reassign.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_RaParams),
                                          C.POINTER(_RaOut)]
+        _lib.oracle_migrate.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_MigParams),
+                                        C.POINTER(_MigOut)]
     return _lib
 
 
@@ -92,7 +104,7 @@ def oracle_validate(s, levels: int = 256):
     return rc, err.value
 
 
-def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None) -> dict:
+def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None, migrate=None) -> dict:
     """One epoch; ``reassign`` = dict(t_min_inst, t_max_inst, u_hi_pct, u_lo_pct)
     also runs O10 (resource reassignment) on the result."""
     lib = _load()
@@ -128,6 +140,18 @@ def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None) -> dict:
         out["t_busy"], out["t_cap"] = ra["t_busy"], ra["t_cap"]
         out["ra_kill"] = ra["kill_inst"][:ro.n_pairs].copy()
         out["ra_prov"] = ra["prov_type"][:ro.n_pairs].copy()
+    if migrate is not None:             # O11 (NEXT-1) on the finished epoch
+        age = np.ascontiguousarray(migrate["f_age"], np.uint32)
+        head = np.ascontiguousarray(migrate["i_head_rem"], np.uint32)
+        mo = {"migrate_to": np.zeros(max(N, 1), np.int16), "i_mig_in": np.zeros(max(I, 1), np.uint32),
+              "i_mig_out": np.zeros(max(I, 1), np.uint32)}
+        prm = _MigParams(_ptr(age), _ptr(head), int(migrate.get("theta_wait", 0)),
+                         int(migrate.get("theta_head", 0)), int(migrate.get("delta", 2)))
+        ro = _MigOut(*[_ptr(mo[k]) for k in ("migrate_to", "i_mig_in", "i_mig_out")], 0)
+        lib.oracle_migrate(C.byref(t), C.byref(o), C.byref(prm), C.byref(ro))
+        out["migrate_to"] = mo["migrate_to"][:N].copy()
+        out["i_mig_in"], out["i_mig_out"] = mo["i_mig_in"][:I].copy(), mo["i_mig_out"][:I].copy()
+        out["n_migrated"] = ro.n_migrated
     na = o.n_assigned
     out["assign_row"] = out["assign_row"][:na].copy()
     out["assign_inst"] = out["assign_inst"][:na].copy()

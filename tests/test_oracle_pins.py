@@ -544,3 +544,116 @@ def test_reassign_c4_shifts_toward_hot_types():
     assert o["ra_kill"].tolist() == kill and o["ra_prov"].tolist() == prov and len(kill) >= 1
     for k, p in zip(kill, prov):
         assert busy[p] * cap[s.i_type[k]] > busy[s.i_type[k]] * cap[p]    # from colder to hotter
+
+
+# --------------------------------------------------------------------------
+# O11 head-of-line-blocking migration (NEXT-1)
+# --------------------------------------------------------------------------
+def _hol_table(q, n_targets=1, target_base=0, src_base=0, aff=AFF_NONE, extra=None):
+    """Type 0 instances: 0 = the blocked source, 1.. = targets.  q QUEUED
+    futures at instance 0 (one per workflow), plus src_base / target_base load."""
+    I = 1 + n_targets
+    tb = TableBuilder(i_type=[0] * I, i_cap=[64] * I, i_base_load=[src_base] + [target_base] * n_targets,
+                      t_affinity=[aff])
+    for k in range(q):
+        tb.add_workflow(k + 1, 0, [(QUEUED, 0, 0, 0, -1, [])] + (extra or []))
+    return tb.build()
+
+
+def _mig(s, theta_wait=5, theta_head=5, delta=2, age=10, head=None):
+    head = head if head is not None else [10] + [0] * (s.n_instances - 1)
+    return oracle_epoch(s, "fcfs", migrate={"f_age": np.full(s.n_futures, age, np.uint32),
+                                            "i_head_rem": np.asarray(head, np.uint32),
+                                            "theta_wait": theta_wait, "theta_head": theta_head,
+                                            "delta": delta})
+
+
+def test_hol_spec_examples():
+    # all queues empty -> no commands (S:444)
+    tb = TableBuilder(i_type=[0, 0], i_cap=[4, 4], i_base_load=[0, 0], t_affinity=[AFF_NONE])
+    tb.add_workflow(1, 0, [(RESOLVED, 0, 0, -1, -1, [])])
+    assert _mig(tb.build())["n_migrated"] == 0
+    # one instance blocked by a long head job, an idle peer -> the blocked
+    # futures migrate to the idle peer (S:445): backlog 3 vs 0, delta 2:
+    # moves while (moved) + 2 <= 3 - (moved) -> 1 move
+    o = _mig(_hol_table(3))
+    assert o["migrate_to"].tolist() == [1, -1, -1] and o["n_migrated"] == 1
+    # two equally loaded instances -> no migration, the margin is unmet (S:446)
+    o = _mig(_hol_table(2, target_base=2))
+    assert o["n_migrated"] == 0
+    # not blocked (head job short) or not waiting long -> nothing
+    assert _mig(_hol_table(6), head=[3, 0])["n_migrated"] == 0
+    assert _mig(_hol_table(6), age=4)["n_migrated"] == 0
+
+
+@pytest.mark.parametrize("q,base,delta,nt", [(q, b, d, nt) for q in (1, 4, 9, 17) for b in (0, 3)
+                                              for d in (0, 1, 2, 5) for nt in (1, 2, 3)])
+def test_hol_closed_form(q, base, delta, nt):
+    """One source with backlog B = q (+ its base), nt idle targets at base b:
+    the j-th move (j = 0, 1, ...) lands on the target level b + floor(j / nt)
+    (fill from below, ties to the lowest id) and happens iff
+    b + floor(j / nt) + delta <= B - j; moves stop at the first failure."""
+    s = _hol_table(q, n_targets=nt, target_base=base)
+    o = _mig(s, delta=delta)
+    B = q
+    m = 0
+    while m < q and base + m // nt + delta <= B - m:
+        m += 1
+    assert o["n_migrated"] == m
+    assert o["migrate_to"].tolist() == [1 + (j % nt) for j in range(m)] + [-1] * (q - m)
+    assert o["i_mig_out"].tolist()[0] == m
+
+
+def test_hol_directives():
+    # STATEFUL futures never move (in-order per session, P:267)
+    assert _mig(_hol_table(6, aff=AFF_STATEFUL))["n_migrated"] == 0
+    # a SESSION future moves only as its session's only queued future ...
+    assert _mig(_hol_table(6, aff=AFF_SESSION))["n_migrated"] == 3
+    # ... and not while the session has a running future (S:535 "deferred")
+    s = _hol_table(6, aff=AFF_SESSION, extra=[(RUNNING, 0, 0, 1, -1, [])])
+    assert _mig(s)["n_migrated"] == 0
+    # ... nor when it has a second queued future
+    s = _hol_table(6, aff=AFF_SESSION, extra=[(QUEUED, 0, 0, 0, -1, [])])
+    assert _mig(s)["n_migrated"] == 0
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_hol_invariants_random(seed):
+    """Validity of every move and maximality of the greedy (a candidate left
+    in place could not move even against the final backlogs)."""
+    rng = np.random.default_rng(seed)
+    s = random_table(seed, n_workflows=3 + seed % 6, max_rows=4 + seed % 20, n_types=1 + seed % 3,
+                     inst_per_type=(1, 2 + seed % 4), consistent=True, max_cap=2 + seed % 8,
+                     max_base=seed % 6)
+    age = rng.integers(0, 20, s.n_futures).astype(np.uint32)
+    head = rng.integers(0, 20, s.n_instances).astype(np.uint32)
+    tw, th, dl = int(rng.integers(0, 15)), int(rng.integers(0, 15)), int(rng.integers(0, 4))
+    o = oracle_epoch(s, "srtf", migrate={"f_age": age, "i_head_rem": head, "theta_wait": tw,
+                                         "theta_head": th, "delta": dl})
+    blocked = head > th
+    backlog = o["i_load"].astype(np.int64) + o["i_assigned"]
+    mt = o["migrate_to"]
+    wf = np.repeat(np.arange(s.n_workflows), np.diff(s.wf_fut_off.astype(np.int64)))
+    final = backlog.copy()
+    cand = np.zeros(s.n_futures, bool)
+    for f in range(s.n_futures):
+        if s.f_state[f] != QUEUED:
+            assert mt[f] == -1
+            continue
+        src, ty = int(s.f_executor[f]), int(s.f_type[f])
+        aff = int(s.t_affinity[ty])
+        sess = (wf == wf[f]) & (s.f_type == ty)
+        ok = blocked[src] and age[f] > tw and aff != AFF_STATEFUL
+        if aff == AFF_SESSION:
+            ok = ok and int((sess & (s.f_state == QUEUED)).sum()) == 1 and not (sess & (s.f_state == RUNNING)).any()
+        cand[f] = ok
+        if mt[f] >= 0:
+            assert ok and s.i_type[mt[f]] == ty and not blocked[mt[f]] and mt[f] != src
+            final[src] -= 1
+            final[mt[f]] += 1
+    assert np.array_equal(np.bincount(mt[mt >= 0], minlength=s.n_instances), o["i_mig_in"])
+    for f in np.nonzero(cand & (mt < 0))[0]:
+        ty = int(s.f_type[f])
+        tg = [i for i in range(s.n_instances) if s.i_type[i] == ty and not blocked[i]]
+        if tg:
+            assert min(final[i] for i in tg) + dl > final[int(s.f_executor[f])]
