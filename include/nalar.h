@@ -131,6 +131,11 @@ typedef struct {
     const uint32_t* i_cap;       /* [I] capacity (queue + running)           */
     const uint32_t* i_base_load; /* [I] load outside the table               */
     const uint8_t*  t_affinity;  /* [T] nalar_aff                            */
+    /* HoL-migration inputs (NEXT-1), may be NULL (then nothing migrates):
+     * wait age of each QUEUED future and the predicted remaining time of
+     * each instance's head job, in one caller-chosen time unit */
+    const uint32_t* f_age;       /* [N]                                      */
+    const uint32_t* i_head_rem;  /* [I]                                      */
 } nalar_snapshot;
 
 /* Delta between two epochs of a dynamic workload (SURVEY §8(c) "Delta
@@ -230,6 +235,13 @@ typedef struct {
     int16_t*  ra_prov;    /* [T]                                               */
     uint32_t  t_cap;      /* elements of the four arrays above (>= T)          */
     uint32_t  n_reassign; /* out                                               */
+    /* HoL migration (only with nalar_policy_params.migrate,
+     * world == 1): migrate_to[f] = destination instance of a QUEUED future
+     * (a SESSION future carries its session: re-home its pin), -1 none.      */
+    int16_t*  migrate_to; /* [N] (capacity f_cap)                              */
+    uint32_t* i_mig_in;   /* [I] (capacity i_cap)                              */
+    uint32_t* i_mig_out;  /* [I]                                               */
+    uint32_t  n_migrated; /* out                                               */
 } nalar_decisions;
 
 /* Policy parameters beyond the per-epoch policy (persist on the context;
@@ -248,6 +260,16 @@ typedef struct {
     const uint16_t* t_min_inst;    /* [n_types] or NULL (all 0)                    */
     const uint16_t* t_max_inst;    /* [n_types] or NULL (all 65535)                */
     uint32_t n_types;              /* <= max_types                                 */
+    /* HoL migration (NEXT-1; "migrates a job if it's waiting in
+     * the queue and observing head-of-line blocking"): a QUEUED
+     * future with age > theta_wait at an instance whose head job has
+     * head_rem > theta_head (blocked) moves, in priority order, to the
+     * least-backlogged (load + assigned) unblocked instance of its type while
+     * that backlog + delta <= the source's; STATEFUL futures never move, a
+     * SESSION future only as its session's sole queued work with nothing of
+     * the session running.  E_NOTIMPL with world > 1. */
+    uint32_t migrate;              /* 0 off, 1 on                                  */
+    uint32_t theta_wait, theta_head, delta;
 } nalar_policy_params;
 
 /* Copies p (host arrays borrowed for the call).  E_INVAL on u_lo > u_hi or

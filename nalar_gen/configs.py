@@ -302,3 +302,53 @@ def random_table(seed: int, n_workflows: int = 3, max_rows: int = 8, n_types: in
 
 
 CONFIGS = {"C1": lambda seed=1: c1(), "C2": c2, "C4": c4, "C5": c5}
+
+
+# ----------------------------------------------------------------------------
+# HoL-migration inputs (NEXT-1): wait ages and head-job remaining times
+# ----------------------------------------------------------------------------
+def with_hol_inputs(s: Snapshot, seed: int = 1, p_blocked: float = 0.25, age_max: int = 100,
+                    head_long: int = 100, head_short_max: int = 20) -> Snapshot:
+    """The same table plus f_age ~ U{0..age_max} (read for QUEUED futures) and
+    i_head_rem = head_long on a p_blocked share of the instances (a long job at
+    the head of the queue), U{0..head_short_max} elsewhere."""
+    rng = np.random.default_rng(seed + 7919)
+    t = s.copy()
+    t.f_age = rng.integers(0, age_max + 1, s.n_futures).astype(np.uint32)
+    blocked = rng.random(s.n_instances) < p_blocked
+    t.i_head_rem = np.where(blocked, head_long,
+                            rng.integers(0, head_short_max + 1, s.n_instances)).astype(np.uint32)
+    t.name = s.name + "+hol"
+    return t
+
+
+def hol_table(seed: int, n_workflows: int = 24, n_types: int = 3, inst_per_type: int = 4,
+              max_rows: int = 6) -> Snapshot:
+    """Small tables with many QUEUED futures piled on a few instances (skewed
+    executors, uneven base loads) and the NEXT-1 inputs: the head-of-line
+    scenario of PAPER.md:663.  Types cycle NONE / SESSION / STATEFUL."""
+    rng = np.random.default_rng(seed)
+    I = n_types * inst_per_type
+    i_type = np.repeat(np.arange(n_types), inst_per_type)
+    tb = TableBuilder(i_type=i_type, i_cap=rng.integers(2, 12, I), i_base_load=rng.integers(0, 5, I),
+                      t_affinity=[(AFF_NONE, AFF_SESSION, AFF_STATEFUL)[t % 3] for t in range(n_types)],
+                      name=f"hol{seed}")
+    skew = np.array([1.0 / (k + 1) ** 1.5 for k in range(inst_per_type)])
+    skew /= skew.sum()
+    wid = 0
+    for _ in range(n_workflows):
+        wid += int(rng.integers(1, 3))
+        n = int(rng.integers(1, max_rows + 1))
+        rows = []
+        for j in range(n):
+            ty = int(rng.integers(0, n_types))
+            st = int(rng.choice([PENDING, QUEUED, RUNNING, RESOLVED], p=[0.3, 0.45, 0.1, 0.15]))
+            ex = ty * inst_per_type + int(rng.choice(inst_per_type, p=skew)) if st in (QUEUED, RUNNING) else -1
+            pin = ex if (st in (QUEUED, RUNNING) and rng.random() < 0.3) else -1
+            preds = [(int(rng.integers(0, j)), False)] if j and rng.random() < 0.5 else []
+            rows.append((st, ty, 0, ex, pin, preds))
+        tb.add_workflow(wid=wid, prio=int(rng.integers(0, 4)), rows=rows)
+    s = tb.build()
+    s.f_age = rng.integers(0, 21, s.n_futures).astype(np.uint32)
+    s.i_head_rem = rng.integers(0, 21, I).astype(np.uint32)
+    return s

@@ -67,12 +67,19 @@ class Snapshot:
     t_affinity: np.ndarray
     global_row_base: int = 0
     name: str = field(default="snapshot")
+    # optional HoL-migration inputs (NEXT-1): wait age of each QUEUED future,
+    # predicted remaining time of each instance's head job (one time unit)
+    f_age: np.ndarray = None
+    i_head_rem: np.ndarray = None
 
     def __post_init__(self):
         for f in fields(self):
             if f.name in _DTYPES:
                 v = np.ascontiguousarray(getattr(self, f.name), dtype=_DTYPES[f.name])
                 setattr(self, f.name, v)
+        for k in ("f_age", "i_head_rem"):
+            if getattr(self, k) is not None:
+                setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=np.uint32))
 
     # sizes --------------------------------------------------------------
     @property
@@ -103,7 +110,9 @@ class Snapshot:
 
     def copy(self) -> "Snapshot":
         kw = {k: v.copy() for k, v in self.arrays().items()}
-        return Snapshot(global_row_base=self.global_row_base, name=self.name, **kw)
+        return Snapshot(global_row_base=self.global_row_base, name=self.name, **kw,
+                        f_age=None if self.f_age is None else self.f_age.copy(),
+                        i_head_rem=None if self.i_head_rem is None else self.i_head_rem.copy())
 
     # data-layout utilities (no method arithmetic) -------------------------
     def slice_workflows(self, w0: int, w1: int) -> "Snapshot":
@@ -127,7 +136,9 @@ class Snapshot:
             f_edge_off=self.f_edge_off[r0:r1 + 1] - np.uint32(e0), edges=edges,
             i_type=self.i_type, i_cap=self.i_cap, i_base_load=self.i_base_load,
             t_affinity=self.t_affinity, global_row_base=self.global_row_base + r0,
-            name=f"{self.name}[w{w0}:{w1}]")
+            name=f"{self.name}[w{w0}:{w1}]",
+            f_age=None if self.f_age is None else self.f_age[r0:r1],
+            i_head_rem=self.i_head_rem)
 
     def save(self, path: str) -> None:
         np.savez(path, global_row_base=np.uint64(self.global_row_base), **self.arrays())

@@ -68,6 +68,7 @@ struct SweepParams {
     const uint8_t* blk_staged;  // [B]   1 = rows staged in shared memory by TMA
     const uint32_t* wf_perm;    // [W]   per block: local workflow indices, largest first (task order)
     uint32_t B, n_types, n_inst, R, levels, policy;
+    uint32_t Rh;                // R + T: bucket / histogram resources (the last T: HoL candidates, NEXT-1)
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
     uint32_t *g_tlo, *g_thi, *g_ifc, *g_ndp;   // [N] step-transfer scratch for unstaged blocks
@@ -101,6 +102,7 @@ struct AssignParams {
     const uint32_t* type_off;   // [T+1] instances of type t: type_inst[type_off[t] ..]
     const uint32_t* type_inst;  // [I]   instance ids grouped by type, ascending
     uint32_t G, slot, R, n_inst, n_types, levels, B;
+    uint32_t Rh;                // histogram row stride (R + T)
     const uint8_t* i_type;
     const uint32_t* i_cap;
     const uint32_t* i_base;

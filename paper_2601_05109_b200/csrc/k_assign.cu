@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     uint32_t hg = 0, hb = 0, hl = 0;
     if (lv < Lv) {
         for (uint32_t s = 0; s < G; ++s) {
-            const uint32_t h = p.H[((size_t)s * R + r) * Lv + lv];
+            const uint32_t h = p.H[((size_t)s * p.Rh + r) * Lv + lv];
             hg += h;
             if (s < p.slot) hb += h;
             if (s == p.slot) hl = h;

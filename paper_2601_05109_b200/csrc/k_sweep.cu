@@ -186,7 +186,7 @@ template <bool kStaged>
 __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t b = blockIdx.x;
-    const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Lv = p.levels;
+    const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Rh = p.Rh, Lv = p.levels;
 
     const uint32_t w0 = p.blk_wf[b], w1 = p.blk_wf[b + 1];
     const uint32_t r0 = p.blk_row0[b], r1 = p.blk_row0[b + 1];
@@ -208,9 +208,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     uint32_t* s_load = (uint32_t*)sp;
     sp += 4 * (size_t)I;
     uint32_t* s_rcnt = (uint32_t*)sp;
-    sp += 4 * (size_t)R;
+    sp += 4 * (size_t)Rh;
     uint32_t* s_roff = (uint32_t*)sp;
-    sp += 4 * (size_t)R;
+    sp += 4 * (size_t)Rh;
     uint32_t* s_list = (uint32_t*)sp;
     sp += 4 * kK1Threads;
     uint32_t* s_wc = (uint32_t*)sp;
@@ -322,7 +322,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
 
     // ---- zero block state while the copies are in flight ------------------
     for (uint32_t i = tid; i < I; i += kK1Threads) s_load[i] = 0;
-    for (uint32_t r = tid; r < R; r += kK1Threads) s_rcnt[r] = 0;
+    for (uint32_t r = tid; r < Rh; r += kK1Threads) s_rcnt[r] = 0;
     for (uint32_t t = tid; t < T; t += kK1Threads) s_aff[t] = p.t_aff[t];
     for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
         s_wfp[k] = 0xFFFFFFFFu; s_wfru[k] = 0xFFFFFFFFu; s_khome[k] = 0xFFFFFFFFu; s_klev[k] = 0u;
@@ -997,8 +997,8 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         if (s_load[i]) atomicAdd(&p.load_part[i], s_load[i]);
     // exclusive scan of s_rcnt over R (serial per thread chunk + warp scan)
     {
-        const uint32_t per = (R + kK1Threads - 1) / kK1Threads;
-        const uint32_t lo = min(R, tid * per), hi = min(R, lo + per);
+        const uint32_t per = (Rh + kK1Threads - 1) / kK1Threads;
+        const uint32_t lo = min(Rh, tid * per), hi = min(Rh, lo + per);
         uint32_t sum = 0;
         for (uint32_t r = lo; r < hi; ++r) sum += s_rcnt[r];
         uint32_t incl = sum;

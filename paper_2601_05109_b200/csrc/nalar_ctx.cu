@@ -80,7 +80,7 @@ struct nalar_ctx {
     uint8_t* arena = nullptr;
     bool own_arena = false;
     size_t arena_bytes = 0;
-    uint32_t Lv = 256, Rmax = 0, Bmax = 0;
+    uint32_t Lv = 256, Rmax = 0, Rhmax = 0, Bmax = 0, Rh = 0;
     // inputs
     uint32_t *d_wf_off = nullptr, *d_eoff = nullptr, *d_edges = nullptr, *d_icap = nullptr, *d_ibase = nullptr;
     int32_t* d_wf_prio = nullptr;
@@ -194,7 +194,7 @@ struct Plan {
     size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
-    uint32_t Rmax, Bmax;
+    uint32_t Rmax, Rhmax, Bmax;
 };
 
 bool plan_layout(const nalar_config* cfg, Plan* p) {
@@ -203,6 +203,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     const size_t I = cfg->max_instances, T = cfg->max_types;
     const uint32_t G = cfg->world > 0 ? (uint32_t)cfg->world : 1u;
     p->Rmax = (uint32_t)(I + T);
+    p->Rhmax = (uint32_t)(I + 2 * T);       // + T HoL-candidate buckets (NEXT-1)
     p->Bmax = (uint32_t)std::min<size_t>(std::max<size_t>(W, 1), kMaxBlocks);
     Layout L;
     p->wf_off = L.take<uint32_t>(W + 1);
@@ -255,14 +256,14 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->iasg = L.take<uint32_t>(I);
     p->arow = L.take<uint32_t>(N);
     p->items = L.take<uint2>(N);
-    p->cnt_rb = L.take<uint32_t>((size_t)p->Rmax * p->Bmax);
-    p->off_rb = L.take<uint32_t>((size_t)p->Rmax * p->Bmax);
-    p->x_words = (size_t)G * p->Rmax * Lv + I + p->Rmax;
+    p->cnt_rb = L.take<uint32_t>((size_t)p->Rhmax * p->Bmax);
+    p->off_rb = L.take<uint32_t>((size_t)p->Rhmax * p->Bmax);
+    p->x_words = (size_t)G * p->Rhmax * Lv + I + p->Rhmax;
     // exchange buffer and scratch are contiguous so one memset clears both
     p->x = L.off;
     L.off += p->x_words * 4;
     p->scr = L.off;
-    L.off += (C_NUM + 2 * (size_t)p->Rmax) * 4;   // counters, n_adm[R], tot_loc[R]
+    L.off += (C_NUM + (size_t)p->Rmax + p->Rhmax) * 4;   // counters, n_adm[R], tot_loc[Rh]
     L.off = (L.off + 255) & ~(size_t)255;
     p->err = L.take<unsigned long long>(2);
     p->total = L.off + 256;
@@ -365,6 +366,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.blk_staged = c->d_blk_staged;
     p.wf_perm = c->d_wf_perm;
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
+    p.Rh = c->Rh;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
     p.g_tlo = c->d_gtlo; p.g_thi = c->d_gthi; p.g_ifc = c->d_gifc; p.g_ndp = c->d_gndp; p.g_aux = c->d_gaux;
@@ -374,9 +376,9 @@ int run_k1(nalar_ctx* c, int policy) {
     p.new_pin = c->d_newpin; p.wf_agg = c->d_wfagg;
     p.kv_hint = c->d_kvh; p.kv_level = c->d_kvl; p.kv_home = c->d_kvhome;
     const uint32_t slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
-    p.H = c->d_x + (size_t)slot * c->R * c->Lv;
+    p.H = c->d_x + (size_t)slot * c->Rh * c->Lv;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
-    p.load_part = c->d_x + (size_t)G * c->R * c->Lv;
+    p.load_part = c->d_x + (size_t)G * c->Rh * c->Lv;
     p.tot = p.load_part + c->I;
     p.items = c->d_items; p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb;
     p.tot_loc = c->d_scr + C_NUM + c->Rmax;
@@ -389,12 +391,13 @@ int run_k4(nalar_ctx* c) {
     AssignParams p{};
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.H = c->d_x;
-    p.load_sum = c->d_x + (size_t)G * c->R * c->Lv;
+    p.load_sum = c->d_x + (size_t)G * c->Rh * c->Lv;
     p.tot = p.load_sum + c->I;
     p.type_off = c->d_type_off;
     p.type_inst = c->d_type_inst;
     p.G = G; p.slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
     p.R = c->R; p.n_inst = c->I; p.n_types = c->T; p.levels = c->Lv; p.B = c->B;
+    p.Rh = c->Rh;
     p.i_type = c->d_itype; p.i_cap = c->d_icap; p.i_base = c->d_ibase; p.t_aff = c->d_taff;
     p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb; p.blk_row0 = c->d_blk_row0; p.items = c->d_items;
     p.status = c->d_status; p.instance = c->d_inst; p.new_pin = c->d_newpin;
@@ -413,7 +416,7 @@ int run_k4(nalar_ctx* c) {
 
 size_t x_used_words(nalar_ctx* c) {
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
-    return (size_t)G * c->R * c->Lv + c->I + c->R;
+    return (size_t)G * c->Rh * c->Lv + c->I + c->Rh;
 }
 
 // an event inside a captured graph must be an external event-record node
@@ -428,7 +431,7 @@ cudaError_t record_ev(nalar_ctx* c, int k) {
 int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
     // clear exchange buffer (used part) + counters + adm_pub; contiguous region
-    CK(launch_zero(c->d_x, c->x_words + C_NUM + 2 * (size_t)c->Rmax, c->stream));
+    CK(launch_zero(c->d_x, c->x_words + C_NUM + (size_t)c->Rmax + c->Rhmax, c->stream));
     if (timing) CK(record_ev(c, 0));
     int rc = run_k1(c, policy);
     if (rc) return rc;
@@ -469,7 +472,7 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch) {
     size_t mx = 0;
     partition(c, c->m_wf_off.data(), c->m_wf_eoff.data(), bw, br, be, bs, &mx);
     c->B = (uint32_t)bs.size();
-    c->fixed_smem = k1_fixed_smem(c->T, c->I, c->R);
+    c->fixed_smem = k1_fixed_smem(c->T, c->I, c->Rh);
     c->smem = c->fixed_smem + mx;
     cudaStream_t st = c->stream;
     // task order inside each block: largest workflow first (longest-processing-
@@ -578,6 +581,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     Plan p;
     plan_layout(cfg, &p);
     c->Rmax = p.Rmax;
+    c->Rhmax = p.Rhmax;
     c->Bmax = p.Bmax;
     c->x_words = p.x_words;
     if (cfg->workspace) {
@@ -722,7 +726,7 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
         if (s->t_affinity[t] > NALAR_AFF_STATEFUL) return fail(c, NALAR_E_INVAL, "affinity out of range");
     if (N && T == 0) return fail(c, NALAR_E_INVAL, "futures without types");
 
-    c->N = N; c->E = E; c->W = W; c->I = I; c->T = T; c->R = I + T;
+    c->N = N; c->E = E; c->W = W; c->I = I; c->T = T; c->R = I + T; c->Rh = I + 2 * T;
     c->assign_valid = false;
     // host mirror of the workflow layout (delta mode re-partitions from it)
     c->m_wf_id.assign(s->wf_id, s->wf_id + W);

@@ -51,7 +51,8 @@ class nalar_snapshot(C.Structure):
                 ("f_state", C.c_void_p), ("f_type", C.c_void_p), ("f_round", C.c_void_p),
                 ("f_executor", C.c_void_p), ("f_pin", C.c_void_p), ("f_edge_off", C.c_void_p),
                 ("edges", C.c_void_p), ("i_type", C.c_void_p), ("i_cap", C.c_void_p),
-                ("i_base_load", C.c_void_p), ("t_affinity", C.c_void_p)]
+                ("i_base_load", C.c_void_p), ("t_affinity", C.c_void_p),
+                ("f_age", C.c_void_p), ("i_head_rem", C.c_void_p)]
 
 
 class nalar_decisions(C.Structure):
@@ -66,12 +67,16 @@ class nalar_decisions(C.Structure):
                 ("kv_hint", C.c_void_p), ("kv_level", C.c_void_p), ("kv_home", C.c_void_p),
                 ("kv_cap", C.c_uint32),
                 ("t_busy", C.c_void_p), ("t_capsum", C.c_void_p), ("ra_kill", C.c_void_p),
-                ("ra_prov", C.c_void_p), ("t_cap", C.c_uint32), ("n_reassign", C.c_uint32)]
+                ("ra_prov", C.c_void_p), ("t_cap", C.c_uint32), ("n_reassign", C.c_uint32),
+                ("migrate_to", C.c_void_p), ("i_mig_in", C.c_void_p), ("i_mig_out", C.c_void_p),
+                ("n_migrated", C.c_uint32)]
 
 
 class nalar_policy_params(C.Structure):
     _fields_ = [("reassign", C.c_uint32), ("u_hi_pct", C.c_uint32), ("u_lo_pct", C.c_uint32),
-                ("t_min_inst", C.c_void_p), ("t_max_inst", C.c_void_p), ("n_types", C.c_uint32)]
+                ("t_min_inst", C.c_void_p), ("t_max_inst", C.c_void_p), ("n_types", C.c_uint32),
+                ("migrate", C.c_uint32), ("theta_wait", C.c_uint32), ("theta_head", C.c_uint32),
+                ("delta", C.c_uint32)]
 
 
 class nalar_delta(C.Structure):
@@ -197,6 +202,14 @@ def snapshot_struct(s) -> tuple:
                                                "f_round", "f_executor", "f_pin", "f_edge_off",
                                                "edges", "i_type", "i_cap", "i_base_load",
                                                "t_affinity")])
+    # optional HoL-migration inputs (NEXT-1)
+    for k in ("f_age", "i_head_rem"):
+        v = getattr(s, k, None)
+        if v is not None:
+            v = np.ascontiguousarray(v, np.uint32)
+            a = dict(a)
+            a[k] = v
+            setattr(st, k, _ptr(v))
     return st, a
 
 
@@ -363,20 +376,24 @@ class Context:
     def stats(self) -> nalar_epoch_stats:
         return nalar_epoch_stats_get(self.h)
 
-    def set_policy_params(self, reassign=True, u_hi_pct=80, u_lo_pct=30, t_min_inst=None,
-                          t_max_inst=None, n_types=None) -> None:
-        """Resource-reassignment parameters (NEXT-2); SPEC defaults u_hi 80 %, u_lo 30 %."""
+    def set_policy_params(self, reassign=False, u_hi_pct=80, u_lo_pct=30, t_min_inst=None,
+                          t_max_inst=None, n_types=None, migrate=False, theta_wait=0, theta_head=0,
+                          delta=2) -> None:
+        """Resource reassignment (NEXT-2; SPEC defaults u_hi 80 %, u_lo 30 %) and
+        HoL migration (NEXT-1; SPEC default delta = 2 jobs)."""
         mn = None if t_min_inst is None else np.ascontiguousarray(t_min_inst, np.uint16)
         mx = None if t_max_inst is None else np.ascontiguousarray(t_max_inst, np.uint16)
         nt = n_types if n_types is not None else (len(mn) if mn is not None else
                                                   (len(mx) if mx is not None else 0))
         p = nalar_policy_params(int(bool(reassign)), int(u_hi_pct), int(u_lo_pct),
                                 _ptr(mn) if mn is not None else None,
-                                _ptr(mx) if mx is not None else None, int(nt))
+                                _ptr(mx) if mx is not None else None, int(nt), int(bool(migrate)),
+                                int(theta_wait), int(theta_head), int(delta))
         _check(self.h, _lib.nalar_set_policy_params(self.h, C.byref(p)), "set_policy_params")
 
     def output_buffers(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg",
-                                     "i_load", "i_spare", "i_assigned", "assign", "kv", "reassign"),
+                                     "i_load", "i_spare", "i_assigned", "assign", "kv", "reassign",
+                                     "migrate"),
                        alloc=None):
         """Host buffers for fetch(); ``alloc(n, dtype)`` may return pinned memory."""
         N, W, I = self.n
@@ -391,6 +408,10 @@ class Context:
             out["kv_hint"] = alloc(W * T, np.uint8)
             out["kv_level"] = alloc(W * T, np.uint8)
             out["kv_home"] = alloc(W * T, np.int16)
+        if "migrate" in fields:
+            out["migrate_to"] = alloc(max(N, 1), np.int16)
+            out["i_mig_in"] = alloc(max(I, 1), np.uint32)
+            out["i_mig_out"] = alloc(max(I, 1), np.uint32)
         if "reassign" in fields:
             T = max(self.n_types, 1)
             out["t_busy"] = alloc(T, np.uint32)
@@ -403,13 +424,14 @@ class Context:
         return out
 
     def fetch(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
-                            "i_spare", "i_assigned", "assign", "kv", "reassign"), out=None) -> dict:
+                            "i_spare", "i_assigned", "assign", "kv", "reassign", "migrate"),
+              out=None) -> dict:
         N, W, I = self.n
         bufs = out if out is not None else self.output_buffers(fields)
         d = nalar_decisions()
         for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
                   "i_spare", "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home",
-                  "t_busy", "t_capsum", "ra_kill", "ra_prov"):
+                  "t_busy", "t_capsum", "ra_kill", "ra_prov", "migrate_to", "i_mig_in", "i_mig_out"):
             if k in bufs:
                 setattr(d, k, _ptr(bufs[k]))
         if "t_busy" in bufs:
@@ -434,6 +456,12 @@ class Context:
             if k in res:
                 res[k] = res[k][:d.n_reassign]
         res["n_reassign"] = d.n_reassign
+        if "migrate_to" in res:
+            res["migrate_to"] = res["migrate_to"][:N]
+        for k in ("i_mig_in", "i_mig_out"):
+            if k in res:
+                res[k] = res[k][:I]
+        res["n_migrated"] = d.n_migrated
         if "assign_row" in res:
             res["assign_row"] = res["assign_row"][:d.n_assigned]
             res["assign_inst"] = res["assign_inst"][:d.n_assigned]
