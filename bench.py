@@ -311,8 +311,22 @@ def main():
     ms_ra = timed_epochs(max(args.steps // 4, 10), True)
     ra_out = ctx.fetch(("reassign", "kv"))
     ctx.set_policy_params(reassign=False)
+    # HoL migration (NEXT-1, single rank): the same table with synthetic wait
+    # ages / head-job times (nalar_gen.with_hol_inputs, SPEC delta = 2)
+    mig = {}
+    if world == 1:
+        from nalar_gen import with_hol_inputs
+        sh = with_hol_inputs(s)
+        ctx.set_policy_params(migrate=True, theta_wait=50, theta_head=50, delta=2)
+        ctx.upload(sh)
+        timed_epochs(args.warmup, True)
+        ms_mig = timed_epochs(max(args.steps // 4, 10), True)
+        mo = ctx.fetch(("migrate",))
+        ctx.set_policy_params(migrate=False)
+        ctx.upload(s)
+        mig = {"migrate_on_epoch_us": float(np.mean(ms_mig)) * 1e3, "migrated": int(mo["n_migrated"])}
     next_rows = {"reassign_on_epoch_us": float(np.mean(ms_ra)) * 1e3,
-                 "reassign_commands": int(ra_out["n_reassign"]),
+                 "reassign_commands": int(ra_out["n_reassign"]), **mig,
                  "kv_hints": {k: int(v) for k, v in zip(("none", "retain", "offload", "drop"),
                                                        np.bincount(ra_out["kv_hint"].ravel(), minlength=4))}}
 

@@ -18,10 +18,11 @@ constexpr int kK4Threads = 256;          // assign: one block per resource
 constexpr int kK4Warps = kK4Threads / 32;
 
 // per-row flags produced by the sweep
-enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8 };
+enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8, FL_MIG = 16 };
 
 // indices into the per-epoch counters array (scratch)
-enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_RA_TICKET = 4, C_RA_PAIRS = 5, C_NUM = 8 };
+enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_RA_TICKET = 4, C_RA_PAIRS = 5, C_MIGRATED = 6,
+       C_NUM = 8 };
 
 // per-type statistics of resource reassignment (NEXT-2), written by K4's type
 // blocks; the last K4 block pairs hot with cold types
@@ -69,6 +70,11 @@ struct SweepParams {
     const uint32_t* wf_perm;    // [W]   per block: local workflow indices, largest first (task order)
     uint32_t B, n_types, n_inst, R, levels, policy;
     uint32_t Rh;                // R + T: bucket / histogram resources (the last T: HoL candidates, NEXT-1)
+    // HoL migration candidates (NEXT-1), active when mig_on
+    uint32_t mig_on, theta_wait, theta_head;
+    const uint32_t* f_age;      // [N]
+    const uint32_t* i_head_rem; // [I]
+    int16_t* migrate_to;        // [N] out (-1 here; K5 writes the moves)
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
     uint32_t *g_tlo, *g_thi, *g_ifc, *g_ndp;   // [N] step-transfer scratch for unstaged blocks
@@ -196,6 +202,28 @@ struct FetchParams {
     uint32_t* out_counters;     // mapped host [C_NUM]
     uint32_t R, a_cap;
 };
+
+// K5 HoL migration (NEXT-1, k_migrate.cu); G == 1
+constexpr uint32_t kK5MaxInst = 256;    // instances per type the migration pass supports
+struct MigrateParams {
+    const uint32_t* H;          // [Rh][Lv] (this rank's slot == the sum when G == 1)
+    const uint32_t* tot;        // [Rh]
+    const uint32_t* cnt_rb;     // [Rh][B]
+    const uint32_t* off_rb;
+    const uint32_t* blk_row0;
+    const uint2* items;
+    const uint32_t* type_off;
+    const uint32_t* type_inst;
+    const uint32_t* i_load;     // after K4
+    const uint32_t* i_assigned;
+    const uint32_t* i_head_rem;
+    uint32_t R, Rh, B, n_inst, n_types, levels, theta_head, delta;
+    int16_t* migrate_to;
+    uint32_t* i_mig_in;
+    uint32_t* i_mig_out;
+    uint32_t* counters;
+};
+cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s);
 
 cudaError_t launch_copy_segs(const CopyParams& p, cudaStream_t s);
 cudaError_t launch_fetch(const FetchParams& f, const CopyParams& p, cudaStream_t s);

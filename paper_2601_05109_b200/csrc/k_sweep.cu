@@ -170,7 +170,8 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
 size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
     size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs) +
                align16(4 * ((size_t)wfs + 1)) + align16(4 * (size_t)wfs) +
-               align16(32 * (size_t)wfs) + align16(8 * (size_t)wfs * T);                 // per-workflow tables
+               align16(32 * (size_t)wfs) + align16(8 * (size_t)wfs * T) +
+               align16(8 * (size_t)wfs * T) + align16(8 * (size_t)wfs);                 // per-workflow tables
     if (staged)
         b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
              align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
@@ -234,6 +235,11 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     uint32_t* s_khome = (uint32_t*)q;                        // [nw][T] session home (min pin) -- NEXT-3
     uint32_t* s_klev = s_khome + (size_t)nw * T;             // [nw][T] 1 + max level of live futures
     q += align16(8 * (size_t)nw * T);
+    uint32_t* s_mq = (uint32_t*)q;                           // [nw][T] QUEUED futures (NEXT-1)
+    uint32_t* s_mqrow = s_mq + (size_t)nw * T;               // [nw][T] a QUEUED row | candidate bit
+    q += align16(8 * (size_t)nw * T);
+    uint32_t* s_mrun = (uint32_t*)q;                         // [nw][2] types with a RUNNING future
+    q += align16(8 * (size_t)nw);
 
     // ---- the block's slice of the table: staged in smem by TMA, or in place --
     const uint8_t* st;    // state, type, round, pin, executor: indexed by local row
@@ -326,8 +332,12 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     for (uint32_t t = tid; t < T; t += kK1Threads) s_aff[t] = p.t_aff[t];
     for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
         s_wfp[k] = 0xFFFFFFFFu; s_wfru[k] = 0xFFFFFFFFu; s_khome[k] = 0xFFFFFFFFu; s_klev[k] = 0u;
+        s_mq[k] = 0u; s_mqrow[k] = 0u;
     }
-    for (uint32_t k = tid; k < nw; k += kK1Threads) { s_winfl[2 * k] = 0u; s_winfl[2 * k + 1] = 0u; s_perm[k] = p.wf_perm[w0 + k]; }
+    for (uint32_t k = tid; k < nw; k += kK1Threads) {
+        s_winfl[2 * k] = 0u; s_winfl[2 * k + 1] = 0u; s_mrun[2 * k] = 0u; s_mrun[2 * k + 1] = 0u;
+        s_perm[k] = p.wf_perm[w0 + k];
+    }
     for (uint32_t k = tid; k < 8 * nw; k += kK1Threads) s_agg[k] = 0;
     for (uint32_t k = tid; k < nr; k += kK1Threads) aux[k] = 0;   // step-done flags
     if (tid == 0) {
@@ -881,9 +891,31 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
             else if (doom) status = 4;
             else if (!ready) status = 3;
             else status = elig ? 6u : 5u;
+            // HoL-migration candidates (NEXT-1): a QUEUED
+            // future waiting past theta_wait at an instance whose head job runs
+            // past theta_head; STATEFUL never moves; a SESSION future only as
+            // its session's sole queued work with nothing running (decided in P4)
+            bool mig = false;
+            if (p.mig_on) {
+                if (stf == 1u && aff != 2u) {
+                    const bool c = p.f_age[r0 + f] > p.theta_wait && p.i_head_rem[ex[f]] > p.theta_head;
+                    if (aff == 0u) {
+                        mig = c;
+                    } else {
+                        atomicAdd(&s_mq[wl * T + tyf], 1u);
+                        atomicMax(&s_mqrow[wl * T + tyf], f | (c ? 0x80000000u : 0u));
+                    }
+                }
+                if (stf == 2u && aff == 1u) atomicOr(&s_mrun[2 * wl + (tyf >> 5)], 1u << (tyf & 31u));
+                p.migrate_to[r0 + f] = -1;
+                if (mig) {
+                    atomicAdd(&p.H[(size_t)(R + tyf) * Lv + lv], 1u);
+                    atomicAdd(&s_rcnt[R + tyf], 1u);
+                }
+            }
             const uint32_t g = r0 + f;
             lev[f] = (uint8_t)lv;
-            flg[f] = (uint8_t)(fl | (ready ? FL_READY : 0) | (elig ? FL_ELIG : 0));
+            flg[f] = (uint8_t)(fl | (ready ? FL_READY : 0) | (elig ? FL_ELIG : 0) | (mig ? FL_MIG : 0));
             p.status[g] = (uint8_t)status;
             if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
             p.instance[g] = inst;
@@ -980,6 +1012,13 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         } else if (aff == 1u) {
             f = s_wfru[k];
         }
+        if (p.mig_on && aff == 1u && s_mq[k] == 1u && !((s_mrun[2 * wl + (t >> 5)] >> (t & 31u)) & 1u) &&
+            (s_mqrow[k] & 0x80000000u)) {
+            const uint32_t fm = s_mqrow[k] & 0x7FFFFFFFu;   // the session's sole queued future moves
+            flg[fm] |= FL_MIG;
+            atomicAdd(&p.H[(size_t)(R + t) * Lv + lev[fm]], 1u);
+            atomicAdd(&s_rcnt[R + t], 1u);
+        }
         if (f != 0xFFFFFFFFu) {
             flg[f] |= FL_ELIG;
             p.status[r0 + f] = 6;
@@ -1023,10 +1062,13 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
         }
         __syncthreads();
     }
-    uint32_t n_elig = 0;
     for (uint32_t t0 = 0; t0 < nr; t0 += kK1Threads) {
         const uint32_t f = t0 + tid;
-        const bool el = f < nr && (flg[f] & FL_ELIG);
+        const bool el = f < nr && (flg[f] & (FL_ELIG | FL_MIG));
+        {
+            const uint32_t be = __ballot_sync(0xFFFFFFFFu, f < nr && (flg[f] & FL_ELIG));
+            if (lane == 0 && be) atomicAdd(&s_cnt[1], __popc(be));
+        }
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, el);
         if (lane == 0) s_wc[warp] = __popc(bal);
         __syncthreads();
@@ -1043,28 +1085,30 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                 const uint32_t j = j0 + lane;
                 const bool ok = j < tot;
                 uint32_t r = 0xFFFFFFFFu, ff = 0;
+                bool mg = false;
                 if (ok) {
                     ff = s_list[j];
+                    mg = !(flg[ff] & FL_ELIG);                  // a HoL candidate (NEXT-1)
                     const int pinf = pn[ff];
-                    r = pinf >= 0 ? (uint32_t)pinf : I + ty[ff];
+                    r = mg ? R + ty[ff] : (pinf >= 0 ? (uint32_t)pinf : I + ty[ff]);
                 }
                 const uint32_t peers = __match_any_sync(0xFFFFFFFFu, r);
                 const uint32_t rank = ok ? s_rcnt[r] + __popc(peers & ((1u << lane) - 1u)) : 0u;
                 __syncwarp();
                 if (ok) {
-                    p.items[r0 + s_roff[r] + rank] = make_uint2(r0 + ff, lev[ff]);
+                    p.items[r0 + s_roff[r] + rank] =
+                        make_uint2(r0 + ff, lev[ff] | (mg ? (uint32_t)(ex[ff] + 1) << 16 : 0u));
                     if ((__ffs(peers) - 1) == (int)lane) s_rcnt[r] += __popc(peers);
                 }
                 __syncwarp();
             }
         }
-        n_elig += tot;
         __syncthreads();
     }
     if (bprof && tid == 0) bprof[2] = gtimer();
     if (tid == 0) {
         atomicAdd(&p.counters[C_READY], s_cnt[0]);
-        atomicAdd(&p.counters[C_ELIG], n_elig);
+        atomicAdd(&p.counters[C_ELIG], s_cnt[1]);
         atomicAdd(&p.counters[C_DOOMED], s_cnt[2]);
     }
 }

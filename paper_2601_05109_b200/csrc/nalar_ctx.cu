@@ -103,6 +103,14 @@ struct nalar_ctx {
     uint32_t *d_tbusy = nullptr, *d_tcap = nullptr;
     int16_t *d_rakill = nullptr, *d_raprov = nullptr;
     uint32_t ra_on = 0, u_hi = 80, u_lo = 30, params_gen = 0;
+    // HoL migration (NEXT-1)
+    uint32_t* d_age = nullptr;
+    uint32_t* d_head = nullptr;
+    int16_t* d_migto = nullptr;
+    uint32_t *d_migin = nullptr, *d_migout = nullptr;
+    uint32_t mig_on = 0, theta_wait = 0, theta_head = 0, mig_delta = 2, max_inst_per_type = 0;
+    bool have_mig = false;
+    bool mig_active() const { return mig_on && have_mig; }
     uint8_t *d_kvh = nullptr, *d_kvl = nullptr;
     int16_t* d_kvhome = nullptr;
     uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
@@ -191,7 +199,7 @@ struct Plan {
     size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, wf_perm, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
-    size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov;
+    size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov, age, head, migto, migin, migout;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
     uint32_t Rmax, Rhmax, Bmax;
@@ -251,6 +259,11 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->tcap = L.take<uint32_t>(T);
     p->rakill = L.take<int16_t>(T);
     p->raprov = L.take<int16_t>(T);
+    p->age = L.take<uint32_t>(N);
+    p->head = L.take<uint32_t>(I);
+    p->migto = L.take<int16_t>(N);
+    p->migin = L.take<uint32_t>(I);
+    p->migout = L.take<uint32_t>(I);
     p->iload = L.take<uint32_t>(I);
     p->ispare = L.take<uint32_t>(I);
     p->iasg = L.take<uint32_t>(I);
@@ -367,6 +380,8 @@ int run_k1(nalar_ctx* c, int policy) {
     p.wf_perm = c->d_wf_perm;
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.Rh = c->Rh;
+    p.mig_on = c->mig_active() ? 1u : 0u; p.theta_wait = c->theta_wait; p.theta_head = c->theta_head;
+    p.f_age = c->d_age; p.i_head_rem = c->d_head; p.migrate_to = c->d_migto;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
     p.g_tlo = c->d_gtlo; p.g_thi = c->d_gthi; p.g_ifc = c->d_gifc; p.g_ndp = c->d_gndp; p.g_aux = c->d_gaux;
@@ -454,11 +469,24 @@ int enqueue_second_half(nalar_ctx* c) {
     if (timing) CK(record_ev(c, 2));
     int rc = run_k4(c);
     if (rc) return rc;
+    if (c->mig_active()) {          // K5 HoL migration (NEXT-1), after admission
+        MigrateParams m{};
+        m.H = c->d_x; m.tot = c->d_x + (size_t)c->Rh * c->Lv + c->I;
+        m.cnt_rb = c->d_cnt_rb; m.off_rb = c->d_off_rb; m.blk_row0 = c->d_blk_row0; m.items = c->d_items;
+        m.type_off = c->d_type_off; m.type_inst = c->d_type_inst;
+        m.i_load = c->d_iload; m.i_assigned = c->d_iasg; m.i_head_rem = c->d_head;
+        m.R = c->R; m.Rh = c->Rh; m.B = c->B; m.n_inst = c->I; m.n_types = c->T; m.levels = c->Lv;
+        m.theta_head = c->theta_head; m.delta = c->mig_delta;
+        m.migrate_to = c->d_migto; m.i_mig_in = c->d_migin; m.i_mig_out = c->d_migout; m.counters = c->d_scr;
+        CK(launch_migrate(m, c->stream));
+    }
     if (timing) CK(record_ev(c, 3));
     return NALAR_OK;
 }
 
 int enqueue_epoch(nalar_ctx* c, int policy) {
+    if (c->mig_active() && c->max_inst_per_type > kK5MaxInst)
+        return fail(c, NALAR_E_NOTIMPL, "HoL migration supports <= %u instances per type", kK5MaxInst);
     int rc = enqueue_first_half(c, policy);
     if (!rc) rc = enqueue_collective(c);
     if (!rc) rc = enqueue_second_half(c);
@@ -617,6 +645,8 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_tmin = at<uint16_t>(a, p.tmin); c->d_tmax = at<uint16_t>(a, p.tmax); c->d_tstat = at<TypeStat>(a, p.tstat);
     c->d_tbusy = at<uint32_t>(a, p.tbusy); c->d_tcap = at<uint32_t>(a, p.tcap);
     c->d_rakill = at<int16_t>(a, p.rakill); c->d_raprov = at<int16_t>(a, p.raprov);
+    c->d_age = at<uint32_t>(a, p.age); c->d_head = at<uint32_t>(a, p.head); c->d_migto = at<int16_t>(a, p.migto);
+    c->d_migin = at<uint32_t>(a, p.migin); c->d_migout = at<uint32_t>(a, p.migout);
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
     c->d_items = at<uint2>(a, p.items); c->d_cnt_rb = at<uint32_t>(a, p.cnt_rb); c->d_off_rb = at<uint32_t>(a, p.off_rb);
     c->d_x = at<uint32_t>(a, p.x); c->d_scr = at<uint32_t>(a, p.scr);
@@ -753,12 +783,19 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     CK(h2d(c->d_icap, s->i_cap, 4ull * I));
     CK(h2d(c->d_ibase, s->i_base_load, 4ull * I));
     CK(h2d(c->d_taff, s->t_affinity, T));
+    c->have_mig = s->f_age && s->i_head_rem;
+    if (c->have_mig) {
+        CK(h2d(c->d_age, s->f_age, 4ull * N));
+        CK(h2d(c->d_head, s->i_head_rem, 4ull * I));
+    }
     // instances grouped by type (ascending id), for the assignment pass
     if (trace) tt[2] = now();
     uint32_t* toff = (uint32_t*)(c->h_tab + c->tab_off[0]);
     uint32_t* tinst = (uint32_t*)(c->h_tab + c->tab_off[1]);
     std::fill(toff, toff + T + 1, 0u);
     for (uint32_t i = 0; i < I; ++i) toff[s->i_type[i] + 1]++;
+    c->max_inst_per_type = 0;
+    for (uint32_t t = 0; t < T; ++t) c->max_inst_per_type = std::max(c->max_inst_per_type, toff[t + 1]);
     for (uint32_t t = 0; t < T; ++t) toff[t + 1] += toff[t];
     {
         std::vector<uint32_t> cur(toff, toff + T);
@@ -963,6 +1000,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     noff[W2] = N2; neoff[W2] = E2;
     c->m_wf_id.swap(nid); c->m_wf_off.swap(noff); c->m_wf_eoff.swap(neoff);
     c->N = N2; c->E = E2; c->W = W2;
+    c->have_mig = false;             // HoL inputs are per upload (row indices moved)
     int rc = set_blocks(c, nullptr);
     if (!rc) rc = validate_table(c, err_index, nullptr);
     if (rc) { c->uploaded = false; return rc; }
@@ -1036,12 +1074,19 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     if (!c || !o) return NALAR_E_INVAL;
     if (!c->epoch_done) return fail(c, NALAR_E_STATE, "fetch before epoch");
     cudaStream_t st = c->stream;
+    // without an active migration pass nothing moves: answer on the host
+    const bool mig = c->mig_active();
+    if (!mig) {
+        if (o->migrate_to && o->f_cap >= c->N) std::fill_n(o->migrate_to, c->N, (int16_t)-1);
+        if (o->i_mig_in && o->i_cap >= c->I) memset(o->i_mig_in, 0, 4ull * c->I);
+        if (o->i_mig_out && o->i_cap >= c->I) memset(o->i_mig_out, 0, 4ull * c->I);
+    }
     // Fast path: every requested output buffer is pinned (device-mapped) host
     // memory -> one kernel writes them all, compacting the assignment list on
     // the way, and one synchronisation.
     {
         struct Out { void* h; const void* d; size_t bytes; };
-        const Out outs[16] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
+        const Out outs[19] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
                              {o->depth, c->d_depth, 2ull * c->N}, {o->instance, c->d_inst, 2ull * c->N},
                              {o->new_pin, c->d_newpin, c->N},
                              {o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W},
@@ -1051,7 +1096,10 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
                              {o->kv_level, c->d_kvl, (size_t)c->W * c->T},
                              {o->kv_home, c->d_kvhome, 2ull * c->W * c->T},
                              {o->t_busy, c->d_tbusy, 4ull * c->T}, {o->t_capsum, c->d_tcap, 4ull * c->T},
-                             {o->ra_kill, c->d_rakill, 2ull * c->T}, {o->ra_prov, c->d_raprov, 2ull * c->T}};
+                             {o->ra_kill, c->d_rakill, 2ull * c->T}, {o->ra_prov, c->d_raprov, 2ull * c->T},
+                             {mig ? o->migrate_to : nullptr, c->d_migto, 2ull * c->N},
+                             {mig ? o->i_mig_in : nullptr, c->d_migin, 4ull * c->I},
+                             {mig ? o->i_mig_out : nullptr, c->d_migout, 4ull * c->I}};
         const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
         const bool wbad = o->wf_agg && o->wf_cap < c->W;
         const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
@@ -1086,6 +1134,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
             const uint32_t na = c->h_cnt[C_ASSIGNED];
             o->n_f = c->N; o->n_w = c->W; o->n_i = c->I; o->n_assigned = na;
             o->n_reassign = c->ra_on ? c->h_cnt[C_RA_PAIRS] : 0u;
+            o->n_migrated = mig ? c->h_cnt[C_MIGRATED] : 0u;
             if ((o->assign_row || o->assign_inst) && o->a_cap < na)
                 return fail(c, NALAR_E_SIZE, "output buffer too small");
             return NALAR_OK;
@@ -1103,6 +1152,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     const bool tbad = (o->t_busy || o->t_capsum || o->ra_kill || o->ra_prov) && o->t_cap < c->T;
     if (fbad || wbad || ibad || abad || kbad || tbad) return fail(c, NALAR_E_SIZE, "output buffer too small");
     o->n_reassign = c->ra_on ? c->h_cnt[C_RA_PAIRS] : 0u;
+    o->n_migrated = mig ? c->h_cnt[C_MIGRATED] : 0u;
     auto d2h = [&](void* h, const void* d, size_t bytes) -> cudaError_t {
         return (h && bytes) ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
     };
@@ -1119,6 +1169,11 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     CK(d2h(o->t_capsum, c->d_tcap, 4ull * c->T));
     CK(d2h(o->ra_kill, c->d_rakill, 2ull * c->T));
     CK(d2h(o->ra_prov, c->d_raprov, 2ull * c->T));
+    if (mig) {
+        CK(d2h(o->migrate_to, c->d_migto, 2ull * c->N));
+        CK(d2h(o->i_mig_in, c->d_migin, 4ull * c->I));
+        CK(d2h(o->i_mig_out, c->d_migout, 4ull * c->I));
+    }
     CK(d2h(o->i_load, c->d_iload, 4ull * c->I));
     CK(d2h(o->i_spare, c->d_ispare, 4ull * c->I));
     CK(d2h(o->i_assigned, c->d_iasg, 4ull * c->I));
@@ -1170,9 +1225,15 @@ int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
     CK(cudaMemcpyAsync(c->d_tmin, mn.data(), 2ull * mn.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_tmax, mx.data(), 2ull * mx.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (p->migrate && c->cfg.world > 1)
+        return fail(c, NALAR_E_NOTIMPL, "HoL migration is single-rank (world == 1) in this version");
     c->ra_on = p->reassign ? 1u : 0u;
     c->u_hi = p->u_hi_pct;
     c->u_lo = p->u_lo_pct;
+    c->mig_on = p->migrate ? 1u : 0u;
+    c->theta_wait = p->theta_wait;
+    c->theta_head = p->theta_head;
+    c->mig_delta = p->delta;
     c->params_gen++;                      // epoch graphs bake the parameters in
     return NALAR_OK;
 }
