@@ -494,3 +494,46 @@ int oracle_migrate(const oracle_table* t, const oracle_out* o, const oracle_mig_
     free(backlog); free(blocked); free(cand); free(buf);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* O12 batch coalescing (DESIGN.md Q-batch).             */
+/* "if an agent supports batching ... Nalar can coalesce compatible futures  */
+/* and execute them together" P:261 [§3.4]; `batchable` directive P:250      */
+/* (Table 1); managed state cannot be combined with batchable agents P:576;  */
+/* SPEC schedule_next S:281: greedily coalesces up to max_batch queued       */
+/* futures with identical (agent_type, method) into one Batch, in priority   */
+/* order; compatibility key (agent_type, method) S:341.                       */
+/*   For each instance i of a batchable type (max_batch > 1) and method m:   */
+/*   the futures ASSIGNED to i this epoch with method m, in the O4 order, are */
+/*   cut into consecutive batches of max_batch; batch_head[f] = the row of    */
+/*   its batch's first future; -1 for every other future.                    */
+/* ------------------------------------------------------------------------ */
+int oracle_batch(const oracle_table* t, const oracle_out* o, const oracle_batch_params* p, oracle_batch_out* r) {
+    uint32_t N = t->n_futures, I = t->n_instances, T = t->n_types;
+    for (uint32_t ty = 0; ty < T; ++ty)
+        if (p->t_max_batch[ty] > 1 && t->t_affinity[ty] != A_NONE) return -1;
+    uint32_t* buf = (uint32_t*)malloc(sizeof(uint32_t) * (N ? N : 1));
+    for (uint32_t f = 0; f < N; ++f) r->batch_head[f] = -1;
+    g_level = o->level;
+    uint32_t nb = 0;
+    for (uint32_t i = 0; i < I; ++i) {
+        uint32_t mb = p->t_max_batch[t->i_type[i]];
+        if (mb <= 1) continue;
+        for (uint32_t m = 0; m < 256; ++m) {
+            uint32_t n = 0;
+            for (uint32_t f = 0; f < N; ++f)
+                if (o->status[f] == O_ASSIGNED && o->instance[f] == (int)i &&
+                    (p->f_method ? p->f_method[f] : 0u) == m)
+                    buf[n++] = f;
+            if (!n) continue;
+            qsort(buf, n, sizeof(uint32_t), cmp_order);
+            for (uint32_t k = 0; k < n; ++k) {
+                r->batch_head[buf[k]] = (int32_t)buf[k - k % mb];
+                if (k % mb == 0) nb++;
+            }
+        }
+    }
+    r->n_batches = nb;
+    free(buf);
+    return 0;
+}

@@ -87,6 +87,22 @@ typedef struct {
 
 int oracle_migrate(const oracle_table* t, const oracle_out* o, const oracle_mig_params* p, oracle_mig_out* r);
 
+/* O12 batch coalescing (NEXT-4): per type max_batch (the `batchable`
+ * directive; <= 1 = not batchable), per future its method (the
+ * batch compatibility key with the agent type; NULL = 0). */
+typedef struct {
+    const uint16_t* t_max_batch; /* [T] */
+    const uint8_t*  f_method;    /* [N] or NULL */
+} oracle_batch_params;
+
+typedef struct {
+    int32_t*  batch_head;  /* [N] row of the first future of f's batch, -1 none */
+    uint32_t  n_batches;   /* out */
+} oracle_batch_out;
+
+/* -1 when a batchable type is not of affinity NONE. */
+int oracle_batch(const oracle_table* t, const oracle_out* o, const oracle_batch_params* p, oracle_batch_out* r);
+
 /* O10 from a finished epoch (o from oracle_epoch on the same table). */
 int oracle_reassign(const oracle_table* t, const oracle_out* o, const oracle_ra_params* p, oracle_ra_out* r);
 

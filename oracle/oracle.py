@@ -58,6 +58,14 @@ class _MigOut(C.Structure):
                 ("n_migrated", C.c_uint32)]
 
 
+class _BatchParams(C.Structure):
+    _fields_ = [("t_max_batch", C.c_void_p), ("f_method", C.c_void_p)]
+
+
+class _BatchOut(C.Structure):
+    _fields_ = [("batch_head", C.c_void_p), ("n_batches", C.c_uint32)]
+
+
 _lib = None
 
 
@@ -80,6 +88,8 @@ def _load():
                                          C.POINTER(_RaOut)]
         _lib.oracle_migrate.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_MigParams),
                                         C.POINTER(_MigOut)]
+        _lib.oracle_batch.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_BatchParams),
+                                      C.POINTER(_BatchOut)]
     return _lib
 
 
@@ -104,7 +114,7 @@ def oracle_validate(s, levels: int = 256):
     return rc, err.value
 
 
-def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None, migrate=None) -> dict:
+def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None, migrate=None, batch=None) -> dict:
     """One epoch; ``reassign`` = dict(t_min_inst, t_max_inst, u_hi_pct, u_lo_pct)
     also runs O10 (resource reassignment) on the result."""
     lib = _load()
@@ -152,6 +162,17 @@ def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None, migrate=Non
         out["migrate_to"] = mo["migrate_to"][:N].copy()
         out["i_mig_in"], out["i_mig_out"] = mo["i_mig_in"][:I].copy(), mo["i_mig_out"][:I].copy()
         out["n_migrated"] = ro.n_migrated
+    if batch is not None:               # O12 (NEXT-4) on the finished epoch
+        mb = np.ascontiguousarray(batch["t_max_batch"], np.uint16)
+        meth = batch.get("f_method")
+        meth = None if meth is None else np.ascontiguousarray(meth, np.uint8)
+        bh = np.zeros(max(N, 1), np.int32)
+        prm = _BatchParams(_ptr(mb), _ptr(meth) if meth is not None else None)
+        bo = _BatchOut(_ptr(bh), 0)
+        if lib.oracle_batch(C.byref(t), C.byref(o), C.byref(prm), C.byref(bo)) != 0:
+            raise ValueError("oracle: a batchable type with managed state (PAPER.md:576)")
+        out["batch_head"] = bh[:N].copy()
+        out["n_batches"] = bo.n_batches
     na = o.n_assigned
     out["assign_row"] = out["assign_row"][:na].copy()
     out["assign_inst"] = out["assign_inst"][:na].copy()

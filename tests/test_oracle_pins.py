@@ -657,3 +657,61 @@ def test_hol_invariants_random(seed):
         tg = [i for i in range(s.n_instances) if s.i_type[i] == ty and not blocked[i]]
         if tg:
             assert min(final[i] for i in tg) + dl > final[int(s.f_executor[f])]
+
+
+# --------------------------------------------------------------------------
+# O12 batch coalescing (NEXT-4)
+# --------------------------------------------------------------------------
+def test_batch_spec_example():
+    """batchable, max_batch = 2, three identical-method futures ->
+    a batch of 2, then a batch of 1 -- in priority order (levels 9, 5, 7)."""
+    tb = TableBuilder(i_type=[0], i_cap=[8], i_base_load=[0], t_affinity=[AFF_NONE])
+    for k, prio in enumerate((5, 9, 7)):
+        tb.add_workflow(k + 1, prio, [(PENDING, 0, 0, -1, -1, [])])
+    s = tb.build()
+    o = oracle_epoch(s, "fcfs", batch={"t_max_batch": [2]})
+    assert o["status"].tolist() == [S_ASG] * 3
+    assert o["batch_head"].tolist() == [0, 1, 1] and o["n_batches"] == 2
+    # methods are separate batch keys (S:341): methods (0, 1, 0) -> rows 1 alone
+    o = oracle_epoch(s, "fcfs", batch={"t_max_batch": [2], "f_method": [0, 1, 0]})
+    assert o["batch_head"].tolist() == [2, 1, 2] and o["n_batches"] == 2
+    # not batchable -> nothing
+    o = oracle_epoch(s, "fcfs", batch={"t_max_batch": [1]})
+    assert o["batch_head"].tolist() == [-1, -1, -1] and o["n_batches"] == 0
+
+
+def test_batch_managed_state_rejected():
+    """managed state cannot be combined with batchable agents."""
+    with pytest.raises(ValueError):
+        oracle_epoch(c1(), "srtf", batch={"t_max_batch": [4, 0]})     # type 0 is SESSION
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_batch_properties_random(seed):
+    """Every batch: one instance, one method, size <= max_batch, contiguous in
+    the O4 order of its (instance, method) group, headed by its first member;
+    all but the group's last batch are full; unassigned futures are unbatched."""
+    rng = np.random.default_rng(seed)
+    s = random_table(seed, n_workflows=3 + seed % 6, max_rows=4 + seed % 20, n_types=1 + seed % 3,
+                     inst_per_type=(1, 3), consistent=seed % 2 == 0, max_cap=2 + seed % 9)
+    s.t_affinity[:] = AFF_NONE
+    mb = rng.integers(0, 5, s.n_types)
+    meth = rng.integers(0, 3, s.n_futures)
+    o = oracle_epoch(s, ["fcfs", "srtf", "lpt"][seed % 3], batch={"t_max_batch": mb, "f_method": meth})
+    bh = o["batch_head"]
+    asg = o["status"] == S_ASG
+    inst = o["instance"]
+    assert (bh[~asg] == -1).all()
+    nb = 0
+    for i in range(s.n_instances):
+        m_b = int(mb[s.i_type[i]])
+        for m in range(3):
+            grp = [f for f in range(s.n_futures) if asg[f] and inst[f] == i and meth[f] == m]
+            if m_b <= 1:
+                assert all(bh[f] == -1 for f in grp)
+                continue
+            grp.sort(key=lambda f: (-int(o["level"][f]), f))      # the O4 order
+            for k, f in enumerate(grp):
+                assert bh[f] == grp[k - k % m_b]
+            nb += (len(grp) + m_b - 1) // m_b
+    assert o["n_batches"] == nb
