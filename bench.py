@@ -325,6 +325,18 @@ def main():
         ctx.set_policy_params(migrate=False)
         ctx.upload(s)
         mig = {"migrate_on_epoch_us": float(np.mean(ms_mig)) * 1e3, "migrated": int(mo["n_migrated"])}
+        # batch coalescing (NEXT-4, single rank): max_batch 4 on the NONE-affinity
+        # types, three methods drawn per future
+        sb = s.copy()
+        sb.f_method = np.random.default_rng(3).integers(0, 3, s.n_futures).astype(np.uint8)
+        ctx.set_policy_params(t_max_batch=np.where(s.t_affinity == 0, 4, 0), n_types=s.n_types)
+        ctx.upload(sb)
+        timed_epochs(args.warmup, True)
+        ms_b = timed_epochs(max(args.steps // 4, 10), True)
+        bo = ctx.fetch(("batch",))
+        ctx.set_policy_params()
+        ctx.upload(s)
+        mig.update({"batch_on_epoch_us": float(np.mean(ms_b)) * 1e3, "batches": int(bo["n_batches"])})
     next_rows = {"reassign_on_epoch_us": float(np.mean(ms_ra)) * 1e3,
                  "reassign_commands": int(ra_out["n_reassign"]), **mig,
                  "kv_hints": {k: int(v) for k, v in zip(("none", "retain", "offload", "drop"),

@@ -136,6 +136,9 @@ typedef struct {
      * each instance's head job, in one caller-chosen time unit */
     const uint32_t* f_age;       /* [N]                                      */
     const uint32_t* i_head_rem;  /* [I]                                      */
+    /* batch-coalescing key with the agent type (NEXT-4), may be
+     * NULL (all methods 0)                                                  */
+    const uint8_t*  f_method;    /* [N]                                      */
 } nalar_snapshot;
 
 /* Delta between two epochs of a dynamic workload (SURVEY §8(c) "Delta
@@ -242,6 +245,13 @@ typedef struct {
     uint32_t* i_mig_in;   /* [I] (capacity i_cap)                              */
     uint32_t* i_mig_out;  /* [I]                                               */
     uint32_t  n_migrated; /* out                                               */
+    /* Batch coalescing (only with a max_batch > 1, world
+     * == 1): batch_head[f] = row of the first future of f's batch -- the
+     * futures assigned to one instance this epoch with one method, in
+     * priority order, cut into batches of max_batch (
+     * SPEC S:281) -- or -1.                                                  */
+    int32_t*  batch_head; /* [N] (capacity f_cap)                              */
+    uint32_t  n_batches;  /* out                                               */
 } nalar_decisions;
 
 /* Policy parameters beyond the per-epoch policy (persist on the context;
@@ -270,6 +280,12 @@ typedef struct {
      * the session running.  E_NOTIMPL with world > 1. */
     uint32_t migrate;              /* 0 off, 1 on                                  */
     uint32_t theta_wait, theta_head, delta;
+    /* batch coalescing (NEXT-4): the `batchable` directive as a per-type
+     * max_batch (<= 1: not batchable; Table 1).  A batchable type
+     * must have affinity NONE ("cannot be combined with batchable agents",
+     * PAPER.md:576): the epoch returns E_INVAL otherwise.  E_NOTIMPL with
+     * world > 1. */
+    const uint16_t* t_max_batch;   /* [n_types] or NULL (no batching)              */
 } nalar_policy_params;
 
 /* Copies p (host arrays borrowed for the call).  E_INVAL on u_lo > u_hi or

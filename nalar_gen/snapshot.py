@@ -71,15 +71,17 @@ class Snapshot:
     # predicted remaining time of each instance's head job (one time unit)
     f_age: np.ndarray = None
     i_head_rem: np.ndarray = None
+    # optional batch-coalescing key with the agent type (NEXT-4), u8
+    f_method: np.ndarray = None
 
     def __post_init__(self):
         for f in fields(self):
             if f.name in _DTYPES:
                 v = np.ascontiguousarray(getattr(self, f.name), dtype=_DTYPES[f.name])
                 setattr(self, f.name, v)
-        for k in ("f_age", "i_head_rem"):
+        for k, dt in (("f_age", np.uint32), ("i_head_rem", np.uint32), ("f_method", np.uint8)):
             if getattr(self, k) is not None:
-                setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=np.uint32))
+                setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=dt))
 
     # sizes --------------------------------------------------------------
     @property
@@ -112,7 +114,8 @@ class Snapshot:
         kw = {k: v.copy() for k, v in self.arrays().items()}
         return Snapshot(global_row_base=self.global_row_base, name=self.name, **kw,
                         f_age=None if self.f_age is None else self.f_age.copy(),
-                        i_head_rem=None if self.i_head_rem is None else self.i_head_rem.copy())
+                        i_head_rem=None if self.i_head_rem is None else self.i_head_rem.copy(),
+                        f_method=None if self.f_method is None else self.f_method.copy())
 
     # data-layout utilities (no method arithmetic) -------------------------
     def slice_workflows(self, w0: int, w1: int) -> "Snapshot":
@@ -138,7 +141,8 @@ class Snapshot:
             t_affinity=self.t_affinity, global_row_base=self.global_row_base + r0,
             name=f"{self.name}[w{w0}:{w1}]",
             f_age=None if self.f_age is None else self.f_age[r0:r1],
-            i_head_rem=self.i_head_rem)
+            i_head_rem=self.i_head_rem,
+            f_method=None if self.f_method is None else self.f_method[r0:r1])
 
     def save(self, path: str) -> None:
         np.savez(path, global_row_base=np.uint64(self.global_row_base), **self.arrays())

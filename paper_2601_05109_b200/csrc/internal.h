@@ -22,7 +22,7 @@ enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8, FL_MIG
 
 // indices into the per-epoch counters array (scratch)
 enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_RA_TICKET = 4, C_RA_PAIRS = 5, C_MIGRATED = 6,
-       C_NUM = 8 };
+       C_BATCHES = 7, C_NUM = 8 };
 
 // per-type statistics of resource reassignment (NEXT-2), written by K4's type
 // blocks; the last K4 block pairs hot with cold types
@@ -75,6 +75,7 @@ struct SweepParams {
     const uint32_t* f_age;      // [N]
     const uint32_t* i_head_rem; // [I]
     int16_t* migrate_to;        // [N] out (-1 here; K5 writes the moves)
+    int32_t* batch_head;        // [N] out when batching is on (-1 here; K6 writes the batches)
     uint32_t fixed_smem;        // bytes of fixed smem (carve offset of staged area)
     uint8_t* g_flags;           // [N] flags scratch for unstaged blocks
     uint32_t *g_tlo, *g_thi, *g_ifc, *g_ndp;   // [N] step-transfer scratch for unstaged blocks
@@ -224,6 +225,22 @@ struct MigrateParams {
     uint32_t* counters;
 };
 cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s);
+
+// K6 batch coalescing (NEXT-4, k_batch.cu); G == 1
+struct BatchParams {
+    const uint8_t* i_type;
+    const uint16_t* t_max_batch;   // [T]
+    const uint8_t* f_method;       // [N] or null
+    const uint8_t* level;          // [N]
+    const uint32_t* n_adm;         // [R] admitted per resource
+    const uint32_t* tot_loc;       // [R] region sizes
+    const uint32_t* arow;
+    const int16_t* ainst;
+    uint32_t n_inst;
+    int32_t* batch_head;           // [N] out (-1 preset by K1)
+    uint32_t* counters;
+};
+cudaError_t launch_batch(const BatchParams& p, cudaStream_t s);
 
 cudaError_t launch_copy_segs(const CopyParams& p, cudaStream_t s);
 cudaError_t launch_fetch(const FetchParams& f, const CopyParams& p, cudaStream_t s);

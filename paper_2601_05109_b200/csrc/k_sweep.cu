@@ -908,6 +908,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
                 }
                 if (stf == 2u && aff == 1u) atomicOr(&s_mrun[2 * wl + (tyf >> 5)], 1u << (tyf & 31u));
                 p.migrate_to[r0 + f] = -1;
+            }
+            if (p.batch_head) p.batch_head[r0 + f] = -1;
+            if (p.mig_on) {
                 if (mig) {
                     atomicAdd(&p.H[(size_t)(R + tyf) * Lv + lv], 1u);
                     atomicAdd(&s_rcnt[R + tyf], 1u);

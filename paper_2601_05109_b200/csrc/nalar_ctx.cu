@@ -110,6 +110,13 @@ struct nalar_ctx {
     uint32_t *d_migin = nullptr, *d_migout = nullptr;
     uint32_t mig_on = 0, theta_wait = 0, theta_head = 0, mig_delta = 2, max_inst_per_type = 0;
     bool have_mig = false;
+    // batch coalescing (NEXT-4)
+    uint16_t* d_tmaxb = nullptr;
+    uint8_t* d_method = nullptr;
+    int32_t* d_bhead = nullptr;
+    bool batch_on = false, have_method = false;
+    std::vector<uint16_t> h_tmaxb;
+    std::vector<uint8_t> h_taff;      // affinities of the uploaded table
     bool mig_active() const { return mig_on && have_mig; }
     uint8_t *d_kvh = nullptr, *d_kvl = nullptr;
     int16_t* d_kvhome = nullptr;
@@ -200,6 +207,7 @@ struct Plan {
     size_t blk_wf, blk_row0, blk_edge0, blk_staged, wf_perm, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov, age, head, migto, migin, migout;
+    size_t tmaxb, method, bhead;
     size_t items, cnt_rb, off_rb, x, scr, err;
     size_t x_words, total;
     uint32_t Rmax, Rhmax, Bmax;
@@ -264,6 +272,9 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->migto = L.take<int16_t>(N);
     p->migin = L.take<uint32_t>(I);
     p->migout = L.take<uint32_t>(I);
+    p->tmaxb = L.take<uint16_t>(T);
+    p->method = L.take<uint8_t>(N);
+    p->bhead = L.take<int32_t>(N);
     p->iload = L.take<uint32_t>(I);
     p->ispare = L.take<uint32_t>(I);
     p->iasg = L.take<uint32_t>(I);
@@ -382,6 +393,7 @@ int run_k1(nalar_ctx* c, int policy) {
     p.Rh = c->Rh;
     p.mig_on = c->mig_active() ? 1u : 0u; p.theta_wait = c->theta_wait; p.theta_head = c->theta_head;
     p.f_age = c->d_age; p.i_head_rem = c->d_head; p.migrate_to = c->d_migto;
+    p.batch_head = c->batch_on ? c->d_bhead : nullptr;
     p.fixed_smem = (uint32_t)c->fixed_smem;
     p.g_flags = c->d_gflags;
     p.g_tlo = c->d_gtlo; p.g_thi = c->d_gthi; p.g_ifc = c->d_gifc; p.g_ndp = c->d_gndp; p.g_aux = c->d_gaux;
@@ -480,11 +492,23 @@ int enqueue_second_half(nalar_ctx* c) {
         m.migrate_to = c->d_migto; m.i_mig_in = c->d_migin; m.i_mig_out = c->d_migout; m.counters = c->d_scr;
         CK(launch_migrate(m, c->stream));
     }
+    if (c->batch_on) {              // K6 batch coalescing (NEXT-4), after admission
+        BatchParams bp{};
+        bp.i_type = c->d_itype; bp.t_max_batch = c->d_tmaxb; bp.f_method = c->have_method ? c->d_method : nullptr;
+        bp.level = c->d_level; bp.n_adm = c->d_scr + C_NUM; bp.tot_loc = c->d_scr + C_NUM + c->Rmax;
+        bp.arow = c->d_arow; bp.ainst = c->d_ainst; bp.n_inst = c->I;
+        bp.batch_head = c->d_bhead; bp.counters = c->d_scr;
+        CK(launch_batch(bp, c->stream));
+    }
     if (timing) CK(record_ev(c, 3));
     return NALAR_OK;
 }
 
 int enqueue_epoch(nalar_ctx* c, int policy) {
+    if (c->batch_on)
+        for (uint32_t t = 0; t < c->T && t < c->h_tmaxb.size(); ++t)
+            if (c->h_tmaxb[t] > 1 && c->h_taff[t] != NALAR_AFF_NONE)
+                return fail(c, NALAR_E_INVAL, "type %u: batchable with managed state (PAPER.md:576)", t);
     if (c->mig_active() && c->max_inst_per_type > kK5MaxInst)
         return fail(c, NALAR_E_NOTIMPL, "HoL migration supports <= %u instances per type", kK5MaxInst);
     int rc = enqueue_first_half(c, policy);
@@ -647,6 +671,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_rakill = at<int16_t>(a, p.rakill); c->d_raprov = at<int16_t>(a, p.raprov);
     c->d_age = at<uint32_t>(a, p.age); c->d_head = at<uint32_t>(a, p.head); c->d_migto = at<int16_t>(a, p.migto);
     c->d_migin = at<uint32_t>(a, p.migin); c->d_migout = at<uint32_t>(a, p.migout);
+    c->d_tmaxb = at<uint16_t>(a, p.tmaxb); c->d_method = at<uint8_t>(a, p.method); c->d_bhead = at<int32_t>(a, p.bhead);
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
     c->d_items = at<uint2>(a, p.items); c->d_cnt_rb = at<uint32_t>(a, p.cnt_rb); c->d_off_rb = at<uint32_t>(a, p.off_rb);
     c->d_x = at<uint32_t>(a, p.x); c->d_scr = at<uint32_t>(a, p.scr);
@@ -784,6 +809,9 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     CK(h2d(c->d_ibase, s->i_base_load, 4ull * I));
     CK(h2d(c->d_taff, s->t_affinity, T));
     c->have_mig = s->f_age && s->i_head_rem;
+    c->have_method = s->f_method != nullptr;
+    c->h_taff.assign(s->t_affinity, s->t_affinity + T);
+    if (c->have_method) CK(h2d(c->d_method, s->f_method, N));
     if (c->have_mig) {
         CK(h2d(c->d_age, s->f_age, 4ull * N));
         CK(h2d(c->d_head, s->i_head_rem, 4ull * I));
@@ -1081,12 +1109,13 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
         if (o->i_mig_in && o->i_cap >= c->I) memset(o->i_mig_in, 0, 4ull * c->I);
         if (o->i_mig_out && o->i_cap >= c->I) memset(o->i_mig_out, 0, 4ull * c->I);
     }
+    if (!c->batch_on && o->batch_head && o->f_cap >= c->N) std::fill_n(o->batch_head, c->N, (int32_t)-1);
     // Fast path: every requested output buffer is pinned (device-mapped) host
     // memory -> one kernel writes them all, compacting the assignment list on
     // the way, and one synchronisation.
     {
         struct Out { void* h; const void* d; size_t bytes; };
-        const Out outs[19] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
+        const Out outs[20] = {{o->status, c->d_status, c->N}, {o->level, c->d_level, c->N},
                              {o->depth, c->d_depth, 2ull * c->N}, {o->instance, c->d_inst, 2ull * c->N},
                              {o->new_pin, c->d_newpin, c->N},
                              {o->wf_agg, c->d_wfagg, 4ull * NALAR_WF_AGG_FIELDS * c->W},
@@ -1099,7 +1128,8 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
                              {o->ra_kill, c->d_rakill, 2ull * c->T}, {o->ra_prov, c->d_raprov, 2ull * c->T},
                              {mig ? o->migrate_to : nullptr, c->d_migto, 2ull * c->N},
                              {mig ? o->i_mig_in : nullptr, c->d_migin, 4ull * c->I},
-                             {mig ? o->i_mig_out : nullptr, c->d_migout, 4ull * c->I}};
+                             {mig ? o->i_mig_out : nullptr, c->d_migout, 4ull * c->I},
+                             {c->batch_on ? o->batch_head : nullptr, c->d_bhead, 4ull * c->N}};
         const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
         const bool wbad = o->wf_agg && o->wf_cap < c->W;
         const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
@@ -1135,6 +1165,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
             o->n_f = c->N; o->n_w = c->W; o->n_i = c->I; o->n_assigned = na;
             o->n_reassign = c->ra_on ? c->h_cnt[C_RA_PAIRS] : 0u;
             o->n_migrated = mig ? c->h_cnt[C_MIGRATED] : 0u;
+            o->n_batches = c->batch_on ? c->h_cnt[C_BATCHES] : 0u;
             if ((o->assign_row || o->assign_inst) && o->a_cap < na)
                 return fail(c, NALAR_E_SIZE, "output buffer too small");
             return NALAR_OK;
@@ -1153,6 +1184,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     if (fbad || wbad || ibad || abad || kbad || tbad) return fail(c, NALAR_E_SIZE, "output buffer too small");
     o->n_reassign = c->ra_on ? c->h_cnt[C_RA_PAIRS] : 0u;
     o->n_migrated = mig ? c->h_cnt[C_MIGRATED] : 0u;
+    o->n_batches = c->batch_on ? c->h_cnt[C_BATCHES] : 0u;
     auto d2h = [&](void* h, const void* d, size_t bytes) -> cudaError_t {
         return (h && bytes) ? cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
     };
@@ -1174,6 +1206,7 @@ int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
         CK(d2h(o->i_mig_in, c->d_migin, 4ull * c->I));
         CK(d2h(o->i_mig_out, c->d_migout, 4ull * c->I));
     }
+    if (c->batch_on) CK(d2h(o->batch_head, c->d_bhead, 4ull * c->N));
     CK(d2h(o->i_load, c->d_iload, 4ull * c->I));
     CK(d2h(o->i_spare, c->d_ispare, 4ull * c->I));
     CK(d2h(o->i_assigned, c->d_iasg, 4ull * c->I));
@@ -1227,6 +1260,18 @@ int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
     CK(cudaStreamSynchronize(c->stream));
     if (p->migrate && c->cfg.world > 1)
         return fail(c, NALAR_E_NOTIMPL, "HoL migration is single-rank (world == 1) in this version");
+    bool batch = false;
+    std::vector<uint16_t> mbt(c->cfg.max_types, 0);
+    for (uint32_t t = 0; p->t_max_batch && t < p->n_types; ++t) {
+        mbt[t] = p->t_max_batch[t];
+        batch |= mbt[t] > 1;
+    }
+    if (batch && c->cfg.world > 1)
+        return fail(c, NALAR_E_NOTIMPL, "batch coalescing is single-rank (world == 1) in this version");
+    CK(cudaMemcpyAsync(c->d_tmaxb, mbt.data(), 2ull * mbt.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->batch_on = batch;
+    c->h_tmaxb = mbt;
     c->ra_on = p->reassign ? 1u : 0u;
     c->u_hi = p->u_hi_pct;
     c->u_lo = p->u_lo_pct;

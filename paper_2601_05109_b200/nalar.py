@@ -52,7 +52,7 @@ class nalar_snapshot(C.Structure):
                 ("f_executor", C.c_void_p), ("f_pin", C.c_void_p), ("f_edge_off", C.c_void_p),
                 ("edges", C.c_void_p), ("i_type", C.c_void_p), ("i_cap", C.c_void_p),
                 ("i_base_load", C.c_void_p), ("t_affinity", C.c_void_p),
-                ("f_age", C.c_void_p), ("i_head_rem", C.c_void_p)]
+                ("f_age", C.c_void_p), ("i_head_rem", C.c_void_p), ("f_method", C.c_void_p)]
 
 
 class nalar_decisions(C.Structure):
@@ -69,14 +69,14 @@ class nalar_decisions(C.Structure):
                 ("t_busy", C.c_void_p), ("t_capsum", C.c_void_p), ("ra_kill", C.c_void_p),
                 ("ra_prov", C.c_void_p), ("t_cap", C.c_uint32), ("n_reassign", C.c_uint32),
                 ("migrate_to", C.c_void_p), ("i_mig_in", C.c_void_p), ("i_mig_out", C.c_void_p),
-                ("n_migrated", C.c_uint32)]
+                ("n_migrated", C.c_uint32), ("batch_head", C.c_void_p), ("n_batches", C.c_uint32)]
 
 
 class nalar_policy_params(C.Structure):
     _fields_ = [("reassign", C.c_uint32), ("u_hi_pct", C.c_uint32), ("u_lo_pct", C.c_uint32),
                 ("t_min_inst", C.c_void_p), ("t_max_inst", C.c_void_p), ("n_types", C.c_uint32),
                 ("migrate", C.c_uint32), ("theta_wait", C.c_uint32), ("theta_head", C.c_uint32),
-                ("delta", C.c_uint32)]
+                ("delta", C.c_uint32), ("t_max_batch", C.c_void_p)]
 
 
 class nalar_delta(C.Structure):
@@ -202,11 +202,11 @@ def snapshot_struct(s) -> tuple:
                                                "f_round", "f_executor", "f_pin", "f_edge_off",
                                                "edges", "i_type", "i_cap", "i_base_load",
                                                "t_affinity")])
-    # optional HoL-migration inputs (NEXT-1)
-    for k in ("f_age", "i_head_rem"):
+    # optional HoL-migration inputs (NEXT-1) and batch methods (NEXT-4)
+    for k, dt in (("f_age", np.uint32), ("i_head_rem", np.uint32), ("f_method", np.uint8)):
         v = getattr(s, k, None)
         if v is not None:
-            v = np.ascontiguousarray(v, np.uint32)
+            v = np.ascontiguousarray(v, dt)
             a = dict(a)
             a[k] = v
             setattr(st, k, _ptr(v))
@@ -378,22 +378,26 @@ class Context:
 
     def set_policy_params(self, reassign=False, u_hi_pct=80, u_lo_pct=30, t_min_inst=None,
                           t_max_inst=None, n_types=None, migrate=False, theta_wait=0, theta_head=0,
-                          delta=2) -> None:
+                          delta=2, t_max_batch=None) -> None:
         """Resource reassignment (NEXT-2; SPEC defaults u_hi 80 %, u_lo 30 %) and
         HoL migration (NEXT-1; SPEC default delta = 2 jobs)."""
         mn = None if t_min_inst is None else np.ascontiguousarray(t_min_inst, np.uint16)
         mx = None if t_max_inst is None else np.ascontiguousarray(t_max_inst, np.uint16)
+        mbt = None if t_max_batch is None else np.ascontiguousarray(t_max_batch, np.uint16)
+        self._mbt = mbt
         nt = n_types if n_types is not None else (len(mn) if mn is not None else
-                                                  (len(mx) if mx is not None else 0))
+                                                  (len(mx) if mx is not None else
+                                                   (len(mbt) if mbt is not None else 0)))
         p = nalar_policy_params(int(bool(reassign)), int(u_hi_pct), int(u_lo_pct),
                                 _ptr(mn) if mn is not None else None,
                                 _ptr(mx) if mx is not None else None, int(nt), int(bool(migrate)),
-                                int(theta_wait), int(theta_head), int(delta))
+                                int(theta_wait), int(theta_head), int(delta),
+                                _ptr(mbt) if mbt is not None else None)
         _check(self.h, _lib.nalar_set_policy_params(self.h, C.byref(p)), "set_policy_params")
 
     def output_buffers(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg",
                                      "i_load", "i_spare", "i_assigned", "assign", "kv", "reassign",
-                                     "migrate"),
+                                     "migrate", "batch"),
                        alloc=None):
         """Host buffers for fetch(); ``alloc(n, dtype)`` may return pinned memory."""
         N, W, I = self.n
@@ -408,6 +412,8 @@ class Context:
             out["kv_hint"] = alloc(W * T, np.uint8)
             out["kv_level"] = alloc(W * T, np.uint8)
             out["kv_home"] = alloc(W * T, np.int16)
+        if "batch" in fields:
+            out["batch_head"] = alloc(max(N, 1), np.int32)
         if "migrate" in fields:
             out["migrate_to"] = alloc(max(N, 1), np.int16)
             out["i_mig_in"] = alloc(max(I, 1), np.uint32)
@@ -424,14 +430,15 @@ class Context:
         return out
 
     def fetch(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
-                            "i_spare", "i_assigned", "assign", "kv", "reassign", "migrate"),
+                            "i_spare", "i_assigned", "assign", "kv", "reassign", "migrate", "batch"),
               out=None) -> dict:
         N, W, I = self.n
         bufs = out if out is not None else self.output_buffers(fields)
         d = nalar_decisions()
         for k in ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
                   "i_spare", "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home",
-                  "t_busy", "t_capsum", "ra_kill", "ra_prov", "migrate_to", "i_mig_in", "i_mig_out"):
+                  "t_busy", "t_capsum", "ra_kill", "ra_prov", "migrate_to", "i_mig_in", "i_mig_out",
+                  "batch_head"):
             if k in bufs:
                 setattr(d, k, _ptr(bufs[k]))
         if "t_busy" in bufs:
@@ -462,6 +469,9 @@ class Context:
             if k in res:
                 res[k] = res[k][:I]
         res["n_migrated"] = d.n_migrated
+        if "batch_head" in res:
+            res["batch_head"] = res["batch_head"][:N]
+        res["n_batches"] = d.n_batches
         if "assign_row" in res:
             res["assign_row"] = res["assign_row"][:d.n_assigned]
             res["assign_inst"] = res["assign_inst"][:d.n_assigned]
