@@ -57,6 +57,7 @@ NcclApi g_nccl;
 thread_local std::string g_create_err;   // nalar_last_error(NULL) after a failed nalar_create
 
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
+constexpr double kLongWeight = 1.0;             // cost per row of a long workflow (partition)
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
 constexpr uint32_t kMaxBlocks = 16384;
 constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tables
@@ -166,6 +167,8 @@ struct nalar_ctx {
     std::vector<uint64_t> m_wf_id;
     std::vector<uint32_t> m_wf_off, m_wf_eoff;
     std::vector<uint32_t> m_perm;          // per-block task order (set_blocks)
+    bool blocks_valid = false;              // device block tables match m_wf_off / m_wf_eoff
+    uint32_t blocks_T = 0;
     bool assign_valid = false;        // last epoch's assignment regions match the table
     Key last_key{};
     bool last_key_set = false;
@@ -349,8 +352,25 @@ void destroy_graphs(nalar_ctx* c) {
 // wf_off[W+1]: first row of each workflow; wf_eoff[W+1]: first edge of each workflow
 void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, std::vector<uint32_t>& bw,
                std::vector<uint32_t>& br, std::vector<uint32_t>& be, std::vector<uint8_t>& bs, size_t* max_smem) {
-    const uint32_t W = c->W, N = c->N;
-    uint32_t target = std::max<uint32_t>(64u, (N + kSmSplit - 1) / kSmSplit);
+    const uint32_t W = c->W;
+    // balance by estimated cost, not rows: a long workflow's rows cost more
+    // (transfer + compose) and its compose chain is serial, so its block takes
+    // fewer other rows
+    static const double long_w = [] {
+        const char* e = getenv("NALAR_LONG_WEIGHT");
+        return e ? atof(e) : kLongWeight;
+    }();
+    auto cost = [&](uint32_t w) {
+        const uint32_t wr = wf_off[w + 1] - wf_off[w];
+        return wr >= 32u * kLongSteps ? (uint64_t)(wr * long_w) : (uint64_t)wr;
+    };
+    uint64_t total = 0;
+    for (uint32_t w = 0; w < W; ++w) total += cost(w);
+    // fill the SMs: the greedy cut overshoots each block by part of a workflow,
+    // so start below total / SMs and grow the target until the blocks fit
+    static const bool fill = [] { const char* e = getenv("NALAR_FILL_SMS"); return !e || atoi(e) != 0; }();
+    const uint64_t even = std::max<uint64_t>(64u, (total + kSmSplit - 1) / kSmSplit);
+    uint64_t target = fill ? std::max<uint64_t>(64u, even * 4 / 5) : even;
     for (;;) {
         bw.clear(); br.clear(); be.clear(); bs.clear();
         size_t mx = 0;
@@ -358,6 +378,7 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
         while (w < W) {
             const uint32_t ws = w;
             uint32_t rows = 0;
+            uint64_t cst = 0;
             while (w < W) {
                 const uint32_t wr = wf_off[w + 1] - wf_off[w];
                 const uint32_t e_if = wf_eoff[w + 1] - wf_eoff[ws];
@@ -365,8 +386,9 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
                                w - ws + 1 > kMaxWfPerBlock))
                     break;
                 rows += wr;
+                cst += cost(w);
                 ++w;
-                if (rows >= target) break;
+                if (cst >= target) break;
             }
             const uint32_t ra = wf_off[ws], rb = wf_off[w];
             const size_t need_st = k1_block_smem(rb - ra, wf_eoff[w] - wf_eoff[ws], w - ws, c->T, true);
@@ -375,8 +397,9 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
             bw.push_back(ws); br.push_back(ra); be.push_back(wf_eoff[ws]); bs.push_back(staged ? 1 : 0);
         }
         bw.push_back(W); br.push_back(wf_off[W]); be.push_back(wf_eoff[W]);
-        if (bw.size() - 1 <= c->Bmax) { *max_smem = mx; return; }
-        target *= 2;
+        const size_t nb = bw.size() - 1;
+        if (nb <= c->Bmax && (nb <= kSmSplit || target >= 2 * even)) { *max_smem = mx; return; }
+        target = target < even ? target * 103 / 100 + 1 : target * 2;
     }
 }
 
@@ -784,10 +807,20 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     c->N = N; c->E = E; c->W = W; c->I = I; c->T = T; c->R = I + T; c->Rh = I + 2 * T;
     c->assign_valid = false;
     // host mirror of the workflow layout (delta mode re-partitions from it)
+    // the K1 block partition depends only on the workflow layout (row and edge
+    // offsets) and T: a steady-state controller re-uploading tables of the same
+    // shape keeps its block tables on the device
+    bool same_layout = c->blocks_valid && c->blocks_T == T && c->m_wf_off.size() == (size_t)W + 1 &&
+                       std::equal(s->wf_fut_off, s->wf_fut_off + W + 1, c->m_wf_off.begin());
+    for (uint32_t w = 0; same_layout && w <= W; ++w)
+        same_layout = c->m_wf_eoff[w] == s->f_edge_off[s->wf_fut_off[w]];
+    c->blocks_valid = false;                 // until the tables below are in place
     c->m_wf_id.assign(s->wf_id, s->wf_id + W);
-    c->m_wf_off.assign(s->wf_fut_off, s->wf_fut_off + W + 1);
-    c->m_wf_eoff.resize(W + 1);
-    for (uint32_t w = 0; w <= W; ++w) c->m_wf_eoff[w] = s->f_edge_off[s->wf_fut_off[w]];
+    if (!same_layout) {
+        c->m_wf_off.assign(s->wf_fut_off, s->wf_fut_off + W + 1);
+        c->m_wf_eoff.resize(W + 1);
+        for (uint32_t w = 0; w <= W; ++w) c->m_wf_eoff[w] = s->f_edge_off[s->wf_fut_off[w]];
+    }
 
     if (trace) tt[1] = now();
     cudaStream_t st = c->stream;
@@ -831,9 +864,11 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     }
     CK(cb.add_dev(c->h_tab_dev + c->tab_off[0], c->d_type_off, 4ull * (T + 1)));
     CK(cb.add_dev(c->h_tab_dev + c->tab_off[1], c->d_type_inst, 4ull * I));
-    int rc = set_blocks(c, &cb);
+    int rc = same_layout ? NALAR_OK : set_blocks(c, &cb);
     if (rc) return rc;
     CK(cb.flush());
+    c->blocks_valid = true;
+    c->blocks_T = T;
     if (trace) tt[3] = now();
     rc = validate_table(c, err_row, nullptr);
     if (trace) {

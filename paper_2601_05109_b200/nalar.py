@@ -338,8 +338,21 @@ class Context:
         except Exception:
             pass
 
+    _SNAP_FIELDS = ("wf_id", "wf_fut_off", "wf_prio", "f_state", "f_type", "f_round", "f_executor",
+                    "f_pin", "f_edge_off", "edges", "i_type", "i_cap", "i_base_load", "t_affinity",
+                    "f_age", "i_head_rem", "f_method")
+
     def upload(self, s) -> None:
-        st, keep = snapshot_struct(s)
+        # the marshalled struct is reused while the snapshot holds the same array
+        # objects (they stay referenced by the cache, so their ids are stable)
+        key = (id(s), int(getattr(s, "global_row_base", 0)),
+               tuple(id(getattr(s, k, None)) for k in self._SNAP_FIELDS))
+        cached = getattr(self, "_snap_cache", None)
+        if cached is not None and cached[0] == key:
+            st, keep = cached[1], cached[2]
+        else:
+            st, keep = snapshot_struct(s)
+            self._snap_cache = (key, st, (keep, s))
         rc, row = nalar_snapshot_upload(self.h, st)
         if rc:
             e = NalarError(rc, f"upload: {nalar_last_error(self.h)}")
