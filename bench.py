@@ -171,13 +171,23 @@ def c3_dynamic(nalar, device, epochs, warm=450, seed=1):
     sim = RouterSim(seed)
     sim.warmup(warm)
     s = sim.snapshot()
+    import torch
     ctx = nalar.Context(200000, 400000, 20000, 32, 4, device=device)
     ctx.upload(s)
+    keep = []
+
+    def pinned(n, dt):                   # reservation-sized pinned outputs: the one-kernel fetch
+        t = torch.empty(max(n * np.dtype(dt).itemsize, 1), dtype=torch.uint8, pin_memory=True)
+        keep.append(t)
+        return t.numpy()[:n * np.dtype(dt).itemsize].view(dt)
+    outb = {"new_pin": pinned(200000, np.uint8), "assign_row": pinned(200000, np.uint32),
+            "assign_inst": pinned(200000, np.int16)}
     lat, live, app, upd, ret = [], [], [], [], []
     for k in range(epochs):
         t0 = time.perf_counter()
         ctx.epoch("srtf")
-        r = ctx.fetch(("new_pin", "assign"))
+        r = ctx.fetch(("new_pin", "assign"), out=outb)
+        r["new_pin"] = r["new_pin"][:ctx.n[0]]
         t1 = time.perf_counter()
         d = sim.step(r["assign_row"], r["assign_inst"], r["new_pin"])
         t2 = time.perf_counter()
@@ -400,6 +410,20 @@ def main():
         n_asg = r["n_assigned"]
         if i >= 3:
             e2e_t.append(dt)
+    # where the e2e step goes (separately timed, wall clock, same buffers)
+    parts = {"upload": [], "epoch_sync": [], "fetch": []}
+    for i in range(3 + min(args.e2e_steps, 20)):
+        t0 = time.perf_counter()
+        ctx.upload(sp)
+        t1 = time.perf_counter()
+        ctx.epoch(pol)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        ctx.fetch(("status", "instance", "assign"), out=outb)
+        t3 = time.perf_counter()
+        if i >= 3:
+            parts["upload"].append(t1 - t0); parts["epoch_sync"].append(t2 - t1); parts["fetch"].append(t3 - t2)
+    e2e_parts = {k + "_us_p50": float(np.median(v) * 1e6) for k, v in parts.items()}
     et = torch.tensor(e2e_t, dtype=torch.float64)
     if world > 1:
         et = et.cuda()
@@ -422,7 +446,7 @@ def main():
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": dom_b, "peak_source": peak_src},
             "e2e": {"value": total_fut / e2e_mean, "unit": "futures/s", "ms_per_step": e2e_mean * 1e3,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "parts": e2e_parts},
             # per epoch: k_zero (exchange buffer + counters), k1_sweep, k4_assign
             "gpu_launches": 3 * args.steps,
             "next_rows": next_rows,

@@ -37,7 +37,24 @@ struct TypeStat {
 size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
 // bytes of K1 shared memory that scale with a block's workflows (and, when
 // staged, with its rows / edges)
-size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged);
+// (inline: the host partition evaluates it once per workflow per cut)
+__host__ __device__ inline size_t k1_align16(size_t x) { return (x + 15) & ~(size_t)15; }
+inline size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
+    auto align16 = k1_align16;
+
+    size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs) +
+               align16(4 * ((size_t)wfs + 1)) + align16(4 * (size_t)wfs) +
+               align16(32 * (size_t)wfs) + align16(8 * (size_t)wfs * T) +
+               align16(8 * (size_t)wfs * T) + align16(8 * (size_t)wfs);                 // per-workflow tables
+    if (staged)
+        b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
+             align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
+             align16(2 * (size_t)rows) + 2 * align16(rows) +
+             4 * align16(4 * (size_t)rows) + align16(2 * (size_t)rows);                // step transfers
+    return b;
+}
+
+
 
 struct ValidateParams {
     const uint32_t* wf_fut_off;

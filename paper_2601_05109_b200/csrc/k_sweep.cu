@@ -167,19 +167,6 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
-    size_t b = align16((size_t)wfs * (8 * (size_t)T + 8)) + align16(4 * (size_t)wfs) +
-               align16(4 * ((size_t)wfs + 1)) + align16(4 * (size_t)wfs) +
-               align16(32 * (size_t)wfs) + align16(8 * (size_t)wfs * T) +
-               align16(8 * (size_t)wfs * T) + align16(8 * (size_t)wfs);                 // per-workflow tables
-    if (staged)
-        b += 3 * align16(rows + 32) + 2 * align16(2 * (size_t)rows + 32) + align16(4 * ((size_t)rows + 1) + 32) +
-             align16(4 * (size_t)edges + 32) + align16(4 * ((size_t)wfs + 1) + 32) + align16(4 * (size_t)wfs + 32) +
-             align16(2 * (size_t)rows) + 2 * align16(rows) +
-             4 * align16(4 * (size_t)rows) + align16(2 * (size_t)rows);                // step transfers
-    return b;
-}
-
 // The body is instantiated twice: for a staged block every table pointer
 // derives from the shared-memory window, so the compiler emits LDS/STS; for an
 // unstaged (oversized) block they point into global memory.

@@ -164,6 +164,8 @@ struct nalar_ctx {
     } alt;
     void* d_stage = nullptr;          // delta staging (device)
     size_t stage_bytes = 0;
+    uint8_t* h_dstage = nullptr;      // delta staging (pinned host): one H2D per delta
+    size_t h_dstage_bytes = 0;
     std::vector<uint64_t> m_wf_id;
     std::vector<uint32_t> m_wf_off, m_wf_eoff;
     std::vector<uint32_t> m_perm;          // per-block task order (set_blocks)
@@ -351,11 +353,12 @@ void destroy_graphs(nalar_ctx* c) {
 // Greedy partition of whole workflows into K1 blocks, balanced by rows.
 // wf_off[W+1]: first row of each workflow; wf_eoff[W+1]: first edge of each workflow
 void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, std::vector<uint32_t>& bw,
-               std::vector<uint32_t>& br, std::vector<uint32_t>& be, std::vector<uint8_t>& bs, size_t* max_smem) {
+               std::vector<uint32_t>& br, std::vector<uint32_t>& be, std::vector<uint8_t>& bs, size_t* max_smem,
+               bool fill_sms) {
     const uint32_t W = c->W;
     // balance by estimated cost, not rows: a long workflow's rows cost more
-    // (transfer + compose) and its compose chain is serial, so its block takes
-    // fewer other rows
+    // (transfer + compose) and its compose chain is serial (weight 1 by
+    // default: measured neutral on C4; NALAR_LONG_WEIGHT to experiment)
     static const double long_w = [] {
         const char* e = getenv("NALAR_LONG_WEIGHT");
         return e ? atof(e) : kLongWeight;
@@ -366,12 +369,9 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     };
     uint64_t total = 0;
     for (uint32_t w = 0; w < W; ++w) total += cost(w);
-    // fill the SMs: the greedy cut overshoots each block by part of a workflow,
-    // so start below total / SMs and grow the target until the blocks fit
-    static const bool fill = [] { const char* e = getenv("NALAR_FILL_SMS"); return !e || atoi(e) != 0; }();
     const uint64_t even = std::max<uint64_t>(64u, (total + kSmSplit - 1) / kSmSplit);
-    uint64_t target = fill ? std::max<uint64_t>(64u, even * 4 / 5) : even;
-    for (;;) {
+    // one greedy cut at a given per-block target; returns the block count
+    auto cut = [&](uint64_t target) -> size_t {
         bw.clear(); br.clear(); be.clear(); bs.clear();
         size_t mx = 0;
         uint32_t w = 0;
@@ -397,9 +397,32 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
             bw.push_back(ws); br.push_back(ra); be.push_back(wf_eoff[ws]); bs.push_back(staged ? 1 : 0);
         }
         bw.push_back(W); br.push_back(wf_off[W]); be.push_back(wf_eoff[W]);
-        const size_t nb = bw.size() - 1;
-        if (nb <= c->Bmax && (nb <= kSmSplit || target >= 2 * even)) { *max_smem = mx; return; }
-        target = target < even ? target * 103 / 100 + 1 : target * 2;
+        *max_smem = mx;
+        return bw.size() - 1;
+    };
+    // Fill the SMs (uploads): the greedy cut overshoots each block by part of a
+    // workflow, so a target of total / SMs leaves SMs idle; binary-search the
+    // smallest target in [0.8, 1] x even whose cut still fits one wave.  Deltas
+    // (a new layout every epoch) take the single cut.
+    static const bool fill_env = [] { const char* e = getenv("NALAR_FILL_SMS"); return !e || atoi(e) != 0; }();
+    uint64_t target = even;
+    if (fill_sms && fill_env) {
+        uint64_t lo = std::max<uint64_t>(64u, even * 4 / 5), hi = even;
+        if (cut(lo) <= kSmSplit) {
+            hi = lo;
+        } else {
+            for (int it = 0; it < 5 && hi > lo + 1; ++it) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                if (cut(mid) <= kSmSplit) hi = mid;
+                else lo = mid;
+            }
+        }
+        target = hi;
+    }
+    for (;;) {
+        const size_t nb = cut(target);
+        if (nb <= c->Bmax) return;
+        target *= 2;
     }
 }
 
@@ -541,11 +564,16 @@ int enqueue_epoch(nalar_ctx* c, int policy) {
 }
 
 // K1 block table from the host mirror of the workflow layout; profile buffer
-int set_blocks(nalar_ctx* c, CopyBatch* batch) {
+int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     std::vector<uint32_t> bw, br, be;
     std::vector<uint8_t> bs;
     size_t mx = 0;
-    partition(c, c->m_wf_off.data(), c->m_wf_eoff.data(), bw, br, be, bs, &mx);
+    static const bool trace = getenv("NALAR_TRACE_DELTA") != nullptr || getenv("NALAR_TRACE_UPLOAD") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t0 = trace ? now() : 0;
+    partition(c, c->m_wf_off.data(), c->m_wf_eoff.data(), bw, br, be, bs, &mx, fill_sms);
+    const double t1 = trace ? now() : 0;
     c->B = (uint32_t)bs.size();
     c->fixed_smem = k1_fixed_smem(c->T, c->I, c->Rh);
     c->smem = c->fixed_smem + mx;
@@ -558,10 +586,23 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch) {
         uint32_t* o = c->m_perm.data() + ws;
         for (uint32_t k = 0; k < we - ws; ++k) o[k] = k;
         const uint32_t* off = c->m_wf_off.data() + ws;
-        std::stable_sort(o, o + (we - ws), [off](uint32_t x, uint32_t y) {
-            return off[x + 1] - off[x] > off[y + 1] - off[y];
-        });
+        if (we - ws <= 16) {
+            // (size desc, index asc): a strict total order, so std::sort is
+            // deterministic and allocation-free (stable_sort allocates per call)
+            std::sort(o, o + (we - ws), [off](uint32_t x, uint32_t y) {
+                const uint32_t sx = off[x + 1] - off[x], sy = off[y + 1] - off[y];
+                return sx != sy ? sx > sy : x < y;
+            });
+        } else {
+            // many small workflows (a delta-mode table): only the long ones
+            // need to start first -- a stable O(n) partition keeps the host
+            // cost flat (a full sort per block is ~25 ns per workflow here)
+            std::stable_partition(o, o + (we - ws), [off](uint32_t x) {
+                return off[x + 1] - off[x] >= 32u * kLongSteps;
+            });
+        }
     }
+    const double t2 = trace ? now() : 0;
     // into the pinned staging, then one copy kernel with the caller's batch
     CopyBatch own(st);
     CopyBatch& cb = batch ? *batch : own;
@@ -585,7 +626,10 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch) {
         c->prof_words = need;
         CK(cudaMemsetAsync(c->d_prof, 0, 8 * std::max<size_t>(need, 1), st));
     }
+    const double t3 = trace ? now() : 0;
     if (!batch) CK(own.flush());
+    if (trace) fprintf(stderr, "[nalar set_blocks] partition %.1f us (%u blocks), order %.1f us, staging %.1f, flush %.1f\n",
+                       t1 - t0, c->B, t2 - t1, t3 - t2, now() - t3);
     return NALAR_OK;
 }
 
@@ -754,6 +798,7 @@ int nalar_destroy(nalar_ctx* c) {
     if (c->h_reg) cudaFreeHost(c->h_reg);
     if (c->h_list) cudaFreeHost(c->h_list);
     if (c->h_tab) cudaFreeHost(c->h_tab);
+    if (c->h_dstage) cudaFreeHost(c->h_dstage);
     delete c;
     return NALAR_OK;
 }
@@ -883,6 +928,11 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
 }
 
 int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
+    // NALAR_TRACE_DELTA=1: host-side phase times of this call on stderr
+    static const bool trace = getenv("NALAR_TRACE_DELTA") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double tt[6] = {trace ? now() : 0, 0, 0, 0, 0, 0};
     if (err_index) *err_index = -1;
     if (!c || !d) return NALAR_E_INVAL;
     if (!c->uploaded) return fail(c, NALAR_E_STATE, "delta before upload");
@@ -971,6 +1021,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
         plan.push_back(pl);
     }
     const uint32_t W2 = (uint32_t)plan.size(), N2 = row, E2 = edge;
+    if (trace) tt[1] = now();
     if (N2 > c->cfg.max_futures || E2 > c->cfg.max_edges || W2 > c->cfg.max_workflows)
         return fail(c, NALAR_E_NOMEM, "delta outgrows the reservation");
     // ---- device: second buffer set, staging ----------------------------------
@@ -998,6 +1049,15 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     const size_t s_aed = S.take<uint32_t>(nae);
     const size_t s_pid = S.take<uint64_t>(np), s_pvl = S.take<int32_t>(np);
     const size_t s_iid = S.take<uint32_t>(ni), s_icp = S.take<uint32_t>(ni), s_ibl = S.take<uint32_t>(ni);
+    const size_t s_tail = S.take<uint32_t>(2);
+    if (S.off > c->h_dstage_bytes) {
+        if (c->h_dstage) cudaFreeHost(c->h_dstage);
+        c->h_dstage = nullptr;
+        c->h_dstage_bytes = 0;
+        if (cudaMallocHost(&c->h_dstage, 2 * S.off + 4096) != cudaSuccess)
+            return fail(c, NALAR_E_NOMEM, "pinned delta staging");
+        c->h_dstage_bytes = 2 * S.off + 4096;
+    }
     if (S.off > c->stage_bytes) {
         if (c->d_stage) cudaFree(c->d_stage);
         c->d_stage = nullptr;
@@ -1007,8 +1067,11 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     }
     uint8_t* sb = (uint8_t*)c->d_stage;
     cudaStream_t st = c->stream;
+    // every delta array into the pinned staging area (host memcpy), then one
+    // async H2D -- instead of ~20 pageable cudaMemcpyAsync calls
     auto h2d = [&](size_t off, const void* h, size_t bytes) -> cudaError_t {
-        return bytes ? cudaMemcpyAsync(sb + off, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+        if (bytes) memcpy(c->h_dstage + off, h, bytes);
+        return cudaSuccess;
     };
     CK(h2d(s_uid, d->upd_wf_id, 8ull * nu)); CK(h2d(s_useq, d->upd_seq, 4ull * nu));
     CK(h2d(s_ust, d->upd_state, nu)); CK(h2d(s_uex, d->upd_executor, 2ull * nu)); CK(h2d(s_upn, d->upd_pin, 2ull * nu));
@@ -1019,6 +1082,11 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     CK(h2d(s_aed, d->app_edges, 4ull * nae));
     CK(h2d(s_pid, d->prio_wf_id, 8ull * np)); CK(h2d(s_pvl, d->prio_value, 4ull * np));
     CK(h2d(s_iid, d->inst_id, 4ull * ni)); CK(h2d(s_icp, d->inst_cap, 4ull * ni)); CK(h2d(s_ibl, d->inst_base_load, 4ull * ni));
+    {
+        const uint32_t tails[2] = {N2, E2};        // tails of the new offset arrays
+        CK(h2d(s_tail, tails, 8));
+    }
+    CK(cudaMemcpyAsync(sb, c->h_dstage, S.off, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(c->d_err, 0xFF, 16, st));
     DeltaParams p{};
     p.wf_off = c->d_wf_off; p.wf_prio = c->d_wf_prio; p.wf_id = c->d_wf_id;
@@ -1039,19 +1107,13 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     p.inst_base = at<uint32_t>(sb, s_ibl); p.i_cap = c->d_icap; p.i_base = c->d_ibase;
     p.err = c->d_err;
     CK(launch_delta(p, apply_asg, c->R, st));
-    // tails of the new offset arrays
-    const uint32_t tails[2] = {N2, E2};
-    CK(cudaMemcpyAsync(c->alt.wf_off + W2, &tails[0], 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->alt.eoff + N2, &tails[1], 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->h_err, c->d_err, 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpyAsync(c->alt.wf_off + W2, sb + s_tail, 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->alt.eoff + N2, sb + s_tail + 4, 4, cudaMemcpyDeviceToDevice, st));
+    // the update errors travel to pinned slots 2, 3 now and are checked after
+    // the single synchronisation below (validation reuses d_err)
+    CK(cudaMemcpyAsync(c->h_err + 2, c->d_err, 16, cudaMemcpyDeviceToHost, st));
     c->assign_valid = false;
-    if (c->h_err[0] != ~0ull || c->h_err[1] != ~0ull) {
-        c->uploaded = false;          // the table was partly updated in place
-        const unsigned long long bad = c->h_err[0] != ~0ull ? c->h_err[0] : c->h_err[1];
-        if (err_index) *err_index = (int64_t)bad;
-        return fail(c, NALAR_E_INVAL, "delta update %llu names no live future / workflow / instance", bad);
-    }
+    if (trace) tt[2] = now();
     // ---- swap in the new table, re-partition, validate ------------------------
     std::swap(c->d_wf_off, c->alt.wf_off); std::swap(c->d_wf_prio, c->alt.wf_prio); std::swap(c->d_wf_id, c->alt.wf_id);
     std::swap(c->d_state, c->alt.state); std::swap(c->d_type, c->alt.type); std::swap(c->d_round, c->alt.round);
@@ -1064,8 +1126,22 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     c->m_wf_id.swap(nid); c->m_wf_off.swap(noff); c->m_wf_eoff.swap(neoff);
     c->N = N2; c->E = E2; c->W = W2;
     c->have_mig = false;             // HoL inputs are per upload (row indices moved)
-    int rc = set_blocks(c, nullptr);
-    if (!rc) rc = validate_table(c, err_index, nullptr);
+    int rc = set_blocks(c, nullptr, /*fill_sms=*/false);
+    if (trace) tt[3] = now();
+    if (!rc) rc = validate_table(c, err_index, nullptr);       // synchronises
+    else cudaStreamSynchronize(st);
+    if (trace) {
+        tt[4] = now();
+        fprintf(stderr, "[nalar delta] plan %.1f us, stage+launch %.1f, swap+partition %.1f, validate+sync %.1f, "
+                "total %.1f (W %u -> %u, N %u)\n", tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3],
+                tt[4] - tt[0], W, W2, N2);
+    }
+    if (c->h_err[2] != ~0ull || c->h_err[3] != ~0ull) {
+        c->uploaded = false;          // the table was partly updated in place
+        const unsigned long long bad = c->h_err[2] != ~0ull ? c->h_err[2] : c->h_err[3];
+        if (err_index) *err_index = (int64_t)bad;
+        return fail(c, NALAR_E_INVAL, "delta update %llu names no live future / workflow / instance", bad);
+    }
     if (rc) { c->uploaded = false; return rc; }
     c->epoch_done = false;
     return NALAR_OK;

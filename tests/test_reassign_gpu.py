@@ -107,3 +107,18 @@ def test_reassign_sharded_identical_on_every_rank(G):
         assert np.array_equal(g["ra_kill"], o["ra_kill"]) and np.array_equal(g["ra_prov"], o["ra_prov"])
         assert np.array_equal(g["t_busy"], o["t_busy"]) and np.array_equal(g["t_capsum"], o["t_cap"])
         ctx.close()
+
+
+def test_single_rank_passes_refuse_multi_rank():
+    """NEXT-1 / NEXT-4 are single-rank in this version: E_NOTIMPL, not a wrong answer."""
+    nalar = _nalar()
+    s = c2(1)
+    ctx = nalar.Context.for_snapshot(s, world=2, rank=0, collective=nalar.NALAR_COLL_EXTERNAL)
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.set_policy_params(migrate=True)
+    assert e.value.code == nalar.NALAR_E_NOTIMPL
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.set_policy_params(t_max_batch=[4, 0, 0, 0], n_types=4)
+    assert e.value.code == nalar.NALAR_E_NOTIMPL
+    ctx.set_policy_params(reassign=True)            # NEXT-2 is multi-rank
+    ctx.close()
