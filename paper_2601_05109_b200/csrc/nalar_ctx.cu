@@ -58,6 +58,10 @@ thread_local std::string g_create_err;   // nalar_last_error(NULL) after a faile
 
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
 constexpr double kLongWeight = 1.0;             // cost per row of a long workflow (partition)
+// K1 blocks of one wave (NALAR_K1_BLOCKS): a few SMs stay free for the
+// early-launched (PDL) K4 blocks; measured at C4: 148 blocks 48.5 us / epoch,
+// 145 46.1, 142 45.8, 138 48.8
+constexpr uint32_t kK1Wave = 142;
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
 constexpr uint32_t kMaxBlocks = 16384;
 constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tables
@@ -405,15 +409,20 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     // smallest target in [0.8, 1] x even whose cut still fits one wave.  Deltas
     // (a new layout every epoch) take the single cut.
     static const bool fill_env = [] { const char* e = getenv("NALAR_FILL_SMS"); return !e || atoi(e) != 0; }();
+    // blocks of one wave; a few SMs may be left to the early-launched K4 blocks
+    static const uint32_t wave = [] {
+        const char* e = getenv("NALAR_K1_BLOCKS");
+        return e ? (uint32_t)atoi(e) : kK1Wave;
+    }();
     uint64_t target = even;
     if (fill_sms && fill_env) {
         uint64_t lo = std::max<uint64_t>(64u, even * 4 / 5), hi = even;
-        if (cut(lo) <= kSmSplit) {
+        if (cut(lo) <= wave) {
             hi = lo;
         } else {
             for (int it = 0; it < 5 && hi > lo + 1; ++it) {
                 const uint64_t mid = lo + (hi - lo) / 2;
-                if (cut(mid) <= kSmSplit) hi = mid;
+                if (cut(mid) <= wave) hi = mid;
                 else lo = mid;
             }
         }
