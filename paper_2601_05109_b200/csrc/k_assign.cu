@@ -248,7 +248,10 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
-    const uint32_t r = blockIdx.x;
+    // type resources (the longest walks: phase B of a whole type) take the
+    // lowest block indices, so they are the first to find a free SM while K1
+    // is still running (PDL early launch)
+    const uint32_t r = blockIdx.x < p.n_types ? p.n_inst + blockIdx.x : blockIdx.x - p.n_types;
     unsigned long long* prof = p.prof ? p.prof + (size_t)r * 8 : nullptr;
     if (prof && tid == 0) prof[0] = gtimer();
     const bool is_type = r >= I;
