@@ -356,8 +356,11 @@ int nalar_epoch_stats_get(nalar_ctx* ctx, nalar_epoch_stats* stats);
  * K4: start, admitted count known, slot tables built, done, sweep complete, walk prefix, first
  * live compaction, 0; then per workflow 4 words:
  * SM cycles in the sweep's edge loop / settling rounds / the rest, and the
- * settling-round count (bits 0-15) with steps by slot width (12 bits each).
- * *n_words = 2W + 8B + 8R + 4W. */
+ * settling-round count (bits 0-15) with steps by slot width (12 bits each)
+ * (for a long workflow: its cycles spent waiting on transfers, bits 32-63);
+ * then per K1 block 8 words of summed transfer-step cycles (edges, interface,
+ * settling, stores), settling iterations, steps, sum K, sum k.
+ * *n_words = 2W + 8B + 8R + 4W + 8B. */
 int nalar_debug_profile(nalar_ctx* ctx, uint64_t* host, size_t cap_words, size_t* n_words);
 
 /* Device stream the ctx runs on (cudaStream_t). */

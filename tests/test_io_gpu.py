@@ -135,3 +135,32 @@ def test_c4_pinned_e2e_matches_oracle():
     for k in ("status", "instance", "assign_row", "assign_inst"):
         assert np.array_equal(np.asarray(o[k]), np.asarray(g[k])), k
     ctx.close()
+
+
+def test_pinned_misaligned_arrays_bytewise_path():
+    """Host arrays at odd offsets inside one pinned buffer: the copy kernel's
+    bytewise path (neither side 16-byte aligned) must give the same bits."""
+    from paper_2601_05109_b200 import nalar
+    torch = _torch()
+    s = swe_table(4000, seed=13)
+    o = oracle_epoch(s, "srtf")
+    arrs = s.arrays()
+    total = sum(a.nbytes + 19 for a in arrs.values()) + 64
+    t = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    buf = t.numpy()
+    off, views = 3, {}
+    for k, a in arrs.items():
+        itemsize = a.dtype.itemsize
+        off += (-off) % itemsize                    # element-aligned, not 16-byte aligned
+        if off % 16 == 0:
+            off += itemsize
+        v = buf[off:off + a.nbytes].view(a.dtype).reshape(a.shape)
+        v[...] = a
+        views[k] = v
+        off += a.nbytes + 5
+    sp = Snapshot(global_row_base=0, name="misaligned", **views)
+    ctx = nalar.Context.for_snapshot(s)
+    ctx.upload(sp)
+    ctx.epoch("srtf")
+    same(o, ctx.fetch(), "misaligned")
+    ctx.close()
