@@ -64,6 +64,25 @@ __device__ __forceinline__ void locate_slot(const uint32_t* sp2, uint32_t n, uin
     *j_out = g - slots_above(sp2, n, lo);
 }
 
+// the same on a register copy of spare2 (ni <= 16): pure ALU, no LDS chain
+__device__ __forceinline__ uint64_t slots_above_r(const uint32_t (&sp)[16], uint64_t s) {
+    uint64_t a = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a += sp[k] > s ? sp[k] - s : 0ull;
+    return a;
+}
+__device__ __forceinline__ void locate_slot_r(const uint32_t (&sp)[16], uint64_t maxs, uint64_t g,
+                                              uint64_t* s_out, uint64_t* j_out) {
+    uint64_t lo = 1, hi = maxs;
+    while (lo < hi) {
+        const uint64_t mid = lo + ((hi - lo) >> 1);
+        if (slots_above_r(sp, mid) <= g) hi = mid;
+        else lo = mid + 1;
+    }
+    *s_out = lo;
+    *j_out = g - slots_above_r(sp, lo);
+}
+
 __device__ __forceinline__ uint32_t slot_instance(const uint32_t* sp2, const uint32_t* inst, uint32_t n,
                                                   uint64_t maxs, uint64_t g) {
     uint64_t s, j;
@@ -297,6 +316,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     const uint32_t cnt0 = tid < B ? p.cnt_rb[(size_t)r * B + tid] : 0u;   // first 256 K1 blocks
     const uint32_t off0 = tid < B ? p.off_rb[(size_t)r * B + tid] : 0u;
     uint32_t ls0 = 0, ha0 = 0;
+    uint64_t my_load = 0;                     // load of instance k == tid of the type (kept for NEXT-2)
     const uint32_t ha_unp = (is_type && p.ra_on && tid == 0) ? p.tot[r] : 0u;   // unpinned eligible of t
     if (is_type) {
         if (tid < ni) { ls0 = p.load_sum[s_inst[tid]]; ha0 = p.tot[s_inst[tid]]; }
@@ -315,6 +335,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
             s_spare[k] = spare;
             s_sp2[k] = spare - (ha < spare ? ha : spare);
             p.i_load[i] = load > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)load;
+            if (k == tid) my_load = load;
             ra_busy += load + ha;
             ra_cap += cap;
             p.i_spare[i] = spare;
@@ -333,6 +354,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
         for (int k = 0; k < kK4Warps; ++k) s_wc[k][lv] = 0;
     }
     __syncthreads();
+    if (prof && tid == 0 && !p.ra_on) prof[7] = gtimer();    // loads of the sweep's results landed
 
     // ---- bound of this resource; suffix sums over levels ------------------
     uint64_t bound, maxs = 0;
@@ -402,8 +424,31 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     if (is_type) {
         const uint64_t n_t = (uint64_t)s_A[0] + s_Hg[0];
         const uint64_t used = n_t < bound ? n_t : bound;
+        // small types (ni <= 16, the common case): spare2 in registers, so the
+        // slot arithmetic below is ALU only instead of chains of shared loads
+        const bool small = ni <= 16u;
+        uint32_t spr[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) spr[k] = (small && (uint32_t)k < ni) ? s_sp2[k] : 0u;
         uint64_t s0 = 0, j0 = 0;
-        if (used) locate_slot(s_sp2, ni, maxs, used - 1, &s0, &j0);
+        if (used) {
+            if (small && maxs <= 32u) {
+                // every candidate level at once, one per lane: the level of
+                // slot g is the smallest s with slots_above(s) <= g
+                const uint32_t sv = lane + 1u;
+                uint32_t above = 0;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) above += spr[k] > sv ? spr[k] - sv : 0u;
+                const uint32_t okm = __ballot_sync(0xFFFFFFFFu, sv <= maxs && above <= used - 1);
+                const uint32_t lvl = __ffs(okm);                 // = s0 (1-based lane index)
+                s0 = lvl;
+                j0 = (used - 1) - __shfl_sync(0xFFFFFFFFu, above, lvl - 1u);
+            } else if (small) {
+                locate_slot_r(spr, maxs, used - 1, &s0, &j0);
+            } else {
+                locate_slot(s_sp2, ni, maxs, used - 1, &s0, &j0);
+            }
+        }
         for (uint32_t k = tid; k < ni; k += kK4Threads) {
             uint64_t asg = s_spare[k] - s_sp2[k];     // phase A
             if (used) {
@@ -411,13 +456,18 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
                 asg += sp > s0 ? sp - s0 : 0ull;
                 if (sp >= s0) {
                     uint64_t idx = 0;
-                    for (uint32_t q = 0; q < k; ++q) idx += s_sp2[q] >= s0;
+                    if (small) {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) idx += ((uint32_t)q < k && spr[q] >= s0) ? 1u : 0u;
+                    } else {
+                        for (uint32_t q = 0; q < k; ++q) idx += s_sp2[q] >= s0;
+                    }
                     asg += idx <= j0;
                 }
             }
             p.i_assigned[s_inst[k]] = (uint32_t)asg;
             {   // NEXT-2 kill key: least load + assigned, ties the highest id
-                const uint64_t la = asg + p.i_load[s_inst[k]];
+                const uint64_t la = asg + (k == tid ? my_load : (uint64_t)p.i_load[s_inst[k]]);
                 const uint64_t key = ((la > 0xFFFFFFFFull ? 0xFFFFFFFFull : la) << 32) | (0xFFFFu - s_inst[k]);
                 ra_best = key < ra_best ? key : ra_best;
             }
@@ -426,12 +476,15 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
             // slots in (level desc, instance asc) order, all at once: slot
             // (s, k) sits after every slot of a higher level and after the
             // level-s slots of lower instances
-            for (uint32_t k = 0; k < ni; ++k) {
-                const uint32_t sp = s_sp2[k];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if ((uint32_t)k >= ni) break;
+                const uint32_t sp = spr[k];
                 for (uint32_t sv = 1 + tid; sv <= sp; sv += kK4Threads) {
                     uint32_t pos = 0;
-                    for (uint32_t j = 0; j < ni; ++j) {
-                        const uint32_t x = s_sp2[j];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t x = spr[j];
                         pos += (x > sv ? x - sv : 0u) + (j < k && x >= sv ? 1u : 0u);
                     }
                     s_slot[pos] = (uint16_t)s_inst[k];
@@ -505,7 +558,18 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
                     const uint32_t q = qa + j;
                     it[j] = make_uint2(0u, 0u);
                     if (q < total) {
-                        while (lo + 1 < nb && s_pref[lo + 1] <= q) ++lo;
+                        if (lo + 1 < nb && s_pref[lo + 1] <= q) {
+                            // item q is in a later block: binary search (a sparse
+                            // resource has long runs of empty blocks -- walking
+                            // them one LDS at a time cost microseconds)
+                            uint32_t l2 = lo + 1, h2 = nb - 1;
+                            while (l2 < h2) {
+                                const uint32_t mid = (l2 + h2 + 1) >> 1;
+                                if (s_pref[mid] <= q) l2 = mid;
+                                else h2 = mid - 1;
+                            }
+                            lo = l2;
+                        }
                         it[j] = p.items[s_base[lo] + (q - s_pref[lo])];
                     }
                 }

@@ -105,7 +105,7 @@ if len(last):
 res["k4"]["wait_release_after_k1_end_ns"] = int(k4[:, 4].min() - k1_end)
 slow = np.argsort(-(k4[:, 3] - k1_end))[:6]
 res["k4"]["slowest_ctas"] = [{"r": int(r), **{n: (int(k4[r, j] - k1_end) if k4[r, j] > 0 else None) for n, j in
-                                             (("start", 0), ("released", 4), ("n_adm", 1), ("tables", 2),
+                                             (("start", 0), ("released", 4), ("loaded", 7), ("n_adm", 1), ("tables", 2),
                                               ("prefix", 5), ("pass1", 6), ("done", 3))}} for r in slow]
 print(json.dumps(res, indent=1))
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
