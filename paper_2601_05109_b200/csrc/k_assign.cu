@@ -476,19 +476,18 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
             // slots in (level desc, instance asc) order, all at once: slot
             // (s, k) sits after every slot of a higher level and after the
             // level-s slots of lower instances
+            // one (instance k, level sv) pair per thread
+            const uint32_t npair = ni * (uint32_t)maxs;
+            for (uint32_t idx = tid; idx < npair; idx += kK4Threads) {
+                const uint32_t k = idx / (uint32_t)maxs, sv = idx - k * (uint32_t)maxs + 1u;
+                if (sv > s_sp2[k]) continue;
+                uint32_t pos = 0;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if ((uint32_t)k >= ni) break;
-                const uint32_t sp = spr[k];
-                for (uint32_t sv = 1 + tid; sv <= sp; sv += kK4Threads) {
-                    uint32_t pos = 0;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const uint32_t x = spr[j];
-                        pos += (x > sv ? x - sv : 0u) + (j < k && x >= sv ? 1u : 0u);
-                    }
-                    s_slot[pos] = (uint16_t)s_inst[k];
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t x = spr[j];
+                    pos += (x > sv ? x - sv : 0u) + ((uint32_t)j < k && x >= sv ? 1u : 0u);
                 }
+                s_slot[pos] = (uint16_t)s_inst[k];
             }
         } else if (table && n_adm && warp == 0) {
             // slots in (level desc, instance asc) order, one level per step
