@@ -352,6 +352,33 @@ def main():
                  "kv_hints": {k: int(v) for k, v in zip(("none", "retain", "offload", "drop"),
                                                        np.bincount(ra_out["kv_hint"].ravel(), minlength=4))}}
 
+    # where the epoch's critical path goes (NALAR_F_PROFILE %globaltimer stamps in
+    # a separate, untimed context): K1 staging, the last workflow's sweep /
+    # composition, K1's row-parallel tail, and K4 after K1
+    crit = {}
+    if world == 1:
+        pctx = new_ctx(flags=nalar.NALAR_F_PROFILE | nalar.NALAR_F_NO_GRAPH)
+        pctx.upload(s)
+        for _ in range(3):
+            with torch.cuda.stream(torch.cuda.ExternalStream(pctx.stream)):
+                flush.zero_()
+            pctx.epoch(pol)
+        torch.cuda.synchronize()
+        pr = nalar.nalar_debug_profile(pctx.h).astype(np.int64)
+        pctx.close()
+        Wn, Rn = s.n_workflows, s.n_instances + s.n_types
+        Bn = (len(pr) - 2 * Wn - 8 * Rn - 4 * Wn) // 16
+        wfp = pr[:2 * Wn].reshape(Wn, 2)
+        blk = pr[2 * Wn:2 * Wn + 8 * Bn].reshape(Bn, 8)
+        k4p = pr[2 * Wn + 8 * Bn:2 * Wn + 8 * Bn + 8 * Rn].reshape(Rn, 8)
+        t0 = blk[:, 3].min()
+        k1_end = blk[:, 2].max()
+        crit = {"k1_span": float(k1_end - t0) / 1e3, "k1_staging_max": float((blk[:, 0] - blk[:, 3]).max()) / 1e3,
+                "last_workflow_end": float(wfp[:, 1].max() - t0) / 1e3,
+                "k1_tail_after_last_workflow": float(k1_end - wfp[:, 1].max()) / 1e3,
+                "k4_end_after_k1": float(k4p[:, 3].max() - k1_end) / 1e3,
+                "k4_pdl_release_after_k1": float(k4p[:, 4].min() - k1_end) / 1e3}
+
     # per-kernel device times (CUDA events captured inside the epoch graph)
     tctx = new_ctx(flags=nalar.NALAR_F_TIMING)
     tctx.upload(s)
@@ -450,6 +477,7 @@ def main():
             # per epoch: k_zero (exchange buffer + counters), k1_sweep, k4_assign
             "gpu_launches": 3 * args.steps,
             "next_rows": next_rows,
+            "critical_path_us": crit,
             "clocks": clk.summary(),
             "paper_context": "464 ms per global-control-loop at 131K futures, Python+gRPC+Redis on "
                              "64 emulated CPU nodes (PAPER.md:715); context, not the target"}
