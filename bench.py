@@ -50,14 +50,16 @@ def make_table(n_gpus, seed):
     return swe_table(n_gpus * FUT_PER_GPU, seed=seed, name="C4" if n_gpus == 1 else "C5")
 
 
-def workload_config(n_gpus, table, policy):
+def workload_config(n_gpus, table, policy, collective="peer"):
     return {"workload": ("C4 paper-scale SWE-recursive future table" if n_gpus == 1 else
                          f"C5 scale-out SWE-recursive table sharded by workflow id over {n_gpus} GPUs"),
             "futures_total": table.n_futures, "futures_per_gpu": FUT_PER_GPU,
             "workflows": table.n_workflows, "edges": table.n_edges,
             "instances": table.n_instances, "types": table.n_types, "policy": policy.upper(),
             "levels": 256, "l2": "flushed between epochs (256 MB memset, untimed)",
-            "parallelism": f"workflow-sharded x{n_gpus}" + (" + NCCL allreduce" if n_gpus > 1 else "")}
+            "parallelism": f"workflow-sharded x{n_gpus}" + (
+                (" + peer-memory slot exchange (k_peer)" if collective == "peer" else " + NCCL allreduce")
+                if n_gpus > 1 else "")}
 
 
 def oracle_time(s, policy, budget_s, min_runs=1, max_runs=10**6):
@@ -243,6 +245,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--c3-epochs", type=int, default=60)
+    ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
+                    help="rank exchange for N > 1: kernels storing into peer memory (CUDA IPC), "
+                         "or the library's NCCL allreduce")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if world == 1:
@@ -271,10 +276,30 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
 
+    coll = args.collective
+
     def new_ctx(flags=0):
-        return nalar.Context(max(s.n_futures, 1), max(s.n_edges, 1), max(s.n_workflows, 1),
-                             s.n_instances, s.n_types, device=local, rank=rank, world=world,
-                             nccl_id=nccl_id, flags=flags)
+        nonlocal coll
+        mk = lambda c: nalar.Context(max(s.n_futures, 1), max(s.n_edges, 1), max(s.n_workflows, 1),  # noqa: E731
+                                     s.n_instances, s.n_types, device=local, rank=rank, world=world,
+                                     nccl_id=nccl_id, flags=flags, collective=c)
+        if world == 1 or coll == "nccl":
+            return mk(None)
+        # peer memory over CUDA IPC; every rank falls back to NCCL if any rank cannot open a peer
+        from paper_2601_05109_b200.sharding import connect_peers
+        c, ok = mk(nalar.NALAR_COLL_PEER), 1
+        try:
+            connect_peers(c)
+        except nalar.NalarError as e:
+            print(f"[bench] rank {rank}: peer connect failed ({e}); using NCCL", file=sys.stderr)
+            ok = 0
+        t = torch.tensor([ok], dtype=torch.int32, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()):
+            return c
+        c.close()
+        coll = "nccl"
+        return mk(None)
 
     ctx = new_ctx()
     ctx.upload(s)
@@ -461,7 +486,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "futures/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": workload_config(world, table, args.policy),
+            "data": "synthetic", "config": workload_config(world, table, args.policy, coll),
             "epoch_us_p50": nearest_rank(list(ms * 1e3), 50),
             "epoch_us_p99": nearest_rank(list(ms * 1e3), 99),
             "warm_l2": {"ms_per_step": float(np.mean(ms_warm)),

@@ -80,8 +80,13 @@ enum nalar_status { NALAR_S_RESOLVED = 0, NALAR_S_FAILED = 1, NALAR_S_INFLIGHT =
 /* how ranks exchange the per-epoch histogram / load buffer (world > 1) */
 enum nalar_collective { NALAR_COLL_NONE = 0,     /* world == 1                       */
                         NALAR_COLL_NCCL = 1,     /* library-owned ncclComm, in-graph */
-                        NALAR_COLL_EXTERNAL = 2  /* caller sums the exchange buffer
-                                                    between epoch_begin / finish      */ };
+                        NALAR_COLL_EXTERNAL = 2, /* caller sums the exchange buffer
+                                                    between epoch_begin / finish      */
+                        NALAR_COLL_PEER = 3      /* kernels store each rank's slot into
+                                                    every peer's buffer (NVLink peer
+                                                    memory), world <= 8; connect with
+                                                    nalar_peer_connect before the
+                                                    first epoch                       */ };
 /* nalar_config.flags */
 #define NALAR_F_TIMING          1u  /* record per-kernel CUDA events (stats)      */
 #define NALAR_F_NO_GRAPH        2u  /* launch kernels directly, no CUDA graph     */
@@ -343,6 +348,20 @@ int nalar_policy_epoch(nalar_ctx* ctx, int policy);
 int nalar_epoch_begin(nalar_ctx* ctx, int policy);
 int nalar_exchange_buffer(nalar_ctx* ctx, void** dev_ptr, size_t* n_words);
 int nalar_epoch_finish(nalar_ctx* ctx);
+
+/* NALAR_COLL_PEER.  Every rank owns a receive buffer (library cudaMalloc);
+ * peers write their histogram slot and partial sums into it and raise an
+ * epoch-numbered flag.  nalar_peer_buffer returns this rank's
+ * buffer as a device pointer and as a CUDA IPC handle (64 bytes) for
+ * ranks in other processes.  nalar_peer_connect takes, per rank q < world,
+ * either ptrs[q] (a device pointer valid in this process: ranks driven by one
+ * process, on one device or on peer-enabled devices) or handles[64 q] (an IPC
+ * handle, opened here); ptrs / handles may be NULL, ptrs[rank] is ignored.
+ * Call on every rank before its first epoch; all ranks must run the same
+ * sequence of epochs.  A peer that never arrives makes the epoch's waiting
+ * kernel give up after 5 s: the next fetch / stats call returns NALAR_E_COMM. */
+int nalar_peer_buffer(nalar_ctx* ctx, void** dev_ptr, unsigned char ipc_handle[64]);
+int nalar_peer_connect(nalar_ctx* ctx, void* const* ptrs, const unsigned char* handles);
 
 /* Copy decisions to caller host buffers; synchronises the ctx stream. */
 int nalar_fetch_decisions(nalar_ctx* ctx, nalar_decisions* out);

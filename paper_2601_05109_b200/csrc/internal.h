@@ -3,6 +3,7 @@
 // Nothing here is part of the C ABI (see include/nalar.h).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define NALAR_MAX_INSTANCES_DEV 1024
@@ -13,6 +14,15 @@ constexpr int kK0Threads = 256;          // validate: warp per workflow
 constexpr int kK1Threads = 512;          // sweep: warp per workflow inside a block
 constexpr int kK1Warps = kK1Threads / 32;
 constexpr uint32_t kLongSteps = 6;      // workflows of >= 6 steps use the transfer decomposition
+// the threshold in rows (kLongSteps steps; NALAR_LONG_STEPS to experiment)
+inline uint32_t long_rows() {
+    static const uint32_t v = [] {
+        const char* e = getenv("NALAR_LONG_STEPS");
+        const int s = e ? atoi(e) : (int)kLongSteps;
+        return 32u * (uint32_t)(s > 1 ? s : 1);
+    }();
+    return v;
+}
 constexpr uint32_t kMaxIface = 7;       // interface rows per step in a transfer
 constexpr int kK4Threads = 256;          // assign: one block per resource
 constexpr int kK4Warps = kK4Threads / 32;
@@ -70,6 +80,7 @@ struct ValidateParams {
 };
 
 struct SweepParams {
+    uint32_t long_rows;          // workflows of >= long_rows rows are composed from step transfers
     const uint32_t* wf_fut_off;
     const int32_t* wf_prio;
     const uint8_t* f_state;
@@ -259,6 +270,28 @@ struct BatchParams {
 };
 cudaError_t launch_batch(const BatchParams& p, cudaStream_t s);
 
+// rank exchange over peer memory (k_peer.cu)
+constexpr uint32_t kPeerMaxRanks = 8;
+constexpr uint32_t kPeerFlagWords = 64;                       // flag[2][kPeerMaxRanks], padded
+constexpr unsigned long long kPeerTimeoutNs = 5000000000ull;  // a missing peer: error, not a hang
+struct PeerParams {
+    uint32_t* peers[kPeerMaxRanks];   // every rank's receive buffer (own included)
+    const uint32_t* slot;             // this rank's H slot [Rh*Lv]
+    const uint32_t* load;             // this rank's partial load [I]
+    const uint32_t* tot;              // this rank's partial totals [Rh]
+    uint32_t* x;                      // K4's exchange buffer: H[G][Rh*Lv] | load[I] | tot[Rh]
+    unsigned long long* err;          // mapped host word: set on a timed-out wait
+    size_t par_words;                 // words per parity region (reservation sized)
+    uint32_t G, rank, rh_lv, I, Rh;
+};
+inline size_t peer_par_words(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
+    return (size_t)G * (Rhmax * Lv + Imax + Rhmax);
+}
+inline size_t peer_buffer_bytes(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
+    return 4 * (kPeerFlagWords + 2 * peer_par_words(G, Rhmax, Lv, Imax) + 4);
+}
+cudaError_t launch_peer_exchange(const PeerParams& p, cudaStream_t s);
+
 cudaError_t launch_copy_segs(const CopyParams& p, cudaStream_t s);
 cudaError_t launch_fetch(const FetchParams& f, const CopyParams& p, cudaStream_t s);
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);
@@ -266,5 +299,15 @@ cudaError_t launch_delta(const DeltaParams& p, bool apply_assigned, uint32_t R, 
 cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s);
 cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
+
+// eager loading of every kernel (one per source file)
+cudaError_t preload_k_assign();
+cudaError_t preload_k_batch();
+cudaError_t preload_k_delta();
+cudaError_t preload_k_io();
+cudaError_t preload_k_migrate();
+cudaError_t preload_k_peer();
+cudaError_t preload_k_sweep();
+cudaError_t preload_k_validate();
 
 }  // namespace nalar

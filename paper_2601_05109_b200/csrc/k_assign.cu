@@ -658,4 +658,13 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k4_assign, p);
 }
 
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_assign() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k4_assign)) return e;
+    return cudaSuccess;
+}
+
 }  // namespace nalar

@@ -86,4 +86,13 @@ cudaError_t launch_batch(const BatchParams& p, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k6_batch, p);
 }
 
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_batch() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k6_batch)) return e;
+    return cudaSuccess;
+}
+
 }  // namespace nalar

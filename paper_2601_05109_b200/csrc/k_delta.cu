@@ -128,4 +128,16 @@ cudaError_t launch_delta(const DeltaParams& p, bool apply_assigned, uint32_t R, 
     return cudaGetLastError();
 }
 
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_delta() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, kd1_apply_assigned)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, kd2_updates)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, kd3_rebuild)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, kd4_prio_inst)) return e;
+    return cudaSuccess;
+}
+
 }  // namespace nalar

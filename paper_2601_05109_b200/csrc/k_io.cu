@@ -113,4 +113,14 @@ cudaError_t launch_fetch(const FetchParams& f, const CopyParams& p, cudaStream_t
     return cudaGetLastError();
 }
 
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_io() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k_copy_segs)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k_fetch)) return e;
+    return cudaSuccess;
+}
+
 }  // namespace nalar

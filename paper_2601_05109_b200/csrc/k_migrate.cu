@@ -251,4 +251,13 @@ cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k5_migrate, p);
 }
 
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_migrate() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k5_migrate)) return e;
+    return cudaSuccess;
+}
+
 }  // namespace nalar

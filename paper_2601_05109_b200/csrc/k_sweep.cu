@@ -348,7 +348,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     // steps in order on one warp with a cheap evaluation per step.  Steps that
     // do not fit (wide interface / fan-in) fall back to the ordinary sweep step
     // in P2b.
-    auto is_long = [&](uint32_t wi) { return wfo[wi + 1] - wfo[wi] >= 32u * kLongSteps; };
+    auto is_long = [&](uint32_t wi) { return wfo[wi + 1] - wfo[wi] >= p.long_rows; };
     // long-step task prefix over workflows (warp 0), s_lpref[nw] = total
     if (warp == 0) {
         uint32_t carry = 0, nlong = 0;
@@ -1141,6 +1141,16 @@ cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k1_sweep, p);
+}
+
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_sweep() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k_zero)) return e;
+    return cudaSuccess;
 }
 
 }  // namespace nalar

@@ -50,4 +50,13 @@ cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// load this file's kernels now (CUDA lazy loading would load them at first
+// launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
+cudaError_t preload_k_validate() {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k0_validate)) return e;
+    return cudaSuccess;
+}
+
 }  // namespace nalar

@@ -156,6 +156,13 @@ struct nalar_ctx {
     Key gkey[3]{};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ncclComm_t comm = nullptr;
+    // NALAR_COLL_PEER: this rank's receive buffer and every rank's (k_peer.cu)
+    uint32_t* peer_buf = nullptr;
+    size_t peer_par_words = 0;
+    uint32_t* peers[kPeerMaxRanks] = {};
+    void* peer_ipc[kPeerMaxRanks] = {};      // opened IPC mappings (closed on destroy)
+    bool peers_ready = false;
+    unsigned long long* peer_err_dev = nullptr;   // device view of h_err[4]
     // delta mode: device workflow ids, the second table buffer set, host mirror
     uint64_t* d_wf_id = nullptr;
     struct Alt {
@@ -369,7 +376,7 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     }();
     auto cost = [&](uint32_t w) {
         const uint32_t wr = wf_off[w + 1] - wf_off[w];
-        return wr >= 32u * kLongSteps ? (uint64_t)(wr * long_w) : (uint64_t)wr;
+        return wr >= long_rows() ? (uint64_t)(wr * long_w) : (uint64_t)wr;
     };
     uint64_t total = 0;
     for (uint32_t w = 0; w < W; ++w) total += cost(w);
@@ -437,6 +444,7 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
 
 int run_k1(nalar_ctx* c, int policy) {
     SweepParams p{};
+    p.long_rows = long_rows();
     p.wf_fut_off = c->d_wf_off; p.wf_prio = c->d_wf_prio;
     p.f_state = c->d_state; p.f_type = c->d_type; p.f_round = c->d_round;
     p.f_exec = c->d_exec; p.f_pin = c->d_pin; p.f_edge_off = c->d_eoff; p.edges = c->d_edges;
@@ -522,6 +530,22 @@ int enqueue_first_half(nalar_ctx* c, int policy) {
 }
 
 int enqueue_collective(nalar_ctx* c) {
+    if (c->cfg.collective == NALAR_COLL_PEER) {
+        if (!c->peers_ready) return fail(c, NALAR_E_STATE, "peer collective: nalar_peer_connect first");
+        PeerParams p{};
+        const uint32_t G = (uint32_t)c->cfg.world;
+        for (uint32_t q = 0; q < G; ++q) p.peers[q] = c->peers[q];
+        p.G = G; p.rank = (uint32_t)c->cfg.rank;
+        p.rh_lv = c->Rh * c->Lv; p.I = c->I; p.Rh = c->Rh;
+        p.slot = c->d_x + (size_t)p.rank * p.rh_lv;
+        p.load = c->d_x + (size_t)G * p.rh_lv;
+        p.tot = p.load + c->I;
+        p.x = c->d_x;
+        p.err = c->peer_err_dev;
+        p.par_words = c->peer_par_words;
+        CK(launch_peer_exchange(p, c->stream));
+        return NALAR_OK;
+    }
     if (c->cfg.collective == NALAR_COLL_NCCL) {
         // NOTE: the full reservation-sized layout keeps slot offsets identical on all ranks
         const ncclResult_t r = g_nccl.allReduce(c->d_x, c->d_x, x_used_words(c), ncclUint32, ncclSum, c->comm,
@@ -607,7 +631,7 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
             // need to start first -- a stable O(n) partition keeps the host
             // cost flat (a full sort per block is ~25 ns per workflow here)
             std::stable_partition(o, o + (we - ws), [off](uint32_t x) {
-                return off[x + 1] - off[x] >= 32u * kLongSteps;
+                return off[x + 1] - off[x] >= long_rows();
             });
         }
     }
@@ -697,7 +721,8 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     auto bail = [&](int code) { nalar_destroy(c); return code; };
     if (c->Lv > NALAR_MAX_LEVELS || cfg->max_types > NALAR_MAX_TYPES || cfg->max_instances > NALAR_MAX_INSTANCES ||
         cfg->max_futures > NALAR_MAX_ROWS || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world ||
-        (cfg->world > 1 && cfg->collective == NALAR_COLL_NONE))
+        (cfg->world > 1 && cfg->collective == NALAR_COLL_NONE) ||
+        (cfg->collective == NALAR_COLL_PEER && cfg->world > (int)kPeerMaxRanks))
         return bail(NALAR_E_INVAL);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return bail(NALAR_E_CUDA);
@@ -773,6 +798,24 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     }
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
+    c->h_err[4] = 0;
+    if (cfg->collective == NALAR_COLL_PEER) {
+        // Every kernel is loaded now: under CUDA lazy loading the first launch
+        // of a kernel waits for the device to go idle, and a rank's gather
+        // kernel spins until the other ranks push -- ranks driven by one host
+        // thread would stall until the exchange times out.
+        for (auto f : {preload_k_assign, preload_k_batch, preload_k_delta, preload_k_io, preload_k_migrate,
+                       preload_k_peer, preload_k_sweep, preload_k_validate})
+            if (f() != cudaSuccess) return bail(NALAR_E_CUDA);
+        c->peer_par_words = peer_par_words((uint32_t)cfg->world, c->Rhmax, c->Lv, cfg->max_instances);
+        const size_t bytes = peer_buffer_bytes((uint32_t)cfg->world, c->Rhmax, c->Lv, cfg->max_instances);
+        if (cudaMalloc(&c->peer_buf, bytes) != cudaSuccess) return bail(NALAR_E_NOMEM);
+        if (cudaMemset(c->peer_buf, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+            return bail(NALAR_E_CUDA);
+        c->peers[cfg->rank] = c->peer_buf;
+        c->peer_err_dev = (unsigned long long*)mapped_view(c->h_err + 4);
+        if (!c->peer_err_dev) return bail(NALAR_E_CUDA);
+    }
     if (cfg->collective == NALAR_COLL_NCCL) {   // (world == 1 allowed: a 1-rank comm, for testing)
         if (!g_nccl.load(&c->err)) { g_create_err = c->err; return bail(NALAR_E_COMM); }
         ncclUniqueId id;
@@ -797,6 +840,9 @@ int nalar_destroy(nalar_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->comm) g_nccl.commDestroy(c->comm);
+    for (void* m : c->peer_ipc)
+        if (m) cudaIpcCloseMemHandle(m);
+    if (c->peer_buf) cudaFree(c->peer_buf);
     if (c->own_arena && c->arena) cudaFree(c->arena);
     if (c->d_prof) cudaFree(c->d_prof);
     if (c->alt.mem) cudaFree(c->alt.mem);
@@ -1218,8 +1264,65 @@ int nalar_epoch_finish(nalar_ctx* c) {
     return rc;
 }
 
+static int fetch_impl(nalar_ctx* c, nalar_decisions* o);
+
+// a peer exchange that timed out (k_peer_gather) fails the next synchronising call
+static int peer_check(nalar_ctx* c, int rc) {
+    if (rc == NALAR_OK && c->peer_buf && c->h_err[4]) {
+        c->h_err[4] = 0;
+        return fail(c, NALAR_E_COMM, "peer exchange: a rank's flag never arrived (timed out)");
+    }
+    return rc;
+}
+
 int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     if (!c || !o) return NALAR_E_INVAL;
+    return peer_check(c, fetch_impl(c, o));
+}
+
+int nalar_peer_buffer(nalar_ctx* c, void** dev_ptr, unsigned char ipc_handle[64]) {
+    if (!c) return NALAR_E_INVAL;
+    if (!c->peer_buf) return fail(c, NALAR_E_STATE, "not a NALAR_COLL_PEER context");
+    if (dev_ptr) *dev_ptr = c->peer_buf;
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, c->peer_buf));
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        memcpy(ipc_handle, &h, 64);
+    }
+    return NALAR_OK;
+}
+
+int nalar_peer_connect(nalar_ctx* c, void* const* ptrs, const unsigned char* handles) {
+    if (!c) return NALAR_E_INVAL;
+    if (!c->peer_buf) return fail(c, NALAR_E_STATE, "not a NALAR_COLL_PEER context");
+    const int G = c->cfg.world, me = c->cfg.rank;
+    for (int q = 0; q < G; ++q) {
+        if (q == me) continue;
+        if (c->peer_ipc[q]) { cudaIpcCloseMemHandle(c->peer_ipc[q]); c->peer_ipc[q] = nullptr; }
+        if (ptrs && ptrs[q]) {
+            c->peers[q] = (uint32_t*)ptrs[q];
+        } else if (handles) {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, handles + 64 * (size_t)q, 64);
+            void* m = nullptr;
+            const cudaError_t e = cudaIpcOpenMemHandle(&m, h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                c->peers_ready = false;
+                return fail(c, NALAR_E_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+            }
+            c->peer_ipc[q] = m;
+            c->peers[q] = (uint32_t*)m;
+        } else {
+            c->peers_ready = false;
+            return fail(c, NALAR_E_INVAL, "peer_connect: no pointer or handle for rank %d", q);
+        }
+    }
+    c->peers_ready = true;
+    return NALAR_OK;
+}
+
+static int fetch_impl(nalar_ctx* c, nalar_decisions* o) {
     if (!c->epoch_done) return fail(c, NALAR_E_STATE, "fetch before epoch");
     cudaStream_t st = c->stream;
     // without an active migration pass nothing moves: answer on the host
@@ -1409,6 +1512,7 @@ int nalar_epoch_stats_get(nalar_ctx* c, nalar_epoch_stats* s) {
     memset(s, 0, sizeof *s);
     CK(cudaMemcpyAsync(c->h_cnt, c->d_scr, C_NUM * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (int rc = peer_check(c, NALAR_OK)) return rc;
     s->n_futures = c->N;
     s->n_ready = c->h_cnt[C_READY];
     s->n_eligible = c->h_cnt[C_ELIG];

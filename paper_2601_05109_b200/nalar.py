@@ -15,11 +15,14 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libnalar.so")
+# A/B experiments only: another in-tree build of the same library (scripts/ab.sh)
+if os.environ.get("NALAR_LIB_AB"):
+    LIB_PATH = os.path.join(HERE, os.environ["NALAR_LIB_AB"])
 
 NALAR_OK, NALAR_E_INVAL, NALAR_E_STATE, NALAR_E_NOMEM, NALAR_E_SIZE, NALAR_E_CUDA, NALAR_E_COMM, \
     NALAR_E_NOTIMPL = 0, -1, -2, -3, -4, -5, -6, -7
 NALAR_FCFS, NALAR_SRTF, NALAR_LPT = 0, 1, 2
-NALAR_COLL_NONE, NALAR_COLL_NCCL, NALAR_COLL_EXTERNAL = 0, 1, 2
+NALAR_COLL_NONE, NALAR_COLL_NCCL, NALAR_COLL_EXTERNAL, NALAR_COLL_PEER = 0, 1, 2, 3
 NALAR_F_TIMING, NALAR_F_NO_GRAPH, NALAR_F_FORCE_UNSTAGED, NALAR_F_PROFILE = 1, 2, 4, 8
 POLICIES = {"fcfs": NALAR_FCFS, "srtf": NALAR_SRTF, "lpt": NALAR_LPT}
 ERR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_STATE", -3: "E_NOMEM", -4: "E_SIZE", -5: "E_CUDA",
@@ -30,7 +33,7 @@ EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
            "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile",
-           "nalar_delta_apply", "nalar_set_policy_params")
+           "nalar_delta_apply", "nalar_set_policy_params", "nalar_peer_buffer", "nalar_peer_connect")
 NALAR_DELTA_APPLY_ASSIGNED = 1
 
 
@@ -125,6 +128,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_delta_apply.restype = C.c_int
     lib.nalar_set_policy_params.argtypes = [C.c_void_p, P(nalar_policy_params)]
     lib.nalar_set_policy_params.restype = C.c_int
+    lib.nalar_peer_buffer.argtypes = [C.c_void_p, P(C.c_void_p), C.c_void_p]
+    lib.nalar_peer_buffer.restype = C.c_int
+    lib.nalar_peer_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.nalar_peer_connect.restype = C.c_int
     lib.nalar_stream.argtypes = [C.c_void_p]
     lib.nalar_stream.restype = C.c_void_p
     lib.nalar_last_error.argtypes = [C.c_void_p]
@@ -232,6 +239,26 @@ def nalar_exchange_buffer(h) -> tuple[int, int]:
     n = C.c_size_t()
     _check(h, _lib.nalar_exchange_buffer(h, C.byref(p), C.byref(n)), "exchange_buffer")
     return p.value, n.value
+
+
+def nalar_peer_buffer(h) -> tuple[int, bytes]:
+    """NALAR_COLL_PEER: this rank's receive buffer (device pointer, 64-byte IPC handle)."""
+    p = C.c_void_p()
+    hb = (C.c_ubyte * 64)()
+    _check(h, _lib.nalar_peer_buffer(h, C.byref(p), hb), "peer_buffer")
+    return p.value, bytes(hb)
+
+
+def nalar_peer_connect(h, ptrs=None, handles=None) -> None:
+    """Every rank's receive buffer: ``ptrs[q]`` (device pointers valid in this
+    process, None where absent) and / or ``handles[q]`` (64-byte IPC handles)."""
+    pa = None
+    if ptrs is not None:
+        pa = (C.c_void_p * len(ptrs))(*[p or None for p in ptrs])
+    ha = None
+    if handles is not None:
+        ha = (C.c_ubyte * (64 * len(handles))).from_buffer_copy(b"".join(x or bytes(64) for x in handles))
+    _check(h, _lib.nalar_peer_connect(h, pa, ha), "peer_connect")
 
 
 def nalar_epoch_finish(h) -> int:
@@ -385,6 +412,13 @@ class Context:
 
     def exchange_buffer(self):
         return nalar_exchange_buffer(self.h)
+
+    def peer_buffer(self):
+        """NALAR_COLL_PEER: (device pointer, IPC handle bytes) of this rank's receive buffer."""
+        return nalar_peer_buffer(self.h)
+
+    def peer_connect(self, ptrs=None, handles=None) -> None:
+        nalar_peer_connect(self.h, ptrs, handles)
 
     def stats(self) -> nalar_epoch_stats:
         return nalar_epoch_stats_get(self.h)

@@ -34,3 +34,27 @@ def slot_view(buf: np.ndarray, G: int, R: int, levels: int, n_inst: int):
     """(H[G][R][Lv], load[I], tot[R]) views of an exchange buffer (host side)."""
     n = G * R * levels
     return buf[:n].reshape(G, R, levels), buf[n:n + n_inst], buf[n + n_inst:n + n_inst + R]
+
+
+def connect_peers(ctx, group=None) -> None:
+    """NALAR_COLL_PEER across processes: every rank publishes the CUDA IPC
+    handle of its receive buffer, gathers everyone's (ordered by rank) and
+    opens them in its context.  Collective over ``group`` (any backend that
+    carries Python objects, e.g. gloo or nccl)."""
+    import torch.distributed as dist
+    _, handle = ctx.peer_buffer()
+    world = dist.get_world_size(group)
+    got = [None] * world
+    dist.all_gather_object(got, (dist.get_rank(group), handle), group=group)
+    handles = [None] * world
+    for r, h in got:
+        handles[r] = h
+    ctx.peer_connect(handles=handles)
+
+
+def connect_local(ctxs) -> None:
+    """NALAR_COLL_PEER for ranks driven by one process (one context per rank,
+    in rank order): the receive buffers are exchanged as device pointers."""
+    ptrs = [c.peer_buffer()[0] for c in ctxs]
+    for c in ctxs:
+        c.peer_connect(ptrs=ptrs)

@@ -147,3 +147,63 @@ def test_shard_bounds_balanced():
         for p in parts:
             e = p.edges & 0x7FFFFFFF
             assert (e < max(p.n_futures, 1)).all()
+
+
+class _FakePeerCtx:
+    """Stands in for a NALAR_COLL_PEER context: a per-rank IPC handle, and a
+    record of what peer_connect received."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.got = None
+
+    def peer_buffer(self):
+        return 0x1000 * (self.rank + 1), bytes([self.rank]) * 64
+
+    def peer_connect(self, ptrs=None, handles=None):
+        self.got = (ptrs, handles)
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2601_05109_b200.sharding import connect_peers
+        ctx = _FakePeerCtx(rank)
+        connect_peers(ctx)
+        ptrs, handles = ctx.got
+        assert ptrs is None
+        assert handles == [bytes([r]) * 64 for r in range(world)], handles
+        q.put((rank, "ok", 0))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_connect_peers_gathers_handles_in_rank_order(world):
+    """sharding.connect_peers (NALAR_COLL_PEER across processes): every rank
+    ends up with every rank's IPC handle, indexed by rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    bad = [r for r in res if r[1] != "ok"]
+    assert not bad, bad
+
+
+def test_connect_local_exchanges_pointers():
+    from paper_2601_05109_b200.sharding import connect_local
+    ctxs = [_FakePeerCtx(r) for r in range(4)]
+    connect_local(ctxs)
+    for c in ctxs:
+        assert c.got[0] == [0x1000 * (r + 1) for r in range(4)] and c.got[1] is None
