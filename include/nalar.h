@@ -371,7 +371,7 @@ int nalar_epoch_stats_get(nalar_ctx* ctx, nalar_epoch_stats* stats);
 
 /* Diagnostics (NALAR_F_PROFILE): copy the last epoch's K1 timeline to host:
  * words [0, 2W): start/end ns of each workflow's sweep; then per K1 block b
- * 8 words: staged, swept, bucketed, entered, finished, fenced, prepped, 0; then per resource r 8 words of
+ * 8 words: staged, swept, bucketed, entered, finished, fenced, prepped, dependency-waited; then per resource r 8 words of
  * K4: start, admitted count known, slot tables built, done, sweep complete, walk prefix, first
  * live compaction, 0; then per workflow 4 words:
  * SM cycles in the sweep's edge loop / settling rounds / the rest, and the

@@ -157,7 +157,7 @@ __device__ __forceinline__ bool util_gt(const TypeStat& a, const TypeStat& b) {
 // the last K4 block (ticket) pairs the k-th hottest with the k-th coldest type
 __device__ __forceinline__ uint64_t gtimer2() {
     uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");   // memory: not hoisted across the code it times
     return t;
 }
 __device__ void reassign_finish(const AssignParams& p, uint32_t* s_last, TypeStat* s_ts, const uint16_t* s_tmin,
@@ -233,7 +233,7 @@ __device__ void reassign_finish(const AssignParams& p, uint32_t* s_last, TypeSta
 
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");   // memory: not hoisted across the code it times
     return t;
 }
 
@@ -654,7 +654,12 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // A programmatic (PDL) launch lets K4's blocks load their static tables
+    // while K1 runs, but measured 0.85 us SLOWER per epoch at C4 (44.45 vs
+    // 43.60 us, scripts/env_sweep.sh): a plain launch is the default,
+    // NALAR_K4_PDL=1 restores the early launch.
+    static const bool pdl = [] { const char* e = getenv("NALAR_K4_PDL"); return e && atoi(e) != 0; }();
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k4_assign, p);
 }
 

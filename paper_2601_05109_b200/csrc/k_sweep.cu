@@ -79,7 +79,7 @@ constexpr uint32_t kStepDone = 0x4000u;   // aux[c0] bit: the step's transfer is
 
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");   // memory: not hoisted across the code it times
     return t;
 }
 
@@ -827,7 +827,8 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     // the exchange buffer / counters this kernel accumulates into are cleared by
     // the zero kernel this one depends on programmatically (PDL): everything
     // above only staged inputs and wrote shared memory and plain outputs
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (bprof && tid == 0) bprof[7] = gtimer();
 
     // ---- P3 (row-parallel): level, status, outputs, histogram, minima --------
     const uint32_t pol = p.policy;
@@ -964,37 +965,37 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     __syncthreads();
     if (bprof && tid == 0) bprof[4] = gtimer();
 
-    // per-workflow aggregates out (coalesced): total, pending, ready, inflight,
-    // resolved, failed, doomed, pinned_pending, max_depth, max_round
-    for (uint32_t k = tid; k < nw * 10; k += kK1Threads) {
-        const uint32_t wl = k / 10, j = k - wl * 10;
-        uint32_t v;
-        if (j == 0) v = wfo[wl + 1] - wfo[wl];
-        else if (j <= 7) v = s_agg[wl * 8 + j - 1];
-        else if (j == 8) v = s_agg[wl * 8 + 7];
-        else v = s_wrnd[wl];
-        p.wf_agg[(size_t)w0 * 10 + k] = v;
-    }
-    // K,V-cache retention hints per (workflow, SESSION type) (PAPER.md:524-529,
-    // SPEC kv_hint S:542; DESIGN.md Q-kv): retain while the session has a live
-    // future, offload when only its workflow does, drop when neither
-    for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
-        const uint32_t wl = k / T, t = k - wl * T;
-        const bool sess = s_aff[t] == 1u;
-        const uint32_t home = s_khome[k], kl = s_klev[k];
-        const uint32_t* a = s_agg + (size_t)wl * 8;
-        const uint32_t wf_live = a[0] - a[5] + a[2];      // pending - doomed + in flight
-        const bool has = sess && home != 0xFFFFFFFFu;
-        p.kv_hint[(size_t)w0 * T + k] = (uint8_t)(has ? (kl ? 1u : (wf_live ? 2u : 3u)) : 0u);
-        p.kv_level[(size_t)w0 * T + k] = (uint8_t)(sess && kl ? kl - 1u : 0u);
-        p.kv_home[(size_t)w0 * T + k] = (int16_t)(has ? (int)home : -1);
-    }
-
     // ---- P4: the stateful fence and first placement
-    // make the per-(workflow, type) winner eligible
-    for (uint32_t k = tid; k < nw * T; k += kK1Threads) {
-        const uint32_t wl = k / T, t = k - wl * T;
+    // make the per-(workflow, type) winner eligible; the per-workflow and
+    // per-(workflow, type) outputs ride in the same pass over (w, t)
+    // (T == 0 only for a table without futures: one pseudo-type per workflow)
+    const uint32_t Tp = T ? T : 1u;
+    for (uint32_t k = tid; k < nw * Tp; k += kK1Threads) {
+        const uint32_t wl = k / Tp, t = k - wl * Tp;
         const uint32_t aff = s_aff[t];
+        const uint32_t* a = s_agg + (size_t)wl * 8;
+        if (t == 0) {
+            // per-workflow aggregates: total, pending, ready, inflight, resolved,
+            // failed, doomed, pinned_pending, max_depth, max_round
+            uint32_t* o = p.wf_agg + (size_t)(w0 + wl) * 10;
+            o[0] = wfo[wl + 1] - wfo[wl];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[1 + j] = a[j];
+            o[9] = s_wrnd[wl];
+        }
+        if (T == 0) continue;
+        {
+            // K,V-cache retention hints per (workflow, SESSION type) (PAPER.md:524-529,
+            // SPEC kv_hint S:542; DESIGN.md Q-kv): retain while the session has a
+            // live future, offload when only its workflow does, drop when neither
+            const bool sess = aff == 1u;
+            const uint32_t home = s_khome[k], kl = s_klev[k];
+            const uint32_t wf_live = a[0] - a[5] + a[2];      // pending - doomed + in flight
+            const bool has = sess && home != 0xFFFFFFFFu;
+            p.kv_hint[(size_t)w0 * T + k] = (uint8_t)(has ? (kl ? 1u : (wf_live ? 2u : 3u)) : 0u);
+            p.kv_level[(size_t)w0 * T + k] = (uint8_t)(sess && kl ? kl - 1u : 0u);
+            p.kv_home[(size_t)w0 * T + k] = (int16_t)(has ? (int)home : -1);
+        }
         uint32_t f = 0xFFFFFFFFu;
         if (aff == 2u) {
             const uint32_t c = s_wfp[k];
@@ -1122,8 +1123,9 @@ cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s) {
-    if (p.B == 0) return cudaSuccess;
+cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
+    if (p_in.B == 0) return cudaSuccess;
+    SweepParams p = p_in;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1139,7 +1141,9 @@ cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool pdl = [] { const char* e = getenv("NALAR_K1_PDL"); return !e || atoi(e) != 0; }();
+    cfg.numAttrs = pdl ? 1 : 0;
+    p.pdl = pdl ? 1u : 0u;
     return cudaLaunchKernelEx(&cfg, k1_sweep, p);
 }
 

@@ -56,6 +56,8 @@ res = {
     "bucket_ns_max": int(np.max(blk[:, 2] - blk[:, 1])), "bucket_ns_mean": float(np.mean(blk[:, 2] - blk[:, 1])),
     "p1_ns_max": int(np.max(blk[:, 6] - blk[:, 0])), "stage_to_p1_ns_max": int(np.max(blk[:, 0] - blk[:, 3])),
     "p3_ns_max": int(np.max(blk[:, 4] - blk[:, 1])), "p3_ns_mean": float(np.mean(blk[:, 4] - blk[:, 1])),
+    "gdc_wait_ns_max": int(np.max(blk[:, 7] - blk[:, 1])), "gdc_wait_ns_mean": float(np.mean(blk[:, 7] - blk[:, 1])),
+    "p3_body_ns_max": int(np.max(blk[:, 4] - blk[:, 7])), "p3_body_ns_mean": float(np.mean(blk[:, 4] - blk[:, 7])),
     "p4_ns_max": int(np.max(blk[:, 5] - blk[:, 4])), "p5_ns_max": int(np.max(blk[:, 2] - blk[:, 5])),
     "p5_ns_mean": float(np.mean(blk[:, 2] - blk[:, 5])),
     "wf_dur_ns_max": int(dur.max()), "wf_dur_ns_mean": float(dur.mean()),
