@@ -799,14 +799,22 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
     c->h_err[4] = 0;
+    // Every kernel is loaded now (once per process): under CUDA lazy loading
+    // the first launch of a kernel waits for the device to go idle -- a
+    // latency spike in the first epoch / delta, and in NALAR_COLL_PEER, where
+    // a rank's wait kernel spins until the other ranks push, ranks driven by
+    // one host thread would stall until the exchange times out.
+    {
+        static uint64_t loaded = 0;            // per device (modules load per context)
+        const uint64_t bit = 1ull << (cfg->device & 63);
+        if (!(loaded & bit)) {
+            for (auto f : {preload_k_assign, preload_k_batch, preload_k_delta, preload_k_io, preload_k_migrate,
+                           preload_k_peer, preload_k_sweep, preload_k_validate})
+                if (f() != cudaSuccess) return bail(NALAR_E_CUDA);
+            loaded |= bit;
+        }
+    }
     if (cfg->collective == NALAR_COLL_PEER) {
-        // Every kernel is loaded now: under CUDA lazy loading the first launch
-        // of a kernel waits for the device to go idle, and a rank's gather
-        // kernel spins until the other ranks push -- ranks driven by one host
-        // thread would stall until the exchange times out.
-        for (auto f : {preload_k_assign, preload_k_batch, preload_k_delta, preload_k_io, preload_k_migrate,
-                       preload_k_peer, preload_k_sweep, preload_k_validate})
-            if (f() != cudaSuccess) return bail(NALAR_E_CUDA);
         c->peer_par_words = peer_par_words((uint32_t)cfg->world, c->Rhmax, c->Lv, cfg->max_instances);
         const size_t bytes = peer_buffer_bytes((uint32_t)cfg->world, c->Rhmax, c->Lv, cfg->max_instances);
         if (cudaMalloc(&c->peer_buf, bytes) != cudaSuccess) return bail(NALAR_E_NOMEM);
