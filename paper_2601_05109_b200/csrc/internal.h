@@ -76,7 +76,9 @@ struct ValidateParams {
     const uint32_t* edges;
     const uint8_t* i_type;
     uint32_t n_wf, n_fut, n_edges, n_types, n_inst;
-    unsigned long long* err;   // [0] = min bad row (init ~0), [1] = structural flag
+    unsigned long long* err;   // [0] = min bad row (init ~0), [1] = structural flag (device)
+    uint32_t* done;            // block-completion counter (0 between launches)
+    unsigned long long* host_err;   // mapped host words: the last block publishes err here and re-arms it
 };
 
 struct SweepParams {

@@ -46,6 +46,7 @@ __device__ __forceinline__ void copy_chunk(const CopyParams& p, uint64_t q) {
 // grid-stride over the chunks, four chunks per thread per trip so several
 // bus reads are in flight per thread
 __global__ void __launch_bounds__(256) k_copy_segs(CopyParams p) {
+    asm volatile("griddepcontrol.launch_dependents;");   // K0 may launch (it waits for completion)
     const uint64_t total = p.chunk_off[p.n];
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t q0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += 4 * stride) {

@@ -163,6 +163,7 @@ struct nalar_ctx {
     void* peer_ipc[kPeerMaxRanks] = {};      // opened IPC mappings (closed on destroy)
     bool peers_ready = false;
     unsigned long long* peer_err_dev = nullptr;   // device view of h_err[4]
+    unsigned long long* h_err_dev = nullptr;      // device view of h_err
     // delta mode: device workflow ids, the second table buffer set, host mirror
     uint64_t* d_wf_id = nullptr;
     struct Alt {
@@ -305,7 +306,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->scr = L.off;
     L.off += (C_NUM + (size_t)p->Rmax + p->Rhmax) * 4;   // counters, n_adm[R], tot_loc[Rh]
     L.off = (L.off + 255) & ~(size_t)255;
-    p->err = L.take<unsigned long long>(2);
+    p->err = L.take<unsigned long long>(5);   // [0,1] delta, [2,3] K0, [4] K0 block counter
     p->total = L.off + 256;
     return true;
 }
@@ -669,14 +670,16 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
 // K0 over the current table; synchronises
 int validate_table(nalar_ctx* c, int64_t* err_row, const char*) {
     cudaStream_t st = c->stream;
-    CK(cudaMemsetAsync(c->d_err, 0xFF, 8, st));
-    CK(cudaMemsetAsync(c->d_err + 1, 0, 8, st));
+    c->h_err[0] = ~0ull;                  // the verdict when there is nothing to check
+    c->h_err[1] = 0ull;
     ValidateParams v{};
     v.wf_fut_off = c->d_wf_off; v.f_state = c->d_state; v.f_type = c->d_type; v.f_exec = c->d_exec;
     v.f_pin = c->d_pin; v.f_edge_off = c->d_eoff; v.edges = c->d_edges; v.i_type = c->d_itype;
-    v.n_wf = c->W; v.n_fut = c->N; v.n_edges = c->E; v.n_types = c->T; v.n_inst = c->I; v.err = c->d_err;
+    v.n_wf = c->W; v.n_fut = c->N; v.n_edges = c->E; v.n_types = c->T; v.n_inst = c->I;
+    v.err = c->d_err + 2;                 // K0's own words (re-armed by its last block)
+    v.done = (uint32_t*)(c->d_err + 4);
+    v.host_err = c->h_err_dev;            // K0 publishes [0] / [1] here
     CK(launch_validate(v, st));
-    CK(cudaMemcpyAsync(c->h_err, c->d_err, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (c->h_err[1]) return fail(c, NALAR_E_INVAL, "edge offsets not monotone");
     if (c->h_err[0] != ~0ull) {
@@ -799,6 +802,14 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
     c->h_err[4] = 0;
+    c->h_err_dev = (unsigned long long*)mapped_view(c->h_err);
+    if (!c->h_err_dev) return bail(NALAR_E_CUDA);
+    {   // K0's device words: min bad row ~0, structural 0, block counter 0
+        const unsigned long long init[5] = {~0ull, ~0ull, ~0ull, 0ull, 0ull};
+        if (cudaMemcpyAsync(c->d_err, init, sizeof init, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+            cudaStreamSynchronize(c->stream) != cudaSuccess)
+            return bail(NALAR_E_CUDA);
+    }
     // Every kernel is loaded now (once per process): under CUDA lazy loading
     // the first launch of a kernel waits for the device to go idle -- a
     // latency spike in the first epoch / delta, and in NALAR_COLL_PEER, where
