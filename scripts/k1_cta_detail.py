@@ -62,7 +62,7 @@ for c in order:
     ws = np.nonzero(cta == c)[0]
     res["ctas"].append({
         "cta": int(c), "end_ns": int(end_blk[c]), "swept_ns": int(blk[c, 1] - t0),
-        "p3_done_ns": int(blk[c, 4] - t0), "p4_done_ns": int(blk[c, 5] - t0),
+        "p2_done_ns": int(blk[c, 7] - t0), "p3_done_ns": int(blk[c, 4] - t0), "p4_done_ns": int(blk[c, 5] - t0),
         "staged_ns": int(blk[c, 0] - t0),
         "transfer": {"n": int(tx[c, 5]), "cyc_edges_iface_settle_store": [int(x) for x in tx[c, :4]],
                      "iters": int(tx[c, 4]), "K_sum": int(tx[c, 6]), "k_sum": int(tx[c, 7])},
