@@ -176,3 +176,53 @@ def test_peer_exchange_across_processes_ipc():
         p.join(timeout=60)
     bad = [r for r in res if r[1] != "ok"]
     assert not bad, bad
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_peer_exchange_with_reassignment(G):
+    """NEXT-2 over the peer exchange: every rank reports the oracle's global
+    kill / provision commands (the type statistics are built from the gathered
+    buffer, identical on every rank)."""
+    s = c4(2)
+    o = oracle_epoch(s, "srtf", reassign={"u_hi_pct": 80, "u_lo_pct": 30})
+    ctxs, shards, _ = _ranks(s, G)
+    for c, sh in zip(ctxs, shards):
+        c.set_policy_params(reassign=True, u_hi_pct=80, u_lo_pct=30)
+        c.upload(sh)
+    for _ in range(3):
+        for c in ctxs:
+            c.epoch("srtf")
+    outs = [(c.fetch(), sh) for c, sh in zip(ctxs, shards)]
+    _check(o, outs, f"reassign G={G}")
+    for g, _ in outs:
+        assert np.array_equal(g["ra_kill"], o["ra_kill"]) and np.array_equal(g["ra_prov"], o["ra_prov"])
+        assert np.array_equal(g["t_busy"], o["t_busy"]) and np.array_equal(g["t_capsum"], o["t_cap"])
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("levels", [1, 7, 256])
+def test_peer_exchange_levels(levels):
+    """Other level counts change the slot size (R x Lv): layout offsets on
+    both sides of the exchange must agree."""
+    import torch
+    from paper_2601_05109_b200 import nalar
+    from paper_2601_05109_b200.sharding import connect_local, shard_bounds
+    s = swe_table(7000, seed=31)
+    o = oracle_epoch(s, "srtf", levels=levels)
+    G = 3
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    ctxs, shards = [], []
+    for k, (w0, w1) in enumerate(shard_bounds(s.wf_fut_off, G)):
+        ctxs.append(nalar.Context.for_snapshot(s, world=G, rank=k, collective=nalar.NALAR_COLL_PEER,
+                                               stream=streams[k].cuda_stream, levels=levels))
+        shards.append(s.slice_workflows(w0, w1))
+    connect_local(ctxs)
+    for c, sh in zip(ctxs, shards):
+        c.upload(sh)
+    for _ in range(2):
+        for c in ctxs:
+            c.epoch("srtf")
+    _check(o, [(c.fetch(), sh) for c, sh in zip(ctxs, shards)], f"levels={levels}")
+    for c in ctxs:
+        c.close()
