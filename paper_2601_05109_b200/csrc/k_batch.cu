@@ -12,16 +12,22 @@
 // both are already in the O4 order (K4 places an admitted future at its rank),
 // so a two-way merge on (level desc, row asc) yields the instance's sequence,
 // which is then cut per method into batches of max_batch.  The sequences are
-// short (at most the instance's spare capacity), so the merge runs on one
-// thread while the others stage the per-method counters.
+// short (at most the instance's spare capacity): both are staged in shared
+// memory by the block (the phase-B entries naming the instance compacted in
+// order), then merged on one thread.
 #include "internal.h"
 
 namespace nalar {
 
+constexpr uint32_t kK6Stage = 1024;     // staged entries per sequence
+constexpr uint32_t kK6Scan = 1u << 16;  // phase-B region scanned by one warp at most
+
 __global__ void __launch_bounds__(64) k6_batch(BatchParams p) {
     __shared__ uint32_t s_cnt[256];
     __shared__ int32_t s_head[256];
-    __shared__ uint32_t s_offA, s_offB;
+    __shared__ uint32_t s_offA, s_offB, s_nbi;
+    __shared__ uint32_t s_a[kK6Stage], s_b[kK6Stage];
+    __shared__ uint8_t s_la[kK6Stage], s_lb[kK6Stage], s_ma[kK6Stage], s_mb[kK6Stage];
     const uint32_t i = blockIdx.x, tid = threadIdx.x;
     const uint32_t t = p.i_type[i];
     const uint32_t mb = p.t_max_batch[t];
@@ -41,12 +47,68 @@ __global__ void __launch_bounds__(64) k6_batch(BatchParams p) {
     if (a) atomicAdd(&s_offA, a);
     if (b) atomicAdd(&s_offB, b);
     __syncthreads();
-    if (tid != 0) return;
     const uint32_t nA = p.n_adm[i], nB = p.n_adm[rB];
     const uint32_t* A = p.arow + s_offA;
     const uint32_t* Brow = p.arow + s_offB;
     const int16_t* Binst = p.ainst + s_offB;
-    uint32_t ia = 0, ib = 0, nb = 0;
+    uint32_t nb = 0;
+    if (nA <= kK6Stage && nB <= kK6Scan) {
+        // stage both sequences in shared memory with their levels and methods
+        // (warp 0: the phase-B entries naming this instance, compacted in
+        // order; warp 1: the phase-A rows) -- the merge then runs on shared
+        // memory instead of one dependent global load per entry
+        const uint32_t lane = tid & 31u, warp = tid >> 5;
+        if (warp == 0) {
+            uint32_t n = 0;
+            for (uint32_t k0 = 0; k0 < nB; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                const bool hit = k < nB && Binst[k] == (int16_t)i;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+                if (hit) {
+                    const uint32_t o = n + __popc(bal & ((1u << lane) - 1u));
+                    if (o < kK6Stage) {
+                        const uint32_t f = Brow[k];
+                        s_b[o] = f;
+                        s_lb[o] = p.level[f];
+                        s_mb[o] = p.f_method ? p.f_method[f] : 0u;
+                    }
+                }
+                n += __popc(bal);
+            }
+            if (lane == 0) s_nbi = n;
+        } else {
+            for (uint32_t k = lane; k < nA; k += 32) {
+                const uint32_t f = A[k];
+                s_a[k] = f;
+                s_la[k] = p.level[f];
+                s_ma[k] = p.f_method ? p.f_method[f] : 0u;
+            }
+        }
+        __syncthreads();
+        if (tid != 0) return;
+        const uint32_t nBi = s_nbi;
+        if (nBi <= kK6Stage) {
+            uint32_t ia = 0, ib = 0;
+            while (ia < nA || ib < nBi) {
+                bool take_a;
+                if (ib >= nBi) take_a = true;
+                else if (ia >= nA) take_a = false;
+                else take_a = s_la[ia] > s_lb[ib] || (s_la[ia] == s_lb[ib] && s_a[ia] < s_b[ib]);
+                const uint32_t f = take_a ? s_a[ia] : s_b[ib];
+                const uint32_t m = take_a ? s_ma[ia] : s_mb[ib];
+                if (take_a) ++ia; else ++ib;
+                const uint32_t k = s_cnt[m]++;
+                if (k % mb == 0u) { s_head[m] = (int32_t)f; ++nb; }
+                p.batch_head[f] = s_head[m];
+            }
+            if (nb) atomicAdd(&p.counters[C_BATCHES], nb);
+            return;
+        }
+    } else if (tid != 0) {
+        return;
+    }
+    // large sequences: merge straight from global memory on one thread
+    uint32_t ia = 0, ib = 0;
     // next phase-B entry at this instance
     auto nextB = [&](uint32_t k) {
         while (k < nB && Binst[k] != (int16_t)i) ++k;

@@ -62,3 +62,26 @@ def test_batch_managed_state_rejected_and_off():
     g = ctx.fetch()
     assert g["n_batches"] == 0 and (g["batch_head"] == -1).all()
     ctx.close()
+
+
+@pytest.mark.parametrize("unpin", [False, True])
+def test_batch_long_sequences_fallback(unpin):
+    """Instances receiving more futures than K6 stages in shared memory (1024
+    per sequence): one instance per type takes all of its type's work, so its
+    sequence (phase B, or phase A once every future is pinned to it) exceeds
+    the staging and the global-memory merge runs -- the same batches."""
+    from nalar_gen import swe_table
+    s = swe_table(400000, seed=7)
+    s.t_affinity[:] = AFF_NONE
+    first = np.array([np.nonzero(s.i_type == t)[0][0] for t in range(s.n_types)])
+    cap = np.zeros(s.n_instances, dtype=s.i_cap.dtype)
+    cap[first] = 1000000
+    s.i_cap[:] = cap
+    s.i_base_load[:] = 0
+    if unpin:
+        s.f_pin[:] = np.where(s.f_state == 0, first[s.f_type], s.f_pin)
+    rng = np.random.default_rng(5)
+    s.f_method = rng.integers(0, 3, s.n_futures)
+    o = check(s, np.full(s.n_types, 5), epochs=2)
+    inst = o["instance"][o["status"] == 7]
+    assert np.bincount(inst).max() > 1024
