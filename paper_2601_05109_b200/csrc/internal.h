@@ -84,6 +84,7 @@ struct ValidateParams {
 struct SweepParams {
     uint32_t long_rows;          // workflows of >= long_rows rows are composed from step transfers
     uint32_t pdl;                // launched as a programmatic dependent of the zero kernel
+    uint32_t trig;               // where K1 lets its dependent launch: 0 entry, 1 after P2, 2 before P5
     const uint32_t* wf_fut_off;
     const int32_t* wf_prio;
     const uint8_t* f_state;

@@ -655,10 +655,10 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     // A programmatic (PDL) launch lets K4's blocks load their static tables
-    // while K1 runs, but measured 0.85 us SLOWER per epoch at C4 (44.45 vs
-    // 43.60 us, scripts/env_sweep.sh): a plain launch is the default,
-    // NALAR_K4_PDL=1 restores the early launch.
-    static const bool pdl = [] { const char* e = getenv("NALAR_K4_PDL"); return e && atoi(e) != 0; }();
+    // while K1 finishes.  Released at K1's entry it measured 0.85 us slower
+    // per epoch than a plain launch; released before K1's P5 (SweepParams::trig)
+    // 0.6 us faster (scripts/trig_sweep.sh).  NALAR_K4_PDL=0: plain launch.
+    static const bool pdl = [] { const char* e = getenv("NALAR_K4_PDL"); return !e || atoi(e) != 0; }();
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k4_assign, p);
 }

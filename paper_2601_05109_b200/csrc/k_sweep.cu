@@ -183,9 +183,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     constexpr bool staged = kStaged;
     unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;
     if (bprof && tid == 0) bprof[3] = gtimer();
-    // let the assignment kernel launch now (PDL); it waits for this grid's
-    // completion before reading anything the sweep writes
-    asm volatile("griddepcontrol.launch_dependents;");
+    // the point where the assignment kernel may launch (PDL) is p.trig; it
+    // waits for this grid's completion before reading anything the sweep writes
+    if (p.trig == 0) asm volatile("griddepcontrol.launch_dependents;");
 
     // ---- carve the fixed part --------------------------------------------
     uint8_t* sp = smem;
@@ -828,6 +828,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     // the zero kernel this one depends on programmatically (PDL): everything
     // above only staged inputs and wrote shared memory and plain outputs
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.trig == 1) asm volatile("griddepcontrol.launch_dependents;");
     if (bprof && tid == 0) bprof[7] = gtimer();
 
     // ---- P3 (row-parallel): level, status, outputs, histogram, minima --------
@@ -1022,6 +1023,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     __syncthreads();
     if (bprof && tid == 0) bprof[5] = gtimer();
 
+    if (p.trig == 2) asm volatile("griddepcontrol.launch_dependents;");
     // ---- P5 (epilogue): loads, per-resource offsets, stable bucketing ---------
     for (uint32_t i = tid; i < I; i += kK1Threads)
         if (s_load[i]) atomicAdd(&p.load_part[i], s_load[i]);
@@ -1144,6 +1146,11 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     static const bool pdl = [] { const char* e = getenv("NALAR_K1_PDL"); return !e || atoi(e) != 0; }();
     cfg.numAttrs = pdl ? 1 : 0;
     p.pdl = pdl ? 1u : 0u;
+    // K4's early launch is released before P5 (measured: at K1's entry the
+    // early K4 blocks cost as much as they save; before P5 -0.6 us / epoch;
+    // NALAR_K1_TRIGGER=0 / 1 / 2 = entry / after P2 / before P5)
+    static const uint32_t trig = [] { const char* e = getenv("NALAR_K1_TRIGGER"); return e ? (uint32_t)atoi(e) : 2u; }();
+    p.trig = trig;
     return cudaLaunchKernelEx(&cfg, k1_sweep, p);
 }
 
