@@ -226,3 +226,23 @@ def test_peer_exchange_levels(levels):
     _check(o, [(c.fetch(), sh) for c, sh in zip(ctxs, shards)], f"levels={levels}")
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_peer_exchange_random_tables(seed):
+    """Random small tables (pins, mixed affinities, empty shards at larger G)
+    over the peer exchange, three policies."""
+    G = 2 + seed % 6
+    s = random_table(300 + seed, n_workflows=4 + seed % 9, max_rows=6 + seed % 20, n_types=1 + seed % 3,
+                     inst_per_type=(1, 3), consistent=seed % 2 == 0, max_cap=2 + seed % 7, p_pin=0.3)
+    pol = ["fcfs", "srtf", "lpt"][seed % 3]
+    o = oracle_epoch(s, pol)
+    ctxs, shards, _ = _ranks(s, G)
+    for c, sh in zip(ctxs, shards):
+        c.upload(sh)
+    for _ in range(2):
+        for c in ctxs:
+            c.epoch(pol)
+    _check(o, [(c.fetch(), sh) for c, sh in zip(ctxs, shards)], f"seed={seed} G={G}")
+    for c in ctxs:
+        c.close()
