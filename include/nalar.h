@@ -363,6 +363,17 @@ int nalar_epoch_finish(nalar_ctx* ctx);
 int nalar_peer_buffer(nalar_ctx* ctx, void** dev_ptr, unsigned char ipc_handle[64]);
 int nalar_peer_connect(nalar_ctx* ctx, void* const* ptrs, const unsigned char* handles);
 
+/* One controller step in one call: upload `snap` (as nalar_snapshot_upload),
+ * run the policy epoch and fetch the decisions into `out` (as
+ * nalar_fetch_decisions), with ONE synchronisation instead of three: the
+ * table's validation (K0) is queued ahead of the epoch and its verdict is read
+ * after the fetch; the epoch kernels read it on the device and skip an invalid
+ * table.  Errors: those of the three calls; on NALAR_E_INVAL (invalid table,
+ * *err_row = the smallest offending row as for upload) the contents of `out`
+ * are unspecified and the context is left not uploaded.  Not with
+ * NALAR_COLL_EXTERNAL (use the split calls). */
+int nalar_step(nalar_ctx* ctx, const nalar_snapshot* snap, int policy, nalar_decisions* out, int64_t* err_row);
+
 /* Copy decisions to caller host buffers; synchronises the ctx stream. */
 int nalar_fetch_decisions(nalar_ctx* ctx, nalar_decisions* out);
 

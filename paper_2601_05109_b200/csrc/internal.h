@@ -79,9 +79,11 @@ struct ValidateParams {
     unsigned long long* err;   // [0] = min bad row (init ~0), [1] = structural flag (device)
     uint32_t* done;            // block-completion counter (0 between launches)
     unsigned long long* host_err;   // mapped host words: the last block publishes err here and re-arms it
+    unsigned long long* verdict;    // device word: 1 if the table is invalid (the epoch kernels skip)
 };
 
 struct SweepParams {
+    const unsigned long long* verdict;   // K0's verdict: nonzero = invalid table, do nothing
     uint32_t long_rows;          // workflows of >= long_rows rows are composed from step transfers
     uint32_t pdl;                // launched as a programmatic dependent of the zero kernel
     uint32_t trig;               // where K1 lets its dependent launch: 0 entry, 1 after P2, 2 before P5
@@ -135,6 +137,7 @@ struct SweepParams {
 };
 
 struct AssignParams {
+    const unsigned long long* verdict;   // K0's verdict (see SweepParams)
     const uint32_t* H;          // [G][R][Lv] summed over ranks
     const uint32_t* load_sum;   // [I] summed over ranks
     const uint32_t* tot;        // [R] eligible futures per resource, summed over ranks
@@ -239,6 +242,7 @@ struct FetchParams {
 // K5 HoL migration (NEXT-1, k_migrate.cu); G == 1
 constexpr uint32_t kK5MaxInst = 256;    // instances per type the migration pass supports
 struct MigrateParams {
+    const unsigned long long* verdict;
     const uint32_t* H;          // [Rh][Lv] (this rank's slot == the sum when G == 1)
     const uint32_t* tot;        // [Rh]
     const uint32_t* cnt_rb;     // [Rh][B]
@@ -260,6 +264,7 @@ cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s);
 
 // K6 batch coalescing (NEXT-4, k_batch.cu); G == 1
 struct BatchParams {
+    const unsigned long long* verdict;
     const uint8_t* i_type;
     const uint16_t* t_max_batch;   // [T]
     const uint8_t* f_method;       // [N] or null

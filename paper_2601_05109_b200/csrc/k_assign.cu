@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     unsigned long long ra_busy = 0, ra_cap = 0;      // NEXT-2 partials of this thread's instances
     uint64_t ra_best = ~0ull;
 
+    if (*p.verdict) return;              // an invalid table (K0): nothing to assign
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     // type resources (the longest walks: phase B of a whole type) take the

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(64) k6_batch(BatchParams p) {
     __shared__ uint32_t s_offA, s_offB, s_nbi;
     __shared__ uint32_t s_a[kK6Stage], s_b[kK6Stage];
     __shared__ uint8_t s_la[kK6Stage], s_lb[kK6Stage], s_ma[kK6Stage], s_mb[kK6Stage];
+    if (*p.verdict) return;              // an invalid table (K0)
     const uint32_t i = blockIdx.x, tid = threadIdx.x;
     const uint32_t t = p.i_type[i];
     const uint32_t mb = p.t_max_batch[t];

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
     __shared__ uint2 s_c[kMigWin];                          // (row, local source) by rank - w0
     __shared__ uint32_t s_nt, s_lmin;
 
+    if (*p.verdict) return;              // an invalid table (K0)
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t t = blockIdx.x, r = p.R + t, Lv = p.levels, B = p.B;
     // ---- static: the type's instances, blocked flags (before the PDL wait) --

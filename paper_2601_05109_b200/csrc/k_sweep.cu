@@ -1108,6 +1108,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
 
 __global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
+    // an invalid table (K0's verdict, complete before the zero kernel ran)
+    // is never swept: nalar_step queues this kernel before the host has seen it
+    if (*p.verdict) return;
     if (p.blk_staged[blockIdx.x]) k1_body<true>(p, smem);
     else k1_body<false>(p, smem);
 }

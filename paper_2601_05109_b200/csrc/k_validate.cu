@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(kK0Threads) k0_validate(ValidateParams p) {
             volatile unsigned long long* h = p.host_err;
             h[0] = bad;
             h[1] = structural;
+            // the epoch kernels of a combined step (nalar_step) may already be
+            // queued behind this one: they read this word and skip an invalid table
+            *p.verdict = (bad != ~0ull || structural) ? 1ull : 0ull;
             *p.done = 0;
         }
     }

@@ -306,7 +306,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->scr = L.off;
     L.off += (C_NUM + (size_t)p->Rmax + p->Rhmax) * 4;   // counters, n_adm[R], tot_loc[Rh]
     L.off = (L.off + 255) & ~(size_t)255;
-    p->err = L.take<unsigned long long>(5);   // [0,1] delta, [2,3] K0, [4] K0 block counter
+    p->err = L.take<unsigned long long>(6);   // [0,1] delta, [2,3] K0, [4] K0 block counter, [5] verdict
     p->total = L.off + 256;
     return true;
 }
@@ -445,6 +445,7 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
 
 int run_k1(nalar_ctx* c, int policy) {
     SweepParams p{};
+    p.verdict = c->d_err + 5;
     p.long_rows = long_rows();
     p.wf_fut_off = c->d_wf_off; p.wf_prio = c->d_wf_prio;
     p.f_state = c->d_state; p.f_type = c->d_type; p.f_round = c->d_round;
@@ -480,6 +481,7 @@ int run_k1(nalar_ctx* c, int policy) {
 
 int run_k4(nalar_ctx* c) {
     AssignParams p{};
+    p.verdict = c->d_err + 5;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.H = c->d_x;
     p.load_sum = c->d_x + (size_t)G * c->Rh * c->Lv;
@@ -563,6 +565,7 @@ int enqueue_second_half(nalar_ctx* c) {
     if (rc) return rc;
     if (c->mig_active()) {          // K5 HoL migration (NEXT-1), after admission
         MigrateParams m{};
+        m.verdict = c->d_err + 5;
         m.H = c->d_x; m.tot = c->d_x + (size_t)c->Rh * c->Lv + c->I;
         m.cnt_rb = c->d_cnt_rb; m.off_rb = c->d_off_rb; m.blk_row0 = c->d_blk_row0; m.items = c->d_items;
         m.type_off = c->d_type_off; m.type_inst = c->d_type_inst;
@@ -574,6 +577,7 @@ int enqueue_second_half(nalar_ctx* c) {
     }
     if (c->batch_on) {              // K6 batch coalescing (NEXT-4), after admission
         BatchParams bp{};
+        bp.verdict = c->d_err + 5;
         bp.i_type = c->d_itype; bp.t_max_batch = c->d_tmaxb; bp.f_method = c->have_method ? c->d_method : nullptr;
         bp.level = c->d_level; bp.n_adm = c->d_scr + C_NUM; bp.tot_loc = c->d_scr + C_NUM + c->Rmax;
         bp.arow = c->d_arow; bp.ainst = c->d_ainst; bp.n_inst = c->I;
@@ -668,7 +672,17 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
 }
 
 // K0 over the current table; synchronises
-int validate_table(nalar_ctx* c, int64_t* err_row, const char*) {
+// K0's verdict as published into mapped host memory (valid after a sync)
+int validate_verdict(nalar_ctx* c, int64_t* err_row) {
+    if (c->h_err[1]) return fail(c, NALAR_E_INVAL, "edge offsets not monotone");
+    if (c->h_err[0] != ~0ull) {
+        if (err_row) *err_row = (int64_t)c->h_err[0];
+        return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
+    }
+    return NALAR_OK;
+}
+
+int validate_table(nalar_ctx* c, int64_t* err_row, const char*, bool sync = true) {
     cudaStream_t st = c->stream;
     c->h_err[0] = ~0ull;                  // the verdict when there is nothing to check
     c->h_err[1] = 0ull;
@@ -679,14 +693,11 @@ int validate_table(nalar_ctx* c, int64_t* err_row, const char*) {
     v.err = c->d_err + 2;                 // K0's own words (re-armed by its last block)
     v.done = (uint32_t*)(c->d_err + 4);
     v.host_err = c->h_err_dev;            // K0 publishes [0] / [1] here
+    v.verdict = c->d_err + 5;
     CK(launch_validate(v, st));
+    if (!sync) return NALAR_OK;           // nalar_step: the verdict is read after its one sync
     CK(cudaStreamSynchronize(st));
-    if (c->h_err[1]) return fail(c, NALAR_E_INVAL, "edge offsets not monotone");
-    if (c->h_err[0] != ~0ull) {
-        if (err_row) *err_row = (int64_t)c->h_err[0];
-        return fail(c, NALAR_E_INVAL, "invalid future row %llu", (unsigned long long)c->h_err[0]);
-    }
-    return NALAR_OK;
+    return validate_verdict(c, err_row);
 }
 
 }  // namespace
@@ -805,7 +816,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->h_err_dev = (unsigned long long*)mapped_view(c->h_err);
     if (!c->h_err_dev) return bail(NALAR_E_CUDA);
     {   // K0's device words: min bad row ~0, structural 0, block counter 0
-        const unsigned long long init[5] = {~0ull, ~0ull, ~0ull, 0ull, 0ull};
+        const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
         if (cudaMemcpyAsync(c->d_err, init, sizeof init, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
             cudaStreamSynchronize(c->stream) != cudaSuccess)
             return bail(NALAR_E_CUDA);
@@ -891,7 +902,36 @@ void* nalar_stream(nalar_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
+static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync);
+
 int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row) {
+    return upload_impl(c, s, err_row, true);
+}
+
+static int fetch_impl(nalar_ctx* c, nalar_decisions* o);
+static int peer_check(nalar_ctx* c, int rc);
+
+int nalar_step(nalar_ctx* c, const nalar_snapshot* s, int policy, nalar_decisions* out, int64_t* err_row) {
+    if (!c || !s || !out) return NALAR_E_INVAL;
+    if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
+        return fail(c, NALAR_E_STATE, "external collective: use the split calls");
+    if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
+    int rc = upload_impl(c, s, err_row, false);       // copies + K0 queued, no sync
+    if (rc) return rc;
+    rc = nalar_policy_epoch(c, policy);                // kernels skip an invalid table on the device
+    if (rc) { c->uploaded = false; return rc; }
+    rc = fetch_impl(c, out);                           // the one synchronisation
+    const int vr = validate_verdict(c, err_row);       // K0 ran before everything above
+    if (vr) {
+        c->uploaded = false;
+        c->epoch_done = false;
+        c->assign_valid = false;
+        return vr;
+    }
+    return peer_check(c, rc);
+}
+
+static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync) {
     // NALAR_TRACE_UPLOAD=1: host-side phase times of this call on stderr
     static const bool trace = getenv("NALAR_TRACE_UPLOAD") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::micro>(
@@ -989,7 +1029,7 @@ int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_ro
     c->blocks_valid = true;
     c->blocks_T = T;
     if (trace) tt[3] = now();
-    rc = validate_table(c, err_row, nullptr);
+    rc = validate_table(c, err_row, nullptr, sync);
     if (trace) {
         tt[4] = now();
         fprintf(stderr, "[nalar upload] checks+mirror %.1f us, array copies issued %.1f, tables+partition+kernel %.1f, "

@@ -33,7 +33,8 @@ EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
            "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile",
-           "nalar_delta_apply", "nalar_set_policy_params", "nalar_peer_buffer", "nalar_peer_connect")
+           "nalar_delta_apply", "nalar_set_policy_params", "nalar_peer_buffer", "nalar_peer_connect",
+           "nalar_step")
 NALAR_DELTA_APPLY_ASSIGNED = 1
 
 
@@ -128,6 +129,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_delta_apply.restype = C.c_int
     lib.nalar_set_policy_params.argtypes = [C.c_void_p, P(nalar_policy_params)]
     lib.nalar_set_policy_params.restype = C.c_int
+    lib.nalar_step.argtypes = [C.c_void_p, P(nalar_snapshot), C.c_int, P(nalar_decisions), P(C.c_int64)]
+    lib.nalar_step.restype = C.c_int
     lib.nalar_peer_buffer.argtypes = [C.c_void_p, P(C.c_void_p), C.c_void_p]
     lib.nalar_peer_buffer.restype = C.c_int
     lib.nalar_peer_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -369,17 +372,20 @@ class Context:
                     "f_pin", "f_edge_off", "edges", "i_type", "i_cap", "i_base_load", "t_affinity",
                     "f_age", "i_head_rem", "f_method")
 
-    def upload(self, s) -> None:
+    def _snap(self, s):
         # the marshalled struct is reused while the snapshot holds the same array
         # objects (they stay referenced by the cache, so their ids are stable)
         key = (id(s), int(getattr(s, "global_row_base", 0)),
                tuple(id(getattr(s, k, None)) for k in self._SNAP_FIELDS))
         cached = getattr(self, "_snap_cache", None)
         if cached is not None and cached[0] == key:
-            st, keep = cached[1], cached[2]
-        else:
-            st, keep = snapshot_struct(s)
-            self._snap_cache = (key, st, (keep, s))
+            return cached[1]
+        st, keep = snapshot_struct(s)
+        self._snap_cache = (key, st, (keep, s))
+        return st
+
+    def upload(self, s) -> None:
+        st = self._snap(s)
         rc, row = nalar_snapshot_upload(self.h, st)
         if rc:
             e = NalarError(rc, f"upload: {nalar_last_error(self.h)}")
@@ -445,9 +451,13 @@ class Context:
     def output_buffers(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg",
                                      "i_load", "i_spare", "i_assigned", "assign", "kv", "reassign",
                                      "migrate", "batch"),
-                       alloc=None):
-        """Host buffers for fetch(); ``alloc(n, dtype)`` may return pinned memory."""
-        N, W, I = self.n
+                       alloc=None, like=None):
+        """Host buffers for fetch() / step(); ``alloc(n, dtype)`` may return
+        pinned memory; sized for the uploaded table, or for snapshot ``like``."""
+        if like is not None:
+            N, W, I, Tn = like.n_futures, like.n_workflows, like.n_instances, like.n_types
+        else:
+            (N, W, I), Tn = self.n, self.n_types
         alloc = alloc or (lambda n, dt: np.zeros(n, dt))
         spec = {"status": (N, np.uint8), "level": (N, np.uint8), "depth": (N, np.uint16),
                 "instance": (N, np.int16), "new_pin": (N, np.uint8),
@@ -455,7 +465,7 @@ class Context:
                 "i_spare": (I, np.uint32), "i_assigned": (I, np.uint32)}
         out = {k: alloc(n, dt) for k, (n, dt) in spec.items() if k in fields}
         if "kv" in fields:
-            T = self.n_types
+            T = Tn
             out["kv_hint"] = alloc(W * T, np.uint8)
             out["kv_level"] = alloc(W * T, np.uint8)
             out["kv_home"] = alloc(W * T, np.int16)
@@ -466,7 +476,7 @@ class Context:
             out["i_mig_in"] = alloc(max(I, 1), np.uint32)
             out["i_mig_out"] = alloc(max(I, 1), np.uint32)
         if "reassign" in fields:
-            T = max(self.n_types, 1)
+            T = max(Tn, 1)
             out["t_busy"] = alloc(T, np.uint32)
             out["t_capsum"] = alloc(T, np.uint32)
             out["ra_kill"] = alloc(T, np.int16)
@@ -479,8 +489,33 @@ class Context:
     def fetch(self, fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
                             "i_spare", "i_assigned", "assign", "kv", "reassign", "migrate", "batch"),
               out=None) -> dict:
-        N, W, I = self.n
         bufs = out if out is not None else self.output_buffers(fields)
+        d = self._decisions(bufs, out is not None)
+        _check(self.h, nalar_fetch_decisions(self.h, d), "fetch_decisions")
+        return self._results(bufs, d)
+
+    def step(self, s, policy="srtf",
+             fields=("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load",
+                     "i_spare", "i_assigned", "assign", "kv", "reassign", "migrate", "batch"),
+             out=None) -> dict:
+        """upload + epoch + fetch in one library call (nalar_step): one
+        synchronisation, the table's validation checked on the device."""
+        pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        st = self._snap(s)
+        self.n = (s.n_futures, s.n_workflows, s.n_instances)
+        self.n_types = s.n_types
+        bufs = out if out is not None else self.output_buffers(fields)
+        d = self._decisions(bufs, out is not None)
+        row = C.c_int64(-1)
+        rc = _lib.nalar_step(self.h, C.byref(st), pol, C.byref(d), C.byref(row))
+        if rc:
+            e = NalarError(rc, f"step: {nalar_last_error(self.h)}")
+            e.err_row = row.value
+            raise e
+        return self._results(bufs, d)
+
+    def _decisions(self, bufs, cache):
+        N, W, I = self.n
         # the marshalled struct is reused while the caller passes the same
         # output arrays (they stay referenced by the cache, so ids are stable)
         key = (N, W, I, tuple((k, id(v), len(v)) for k, v in bufs.items()))
@@ -503,9 +538,12 @@ class Context:
             d.f_cap, d.wf_cap, d.i_cap = N, W, I
             if "assign_row" in bufs:
                 d.a_cap = min(len(bufs["assign_row"]), len(bufs["assign_inst"]))
-            if out is not None:
+            if cache:
                 self._out_cache = (key, d, dict(bufs))
-        _check(self.h, nalar_fetch_decisions(self.h, d), "fetch_decisions")
+        return d
+
+    def _results(self, bufs, d) -> dict:
+        N, W, I = self.n
         res = dict(bufs)
         if "wf_agg" in res:
             res["wf_agg"] = res["wf_agg"].reshape(W, 10)

@@ -1,0 +1,127 @@
+"""nalar_step (upload + epoch + fetch with one synchronisation) against the
+oracle and against the three split calls; invalid tables through the step
+(validation verdict read after the fetch, the epoch kernels skipping the
+table on the device)."""
+import numpy as np
+import pytest
+
+from nalar_gen import Snapshot, c1, c2, c4, random_table, swe_table
+from oracle import oracle_epoch
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load", "i_spare",
+        "i_assigned", "assign_row", "assign_inst", "kv_hint", "kv_level", "kv_home")
+
+
+def _nalar():
+    from paper_2601_05109_b200 import nalar
+    return nalar
+
+
+def same(o, g, tag):
+    for k in KEYS:
+        assert np.array_equal(np.asarray(o[k]), np.asarray(g[k])), (tag, k)
+
+
+def pinned_like(a, keep):
+    import torch
+    t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    keep.append(t)
+    v = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+    v[...] = a
+    return v
+
+
+@pytest.mark.parametrize("mk", [c1, lambda: c2(1), lambda: swe_table(5000, seed=3), c4,
+                                lambda: random_table(9, n_workflows=7, max_rows=30, consistent=True)])
+@pytest.mark.parametrize("policy", ["srtf", "lpt", "fcfs"])
+def test_step_matches_oracle(mk, policy):
+    nalar = _nalar()
+    s = mk()
+    o = oracle_epoch(s, policy)
+    ctx = nalar.Context.for_snapshot(s)
+    for _ in range(3):                       # direct launch, graph capture, replay
+        same(o, ctx.step(s, policy), f"{s.name} {policy}")
+    ctx.close()
+
+
+def test_step_pinned_in_and_out():
+    """The configuration bench.py's e2e leg times: pinned inputs and outputs."""
+    nalar = _nalar()
+    keep = []
+    s = c4()
+    o = oracle_epoch(s, "srtf")
+    sp = Snapshot(global_row_base=0, name="pinned", **{k: pinned_like(v, keep) for k, v in s.arrays().items()})
+    ctx = nalar.Context.for_snapshot(s)
+    out = ctx.output_buffers(("status", "instance", "assign"),
+                             alloc=lambda n, dt: pinned_like(np.zeros(n, dt), keep), like=s)
+    for _ in range(3):
+        g = ctx.step(sp, "srtf", ("status", "instance", "assign"), out=out)
+        for k in ("status", "instance", "assign_row", "assign_inst"):
+            assert np.array_equal(np.asarray(o[k]), np.asarray(g[k])), k
+    ctx.close()
+
+
+def _bad_edge(s, row, to):
+    arrs = s.arrays()
+    edges = arrs["edges"].copy()
+    edges[int(arrs["f_edge_off"][row])] = to
+    return Snapshot(global_row_base=0, name="bad", **{**arrs, "edges": edges})
+
+
+def test_step_invalid_table_reports_row_then_recovers():
+    nalar = _nalar()
+    s = swe_table(6000, seed=4)
+    # a forward edge from some row with edges: the smallest offending row is reported
+    rows = np.nonzero(np.diff(s.f_edge_off.astype(np.int64)) > 0)[0]
+    r = int(rows[len(rows) // 2])
+    bad = _bad_edge(s, r, r + 1)
+    ctx = nalar.Context.for_snapshot(s)
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.upload(bad)
+    want = e.value.err_row
+    assert want == r
+    for _ in range(2):
+        with pytest.raises(nalar.NalarError) as e:
+            ctx.step(bad, "srtf")
+        assert e.value.code == nalar.NALAR_E_INVAL and e.value.err_row == want
+        with pytest.raises(nalar.NalarError) as e:
+            ctx.fetch()                      # the failed step left nothing to fetch
+        assert e.value.code == nalar.NALAR_E_STATE
+    # a valid table through the same context afterwards (graph replays included)
+    o = oracle_epoch(s, "srtf")
+    for _ in range(3):
+        same(o, ctx.step(s, "srtf"), "after invalid")
+    ctx.close()
+
+
+def test_step_structurally_invalid_offsets_do_not_crash():
+    """Non-monotone edge offsets (the K1 block tables computed from them are
+    garbage): the device skips the epoch, the step reports E_INVAL."""
+    nalar = _nalar()
+    s = swe_table(4000, seed=8)
+    arrs = s.arrays()
+    eo = arrs["f_edge_off"].copy()
+    mid = len(eo) // 2
+    eo[mid], eo[mid + 1] = eo[mid + 1] + 5, eo[mid]
+    bad = Snapshot(global_row_base=0, name="badoff", **{**arrs, "f_edge_off": eo})
+    ctx = nalar.Context.for_snapshot(s)
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.step(bad, "srtf")
+    assert e.value.code == nalar.NALAR_E_INVAL
+    same(oracle_epoch(s, "lpt"), ctx.step(s, "lpt"), "after structural")
+    ctx.close()
+
+
+def test_step_with_next_rows():
+    nalar = _nalar()
+    s = c4()
+    o = oracle_epoch(s, "srtf", reassign={"u_hi_pct": 80, "u_lo_pct": 30})
+    ctx = nalar.Context.for_snapshot(s)
+    ctx.set_policy_params(reassign=True, u_hi_pct=80, u_lo_pct=30)
+    for _ in range(2):
+        g = ctx.step(s, "srtf")
+        same(o, g, "reassign")
+        assert np.array_equal(g["ra_kill"], o["ra_kill"]) and np.array_equal(g["ra_prov"], o["ra_prov"])
+    ctx.close()
