@@ -1131,7 +1131,11 @@ cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s) {
 cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     if (p_in.B == 0) return cudaSuccess;
     SweepParams p = p_in;
-    static size_t configured = 0;
+    // the dynamic shared-memory ceiling is a per-device function attribute
+    static size_t configured_dev[64] = {};
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    size_t& configured = configured_dev[dev & 63];
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -702,6 +702,19 @@ int validate_table(nalar_ctx* c, int64_t* err_row, const char*, bool sync = true
 
 }  // namespace
 
+// Every entry point runs on its context's device and restores the caller's
+// (several contexts on several devices may share a host thread).
+struct DevGuard {
+    int prev = -1, dev;
+    explicit DevGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+        else prev = -1;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // ============================================================== C ABI
 extern "C" {
 
@@ -742,7 +755,8 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return bail(NALAR_E_CUDA);
     if (cfg->device < 0 || cfg->device >= ndev) return bail(NALAR_E_INVAL);
     cudaDeviceProp prop;
-    if (cudaSetDevice(cfg->device) != cudaSuccess || cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess)
+    DevGuard dg(cfg->device);             // the caller's current device is restored on return
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess)
         return bail(NALAR_E_CUDA);
     if (prop.major != 10) return bail(NALAR_E_CUDA);   // built for sm_100a only
     Plan p;
@@ -865,6 +879,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
 
 int nalar_destroy(nalar_ctx* c) {
     if (!c) return NALAR_OK;
+    DevGuard dg(c->cfg.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     destroy_graphs(c);
     for (auto& e : c->ev)
@@ -890,6 +905,7 @@ int nalar_destroy(nalar_ctx* c) {
 
 int nalar_debug_profile(nalar_ctx* c, uint64_t* host, size_t cap, size_t* n_words) {
     if (!c || !n_words) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->d_prof) return fail(c, NALAR_E_STATE, "profiling not enabled (NALAR_F_PROFILE)");
     *n_words = c->prof_words;
     if (!host || cap < c->prof_words) return NALAR_E_SIZE;
@@ -905,6 +921,8 @@ const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : g
 static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync);
 
 int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row) {
+    if (!c) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     return upload_impl(c, s, err_row, true);
 }
 
@@ -913,6 +931,7 @@ static int peer_check(nalar_ctx* c, int rc);
 
 int nalar_step(nalar_ctx* c, const nalar_snapshot* s, int policy, nalar_decisions* out, int64_t* err_row) {
     if (!c || !s || !out) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
         return fail(c, NALAR_E_STATE, "external collective: use the split calls");
     if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
@@ -1049,6 +1068,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     double tt[6] = {trace ? now() : 0, 0, 0, 0, 0, 0};
     if (err_index) *err_index = -1;
     if (!c || !d) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->uploaded) return fail(c, NALAR_E_STATE, "delta before upload");
     const bool apply_asg = d->flags & NALAR_DELTA_APPLY_ASSIGNED;
     if (apply_asg && !c->assign_valid) return fail(c, NALAR_E_STATE, "APPLY_ASSIGNED without a preceding epoch");
@@ -1263,6 +1283,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
 
 int nalar_policy_epoch(nalar_ctx* c, int policy) {
     if (!c) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->uploaded) return fail(c, NALAR_E_STATE, "epoch before upload");
     if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
     if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
@@ -1300,6 +1321,7 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
 
 int nalar_epoch_begin(nalar_ctx* c, int policy) {
     if (!c) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->uploaded) return fail(c, NALAR_E_STATE, "epoch before upload");
     if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
     int rc = enqueue_first_half(c, policy);
@@ -1316,6 +1338,7 @@ int nalar_exchange_buffer(nalar_ctx* c, void** dev_ptr, size_t* n_words) {
 
 int nalar_epoch_finish(nalar_ctx* c) {
     if (!c) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->in_epoch) return fail(c, NALAR_E_STATE, "finish without begin");
     c->in_epoch = false;
     int rc = enqueue_second_half(c);
@@ -1336,11 +1359,13 @@ static int peer_check(nalar_ctx* c, int rc) {
 
 int nalar_fetch_decisions(nalar_ctx* c, nalar_decisions* o) {
     if (!c || !o) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     return peer_check(c, fetch_impl(c, o));
 }
 
 int nalar_peer_buffer(nalar_ctx* c, void** dev_ptr, unsigned char ipc_handle[64]) {
     if (!c) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->peer_buf) return fail(c, NALAR_E_STATE, "not a NALAR_COLL_PEER context");
     if (dev_ptr) *dev_ptr = c->peer_buf;
     if (ipc_handle) {
@@ -1354,6 +1379,7 @@ int nalar_peer_buffer(nalar_ctx* c, void** dev_ptr, unsigned char ipc_handle[64]
 
 int nalar_peer_connect(nalar_ctx* c, void* const* ptrs, const unsigned char* handles) {
     if (!c) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->peer_buf) return fail(c, NALAR_E_STATE, "not a NALAR_COLL_PEER context");
     const int G = c->cfg.world, me = c->cfg.rank;
     for (int q = 0; q < G; ++q) {
@@ -1530,6 +1556,7 @@ static int fetch_impl(nalar_ctx* c, nalar_decisions* o) {
 
 int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
     if (!c || !p) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (p->u_lo_pct > p->u_hi_pct) return fail(c, NALAR_E_INVAL, "u_lo_pct > u_hi_pct");
     if (p->n_types > c->cfg.max_types) return fail(c, NALAR_E_INVAL, "n_types > max_types");
     std::vector<uint16_t> mn(c->cfg.max_types, 0), mx(c->cfg.max_types, 0xFFFF);
@@ -1567,6 +1594,7 @@ int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
 
 int nalar_epoch_stats_get(nalar_ctx* c, nalar_epoch_stats* s) {
     if (!c || !s) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
     if (!c->epoch_done) return fail(c, NALAR_E_STATE, "stats before epoch");
     memset(s, 0, sizeof *s);
     CK(cudaMemcpyAsync(c->h_cnt, c->d_scr, C_NUM * 4, cudaMemcpyDeviceToHost, c->stream));
