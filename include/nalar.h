@@ -25,7 +25,8 @@
  *    caller memory given in nalar_config.workspace.  Input host pointers are
  *    borrowed only for the duration of a call.  Outputs go to caller buffers.
  *  - Call order: upload -> epoch -> fetch; fetch/epoch before any successful
- *    upload return NALAR_E_STATE.  A ctx is not thread-safe.
+ *    upload return NALAR_E_STATE.  A ctx is not thread-safe.  Every call
+ *    runs on the ctx's device and leaves the caller's current device as it was.
  *  - Multi-GPU: one ctx per GPU/rank; every rank uploads its contiguous
  *    workflow range (plus the replicated instance and type tables) and calls
  *    every function; nalar_policy_epoch is then a collective.
