@@ -84,6 +84,8 @@ struct ValidateParams {
 
 struct SweepParams {
     const unsigned long long* verdict;   // K0's verdict: nonzero = invalid table, do nothing
+    uint32_t* rb_mine;           // world > 1: this rank's (global_row_base, rows) words of the exchange
+    uint32_t row_base, n_rows;
     uint32_t long_rows;          // workflows of >= long_rows rows are composed from step transfers
     uint32_t pdl;                // launched as a programmatic dependent of the zero kernel
     uint32_t trig;               // where K1 lets its dependent launch: 0 entry, 1 after P2, 2 before P5
@@ -138,6 +140,8 @@ struct SweepParams {
 
 struct AssignParams {
     const unsigned long long* verdict;   // K0's verdict (see SweepParams)
+    const uint32_t* rb;                  // world > 1: every rank's (global_row_base, rows)
+    unsigned long long* order_err;       // mapped host word: set when the ranks' row ranges are out of order
     const uint32_t* H;          // [G][R][Lv] summed over ranks
     const uint32_t* load_sum;   // [I] summed over ranks
     const uint32_t* tot;        // [R] eligible futures per resource, summed over ranks
@@ -288,13 +292,14 @@ struct PeerParams {
     const uint32_t* slot;             // this rank's H slot [Rh*Lv]
     const uint32_t* load;             // this rank's partial load [I]
     const uint32_t* tot;              // this rank's partial totals [Rh]
+    const uint32_t* rb_mine;          // this rank's (global_row_base, rows)
     uint32_t* x;                      // K4's exchange buffer: H[G][Rh*Lv] | load[I] | tot[Rh]
     unsigned long long* err;          // mapped host word: set on a timed-out wait
     size_t par_words;                 // words per parity region (reservation sized)
     uint32_t G, rank, rh_lv, I, Rh;
 };
 inline size_t peer_par_words(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
-    return (size_t)G * (Rhmax * Lv + Imax + Rhmax);
+    return (size_t)G * (Rhmax * Lv + Imax + Rhmax + 2);
 }
 inline size_t peer_buffer_bytes(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
     return 4 * (kPeerFlagWords + 2 * peer_par_words(G, Rhmax, Lv, Imax) + 4);

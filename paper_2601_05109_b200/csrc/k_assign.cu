@@ -298,6 +298,21 @@ __global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) {
     }
     // everything below reads the sweep's results
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.rb && blockIdx.x == 0 && tid == 0) {
+        // world > 1: the ranks' shards must be consecutive in the global row
+        // order (global rank = the row order across shards); ranks without
+        // rows or with an unknown base (after a delta) are not checked
+        uint32_t prev_end = 0xFFFFFFFFu;
+        bool bad = false;
+        for (uint32_t s = 0; s < G; ++s) {
+            const uint32_t base = p.rb[2 * s], n = p.rb[2 * s + 1];
+            if (n == 0u) continue;
+            if (base == 0xFFFFFFFFu) { prev_end = 0xFFFFFFFFu; continue; }
+            if (prev_end != 0xFFFFFFFFu && base != prev_end) bad = true;
+            prev_end = base + n;
+        }
+        if (bad) *(volatile unsigned long long*)p.order_err = 1ull;
+    }
     if (prof && tid == 0) prof[4] = gtimer();
 
     // ---- every load of the sweep's results this block needs first, issued

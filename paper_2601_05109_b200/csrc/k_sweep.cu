@@ -829,6 +829,10 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem) {
     // above only staged inputs and wrote shared memory and plain outputs
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (p.trig == 1) asm volatile("griddepcontrol.launch_dependents;");
+    if (p.rb_mine && b == 0 && tid == 0) {        // world > 1: this rank's place in the row order
+        p.rb_mine[0] = p.row_base;
+        p.rb_mine[1] = p.n_rows;
+    }
     if (bprof && tid == 0) bprof[7] = gtimer();
 
     // ---- P3 (row-parallel): level, status, outputs, histogram, minima --------

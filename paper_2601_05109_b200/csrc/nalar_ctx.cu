@@ -164,6 +164,8 @@ struct nalar_ctx {
     bool peers_ready = false;
     unsigned long long* peer_err_dev = nullptr;   // device view of h_err[4]
     unsigned long long* h_err_dev = nullptr;      // device view of h_err
+    uint64_t row_base = 0;                        // the snapshot's global_row_base
+    bool row_base_known = false;
     // delta mode: device workflow ids, the second table buffer set, host mirror
     uint64_t* d_wf_id = nullptr;
     struct Alt {
@@ -299,7 +301,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->items = L.take<uint2>(N);
     p->cnt_rb = L.take<uint32_t>((size_t)p->Rhmax * p->Bmax);
     p->off_rb = L.take<uint32_t>((size_t)p->Rhmax * p->Bmax);
-    p->x_words = (size_t)G * p->Rhmax * Lv + I + p->Rhmax;
+    p->x_words = (size_t)G * p->Rhmax * Lv + I + p->Rhmax + 2ull * G;   // + (row base, rows) per rank
     // exchange buffer and scratch are contiguous so one memset clears both
     p->x = L.off;
     L.off += p->x_words * 4;
@@ -443,6 +445,12 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     }
 }
 
+// the (global_row_base, rows) words of rank s in the exchange buffer
+uint32_t* x_rb(nalar_ctx* c) {
+    const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
+    return c->d_x + (size_t)G * c->Rh * c->Lv + c->I + c->Rh;
+}
+
 int run_k1(nalar_ctx* c, int policy) {
     SweepParams p{};
     p.verdict = c->d_err + 5;
@@ -469,6 +477,10 @@ int run_k1(nalar_ctx* c, int policy) {
     p.kv_hint = c->d_kvh; p.kv_level = c->d_kvl; p.kv_home = c->d_kvhome;
     const uint32_t slot = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
     p.H = c->d_x + (size_t)slot * c->Rh * c->Lv;
+    p.rb_mine = c->cfg.world > 1 ? x_rb(c) + 2 * slot : nullptr;
+    // unknown after a delta (nalar_delta carries no row base): not checked
+    p.row_base = c->row_base_known ? (uint32_t)c->row_base : 0xFFFFFFFFu;
+    p.n_rows = c->N;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.load_part = c->d_x + (size_t)G * c->Rh * c->Lv;
     p.tot = p.load_part + c->I;
@@ -484,6 +496,8 @@ int run_k4(nalar_ctx* c) {
     p.verdict = c->d_err + 5;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.H = c->d_x;
+    p.rb = c->cfg.world > 1 ? x_rb(c) : nullptr;
+    p.order_err = c->h_err_dev + 6;
     p.load_sum = c->d_x + (size_t)G * c->Rh * c->Lv;
     p.tot = p.load_sum + c->I;
     p.type_off = c->d_type_off;
@@ -509,8 +523,9 @@ int run_k4(nalar_ctx* c) {
 
 size_t x_used_words(nalar_ctx* c) {
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
-    return (size_t)G * c->Rh * c->Lv + c->I + c->Rh;
+    return (size_t)G * c->Rh * c->Lv + c->I + c->Rh + 2ull * G;
 }
+
 
 // an event inside a captured graph must be an external event-record node
 cudaError_t record_ev(nalar_ctx* c, int k) {
@@ -544,6 +559,7 @@ int enqueue_collective(nalar_ctx* c) {
         p.load = c->d_x + (size_t)G * p.rh_lv;
         p.tot = p.load + c->I;
         p.x = c->d_x;
+        p.rb_mine = x_rb(c) + 2 * p.rank;
         p.err = c->peer_err_dev;
         p.par_words = c->peer_par_words;
         CK(launch_peer_exchange(p, c->stream));
@@ -827,6 +843,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
     c->h_err[4] = 0;
+    c->h_err[6] = 0;
     c->h_err_dev = (unsigned long long*)mapped_view(c->h_err);
     if (!c->h_err_dev) return bail(NALAR_E_CUDA);
     {   // K0's device words: min bad row ~0, structural 0, block counter 0
@@ -983,6 +1000,8 @@ static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, 
     if (N && T == 0) return fail(c, NALAR_E_INVAL, "futures without types");
 
     c->N = N; c->E = E; c->W = W; c->I = I; c->T = T; c->R = I + T; c->Rh = I + 2 * T;
+    c->row_base = s->global_row_base;
+    c->row_base_known = true;
     c->assign_valid = false;
     // host mirror of the workflow layout (delta mode re-partitions from it)
     // the K1 block partition depends only on the workflow layout (row and edge
@@ -1070,6 +1089,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     if (!c || !d) return NALAR_E_INVAL;
     DevGuard dg(c->cfg.device);
     if (!c->uploaded) return fail(c, NALAR_E_STATE, "delta before upload");
+    c->row_base_known = false;
     const bool apply_asg = d->flags & NALAR_DELTA_APPLY_ASSIGNED;
     if (apply_asg && !c->assign_valid) return fail(c, NALAR_E_STATE, "APPLY_ASSIGNED without a preceding epoch");
     if ((d->n_updates && (!d->upd_wf_id || !d->upd_seq || !d->upd_state || !d->upd_executor || !d->upd_pin)) ||
@@ -1353,6 +1373,10 @@ static int peer_check(nalar_ctx* c, int rc) {
     if (rc == NALAR_OK && c->peer_buf && c->h_err[4]) {
         c->h_err[4] = 0;
         return fail(c, NALAR_E_COMM, "peer exchange: a rank's flag never arrived (timed out)");
+    }
+    if (rc == NALAR_OK && c->h_err[6]) {        // K4: the ranks' row ranges (world > 1)
+        c->h_err[6] = 0;
+        return fail(c, NALAR_E_INVAL, "ranks' workflow ranges out of order (global_row_base)");
     }
     return rc;
 }

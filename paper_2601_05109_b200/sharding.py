@@ -26,8 +26,10 @@ def shard_bounds(wf_fut_off: np.ndarray, G: int) -> list[tuple[int, int]]:
 
 
 def exchange_words(G: int, R: int, levels: int, n_inst: int) -> int:
-    """u32 words of the per-epoch exchange buffer: H[G][R][Lv], load[I], tot[R]."""
-    return G * R * levels + n_inst + R
+    """u32 words of the per-epoch exchange buffer: H[G][R][Lv], load[I], tot[R],
+    then (global_row_base, rows) per rank (the library checks that the ranks'
+    shards are consecutive in the global row order)."""
+    return G * R * levels + n_inst + R + 2 * G
 
 
 def slot_view(buf: np.ndarray, G: int, R: int, levels: int, n_inst: int):

@@ -246,3 +246,31 @@ def test_peer_exchange_random_tables(seed):
     _check(o, [(c.fetch(), sh) for c, sh in zip(ctxs, shards)], f"seed={seed} G={G}")
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_ranks_out_of_order_rejected(G):
+    """Shards uploaded to the wrong ranks (the global rank is the row order
+    across ranks, SURVEY 8(b) E_INVAL case): every rank's fetch reports
+    NALAR_E_INVAL instead of silently mis-ranked admissions; in order again,
+    the same contexts are bit-exact."""
+    from paper_2601_05109_b200 import nalar
+    s = swe_table(9000, seed=17)
+    ctxs, shards, _ = _ranks(s, G)
+    rev = shards[::-1]
+    for c, sh in zip(ctxs, rev):
+        c.upload(sh)
+    for c in ctxs:
+        c.epoch("srtf")
+    for c in ctxs:
+        with pytest.raises(nalar.NalarError) as e:
+            c.fetch()
+        assert e.value.code == nalar.NALAR_E_INVAL
+    o = oracle_epoch(s, "srtf")
+    for c, sh in zip(ctxs, shards):
+        c.upload(sh)
+    for c in ctxs:
+        c.epoch("srtf")
+    _check(o, [(c.fetch(), sh) for c, sh in zip(ctxs, shards)], "in order again")
+    for c in ctxs:
+        c.close()
