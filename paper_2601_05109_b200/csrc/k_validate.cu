@@ -5,28 +5,22 @@
 // futures carry an executor of their type (PAPER.md:479 executor metadata);
 // pins name an instance of the future's type (state placement).
 //
-// Row-parallel: one thread per row (the workflow of a row by binary search
-// over the workflow offsets, which the host has checked to be monotone), so a
-// deep workflow costs no more than any other -- the check is a few dependent
-// loads deep, not one round trip per 32 rows of the longest workflow.  The
+// Row-parallel: one thread per row (the workflow of a row from the block's
+// window of workflow offsets in shared memory, which the host has checked to
+// be monotone), so a deep workflow costs no more than any other -- the check
+// is a few dependent loads deep, not one round trip per 32 rows of the
+// longest workflow.  The
 // smallest offending row wins (atomicMin), so the reported row is
 // deterministic.
 #include "internal.h"
 
 namespace nalar {
 
-__device__ __forceinline__ void validate_row(const ValidateParams& p, uint32_t f) {
+// a = first row of f's workflow (found by the caller)
+__device__ __forceinline__ void validate_row(const ValidateParams& p, uint32_t f, uint32_t a) {
     const uint32_t st = p.f_state[f], ty = p.f_type[f];
     const int pin = p.f_pin[f], ex = p.f_exec[f];
     const uint32_t e0 = p.f_edge_off[f], e1 = p.f_edge_off[f + 1];
-    // first row of f's workflow: the last w with wf_fut_off[w] <= f
-    uint32_t lo = 0, hi = p.n_wf - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (p.wf_fut_off[mid] <= f) lo = mid;
-        else hi = mid - 1;
-    }
-    const uint32_t a = p.wf_fut_off[lo];
     if (e1 < e0 || e1 > p.n_edges) {       // structural: CSR offsets not monotone
         atomicOr(&p.err[1], 1ull);
         return;
@@ -48,8 +42,57 @@ __global__ void __launch_bounds__(kK0Threads) k0_validate(ValidateParams p) {
     // a programmatic dependent of the upload's copy kernel: launched while the
     // copy runs, it reads the table only after the copy has completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f < p.n_fut) validate_row(p, f);
+    // The workflows of this block's rows: one warp finds the workflow of the
+    // block's first row by a 32-ary search over the offsets (3 rounds of 32
+    // parallel loads instead of an 11-deep binary search per thread), then
+    // the offsets covering the block (at most one per row, plus one) go to
+    // shared memory, where each row finds its workflow.
+    __shared__ uint32_t s_off[kK0Threads + 2];
+    __shared__ uint32_t s_w0;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    const uint32_t f0 = blockIdx.x * blockDim.x;
+    const uint32_t f = f0 + tid;
+    if (tid < 32) {
+        uint32_t lo = 0, hi = p.n_wf - 1;          // last w with wf_fut_off[w] <= f0, in [lo, hi]
+        while (hi > lo) {
+            const uint32_t step = (hi - lo + 32u) / 32u;   // 32 segments cover [lo, hi]
+            const uint32_t w = lo + lane * step;
+            const bool le = w <= hi && p.wf_fut_off[w] <= f0;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, le);   // lane 0 (w = lo) always set
+            const uint32_t k = 31u - __clz(bal);
+            lo = lo + k * step;
+            hi = min(hi, lo + step - 1u);
+        }
+        if (lane == 0) s_w0 = lo;
+    }
+    __syncthreads();
+    const uint32_t w0 = s_w0;
+    // offsets wf_fut_off[w0 .. w0 + L - 1]; L - 1 workflows (empty ones
+    // included) -- enough unless many empty workflows sit inside the block
+    const uint32_t L = min(p.n_wf - w0, (uint32_t)kK0Threads + 1u) + 1u;
+    for (uint32_t k = tid; k < L; k += blockDim.x) s_off[k] = p.wf_fut_off[w0 + k];
+    __syncthreads();
+    if (f < p.n_fut) {
+        uint32_t a;
+        if (w0 + L - 1u == p.n_wf || f < s_off[L - 1u]) {
+            uint32_t lo = 0, hi = L - 2u;          // last local w with s_off[w] <= f
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (s_off[mid] <= f) lo = mid;
+                else hi = mid - 1;
+            }
+            a = s_off[lo];
+        } else {                                   // beyond the window: search globally
+            uint32_t lo = w0 + L - 1u, hi = p.n_wf - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (p.wf_fut_off[mid] <= f) lo = mid;
+                else hi = mid - 1;
+            }
+            a = p.wf_fut_off[lo];
+        }
+        validate_row(p, f, a);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();

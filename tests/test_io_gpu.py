@@ -164,3 +164,44 @@ def test_pinned_misaligned_arrays_bytewise_path():
     ctx.epoch("srtf")
     same(o, ctx.fetch(), "misaligned")
     ctx.close()
+
+
+def test_validation_window_with_many_empty_workflows():
+    """K0 finds each row's workflow from a window of offsets per block; many
+    empty workflows inside one block overflow the window and the rows beyond
+    it take the global search: a cross-workflow edge there is still caught."""
+    from paper_2601_05109_b200 import nalar
+    n_empty = 700
+    rows_a, rows_b = 10, 10
+    W = 2 + n_empty
+    off = np.concatenate([[0], np.full(1, rows_a), np.full(n_empty, rows_a), [rows_a + rows_b]]).astype(np.uint32)
+    N = rows_a + rows_b
+    eoff = np.zeros(N + 1, np.uint32)
+    edges = []
+    for f in range(N):
+        w0 = 0 if f < rows_a else rows_a
+        if f > w0:
+            edges.append(f - 1)                 # chain inside the workflow
+        eoff[f + 1] = len(edges)
+    bad_row = rows_a + 5
+    edges = np.array(edges, np.uint32)
+    edges[int(eoff[bad_row])] = 3               # into the first workflow
+    s = Snapshot(global_row_base=0, name="empties",
+                 wf_id=np.arange(1, W + 1, dtype=np.uint64), wf_fut_off=off, wf_prio=np.zeros(W, np.int32),
+                 f_state=np.zeros(N, np.uint8), f_type=np.zeros(N, np.uint8), f_round=np.zeros(N, np.uint8),
+                 f_executor=np.full(N, -1, np.int16), f_pin=np.full(N, -1, np.int16), f_edge_off=eoff,
+                 edges=edges, i_type=np.zeros(2, np.uint8), i_cap=np.full(2, 4, np.uint32),
+                 i_base_load=np.zeros(2, np.uint32), t_affinity=np.zeros(1, np.uint8))
+    ctx = nalar.Context.for_snapshot(s)
+    with pytest.raises(nalar.NalarError) as e:
+        ctx.upload(s)
+    assert e.value.err_row == bad_row
+    # the same table with the edge kept inside its workflow is accepted and exact
+    good = s.arrays()
+    good_edges = good["edges"].copy()
+    good_edges[int(eoff[bad_row])] = bad_row - 1
+    sg = Snapshot(global_row_base=0, name="empties-ok", **{**good, "edges": good_edges})
+    ctx.upload(sg)
+    ctx.epoch("srtf")
+    same(oracle_epoch(sg, "srtf"), ctx.fetch(), "empties")
+    ctx.close()
