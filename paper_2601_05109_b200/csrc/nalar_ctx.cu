@@ -62,6 +62,8 @@ constexpr double kLongWeight = 1.0;             // cost per row of a long workfl
 // early-launched (PDL) K4 blocks; measured at C4: 148 blocks 48.5 us / epoch,
 // 145 46.1, 142 45.8, 138 48.8
 constexpr uint32_t kK1Wave = 142;
+constexpr uint32_t kDeepAlone = 20;      // steps: a workflow this deep gets its own K1 block
+constexpr uint32_t kDeepAloneMax = 16;   // ... while there are at most this many
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
 constexpr uint32_t kMaxBlocks = 16384;
 constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tables
@@ -384,6 +386,21 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     uint64_t total = 0;
     for (uint32_t w = 0; w < W; ++w) total += cost(w);
     const uint64_t even = std::max<uint64_t>(64u, (total + kSmSplit - 1) / kSmSplit);
+    // A workflow of at least kDeepAlone 32-row steps (NALAR_DEEP_ALONE, 0 =
+    // off) gets a K1 block of its own, so its composition chain -- the
+    // longest in the epoch -- runs without sweeps co-scheduled on its SM.
+    // Measured on C4 tables of four seeds: -0.4 / 0 / -0.7 / -1.3 us per epoch
+    // at 20 steps, never slower; at 12-16 steps too many blocks go to single
+    // workflows and the rest overflow one wave (+8-12 us), so it applies only
+    // while such workflows are few (<= kDeepAloneMax; C4 tables have 10-13).
+    static const uint32_t deep_alone = [] {
+        const char* e = getenv("NALAR_DEEP_ALONE");
+        return e ? (uint32_t)atoi(e) : kDeepAlone;
+    }();
+    uint32_t n_deep = 0;
+    for (uint32_t w = 0; deep_alone && w < W; ++w) n_deep += wf_off[w + 1] - wf_off[w] >= 32u * deep_alone;
+    const bool alone = deep_alone && n_deep <= kDeepAloneMax;
+    auto is_deep = [&](uint32_t w) { return alone && wf_off[w + 1] - wf_off[w] >= 32u * deep_alone; };
     // one greedy cut at a given per-block target; returns the block count
     auto cut = [&](uint64_t target) -> size_t {
         bw.clear(); br.clear(); be.clear(); bs.clear();
@@ -397,12 +414,12 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
                 const uint32_t wr = wf_off[w + 1] - wf_off[w];
                 const uint32_t e_if = wf_eoff[w + 1] - wf_eoff[ws];
                 if (w > ws && (k1_block_smem(rows + wr, e_if, w - ws + 1, c->T, true) > kStageBudget ||
-                               w - ws + 1 > kMaxWfPerBlock))
+                               w - ws + 1 > kMaxWfPerBlock || is_deep(w)))
                     break;
                 rows += wr;
                 cst += cost(w);
                 ++w;
-                if (cst >= target) break;
+                if (cst >= target || is_deep(w - 1)) break;
             }
             const uint32_t ra = wf_off[ws], rb = wf_off[w];
             const size_t need_st = k1_block_smem(rb - ra, wf_eoff[w] - wf_eoff[ws], w - ws, c->T, true);
