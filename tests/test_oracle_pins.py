@@ -361,6 +361,119 @@ def test_invariants_c2_c4():
 
 
 # --------------------------------------------------------------------------
+# O2 aggregates and O3 eligibility re-derived from brute force (not from the
+# oracle's statuses): every wf_agg field by numpy bincount over the workflow of
+# each row, eligibility by scanning (w, t) groups in row order.
+# P:338 [§4.1] aggregating metadata; P:267-268 [§3.4] stateful; P:575 [§5]
+# managed state (Q12, Q13).
+# --------------------------------------------------------------------------
+def _bf_ready_doomed(s):
+    doomed = np.array(bf.doomed_by_reachability(s), dtype=bool)
+    ready = np.zeros(s.n_futures, dtype=bool)
+    for f in range(s.n_futures):
+        ready[f] = (s.f_state[f] == PENDING and not doomed[f]
+                    and all(s.f_state[p] == RESOLVED for (p, _) in bf.preds(s, f, "dep")))
+    return ready, doomed
+
+
+def _bf_wf_agg(s):
+    N, W = s.n_futures, s.n_workflows
+    wf = np.repeat(np.arange(W), np.diff(s.wf_fut_off.astype(np.int64)))
+    ready, doomed = _bf_ready_doomed(s)
+    st = s.f_state
+    depth = np.array([bf.depth_by_path_enumeration(s, f) for f in range(N)], dtype=np.int64)
+
+    def count(mask):
+        return np.bincount(wf[mask], minlength=W)
+
+    def gmax(v):
+        out = np.zeros(W, dtype=np.int64)
+        np.maximum.at(out, wf, v) if N else None
+        return out
+    inflight = (st == QUEUED) | (st == RUNNING)
+    return np.stack([count(np.ones(N, dtype=bool)), count(st == PENDING), count(ready),
+                     count(inflight), count(st == RESOLVED), count(st == FAILED), count(doomed),
+                     count((st == PENDING) & (s.f_pin >= 0)), gmax(depth),
+                     gmax(s.f_round.astype(np.int64))], axis=1), ready, doomed
+
+
+def _bf_eligible(s, ready, doomed):
+    """Eligibility of each ready future by scanning its (workflow, type) group in
+    row order: STATEFUL = nothing of the group in flight and the lowest-row
+    PENDING non-doomed future; SESSION without a pin = the lowest-row ready
+    unpinned future; otherwise eligible."""
+    elig = np.zeros(s.n_futures, dtype=bool)
+    for w in range(s.n_workflows):
+        rows = range(int(s.wf_fut_off[w]), int(s.wf_fut_off[w + 1]))
+        for f in rows:
+            if not ready[f]:
+                continue
+            t = s.f_type[f]
+            grp = [g for g in rows if s.f_type[g] == t]
+            aff = s.t_affinity[t]
+            if aff == AFF_STATEFUL:
+                busy = any(s.f_state[g] in (QUEUED, RUNNING) for g in grp)
+                first = min(g for g in grp if s.f_state[g] == PENDING and not doomed[g])
+                elig[f] = not busy and first == f
+            elif aff == AFF_SESSION and s.f_pin[f] < 0:
+                elig[f] = min(g for g in grp if ready[g] and s.f_pin[g] < 0) == f
+            else:
+                elig[f] = True
+    return elig
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_wf_agg_and_eligibility_bruteforce(seed):
+    s = random_table(7000 + seed, n_workflows=2 + seed % 5, max_rows=3 + seed % 9,
+                     n_types=1 + seed % 3, consistent=seed % 2 == 0, p_pin=0.6)
+    o = oracle_epoch(s, ["fcfs", "srtf", "lpt"][seed % 3])
+    agg, ready, doomed = _bf_wf_agg(s)
+    assert o["wf_agg"].astype(np.int64).tolist() == agg.tolist(), seed
+    elig = _bf_eligible(s, ready, doomed)
+    st = o["status"]
+    assert ((st == S_DEF) | (st == S_ASG)).tolist() == elig.tolist(), seed
+    assert (st == S_INEL).tolist() == (ready & ~elig).tolist(), seed
+
+
+def test_wf_agg_pinned_pending_counts_pending_only():
+    # pinned_pending counts PENDING futures carrying a pin, whatever else they
+    # are (a doomed pinned PENDING counts); pinned RESOLVED / RUNNING do not.
+    tb = TableBuilder(i_type=[0, 0], i_cap=[4, 4], i_base_load=[0, 0], t_affinity=[AFF_SESSION])
+    tb.add_workflow(1, 0, [(RESOLVED, 0, 0, 0, 0, []), (RUNNING, 0, 0, 0, 0, []),
+                           (FAILED, 0, 0, 1, 1, []), (PENDING, 0, 0, -1, 1, [(2, False)]),
+                           (PENDING, 0, 0, -1, 0, []), (PENDING, 0, 0, -1, -1, [])])
+    o = oracle_epoch(tb.build())
+    # total pending ready inflight resolved failed doomed pinned_pending maxd maxr
+    assert o["wf_agg"][0].tolist() == [6, 3, 2, 1, 1, 1, 1, 2, 1, 0]
+
+
+def test_session_first_placement_q13():
+    # Q13 / P:575: an unpinned SESSION future places only as the lowest-row READY
+    # unpinned future of its (w, t).  The lowest PENDING one (r1) is still
+    # waiting on r0, so the later ready r2 is the first placement.
+    tb = TableBuilder(i_type=[0, 0], i_cap=[4, 4], i_base_load=[0, 0], t_affinity=[AFF_SESSION])
+    tb.add_workflow(1, 0, [(RUNNING, 0, 0, 0, -1, []), (PENDING, 0, 0, -1, -1, [(0, False)]),
+                           (PENDING, 0, 0, -1, -1, []), (PENDING, 0, 0, -1, -1, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"].tolist() == [S_INF, S_WAIT, S_ASG, S_INEL]
+    assert o["new_pin"].tolist() == [0, 0, 1, 0]
+    # the first ready future carries a pin: it goes to its pin (phase A) and
+    # does not take the first-placement slot; the lowest ready UNPINNED one does.
+    tb = TableBuilder(i_type=[0, 0], i_cap=[4, 4], i_base_load=[0, 0], t_affinity=[AFF_SESSION])
+    tb.add_workflow(1, 0, [(PENDING, 0, 0, -1, 1, []), (PENDING, 0, 0, -1, -1, []),
+                           (PENDING, 0, 0, -1, -1, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"].tolist() == [S_ASG, S_ASG, S_INEL]
+    assert o["instance"][0] == 1 and o["new_pin"].tolist() == [0, 1, 0]
+    # a doomed future is not ready, so it never takes the slot
+    tb = TableBuilder(i_type=[0, 0], i_cap=[4, 4], i_base_load=[0, 0], t_affinity=[AFF_SESSION])
+    tb.add_workflow(1, 0, [(FAILED, 0, 0, 0, -1, []), (PENDING, 0, 0, -1, -1, [(0, False)]),
+                           (PENDING, 0, 0, -1, -1, [])])
+    o = oracle_epoch(tb.build())
+    assert o["status"].tolist() == [S_FAIL, S_DOOM, S_ASG]
+
+
+# --------------------------------------------------------------------------
 # input contract (Q1): invalid tables are rejected with the first bad row
 # --------------------------------------------------------------------------
 def test_validation():
