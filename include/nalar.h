@@ -164,6 +164,9 @@ typedef struct {
  *     workflow by seq (bit 31 = NALAR_CALL_EDGE);
  *  5. set_priority updates by workflow id, then instance cap / base-load
  *     updates.
+ * The per-upload optional inputs (f_age / i_head_rem, f_method) describe rows
+ * of the uploaded table; a delta moves rows, so it clears them (nothing
+ * migrates, every method is 0) until the next nalar_snapshot_upload.
  * All pointers are HOST pointers borrowed for the call. */
 #define NALAR_DELTA_APPLY_ASSIGNED 1u
 #define NALAR_KEEP_STATE 0xFFu
@@ -360,7 +363,13 @@ int nalar_epoch_finish(nalar_ctx* ctx);
  * handle, opened here); ptrs / handles may be NULL, ptrs[rank] is ignored.
  * Call on every rank before its first epoch; all ranks must run the same
  * sequence of epochs.  A peer that never arrives makes the epoch's waiting
- * kernel give up after 5 s: the next fetch / stats call returns NALAR_E_COMM. */
+ * kernel give up after 5 s: the next fetch / stats call returns NALAR_E_COMM.
+ * The failure is sticky and spreads: the failing rank poisons its flags in
+ * every peer's buffer, so each peer's next exchange fails at once (never
+ * pairing its epoch with stale data); later epochs on a failed context
+ * return NALAR_E_COMM.  Recover by calling nalar_peer_buffer (which clears
+ * this rank's buffer and epoch counter; the context's stream must be idle and
+ * no peer may be mid-epoch) and then nalar_peer_connect on every rank. */
 int nalar_peer_buffer(nalar_ctx* ctx, void** dev_ptr, unsigned char ipc_handle[64]);
 int nalar_peer_connect(nalar_ctx* ctx, void* const* ptrs, const unsigned char* handles);
 

@@ -287,6 +287,8 @@ cudaError_t launch_batch(const BatchParams& p, cudaStream_t s);
 constexpr uint32_t kPeerMaxRanks = 8;
 constexpr uint32_t kPeerFlagWords = 64;                       // flag[2][kPeerMaxRanks], padded
 constexpr unsigned long long kPeerTimeoutNs = 5000000000ull;  // a missing peer: error, not a hang
+constexpr uint32_t kPeerPoison = 0xFFFFFFFFu;   // flag value of a rank whose exchange failed
+constexpr uint32_t kPeerLocalWords = 8;         // epoch, push ctr, gather ctr, wait ok, sticky failed
 struct PeerParams {
     uint32_t* peers[kPeerMaxRanks];   // every rank's receive buffer (own included)
     const uint32_t* slot;             // this rank's H slot [Rh*Lv]
@@ -302,7 +304,7 @@ inline size_t peer_par_words(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax)
     return (size_t)G * (Rhmax * Lv + Imax + Rhmax + 2);
 }
 inline size_t peer_buffer_bytes(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
-    return 4 * (kPeerFlagWords + 2 * peer_par_words(G, Rhmax, Lv, Imax) + 4);
+    return 4 * (kPeerFlagWords + 2 * peer_par_words(G, Rhmax, Lv, Imax) + kPeerLocalWords);
 }
 cudaError_t launch_peer_exchange(const PeerParams& p, cudaStream_t s);
 

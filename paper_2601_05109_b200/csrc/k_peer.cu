@@ -17,7 +17,14 @@
 // Receive buffer (u32 words, identical layout on every rank):
 //   [0, 64)                          flag[parity][src] = epoch number (parity = epoch & 1)
 //   [64 + par * par_words, ...)      H[G][Rh*Lv] | loadS[G][I] | totS[G][Rh]
-//   [64 + 2 * par_words, +4)         local words: epoch counter, push / gather block counters, wait ok
+//   [64 + 2 * par_words, +8)         local words: epoch counter, push / gather block counters, wait ok,
+//                                    sticky failure
+// A failed exchange is sticky: the rank that timed out (or saw a peer's
+// poison) writes kPeerPoison into its flag slots in every peer's buffer, so
+// each peer's next wait fails at once instead of pairing its epoch with this
+// rank's stale data, and its own later waits fail without polling.  Only a
+// reconnect (nalar_peer_buffer + nalar_peer_connect on every rank, which
+// clears the buffers) resumes the exchange.
 // Two parities: a rank can run one epoch ahead of a peer still reading the
 // previous epoch's data (it cannot run two ahead -- it waits for that peer's
 // flag of the epoch in between, which the peer raises only after finishing
@@ -91,19 +98,23 @@ __global__ void __launch_bounds__(32) k_peer_wait(PeerParams p) {
     uint32_t* loc = own + kPeerFlagWords + 2 * p.par_words;
     const uint32_t e = loc[0] + 1u, par = e & 1u;
     const uint32_t s = threadIdx.x;
-    bool ok = true;
-    if (s < p.G) {
+    bool ok = loc[4] == 0u;                       // sticky: an earlier exchange failed
+    if (ok && s < p.G) {
         const uint64_t t0 = gtimer_ns();
         const uint32_t* f = own + par * kPeerMaxRanks + s;
-        while (ld_acquire_sys(f) != e) {
-            if (gtimer_ns() - t0 > kPeerTimeoutNs) { ok = false; break; }
+        uint32_t v;
+        while ((v = ld_acquire_sys(f)) != e) {
+            if (v == kPeerPoison || gtimer_ns() - t0 > kPeerTimeoutNs) { ok = false; break; }
             __nanosleep(64);
         }
     }
     ok = __all_sync(0xFFFFFFFFu, ok);
+    if (!ok && s < p.G)                           // poison my flag slots (both parities) at every rank
+        for (uint32_t q = 0; q < 2; ++q) st_release_sys(p.peers[s] + q * kPeerMaxRanks + p.rank, kPeerPoison);
     if (threadIdx.x == 0) {
         if (!ok && p.err) *(volatile unsigned long long*)p.err = 1ull;
         loc[3] = ok ? 1u : 0u;
+        if (!ok) loc[4] = 1u;
     }
 }
 

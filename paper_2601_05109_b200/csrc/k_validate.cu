@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(kK0Threads) k0_validate(ValidateParams p) {
 }
 
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s) {
-    if (p.n_fut == 0 || p.n_wf == 0) return cudaSuccess;
+    // nothing to check: the table is valid; clear the verdict word the epoch
+    // kernels read (a previous invalid upload may have set it)
+    if (p.n_fut == 0 || p.n_wf == 0) return cudaMemsetAsync(p.verdict, 0, sizeof(unsigned long long), s);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((uint32_t)((p.n_fut + kK0Threads - 1) / kK0Threads));
     cfg.blockDim = dim3(kK0Threads);

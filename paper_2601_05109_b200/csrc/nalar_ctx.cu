@@ -68,13 +68,22 @@ constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
 constexpr uint32_t kMaxBlocks = 16384;
 constexpr uint32_t kMaxWfPerBlock = 4096;    // bounds the per-workflow smem tables
 
+// Everything enqueue_epoch bakes into a captured graph or checks on the host:
+// the shape, policy and parameters, the buffer set, and the per-upload inputs
+// that change which kernels run or what they read (HoL inputs present, methods
+// present, the type affinities the batch / migration checks depend on).
 struct Key {
     uint32_t N, E, W, I, T, B, R, policy, params_gen;
     size_t smem;
     const void* table;   // current buffer set (deltas swap sets)
+    uint32_t upload_flags;   // bit 0 have_mig, bit 1 have_method
+    uint64_t taff_hash;      // FNV-1a of the uploaded type affinities
+    uint32_t max_inst_per_type;
     bool operator==(const Key& o) const {
         return N == o.N && E == o.E && W == o.W && I == o.I && T == o.T && B == o.B && R == o.R &&
-               policy == o.policy && params_gen == o.params_gen && smem == o.smem && table == o.table;
+               policy == o.policy && params_gen == o.params_gen && smem == o.smem && table == o.table &&
+               upload_flags == o.upload_flags && taff_hash == o.taff_hash &&
+               max_inst_per_type == o.max_inst_per_type;
     }
 };
 
@@ -164,6 +173,7 @@ struct nalar_ctx {
     uint32_t* peers[kPeerMaxRanks] = {};
     void* peer_ipc[kPeerMaxRanks] = {};      // opened IPC mappings (closed on destroy)
     bool peers_ready = false;
+    bool peer_failed = false;                     // sticky until the next reconnect
     unsigned long long* peer_err_dev = nullptr;   // device view of h_err[4]
     unsigned long long* h_err_dev = nullptr;      // device view of h_err
     uint64_t row_base = 0;                        // the snapshot's global_row_base
@@ -567,6 +577,7 @@ int enqueue_first_half(nalar_ctx* c, int policy) {
 int enqueue_collective(nalar_ctx* c) {
     if (c->cfg.collective == NALAR_COLL_PEER) {
         if (!c->peers_ready) return fail(c, NALAR_E_STATE, "peer collective: nalar_peer_connect first");
+
         PeerParams p{};
         const uint32_t G = (uint32_t)c->cfg.world;
         for (uint32_t q = 0; q < G; ++q) p.peers[q] = c->peers[q];
@@ -621,14 +632,25 @@ int enqueue_second_half(nalar_ctx* c) {
     return NALAR_OK;
 }
 
-int enqueue_epoch(nalar_ctx* c, int policy) {
+// host-side checks of the epoch configuration; run before every epoch, graph
+// replays included (a replay must not skip them)
+int epoch_checks(nalar_ctx* c) {
+    if (c->cfg.collective == NALAR_COLL_PEER && c->cfg.world > 1 && c->peer_failed)
+        return fail(c, NALAR_E_COMM, "peer exchange failed earlier: reconnect every rank "
+                    "(nalar_peer_buffer + nalar_peer_connect)");
     if (c->batch_on)
         for (uint32_t t = 0; t < c->T && t < c->h_tmaxb.size(); ++t)
             if (c->h_tmaxb[t] > 1 && c->h_taff[t] != NALAR_AFF_NONE)
                 return fail(c, NALAR_E_INVAL, "type %u: batchable with managed state (PAPER.md:576)", t);
     if (c->mig_active() && c->max_inst_per_type > kK5MaxInst)
         return fail(c, NALAR_E_NOTIMPL, "HoL migration supports <= %u instances per type", kK5MaxInst);
-    int rc = enqueue_first_half(c, policy);
+    return NALAR_OK;
+}
+
+int enqueue_epoch(nalar_ctx* c, int policy) {
+    int rc = epoch_checks(c);
+    if (rc) return rc;
+    rc = enqueue_first_half(c, policy);
     if (!rc) rc = enqueue_collective(c);
     if (!rc) rc = enqueue_second_half(c);
     return rc;
@@ -1297,6 +1319,7 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     c->m_wf_id.swap(nid); c->m_wf_off.swap(noff); c->m_wf_eoff.swap(neoff);
     c->N = N2; c->E = E2; c->W = W2;
     c->have_mig = false;             // HoL inputs are per upload (row indices moved)
+    c->have_method = false;          // so are the batch methods (d_method is in pre-delta row order)
     int rc = set_blocks(c, nullptr, /*fill_sms=*/false);
     if (trace) tt[3] = now();
     if (!rc) rc = validate_table(c, err_index, nullptr);       // synchronises
@@ -1325,8 +1348,12 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
     if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
     if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
         return fail(c, NALAR_E_STATE, "external collective: use nalar_epoch_begin/finish");
-    int rc;
-    Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->params_gen, c->smem, c->d_state};
+    int rc = epoch_checks(c);
+    if (rc) return rc;
+    uint64_t th = 1469598103934665603ull;
+    for (uint8_t a : c->h_taff) th = (th ^ a) * 1099511628211ull;
+    Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->params_gen, c->smem, c->d_state,
+            (c->have_mig ? 1u : 0u) | (c->have_method ? 2u : 0u), th, c->max_inst_per_type};
     // a graph pays off only for a shape that repeats (not after every delta)
     const bool repeat = c->last_key_set && c->last_key == key;
     const bool cached = c->gexec[policy] && c->gkey[policy] == key;
@@ -1361,7 +1388,8 @@ int nalar_epoch_begin(nalar_ctx* c, int policy) {
     DevGuard dg(c->cfg.device);
     if (!c->uploaded) return fail(c, NALAR_E_STATE, "epoch before upload");
     if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
-    int rc = enqueue_first_half(c, policy);
+    int rc = epoch_checks(c);
+    if (!rc) rc = enqueue_first_half(c, policy);
     if (!rc) { c->in_epoch = true; c->last_policy = policy; }
     return rc;
 }
@@ -1389,6 +1417,7 @@ static int fetch_impl(nalar_ctx* c, nalar_decisions* o);
 static int peer_check(nalar_ctx* c, int rc) {
     if (rc == NALAR_OK && c->peer_buf && c->h_err[4]) {
         c->h_err[4] = 0;
+        c->peer_failed = true;
         return fail(c, NALAR_E_COMM, "peer exchange: a rank's flag never arrived (timed out)");
     }
     if (rc == NALAR_OK && c->h_err[6]) {        // K4: the ranks' row ranges (world > 1)
@@ -1408,6 +1437,13 @@ int nalar_peer_buffer(nalar_ctx* c, void** dev_ptr, unsigned char ipc_handle[64]
     if (!c) return NALAR_E_INVAL;
     DevGuard dg(c->cfg.device);
     if (!c->peer_buf) return fail(c, NALAR_E_STATE, "not a NALAR_COLL_PEER context");
+    // (re)connection starts from clean flags and epoch counters on every rank
+    const size_t bytes = peer_buffer_bytes((uint32_t)c->cfg.world, c->Rhmax, c->Lv, c->cfg.max_instances);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemset(c->peer_buf, 0, bytes));
+    CK(cudaDeviceSynchronize());
+    c->h_err[4] = 0;
+    c->peers_ready = false;
     if (dev_ptr) *dev_ptr = c->peer_buf;
     if (ipc_handle) {
         cudaIpcMemHandle_t h;
@@ -1445,6 +1481,7 @@ int nalar_peer_connect(nalar_ctx* c, void* const* ptrs, const unsigned char* han
         }
     }
     c->peers_ready = true;
+    c->peer_failed = false;
     return NALAR_OK;
 }
 
@@ -1479,9 +1516,11 @@ static int fetch_impl(nalar_ctx* c, nalar_decisions* o) {
                              {mig ? o->i_mig_in : nullptr, c->d_migin, 4ull * c->I},
                              {mig ? o->i_mig_out : nullptr, c->d_migout, 4ull * c->I},
                              {c->batch_on ? o->batch_head : nullptr, c->d_bhead, 4ull * c->N}};
-        const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
+        const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin ||
+                           (mig && o->migrate_to) || (c->batch_on && o->batch_head)) && o->f_cap < c->N;
         const bool wbad = o->wf_agg && o->wf_cap < c->W;
-        const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
+        const bool ibad = (o->i_load || o->i_spare || o->i_assigned ||
+                           (mig && (o->i_mig_in || o->i_mig_out))) && o->i_cap < c->I;
         const bool kbad = (o->kv_hint || o->kv_level || o->kv_home) && o->kv_cap < (size_t)c->W * c->T;
         const bool tbad = (o->t_busy || o->t_capsum || o->ra_kill || o->ra_prov) && o->t_cap < c->T;
         bool mapped = !(fbad || wbad || ibad || kbad || tbad);
@@ -1524,9 +1563,11 @@ static int fetch_impl(nalar_ctx* c, nalar_decisions* o) {
     CK(cudaStreamSynchronize(st));
     const uint32_t na = c->h_cnt[C_ASSIGNED];
     o->n_f = c->N; o->n_w = c->W; o->n_i = c->I; o->n_assigned = na;
-    const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin) && o->f_cap < c->N;
+    const bool fbad = (o->status || o->level || o->depth || o->instance || o->new_pin ||
+                       (mig && o->migrate_to) || (c->batch_on && o->batch_head)) && o->f_cap < c->N;
     const bool wbad = o->wf_agg && o->wf_cap < c->W;
-    const bool ibad = (o->i_load || o->i_spare || o->i_assigned) && o->i_cap < c->I;
+    const bool ibad = (o->i_load || o->i_spare || o->i_assigned ||
+                       (mig && (o->i_mig_in || o->i_mig_out))) && o->i_cap < c->I;
     const bool abad = (o->assign_row || o->assign_inst) && o->a_cap < na;
     const bool kbad = (o->kv_hint || o->kv_level || o->kv_home) && o->kv_cap < (size_t)c->W * c->T;
     const bool tbad = (o->t_busy || o->t_capsum || o->ra_kill || o->ra_prov) && o->t_cap < c->T;

@@ -535,7 +535,15 @@ class Context:
             if "kv_hint" in bufs:
                 d.kv_cap = min(len(bufs["kv_hint"]), len(bufs.get("kv_level", bufs["kv_hint"])),
                                len(bufs.get("kv_home", bufs["kv_hint"])))
-            d.f_cap, d.wf_cap, d.i_cap = N, W, I
+            # capacities are the caller's buffer lengths (the library checks
+            # them against the table: E_SIZE, never a short write)
+            def cap(keys, per=1, default=0):
+                ns = [bufs[k].size // per for k in keys if k in bufs]
+                return min(ns) if ns else default
+            d.f_cap = cap(("status", "level", "depth", "instance", "new_pin", "migrate_to", "batch_head"),
+                          default=N)
+            d.wf_cap = cap(("wf_agg",), per=10, default=W)
+            d.i_cap = cap(("i_load", "i_spare", "i_assigned", "i_mig_in", "i_mig_out"), default=I)
             if "assign_row" in bufs:
                 d.a_cap = min(len(bufs["assign_row"]), len(bufs["assign_inst"]))
             if cache:
