@@ -199,7 +199,7 @@ def _swe_workflow(rng, deep):
     return types, rounds, deps, calls
 
 
-def swe_table(n_futures: int, seed: int = 1, name: str = "C4") -> Snapshot:
+def swe_table(n_futures: int, seed: int = 1, name: str = "C4", p_deep: float = 0.05) -> Snapshot:
     rng = np.random.default_rng(seed)
     n_inst = 64
     i_type = np.repeat(np.arange(8), 8)
@@ -212,7 +212,7 @@ def swe_table(n_futures: int, seed: int = 1, name: str = "C4") -> Snapshot:
     wid = 0
     while tb.n_rows < n_futures:
         wid += 1
-        deep = rng.random() < 0.05
+        deep = rng.random() < p_deep
         types, rounds, deps, calls = _swe_workflow(rng, deep)
         n = len(types)
         left = n_futures - tb.n_rows
