@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnalar.so")
 SOURCES = ["nalar_ctx.cu", "k_validate.cu", "k_sweep.cu", "k_assign.cu", "k_delta.cu", "k_io.cu", "k_migrate.cu", "k_batch.cu",
            "k_peer.cu"]
-HEADERS = ["internal.h"]
+HEADERS = ["internal.h", "k1_body.cuh", "k4_body.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",

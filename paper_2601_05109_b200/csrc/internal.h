@@ -324,6 +324,7 @@ cudaError_t preload_k_io();
 cudaError_t preload_k_migrate();
 cudaError_t preload_k_peer();
 cudaError_t preload_k_sweep();
+
 cudaError_t preload_k_validate();
 
 }  // namespace nalar

@@ -478,7 +478,7 @@ uint32_t* x_rb(nalar_ctx* c) {
     return c->d_x + (size_t)G * c->Rh * c->Lv + c->I + c->Rh;
 }
 
-int run_k1(nalar_ctx* c, int policy) {
+SweepParams sweep_params(nalar_ctx* c, int policy) {
     SweepParams p{};
     p.verdict = c->d_err + 5;
     p.long_rows = long_rows();
@@ -514,11 +514,15 @@ int run_k1(nalar_ctx* c, int policy) {
     p.items = c->d_items; p.cnt_rb = c->d_cnt_rb; p.off_rb = c->d_off_rb;
     p.tot_loc = c->d_scr + C_NUM + c->Rmax;
     p.counters = c->d_scr;
-    CK(launch_sweep(p, c->smem, c->stream));
+    return p;
+}
+
+int run_k1(nalar_ctx* c, int policy) {
+    CK(launch_sweep(sweep_params(c, policy), c->smem, c->stream));
     return NALAR_OK;
 }
 
-int run_k4(nalar_ctx* c) {
+AssignParams assign_params(nalar_ctx* c) {
     AssignParams p{};
     p.verdict = c->d_err + 5;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
@@ -544,9 +548,15 @@ int run_k4(nalar_ctx* c) {
     p.ra_on = c->ra_on; p.u_hi_pct = c->u_hi; p.u_lo_pct = c->u_lo;
     p.t_min_inst = c->d_tmin; p.t_max_inst = c->d_tmax; p.tstat = c->d_tstat;
     p.t_busy = c->d_tbusy; p.t_capsum = c->d_tcap; p.ra_kill = c->d_rakill; p.ra_prov = c->d_raprov;
-    CK(launch_assign(p, c->stream));
+    return p;
+}
+
+int run_k4(nalar_ctx* c) {
+    CK(launch_assign(assign_params(c), c->stream));
     return NALAR_OK;
 }
+
+
 
 size_t x_used_words(nalar_ctx* c) {
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
@@ -562,6 +572,8 @@ cudaError_t record_ev(nalar_ctx* c, int k) {
     return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(c->ev[k], c->stream, cudaEventRecordExternal)
                                                : cudaEventRecord(c->ev[k], c->stream);
 }
+
+int enqueue_second_tail(nalar_ctx* c);
 
 int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
@@ -607,6 +619,12 @@ int enqueue_second_half(nalar_ctx* c) {
     if (timing) CK(record_ev(c, 2));
     int rc = run_k4(c);
     if (rc) return rc;
+    return enqueue_second_tail(c);
+}
+
+// the optional passes after admission (K5 migration, K6 batches) + timing
+int enqueue_second_tail(nalar_ctx* c) {
+    const bool timing = c->cfg.flags & NALAR_F_TIMING;
     if (c->mig_active()) {          // K5 HoL migration (NEXT-1), after admission
         MigrateParams m{};
         m.verdict = c->d_err + 5;
@@ -900,8 +918,8 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         static uint64_t loaded = 0;            // per device (modules load per context)
         const uint64_t bit = 1ull << (cfg->device & 63);
         if (!(loaded & bit)) {
-            for (auto f : {preload_k_assign, preload_k_batch, preload_k_delta, preload_k_io, preload_k_migrate,
-                           preload_k_peer, preload_k_sweep, preload_k_validate})
+            for (auto f : {preload_k_assign, preload_k_batch, preload_k_delta, preload_k_io,
+                           preload_k_migrate, preload_k_peer, preload_k_sweep, preload_k_validate})
                 if (f() != cudaSuccess) return bail(NALAR_E_CUDA);
             loaded |= bit;
         }
