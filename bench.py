@@ -59,12 +59,57 @@ def workload_config(n_gpus, table, policy, collective="peer"):
             "levels": 256, "l2": "flushed between epochs (256 MB memset, untimed)",
             "parallelism": f"workflow-sharded x{n_gpus}" + (
                 (" + peer-memory slot exchange (k_peer)" if collective == "peer" else " + NCCL allreduce")
-                if n_gpus > 1 else "")}
+                if n_gpus > 1 else ""),
+            "recipe_deviation": "generator drift from SURVEY §8(d) C4 (DESIGN.md §6): base_load U{0..4} "
+                                "(survey U{0..16}), rounds R = min(8, Geometric(0.48)) (survey 1 + "
+                                "Geometric(0.3), cap 8); the benched table is the parity-tested one"}
+
+
+def profile_spans(nalar, make_ctx, s, pol, flush, n=8):
+    """Device-side durations from %globaltimer stamps (NALAR_F_PROFILE, direct
+    launches, L2 flushed before each epoch, mean over n epochs): K1 = first
+    block entry to last block end, K4 = its first block start to last block
+    end, the last workflow's end, K4's end after K1's."""
+    import torch
+    pctx = make_ctx(nalar.NALAR_F_PROFILE | nalar.NALAR_F_NO_GRAPH)
+    pctx.upload(s)
+    st = torch.cuda.ExternalStream(pctx.stream)
+    W, R = s.n_workflows, s.n_instances + s.n_types
+    acc = {}
+    for i in range(n + 2):
+        with torch.cuda.stream(st):
+            flush.zero_()
+        pctx.epoch(pol)
+        torch.cuda.synchronize()
+        if i < 2:
+            continue
+        pr = nalar.nalar_debug_profile(pctx.h).astype(np.int64)
+        B = (len(pr) - 2 * W - 8 * R - 4 * W) // 16
+        wfp = pr[:2 * W].reshape(W, 2)
+        blk = pr[2 * W:2 * W + 8 * B].reshape(B, 8)
+        k4p = pr[2 * W + 8 * B:2 * W + 8 * B + 8 * R].reshape(R, 8)
+        t0, k1_end = blk[:, 3].min(), blk[:, 2].max()
+        k4s = k4p[:, 0][k4p[:, 0] > 0]
+        vals = {"k1_span": (k1_end - t0) / 1e3,
+                "k1_staging_max": (blk[:, 0] - blk[:, 3]).max() / 1e3,
+                "last_workflow_end": (wfp[:, 1].max() - t0) / 1e3,
+                "k1_tail_after_last_workflow": (k1_end - wfp[:, 1].max()) / 1e3,
+                "k4_span": (k4p[:, 3].max() - k4s.min()) / 1e3 if len(k4s) else None,
+                "k4_end_after_k1": (k4p[:, 3].max() - k1_end) / 1e3,
+                "k4_pdl_release_after_k1": (k4p[:, 4].min() - k1_end) / 1e3}
+        for k, v in vals.items():
+            if v is not None:
+                acc.setdefault(k, []).append(float(v))
+    pctx.close()
+    return {k: float(np.mean(v)) for k, v in acc.items()}
 
 
 def oracle_time(s, policy, budget_s, min_runs=1, max_runs=10**6):
-    """Time the CPU oracle as it stands on one host core."""
-    from oracle import oracle_epoch
+    """Time the CPU oracle as it stands on one host core: O1-O9 timed inside C
+    (oracle_epoch_times: CLOCK_MONOTONIC around the epoch function only, no
+    ctypes marshalling or output allocation), in chunks of 5 runs until the
+    budget is spent.  Returns seconds per run."""
+    from oracle import oracle_epoch_times
     try:
         cpus = sorted(os.sched_getaffinity(0))
         os.sched_setaffinity(0, {cpus[-1]})
@@ -73,22 +118,23 @@ def oracle_time(s, policy, budget_s, min_runs=1, max_runs=10**6):
     times = []
     t_end = time.perf_counter() + budget_s
     while (len(times) < min_runs or time.perf_counter() < t_end) and len(times) < max_runs:
-        t0 = time.perf_counter()
-        oracle_epoch(s, policy)
-        times.append(time.perf_counter() - t0)
+        times.extend(oracle_epoch_times(s, policy, min(5, max_runs - len(times))).tolist())
     if cpus:
         os.sched_setaffinity(0, set(cpus))
     return times
 
 
 def cpu_model():
+    """lscpu model name and the host's logical CPU count."""
+    name = "unknown"
     try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                name = line.split(":", 1)[1].strip()
     except Exception:
         pass
-    return "unknown"
+    return f"{name} (lscpu), nproc {os.cpu_count()}"
 
 
 class ClockSampler:
@@ -138,6 +184,14 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def survey_bytes(s, n_elig):
+    """SURVEY §8(d) byte model as written: 22 B per future (fixed inputs 12,
+    written depth / flags 3, outputs 4, ...), 7 B per edge (4 B edge list + 3 B
+    predecessor state / depth gathers), 40 B per workflow, 7 B per eligible
+    future (rank traffic)."""
+    return 22 * s.n_futures + 7 * s.n_edges + 40 * s.n_workflows + 7 * n_elig
 
 
 def k1_algorithmic_bytes(s, n_elig):
@@ -218,7 +272,8 @@ def run_reference(args, world, rank):
     table = make_table(world, args.seed)
     from oracle import build_oracle
     build_oracle()
-    oracle_time(table, args.policy, 0, min_runs=args.warmup, max_runs=args.warmup)
+    if args.warmup:
+        oracle_time(table, args.policy, 0, min_runs=args.warmup, max_runs=args.warmup)
     times = oracle_time(table, args.policy, 0, min_runs=args.steps, max_runs=args.steps)
     mean = float(np.mean(times))
     value = table.n_futures / mean
@@ -229,7 +284,8 @@ def run_reference(args, world, rank):
             "config": workload_config(world, table, args.policy),
             "cpu_baseline": {"value": value, "unit": "futures/s", "cores": 1, "kind": "oracle",
                              "sample": f"full table ({table.n_futures} futures) x {args.steps} epochs, "
-                                       f"single-threaded C oracle (gcc -O2) on 1 core of {cpu_model()}"},
+                                       f"single-threaded C oracle (gcc -O2), O1-O9 timed inside C, on 1 "
+                                       f"core of {cpu_model()}"},
             "e2e": {"value": value, "unit": "futures/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "epoch_ms_p50": nearest_rank([t * 1e3 for t in times], 50),
@@ -248,9 +304,10 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--c3-epochs", type=int, default=60)
-    ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
-                    help="rank exchange for N > 1: kernels storing into peer memory (CUDA IPC), "
-                         "or the library's NCCL allreduce")
+    ap.add_argument("--c5", type=int, default=1, help="also time the 2^20-future C5 table at N=1 (c5_g1)")
+    ap.add_argument("--collective", default="nccl", choices=["peer", "nccl"],
+                    help="rank exchange for N > 1: the library's NCCL allreduce (default; the "
+                         "north_star's collective), or kernels storing into peer memory (CUDA IPC)")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if world == 1:
@@ -380,34 +437,13 @@ def main():
                  "kv_hints": {k: int(v) for k, v in zip(("none", "retain", "offload", "drop"),
                                                        np.bincount(ra_out["kv_hint"].ravel(), minlength=4))}}
 
-    # where the epoch's critical path goes (NALAR_F_PROFILE %globaltimer stamps in
-    # a separate, untimed context): K1 staging, the last workflow's sweep /
-    # composition, K1's row-parallel tail, and K4 after K1
-    crit = {}
-    if world == 1:
-        pctx = new_ctx(flags=nalar.NALAR_F_PROFILE | nalar.NALAR_F_NO_GRAPH)
-        pctx.upload(s)
-        for _ in range(3):
-            with torch.cuda.stream(torch.cuda.ExternalStream(pctx.stream)):
-                flush.zero_()
-            pctx.epoch(pol)
-        torch.cuda.synchronize()
-        pr = nalar.nalar_debug_profile(pctx.h).astype(np.int64)
-        pctx.close()
-        Wn, Rn = s.n_workflows, s.n_instances + s.n_types
-        Bn = (len(pr) - 2 * Wn - 8 * Rn - 4 * Wn) // 16
-        wfp = pr[:2 * Wn].reshape(Wn, 2)
-        blk = pr[2 * Wn:2 * Wn + 8 * Bn].reshape(Bn, 8)
-        k4p = pr[2 * Wn + 8 * Bn:2 * Wn + 8 * Bn + 8 * Rn].reshape(Rn, 8)
-        t0 = blk[:, 3].min()
-        k1_end = blk[:, 2].max()
-        crit = {"k1_span": float(k1_end - t0) / 1e3, "k1_staging_max": float((blk[:, 0] - blk[:, 3]).max()) / 1e3,
-                "last_workflow_end": float(wfp[:, 1].max() - t0) / 1e3,
-                "k1_tail_after_last_workflow": float(k1_end - wfp[:, 1].max()) / 1e3,
-                "k4_end_after_k1": float(k4p[:, 3].max() - k1_end) / 1e3,
-                "k4_pdl_release_after_k1": float(k4p[:, 4].min() - k1_end) / 1e3}
+    # per-kernel device durations from %globaltimer stamps (NALAR_F_PROFILE, a
+    # separate untimed context, L2 flushed, mean of 8 epochs): K1 span, K4
+    # span, the last workflow's end, K4 after K1 -- single rank
+    crit = profile_spans(nalar, lambda f: new_ctx(flags=f), s, pol, flush) if world == 1 else {}
 
-    # per-kernel device times (CUDA events captured inside the epoch graph)
+    # the same per kernel from CUDA event nodes captured inside the epoch graph
+    # (they perturb the graph a little: a cross-check, not the roofline input)
     tctx = new_ctx(flags=nalar.NALAR_F_TIMING)
     tctx.upload(s)
     k1, k4, coll = [], [], []
@@ -428,12 +464,27 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    R = s.n_instances + s.n_types
-    b1 = k1_algorithmic_bytes(s, st.n_eligible)
-    b4 = k4_algorithmic_bytes(R, 256, world, st.n_eligible, st.n_assigned)
-    dom, dom_us, dom_b = ("k1_sweep", k1_us, b1) if k1_us >= k4_us else ("k4_assign", k4_us, b4)
-    achieved = dom_b / (dom_us * 1e-6) / 1e9
-    traffic = load_traffic(dom)
+
+    def roofline_of(tab, n_elig, k1_dev_us, k1_ev_us):
+        """K1 (the dominant kernel) against HBM: SURVEY §8(d) bytes as written
+        (primary) and DESIGN §4's layout bytes, over K1's device duration."""
+        bs, bl = survey_bytes(tab, n_elig), k1_algorithmic_bytes(tab, n_elig)
+        ach = bs / (k1_dev_us * 1e-6) / 1e9
+        out = {"bound": "hbm", "kernel": "k1_sweep", "achieved": ach, "peak": peak, "unit": "GB/s",
+               "frac": ach / peak, "traffic": None, "algorithmic_bytes": bs,
+               "algorithmic_bytes_model": "SURVEY §8(d): 22 B/future + 7 B/edge + 40 B/workflow + "
+                                          "7 B/eligible future",
+               "layout_bytes": bl, "layout_frac": bl / (k1_dev_us * 1e-6) / 1e9 / peak,
+               "duration_us": k1_dev_us,
+               "duration_source": "%globaltimer span of K1 (first block entry to last block end), "
+                                  "mean of 8 L2-flushed epochs",
+               "peak_source": peak_src}
+        if k1_ev_us:
+            out["achieved_events"] = bs / (k1_ev_us * 1e-6) / 1e9
+        return out
+    k1_dev = crit.get("k1_span") or k1_us
+    roof = roofline_of(s, st.n_eligible, k1_dev, k1_us)
+    roof["traffic"] = load_traffic("k1_sweep")
 
     # end to end through the public API: pinned host table -> nalar_step
     # (H2D + validate, epoch, D2H of the decisions, one synchronisation),
@@ -501,12 +552,15 @@ def main():
             "epoch_us_p99": nearest_rank(list(ms * 1e3), 99),
             "warm_l2": {"ms_per_step": float(np.mean(ms_warm)),
                         "value": total_fut / (float(np.mean(ms_warm)) / 1e3)},
-            "kernels_us": {"k1_sweep": k1_us, "allreduce": coll_us, "k4_assign": k4_us},
+            "kernels_us": {"k1_sweep": crit.get("k1_span", k1_us), "k4_assign": crit.get("k4_span", k4_us),
+                           "k4_end_after_k1": crit.get("k4_end_after_k1"),
+                           "exchange": (coll_us if world > 1 else None),
+                           "source": ("%globaltimer spans (profile context)" if crit else "CUDA events"),
+                           "events": {"k1_sweep": k1_us, "k4_assign": k4_us,
+                                      "exchange": (coll_us if world > 1 else None)}},
             "counts": {"ready": st.n_ready, "eligible": st.n_eligible, "assigned": st.n_assigned,
                        "doomed": st.n_doomed},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": dom_b, "peak_source": peak_src},
+            "roofline": roof,
             "e2e": {"value": total_fut / e2e_mean, "unit": "futures/s", "ms_per_step": e2e_mean * 1e3,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "nalar_step",
                     "split_calls_ms_per_step": float(np.mean(split_t) * 1e3), "parts": e2e_parts},
@@ -519,15 +573,53 @@ def main():
                              "64 emulated CPU nodes (PAPER.md:715); context, not the target"}
     if rank == 0 and world == 1 and args.c3_epochs:
         line["c3_dynamic"] = c3_dynamic(nalar, local, args.c3_epochs)
+    if world == 1 and args.c5:
+        # BASELINE config 5 at G = 1: the 2^20-future C5 table on one B200 -- the
+        # bandwidth-meaningful size; epochs timed like the C4 line
+        from nalar_gen import c5
+        s5 = c5(args.seed)
+        c5ctx = nalar.Context.for_snapshot(s5, device=local)
+        c5ctx.upload(s5)
+        st5s = torch.cuda.ExternalStream(c5ctx.stream)
+        n5 = min(args.steps, 300)
+        ev5 = []
+        with torch.cuda.stream(st5s):
+            for i in range(max(args.warmup, 3) + n5):
+                flush.zero_()
+                a5, b5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a5.record(st5s)
+                c5ctx.epoch(pol)
+                b5.record(st5s)
+                if i >= max(args.warmup, 3):
+                    ev5.append((a5, b5))
+        torch.cuda.synchronize()
+        us5 = [a5.elapsed_time(b5) * 1e3 for a5, b5 in ev5]
+        st5 = c5ctx.stats()
+        c5ctx.close()
+        sp5 = profile_spans(nalar, lambda f: nalar.Context.for_snapshot(s5, device=local, flags=f), s5, pol,
+                            flush, n=4)
+        line["c5_g1"] = {"workload": "C5 SWE-recursive table, 2^20 futures, one B200 (BASELINE config 5, G=1)",
+                         "futures": s5.n_futures, "workflows": s5.n_workflows, "edges": s5.n_edges,
+                         "epochs": n5, "epoch_us_mean": float(np.mean(us5)),
+                         "epoch_us_p50": nearest_rank(us5, 50), "epoch_us_p99": nearest_rank(us5, 99),
+                         "value": s5.n_futures / (float(np.mean(us5)) * 1e-6), "unit": "futures/s",
+                         "counts": {"ready": st5.n_ready, "eligible": st5.n_eligible,
+                                    "assigned": st5.n_assigned, "doomed": st5.n_doomed},
+                         "kernels_us": sp5,
+                         "roofline": roofline_of(s5, st5.n_eligible, sp5.get("k1_span"), None)}
+        line["c5_g1"]["roofline"]["traffic"] = load_traffic("k1_sweep_c5")
     if rank == 0 and world == 1:
         from oracle import build_oracle
         build_oracle()
-        times = oracle_time(table, args.policy, args.cpu_budget, min_runs=3)
-        line["cpu_baseline"] = {"value": table.n_futures / float(np.mean(times)), "unit": "futures/s",
-                                "cores": 1, "kind": "oracle",
+        times = oracle_time(table, args.policy, args.cpu_budget, min_runs=5)
+        med = float(np.median(times))
+        line["cpu_baseline"] = {"value": table.n_futures / med, "unit": "futures/s",
+                                "cores": 1, "kind": "oracle", "statistic": "median",
+                                "epoch_ms_median": med * 1e3, "epoch_ms_mean": float(np.mean(times)) * 1e3,
                                 "sample": f"C4 full table ({table.n_futures} futures) x {len(times)} "
-                                          f"epochs (~{args.cpu_budget:.0f} s), single-threaded C "
-                                          f"oracle on 1 core of {cpu_model()}"}
+                                          f"epochs (~{args.cpu_budget:.0f} s budget), single-threaded C "
+                                          f"oracle (gcc -O2), O1-O9 timed inside C, pinned to 1 core of "
+                                          f"{cpu_model()}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -16,10 +16,12 @@
  * admissions (lexicographically greatest admitted set), the closed-form slot
  * list for phase B, SPEC worked examples, and invariants I1-I10.
  */
+#define _POSIX_C_SOURCE 199309L   /* clock_gettime (the timing harness only) */
 #include "nalar_oracle.h"
 
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 enum { S_PENDING = 0, S_QUEUED = 1, S_RUNNING = 2, S_RESOLVED = 3, S_FAILED = 4 };
 enum { A_NONE = 0, A_SESSION = 1, A_STATEFUL = 2 };
@@ -535,5 +537,21 @@ int oracle_batch(const oracle_table* t, const oracle_out* o, const oracle_batch_
     }
     r->n_batches = nb;
     free(buf);
+    return 0;
+}
+
+/* Timing harness for bench.py's cpu_baseline (not part of the method): runs
+ * oracle_epoch `reps` times on the same table and writes each run's
+ * wall-clock nanoseconds (CLOCK_MONOTONIC around O1-O9 only; the caller's
+ * output buffers are allocated once, outside the timed region). */
+int oracle_epoch_timed(const oracle_table* t, int policy, oracle_out* o, int reps, uint64_t* ns) {
+    for (int r = 0; r < reps; ++r) {
+        struct timespec a, b;
+        clock_gettime(CLOCK_MONOTONIC, &a);
+        const int rc = oracle_epoch(t, policy, o);
+        clock_gettime(CLOCK_MONOTONIC, &b);
+        if (rc) return rc;
+        ns[r] = (uint64_t)(b.tv_sec - a.tv_sec) * 1000000000ull + (uint64_t)(b.tv_nsec - a.tv_nsec);
+    }
     return 0;
 }

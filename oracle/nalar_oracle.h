@@ -113,6 +113,9 @@ int oracle_validate(const oracle_table* t, int64_t* err_row);
 /* policy: 0 FCFS, 1 SRTF, 2 LPT.  Returns 0, or -1 on an invalid table. */
 int oracle_epoch(const oracle_table* t, int policy, oracle_out* o);
 
+/* bench.py's cpu_baseline: `reps` timed runs of oracle_epoch, ns per run. */
+int oracle_epoch_timed(const oracle_table* t, int policy, oracle_out* o, int reps, uint64_t* ns);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,7 @@ def _load():
         _lib = C.CDLL(ORACLE_SO)
         _lib.oracle_validate.argtypes = [C.POINTER(_Table), C.POINTER(C.c_int64)]
         _lib.oracle_epoch.argtypes = [C.POINTER(_Table), C.c_int, C.POINTER(_Out)]
+        _lib.oracle_epoch_timed.argtypes = [C.POINTER(_Table), C.c_int, C.POINTER(_Out), C.c_int, C.c_void_p]
         _lib.oracle_reassign.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_RaParams),
                                          C.POINTER(_RaOut)]
         _lib.oracle_migrate.argtypes = [C.POINTER(_Table), C.POINTER(_Out), C.POINTER(_MigParams),
@@ -112,6 +113,24 @@ def oracle_validate(s, levels: int = 256):
     err = C.c_int64(-1)
     rc = lib.oracle_validate(C.byref(t), C.byref(err))
     return rc, err.value
+
+
+def oracle_epoch_times(s, policy="srtf", reps: int = 5, levels: int = 256) -> np.ndarray:
+    """Seconds per oracle epoch (O1-O9), timed inside C around the epoch
+    function only (bench.py's cpu_baseline); outputs allocated once."""
+    lib = _load()
+    pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+    t, keep = _table(s, levels)
+    N, W, I, T = s.n_futures, s.n_workflows, s.n_instances, s.n_types
+    bufs = [np.zeros(N, np.uint8), np.zeros(N, np.uint8), np.zeros(N, np.uint16), np.zeros(N, np.int16),
+            np.zeros(N, np.uint8), np.zeros(W * 10, np.uint32), np.zeros(I, np.uint32), np.zeros(I, np.uint32),
+            np.zeros(I, np.uint32), np.zeros(max(N, 1), np.uint32), np.zeros(max(N, 1), np.int16),
+            np.zeros(W * T, np.uint8), np.zeros(W * T, np.uint8), np.zeros(W * T, np.int16)]
+    o = _Out(*[_ptr(b) for b in bufs], 0, 0, 0, 0)
+    ns = np.zeros(reps, np.uint64)
+    if lib.oracle_epoch_timed(C.byref(t), pol, C.byref(o), reps, ns.ctypes.data_as(C.c_void_p)) != 0:
+        raise ValueError("oracle: invalid table")
+    return ns.astype(np.float64) * 1e-9
 
 
 def oracle_epoch(s, policy="srtf", levels: int = 256, reassign=None, migrate=None, batch=None) -> dict:
