@@ -410,7 +410,10 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         for (; e + 1 < ee; e += 2) {            // two edges per step: loads overlap
             const uint32_t va = e == eb ? pva : ed[e], vb = e == eb ? pvb : ed[e + 1];
             const uint32_t sa = (va & 0x7FFFFFFFu) - r0, sb = (vb & 0x7FFFFFFFu) - r0;
-            const uint32_t dsa = dep[sa], dsb = dep[sb], fsa = flg[sa], fsb = flg[sb];
+            // an in-step predecessor's depth / flags are not final (settled
+            // below): not read here
+            const uint32_t dsa = sa < c0 ? dep[sa] : 0u, dsb = sb < c0 ? dep[sb] : 0u;
+            const uint32_t fsa = sa < c0 ? flg[sa] : 0u, fsb = sb < c0 ? flg[sb] : 0u;
             const uint32_t ssa = st[sa], ssb = st[sb];
             take(va, dsa, fsa, ssa);
             take(vb, dsb, fsb, ssb);
@@ -418,7 +421,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         if (e < ee) {
             const uint32_t va = e == eb ? pva : ed[e];
             const uint32_t sa = (va & 0x7FFFFFFFu) - r0;
-            take(va, dep[sa], flg[sa], st[sa]);
+            take(va, sa < c0 ? dep[sa] : 0u, sa < c0 ? flg[sa] : 0u, st[sa]);
         }
         if (ee > eb) d = max(d, 1u);
         // unused in-step slots repeat slot 0 (a harmless duplicate)
