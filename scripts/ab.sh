@@ -9,8 +9,8 @@ for rep in 1 2 3; do
   done
 done
 for lib in "" $B; do
-  env NALAR_LIB_AB=$lib timeout 300 python scripts/k1_timeline.py --out gpurun_out/ab_tl.json > /dev/null 2>&1
+  env NALAR_LIB_AB=$lib timeout 300 python scripts/k1_timeline.py --out gpurun_out/ab_tl_${lib:-new}.json > /dev/null 2>&1
   python -c "
-import json;d=json.load(open('gpurun_out/ab_tl.json'))
-print('${lib:-new}', {k:d[k] for k in ('kernel_span_ns','sweep_ns_max','wf_end_ns_max','p3_ns_max','p5_ns_max','bucket_ns_max')}, d['transfer_steps']['cycles_per_step'])"
+import json;d=json.load(open('gpurun_out/ab_tl_${lib:-new}.json'))
+print('${lib:-new}', {k:d[k] for k in ('kernel_span_ns','sweep_ns_max','wf_end_ns_max','p3_ns_max','p5_ns_max','bucket_ns_max','p2_end_ns_pct')}, d['transfer_steps']['cycles_per_step'])"
 done

@@ -8,7 +8,7 @@ python -c "import json;d=json.load(open('gpurun_out/bench_$TAG.json'));print('ep
 timeout -s KILL 300 python scripts/k1_timeline.py --out gpurun_out/k1_timeline_$TAG.json > /dev/null 2>&1
 timeout -s KILL 300 python scripts/k1_cta_detail.py --out gpurun_out/k1_cta_$TAG.json > /dev/null 2>&1
 python -c "
-import json;d=json.load(open('gpurun_out/k1_timeline_$TAG.json'));print({k:v for k,v in d.items() if k not in ('slowest',)})
+import json;d=json.load(open('gpurun_out/k1_timeline_$TAG.json'));print({k:v for k,v in d.items() if k not in ('slowest','blocks')})
 c=json.load(open('gpurun_out/k1_cta_$TAG.json'))
 for x in c['ctas'][:3]: print({k:v for k,v in x.items() if k!='wfs'}); [print('   ',w) for w in x['wfs']]
 "

@@ -109,6 +109,10 @@ slow = np.argsort(-(k4[:, 3] - k1_end))[:6]
 res["k4"]["slowest_ctas"] = [{"r": int(r), **{n: (int(k4[r, j] - k1_end) if k4[r, j] > 0 else None) for n, j in
                                              (("start", 0), ("released", 4), ("loaded", 7), ("n_adm", 1), ("tables", 2),
                                               ("prefix", 5), ("pass1", 6), ("done", 3))}} for r in slow]
-print(json.dumps(res, indent=1))
+# per block: [entered, staged, P2 end, P3 end, P4 end, P5 end] (ns from the first entry)
+res["p2_end_ns_pct"] = {q: int(np.percentile(blk[:, 1] - t0, q)) for q in (0, 25, 50, 75, 90, 100)}
+res["blocks"] = [[int(x) for x in (blk[b, 3] - t0, blk[b, 0] - t0, blk[b, 1] - t0, blk[b, 4] - t0, blk[b, 5] - t0,
+                                   blk[b, 2] - t0)] for b in range(B_)]
+print(json.dumps({k: v for k, v in res.items() if k != "blocks"}, indent=1))
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"), indent=1)
