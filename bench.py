@@ -513,6 +513,7 @@ def main():
         r = ctx.step(sp, pol, ("status", "instance", "assign"), out=outb)
         dt = time.perf_counter() - t0
         n_asg = r["n_assigned"]
+        streamed = ctx.last_step_streamed()
         if i >= 3:
             e2e_t.append(dt)
     for i in range(3 + args.e2e_steps):
@@ -563,6 +564,7 @@ def main():
             "roofline": roof,
             "e2e": {"value": total_fut / e2e_mean, "unit": "futures/s", "ms_per_step": e2e_mean * 1e3,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "nalar_step",
+                    "streamed": streamed,
                     "split_calls_ms_per_step": float(np.mean(split_t) * 1e3), "parts": e2e_parts},
             # per epoch: k_zero (exchange buffer + counters), k1_sweep, k4_assign
             "gpu_launches": 3 * args.steps,

@@ -381,8 +381,20 @@ int nalar_peer_connect(nalar_ctx* ctx, void* const* ptrs, const unsigned char* h
  * table.  Errors: those of the three calls; on NALAR_E_INVAL (invalid table,
  * *err_row = the smallest offending row as for upload) the contents of `out`
  * are unspecified and the context is left not uploaded.  Not with
- * NALAR_COLL_EXTERNAL (use the split calls). */
+ * NALAR_COLL_EXTERNAL (use the split calls).
+ * Streamed step: when the per-row arrays (f_state, f_type, f_round, f_pin,
+ * f_executor, f_edge_off, edges) are all in pinned (device-mapped) host memory,
+ * every K1 block fits shared memory and neither HoL migration inputs nor batch
+ * coalescing are in use, the sweep stages its rows straight from the caller's
+ * memory (TMA over PCIe), checks K0's contract on them in shared memory and
+ * writes the context's device copy of the table (so later split calls see the
+ * same table); there is no separate copy of those arrays and no K0 launch.
+ * Results and errors are identical to the plain path (NALAR_STREAM_STEP=0
+ * disables it).  The caller must not modify those arrays until the call returns. */
 int nalar_step(nalar_ctx* ctx, const nalar_snapshot* snap, int policy, nalar_decisions* out, int64_t* err_row);
+
+/* Diagnostics: 1 if the last nalar_step on ctx was streamed (see above), else 0. */
+int nalar_debug_last_step_streamed(const nalar_ctx* ctx);
 
 /* Copy decisions to caller host buffers; synchronises the ctx stream. */
 int nalar_fetch_decisions(nalar_ctx* ctx, nalar_decisions* out);

@@ -32,7 +32,7 @@ enum : uint8_t { FL_DOOMED = 1, FL_READY = 2, FL_ELIG = 4, FL_ALLRES = 8, FL_MIG
 
 // indices into the per-epoch counters array (scratch)
 enum { C_READY = 0, C_ELIG = 1, C_DOOMED = 2, C_ASSIGNED = 3, C_RA_TICKET = 4, C_RA_PAIRS = 5, C_MIGRATED = 6,
-       C_BATCHES = 7, C_NUM = 8 };
+       C_BATCHES = 7, C_STAGED = 8, C_NUM = 9 };
 
 // per-type statistics of resource reassignment (NEXT-2), written by K4's type
 // blocks; the last K4 block pairs hot with cold types
@@ -82,8 +82,34 @@ struct ValidateParams {
     unsigned long long* verdict;    // device word: 1 if the table is invalid (the epoch kernels skip)
 };
 
+// Streamed step (nalar_step with pinned snapshot arrays): K1 stages its rows
+// by TMA straight from the caller's mapped host memory, checks K0's contract
+// on them in shared memory, and writes them back to the device table.
+struct StreamIn {
+    const uint8_t* state;       // device views of the caller's pinned arrays
+    const uint8_t* type;
+    const uint8_t* round;
+    const int16_t* pin;
+    const int16_t* exec;
+    const uint32_t* eoff;
+    const uint32_t* edges;
+    unsigned long long* err;    // [0] min bad row (~0 armed), [1] structural flag (0 armed)
+    unsigned long long* verdict;   // set to 1 by a block holding an invalid row
+    const uint8_t* i_type;
+    uint32_t n_edges, n_types, n_inst;
+};
+
 struct SweepParams {
     const unsigned long long* verdict;   // K0's verdict: nonzero = invalid table, do nothing
+    uint32_t stream_in;          // 1: rows come from `src` (host), validated here (verdict unused at entry)
+    StreamIn src;
+    // CTA i sweeps block blk_order[i] (costliest first).  A streamed step paces
+    // its host reads: CTA i >= stage_window issues its copies once
+    // stage_ctr >= i - stage_window CTAs have staged (bounded wait), so the
+    // costly blocks' rows cross PCIe first and their sweeps overlap the rest.
+    const uint32_t* blk_order;
+    uint32_t* stage_ctr;
+    uint32_t stage_window;
     uint32_t* rb_mine;           // world > 1: this rank's (global_row_base, rows) words of the exchange
     uint32_t row_base, n_rows;
     uint32_t long_rows;          // workflows of >= long_rows rows are composed from step transfers
@@ -140,6 +166,11 @@ struct SweepParams {
 
 struct AssignParams {
     const unsigned long long* verdict;   // K0's verdict (see SweepParams)
+    // streamed step: the verdict is K1's, read after the grid dependency;
+    // block 0 then publishes the error words to mapped host memory and re-arms them
+    uint32_t stream_in;
+    unsigned long long* err;             // [0] min bad row, [1] structural (device)
+    unsigned long long* host_err;        // mapped host words [0], [1]
     const uint32_t* rb;                  // world > 1: every rank's (global_row_base, rows)
     unsigned long long* order_err;       // mapped host word: set when the ranks' row ranges are out of order
     const uint32_t* H;          // [G][R][Lv] summed over ranks
@@ -312,7 +343,7 @@ cudaError_t launch_copy_segs(const CopyParams& p, cudaStream_t s);
 cudaError_t launch_fetch(const FetchParams& f, const CopyParams& p, cudaStream_t s);
 cudaError_t launch_validate(const ValidateParams& p, cudaStream_t s);
 cudaError_t launch_delta(const DeltaParams& p, bool apply_assigned, uint32_t R, cudaStream_t s);
-cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s);
+cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s, unsigned long long* verdict = nullptr);
 cudaError_t launch_sweep(const SweepParams& p, size_t smem, cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 

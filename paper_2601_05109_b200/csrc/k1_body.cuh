@@ -226,10 +226,15 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     uint32_t* ndp;        //   in-step doom ancestors (lane mask)
     uint16_t* aux;        //   DEP-from-interface mask, FAILED pred, all-resolved, k, ok
     if (staged) {
-        const Win ws = window(p.f_state, 1, r0, r1), wt = window(p.f_type, 1, r0, r1);
-        const Win wr = window(p.f_round, 1, r0, r1);
-        const Win wp = window(p.f_pin, 2, r0, r1), wx = window(p.f_exec, 2, r0, r1);
-        const Win we = window(p.f_edge_off, 4, r0, r1 + 1), wg = window(p.edges, 4, e0, e1);
+        // a streamed step stages the rows from the caller's pinned host arrays
+        const bool si = p.stream_in != 0u;
+        const Win ws = window(si ? p.src.state : p.f_state, 1, r0, r1);
+        const Win wt = window(si ? p.src.type : p.f_type, 1, r0, r1);
+        const Win wr = window(si ? p.src.round : p.f_round, 1, r0, r1);
+        const Win wp = window(si ? p.src.pin : p.f_pin, 2, r0, r1);
+        const Win wx = window(si ? p.src.exec : p.f_exec, 2, r0, r1);
+        const Win we = window(si ? p.src.eoff : p.f_edge_off, 4, r0, r1 + 1);
+        const Win wg = window(si ? p.src.edges : p.edges, 4, e0, e1);
         const Win wo = window(p.wf_fut_off, 4, w0, w1 + 1), wq = window(p.wf_prio, 4, w0, w1);
         uint8_t* d_s = q;   q += align16(nr + 32);
         uint8_t* d_t = q;   q += align16(nr + 32);
@@ -250,6 +255,18 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         aux = (uint16_t*)q;
         if (tid == 0) {
             mbar_init(mbar, 1);
+            if (p.stream_in && blockIdx.x >= p.stage_window) {
+                // pacing of a streamed step's host reads (see SweepParams)
+                asm volatile("griddepcontrol.wait;" ::: "memory");   // the counter is the zero kernel's
+                const uint32_t need = blockIdx.x - p.stage_window;
+                const uint64_t t0 = gtimer();
+                for (;;) {
+                    uint32_t v;
+                    asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p.stage_ctr) : "memory");
+                    if (v >= need || gtimer() - t0 > 200000ull) break;   // a hint, never a hang
+                    __nanosleep(256);
+                }
+            }
             const uint32_t total = ws.bytes + wt.bytes + wr.bytes + wp.bytes + wx.bytes + we.bytes +
                                    (ne ? wg.bytes : 0u) + wo.bytes + (nw ? wq.bytes : 0u);
             mbar_arrive_expect_tx(mbar, total);
@@ -306,12 +323,73 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     }
     for (uint32_t k = tid; k < 8 * nw; k += kK1Threads) s_agg[k] = 0;
     for (uint32_t k = tid; k < nr; k += kK1Threads) aux[k] = 0;   // step-done flags
+    uint32_t* s_bad = (uint32_t*)(smem + 32);      // streamed step: an invalid row in this block
     if (tid == 0) {
         *s_ticket = 0;
         s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
+        *s_bad = 0;
     }
     __syncthreads();
     if (staged) mbar_wait(mbar, 0);
+    if (staged && p.stream_in && tid == 0) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        atomicAdd(p.stage_ctr, 1u);
+    }
+    if (staged && p.stream_in) {
+        // K0's input contract (k_validate.cu validate_row, Q1) on the
+        // staged rows: an edge points to an earlier row of the same workflow,
+        // states / types in range, pins and executors name an instance of the
+        // row's type; the smallest bad row over all blocks wins (atomicMin).
+        // Offsets outside the block's edge window mean non-monotone offsets.
+        const StreamIn& q = p.src;
+        bool structural = false;
+        for (uint32_t f = tid; f < nr; f += kK1Threads) {
+            uint32_t lo = 0, hi = nw - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (wfo[mid] - r0 <= f) lo = mid;
+                else hi = mid - 1;
+            }
+            const uint32_t a = wfo[lo];
+            const uint32_t eb = eo[f], ee = eo[f + 1];
+            if (ee < eb || ee > q.n_edges || eb < e0 || ee > e1) { structural = true; continue; }
+            const uint32_t stv = st[f], tyv = ty[f];
+            const int pinv = pn[f], exv = ex[f];
+            bool ok = stv <= 4u && tyv < q.n_types;
+            if (ok && pinv != -1 && (pinv < 0 || (uint32_t)pinv >= q.n_inst || q.i_type[pinv] != tyv)) ok = false;
+            if (ok && (stv == 1u || stv == 2u) && (exv < 0 || (uint32_t)exv >= q.n_inst || q.i_type[exv] != tyv))
+                ok = false;
+            for (uint32_t e = eb; ok && e < ee; ++e) {
+                const uint32_t x = ed[e - e0] & 0x7FFFFFFFu;
+                if (x < a || x >= r0 + f) ok = false;
+            }
+            if (!ok) {
+                atomicMin(&q.err[0], (unsigned long long)(r0 + f));
+                *s_bad = 1u;
+            }
+        }
+        if (structural) {
+            atomicOr(&q.err[1], 1ull);
+            *s_bad = 1u;
+        }
+        __syncthreads();
+        if (*s_bad) {
+            // the zero kernel clears the verdict: set it only after that grid
+            if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (tid == 0) *q.verdict = 1ull;
+            return;
+        }
+        // the device copy of the table (later epochs / deltas read it)
+        for (uint32_t i = tid; i < nr; i += kK1Threads) {
+            const_cast<uint8_t*>(p.f_state)[r0 + i] = st[i];
+            const_cast<uint8_t*>(p.f_type)[r0 + i] = ty[i];
+            const_cast<uint8_t*>(p.f_round)[r0 + i] = rd[i];
+            const_cast<int16_t*>(p.f_pin)[r0 + i] = pn[i];
+            const_cast<int16_t*>(p.f_exec)[r0 + i] = ex[i];
+        }
+        for (uint32_t i = tid; i <= nr; i += kK1Threads) const_cast<uint32_t*>(p.f_edge_off)[r0 + i] = eo[i];
+        for (uint32_t i = tid; i < ne; i += kK1Threads) const_cast<uint32_t*>(p.edges)[e0 + i] = ed[i];
+    }
     if (bprof && tid == 0) bprof[0] = gtimer();
 
     if (bprof && tid == 0) bprof[6] = gtimer();

@@ -264,7 +264,7 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     unsigned long long ra_busy = 0, ra_cap = 0;      // NEXT-2 partials of this thread's instances
     uint64_t ra_best = ~0ull;
 
-    if (*p.verdict) return;              // an invalid table (K0): nothing to assign
+    if (!p.stream_in && *p.verdict) return;   // an invalid table (K0): nothing to assign
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     // type resources (the longest walks: phase B of a whole type) take the
@@ -297,6 +297,16 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     }
     // everything below reads the sweep's results
     if (!kFused) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.stream_in && *p.verdict) {
+        // a streamed step's sweep found an invalid row: publish K0's words to
+        // the host (read after the step's one synchronisation) and re-arm them
+        if (blk == 0 && threadIdx.x == 0) {
+            volatile unsigned long long* h = p.host_err;
+            h[0] = atomicExch(&p.err[0], ~0ull);
+            h[1] = atomicExch(&p.err[1], 0ull);
+        }
+        return;
+    }
     if (p.rb && blk == 0 && tid == 0) {
         // world > 1: the ranks' shards must be consecutive in the global row
         // order (global rank = the row order across shards); ranks without

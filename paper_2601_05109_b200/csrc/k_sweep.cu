@@ -44,21 +44,24 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     // an invalid table (K0's verdict, complete before the zero kernel ran)
     // is never swept: nalar_step queues this kernel before the host has seen it
-    if (*p.verdict) return;
-    if (p.blk_staged[blockIdx.x]) k1_body<true>(p, smem, blockIdx.x);
-    else k1_body<false>(p, smem, blockIdx.x);
+    if (!p.stream_in && *p.verdict) return;
+    const uint32_t b = p.blk_order[blockIdx.x];
+    if (p.blk_staged[b]) k1_body<true>(p, smem, b);
+    else k1_body<false>(p, smem, b);
 }
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once
-__global__ void k_zero(uint32_t* __restrict__ x, size_t n) {
+__global__ void k_zero(uint32_t* __restrict__ x, size_t n, unsigned long long* verdict) {
     asm volatile("griddepcontrol.launch_dependents;");
+    // a streamed step: the sweep sets the verdict (after waiting for this grid)
+    if (verdict && blockIdx.x == 0 && threadIdx.x == 0) *verdict = 0ull;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         x[i] = 0u;
 }
 
-cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s) {
+cudaError_t launch_zero(uint32_t* x, size_t n_words, cudaStream_t s, unsigned long long* verdict) {
     const uint32_t grid = (uint32_t)std::min<size_t>(148, (n_words + 255) / 256 + 1);
-    k_zero<<<grid, 256, 0, s>>>(x, n_words);
+    k_zero<<<grid, 256, 0, s>>>(x, n_words, verdict);
     return cudaGetLastError();
 }
 

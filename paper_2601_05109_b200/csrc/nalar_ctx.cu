@@ -79,11 +79,12 @@ struct Key {
     uint32_t upload_flags;   // bit 0 have_mig, bit 1 have_method
     uint64_t taff_hash;      // FNV-1a of the uploaded type affinities
     uint32_t max_inst_per_type;
+    uint64_t stream_key = 0;  // streamed step: hash of the caller's array addresses (0 otherwise)
     bool operator==(const Key& o) const {
         return N == o.N && E == o.E && W == o.W && I == o.I && T == o.T && B == o.B && R == o.R &&
                policy == o.policy && params_gen == o.params_gen && smem == o.smem && table == o.table &&
                upload_flags == o.upload_flags && taff_hash == o.taff_hash &&
-               max_inst_per_type == o.max_inst_per_type;
+               max_inst_per_type == o.max_inst_per_type && stream_key == o.stream_key;
     }
 };
 
@@ -104,6 +105,7 @@ struct nalar_ctx {
     int16_t *d_exec = nullptr, *d_pin = nullptr;
     uint32_t *d_blk_wf = nullptr, *d_blk_row0 = nullptr, *d_blk_edge0 = nullptr;
     uint8_t* d_blk_staged = nullptr;
+    uint32_t* d_blk_order = nullptr;
     uint32_t* d_wf_perm = nullptr;
     uint32_t *d_type_off = nullptr, *d_type_inst = nullptr;
     // outputs
@@ -134,6 +136,7 @@ struct nalar_ctx {
     std::vector<uint16_t> h_tmaxb;
     std::vector<uint8_t> h_taff;      // affinities of the uploaded table
     bool mig_active() const { return mig_on && have_mig; }
+    bool mig_active_for(const nalar_snapshot* s) const { return mig_on && s->f_age && s->i_head_rem; }
     uint8_t *d_kvh = nullptr, *d_kvl = nullptr;
     int16_t* d_kvhome = nullptr;
     uint32_t *d_wfagg = nullptr, *d_iload = nullptr, *d_ispare = nullptr, *d_iasg = nullptr, *d_arow = nullptr;
@@ -156,7 +159,7 @@ struct nalar_ctx {
     // task order) so they travel in the upload's single copy kernel
     uint8_t* h_tab = nullptr;
     uint8_t* h_tab_dev = nullptr;
-    size_t tab_off[7] = {0, 0, 0, 0, 0, 0, 0};   // type_off, type_inst, blk_wf, blk_row0, blk_edge0, blk_staged, perm
+    size_t tab_off[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // type_off, type_inst, blk_wf, blk_row0, blk_edge0, blk_staged, perm, blk_order
     // current table
     uint32_t N = 0, E = 0, W = 0, I = 0, T = 0, B = 0, R = 0;
     size_t smem = 0, fixed_smem = 0;
@@ -198,6 +201,12 @@ struct nalar_ctx {
     bool blocks_valid = false;              // device block tables match m_wf_off / m_wf_eoff
     uint32_t blocks_T = 0;
     bool assign_valid = false;        // last epoch's assignment regions match the table
+    bool all_staged = false;          // every K1 block stages its rows in shared memory
+    // streamed step (nalar_step, pinned snapshot): K1 reads the per-row arrays
+    // from the caller's host memory, validates them and writes the device copy
+    bool streaming = false;
+    bool last_streamed = false;
+    StreamIn sin{};
     Key last_key{};
     bool last_key_set = false;
     unsigned long long* d_prof = nullptr;
@@ -235,7 +244,7 @@ struct Layout {
 
 struct Plan {
     size_t wf_off, wf_prio, wf_id, state, type, round, exec, pin, eoff, edges, itype, icap, ibase, taff;
-    size_t blk_wf, blk_row0, blk_edge0, blk_staged, wf_perm, type_off, type_inst;
+    size_t blk_wf, blk_row0, blk_edge0, blk_staged, blk_order, wf_perm, type_off, type_inst;
     size_t status, level, newpin, gflags, gwlm, gtlo, gthi, gifc, gndp, gaux, depth, inst, ainst, wfagg, iload, ispare, iasg, arow;
     size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov, age, head, migto, migin, migout;
     size_t tmaxb, method, bhead;
@@ -271,6 +280,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->blk_row0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_edge0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_staged = L.take<uint8_t>(p->Bmax);
+    p->blk_order = L.take<uint32_t>(p->Bmax);
     p->wf_perm = L.take<uint32_t>(W);
     p->type_off = L.take<uint32_t>(T + 1);
     p->type_inst = L.take<uint32_t>(I);
@@ -481,6 +491,8 @@ uint32_t* x_rb(nalar_ctx* c) {
 SweepParams sweep_params(nalar_ctx* c, int policy) {
     SweepParams p{};
     p.verdict = c->d_err + 5;
+    p.stream_in = c->streaming ? 1u : 0u;
+    p.src = c->sin;
     p.long_rows = long_rows();
     p.wf_fut_off = c->d_wf_off; p.wf_prio = c->d_wf_prio;
     p.f_state = c->d_state; p.f_type = c->d_type; p.f_round = c->d_round;
@@ -488,6 +500,10 @@ SweepParams sweep_params(nalar_ctx* c, int policy) {
     p.t_aff = c->d_taff;
     p.blk_wf = c->d_blk_wf; p.blk_row0 = c->d_blk_row0; p.blk_edge0 = c->d_blk_edge0;
     p.blk_staged = c->d_blk_staged;
+    p.blk_order = c->d_blk_order;
+    p.stage_ctr = c->d_scr + C_STAGED;
+    static const uint32_t window = [] { const char* e = getenv("NALAR_STAGE_WINDOW"); return e ? (uint32_t)atoi(e) : 24u; }();
+    p.stage_window = window ? window : 0xFFFFFFFFu;
     p.wf_perm = c->d_wf_perm;
     p.B = c->B; p.n_types = c->T; p.n_inst = c->I; p.R = c->R; p.levels = c->Lv; p.policy = (uint32_t)policy;
     p.Rh = c->Rh;
@@ -525,6 +541,9 @@ int run_k1(nalar_ctx* c, int policy) {
 AssignParams assign_params(nalar_ctx* c) {
     AssignParams p{};
     p.verdict = c->d_err + 5;
+    p.stream_in = c->streaming ? 1u : 0u;
+    p.err = c->d_err + 2;
+    p.host_err = c->h_err_dev;
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.H = c->d_x;
     p.rb = c->cfg.world > 1 ? x_rb(c) : nullptr;
@@ -578,7 +597,8 @@ int enqueue_second_tail(nalar_ctx* c);
 int enqueue_first_half(nalar_ctx* c, int policy) {
     const bool timing = c->cfg.flags & NALAR_F_TIMING;
     // clear exchange buffer (used part) + counters + adm_pub; contiguous region
-    CK(launch_zero(c->d_x, c->x_words + C_NUM + (size_t)c->Rmax + c->Rhmax, c->stream));
+    CK(launch_zero(c->d_x, c->x_words + C_NUM + (size_t)c->Rmax + c->Rhmax, c->stream,
+                   c->streaming ? c->d_err + 5 : nullptr));
     if (timing) CK(record_ev(c, 0));
     int rc = run_k1(c, policy);
     if (rc) return rc;
@@ -686,6 +706,7 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     partition(c, c->m_wf_off.data(), c->m_wf_eoff.data(), bw, br, be, bs, &mx, fill_sms);
     const double t1 = trace ? now() : 0;
     c->B = (uint32_t)bs.size();
+    c->all_staged = std::all_of(bs.begin(), bs.end(), [](uint8_t x) { return x != 0; });
     c->fixed_smem = k1_fixed_smem(c->T, c->I, c->Rh);
     c->smem = c->fixed_smem + mx;
     cudaStream_t st = c->stream;
@@ -718,10 +739,26 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     CopyBatch own(st);
     CopyBatch& cb = batch ? *batch : own;
     struct Part { int slot; const void* src; size_t bytes; void* dst; };
-    const Part parts[5] = {
+    // CTA order: blocks by estimated sweep cost, costliest first (the
+    // longest workflow's 32-row steps, then rows); CTAs are dispatched in
+    // index order and a streamed step stages them in this order
+    std::vector<uint32_t> order(c->B);
+    {
+        std::vector<uint64_t> cost(c->B);
+        for (uint32_t b = 0; b < c->B; ++b) {
+            uint32_t mx = 0;
+            for (uint32_t w = bw[b]; w < bw[b + 1]; ++w) mx = std::max(mx, c->m_wf_off[w + 1] - c->m_wf_off[w]);
+            cost[b] = ((uint64_t)((mx + 31) / 32) << 32) | (br[b + 1] - br[b]);
+        }
+        for (uint32_t b = 0; b < c->B; ++b) order[b] = b;
+        std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+            return cost[x] != cost[y] ? cost[x] > cost[y] : x < y;
+        });
+    }
+    const Part parts[6] = {
         {2, bw.data(), 4ull * bw.size(), c->d_blk_wf}, {3, br.data(), 4ull * br.size(), c->d_blk_row0},
         {4, be.data(), 4ull * be.size(), c->d_blk_edge0}, {5, bs.data(), bs.size(), c->d_blk_staged},
-        {6, c->m_perm.data(), 4ull * c->W, c->d_wf_perm}};
+        {6, c->m_perm.data(), 4ull * c->W, c->d_wf_perm}, {7, order.data(), 4ull * c->B, c->d_blk_order}};
     for (const Part& q : parts) {
         if (!q.bytes) continue;
         memcpy(c->h_tab + c->tab_off[q.slot], q.src, q.bytes);
@@ -858,6 +895,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_taff = at<uint8_t>(a, p.taff);
     c->d_blk_wf = at<uint32_t>(a, p.blk_wf); c->d_blk_row0 = at<uint32_t>(a, p.blk_row0);
     c->d_blk_edge0 = at<uint32_t>(a, p.blk_edge0); c->d_blk_staged = at<uint8_t>(a, p.blk_staged);
+    c->d_blk_order = at<uint32_t>(a, p.blk_order);
     c->d_wf_perm = at<uint32_t>(a, p.wf_perm);
     c->d_type_off = at<uint32_t>(a, p.type_off); c->d_type_inst = at<uint32_t>(a, p.type_inst);
     c->d_status = at<uint8_t>(a, p.status); c->d_level = at<uint8_t>(a, p.level);
@@ -889,9 +927,9 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         return bail(NALAR_E_NOMEM);
     {
         const size_t Tm = cfg->max_types, Im = cfg->max_instances, Wm = cfg->max_workflows, Bm = c->Bmax;
-        const size_t sz[7] = {4 * (Tm + 1), 4 * Im, 4 * (Bm + 1), 4 * (Bm + 1), 4 * (Bm + 1), Bm, 4 * Wm};
+        const size_t sz[8] = {4 * (Tm + 1), 4 * Im, 4 * (Bm + 1), 4 * (Bm + 1), 4 * (Bm + 1), Bm, 4 * Wm, 4 * Bm};
         size_t o = 0;
-        for (int k = 0; k < 7; ++k) { c->tab_off[k] = o; o += (sz[k] + 15) & ~(size_t)15; }
+        for (int k = 0; k < 8; ++k) { c->tab_off[k] = o; o += (sz[k] + 15) & ~(size_t)15; }
         if (cudaMallocHost(&c->h_tab, std::max<size_t>(o, 16)) != cudaSuccess) return bail(NALAR_E_NOMEM);
         c->h_tab_dev = (uint8_t*)mapped_view(c->h_tab);
         c->h_cnt_dev = (uint32_t*)mapped_view(c->h_cnt);
@@ -990,9 +1028,11 @@ int nalar_debug_profile(nalar_ctx* c, uint64_t* host, size_t cap, size_t* n_word
 
 void* nalar_stream(nalar_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+int nalar_debug_last_step_streamed(const nalar_ctx* c) { return c && c->last_streamed ? 1 : 0; }
+
 const char* nalar_last_error(const nalar_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
-static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync);
+static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync, bool stream = false);
 
 int nalar_snapshot_upload(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row) {
     if (!c) return NALAR_E_INVAL;
@@ -1009,11 +1049,61 @@ int nalar_step(nalar_ctx* c, const nalar_snapshot* s, int policy, nalar_decision
     if (c->cfg.world > 1 && c->cfg.collective == NALAR_COLL_EXTERNAL)
         return fail(c, NALAR_E_STATE, "external collective: use the split calls");
     if (policy < NALAR_FCFS || policy > NALAR_LPT) return fail(c, NALAR_E_INVAL, "bad policy");
-    int rc = upload_impl(c, s, err_row, false);       // copies + K0 queued, no sync
+    const double t0 = getenv("NALAR_TRACE_STEP") ? std::chrono::duration<double, std::micro>(
+                          std::chrono::steady_clock::now().time_since_epoch()).count() : 0;
+    // Streamed step: with the per-row arrays in pinned memory, K1 stages its
+    // rows straight from them (TMA over PCIe), validates them in shared memory
+    // and writes the device copy -- no separate copy of the table, no K0.
+    bool stream = false;
+    static const bool stream_env = [] { const char* e = getenv("NALAR_STREAM_STEP"); return !e || atoi(e) != 0; }();
+    if (stream_env && s->n_futures && s->n_workflows && !c->batch_on && !c->mig_active_for(s)) {
+        StreamIn& q = c->sin;
+        q.state = (const uint8_t*)mapped_view(s->f_state);
+        q.type = (const uint8_t*)mapped_view(s->f_type);
+        q.round = (const uint8_t*)mapped_view(s->f_round);
+        q.pin = (const int16_t*)mapped_view(s->f_pin);
+        q.exec = (const int16_t*)mapped_view(s->f_executor);
+        q.eoff = (const uint32_t*)mapped_view(s->f_edge_off);
+        q.edges = s->n_edges ? (const uint32_t*)mapped_view(s->edges) : (const uint32_t*)c->d_edges;
+        stream = q.state && q.type && q.round && q.pin && q.exec && q.eoff && q.edges;
+    }
+    int rc = upload_impl(c, s, err_row, false, stream);   // copies (+ K0 unless streamed) queued, no sync
     if (rc) return rc;
+    if (stream && !c->all_staged) {                    // a block too large to stage: the plain path
+        c->h_err[0] = ~0ull;
+        c->h_err[1] = 0ull;
+        CopyBatch cb(c->stream);
+        CK(cb.h2d(c->d_state, s->f_state, c->N));
+        CK(cb.h2d(c->d_type, s->f_type, c->N));
+        CK(cb.h2d(c->d_round, s->f_round, c->N));
+        CK(cb.h2d(c->d_exec, s->f_executor, 2ull * c->N));
+        CK(cb.h2d(c->d_pin, s->f_pin, 2ull * c->N));
+        CK(cb.h2d(c->d_eoff, s->f_edge_off, 4ull * (c->N + 1)));
+        CK(cb.h2d(c->d_edges, s->edges, 4ull * c->E));
+        CK(cb.flush());
+        stream = false;
+        rc = validate_table(c, err_row, nullptr, false);
+        if (rc) return rc;
+    }
+    if (stream) {
+        c->sin.err = c->d_err + 2;
+        c->sin.verdict = c->d_err + 5;
+        c->sin.i_type = c->d_itype;
+        c->sin.n_edges = c->E; c->sin.n_types = c->T; c->sin.n_inst = c->I;
+    }
+    c->streaming = stream;
+    c->last_streamed = stream;
+    static const bool trace = getenv("NALAR_TRACE_STEP") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t1 = trace ? now() : 0;
     rc = nalar_policy_epoch(c, policy);                // kernels skip an invalid table on the device
+    c->streaming = false;
     if (rc) { c->uploaded = false; return rc; }
+    const double t2 = trace ? now() : 0;
     rc = fetch_impl(c, out);                           // the one synchronisation
+    if (trace) fprintf(stderr, "[nalar step] upload queued %.1f us, epoch queued %.1f, fetch+sync %.1f (streamed %d)\n",
+                       t1 - t0, t2 - t1, now() - t2, (int)stream);
     const int vr = validate_verdict(c, err_row);       // K0 ran before everything above
     if (vr) {
         c->uploaded = false;
@@ -1024,7 +1114,7 @@ int nalar_step(nalar_ctx* c, const nalar_snapshot* s, int policy, nalar_decision
     return peer_check(c, rc);
 }
 
-static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync) {
+static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, bool sync, bool stream) {
     // NALAR_TRACE_UPLOAD=1: host-side phase times of this call on stderr
     static const bool trace = getenv("NALAR_TRACE_UPLOAD") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::micro>(
@@ -1084,13 +1174,15 @@ static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, 
     CK(h2d(c->d_wf_off, s->wf_fut_off, 4ull * (W + 1)));
     CK(h2d(c->d_wf_prio, s->wf_prio, 4ull * W));
     CK(h2d(c->d_wf_id, s->wf_id, 8ull * W));
-    CK(h2d(c->d_state, s->f_state, N));
-    CK(h2d(c->d_type, s->f_type, N));
-    CK(h2d(c->d_round, s->f_round, N));
-    CK(h2d(c->d_exec, s->f_executor, 2ull * N));
-    CK(h2d(c->d_pin, s->f_pin, 2ull * N));
-    CK(h2d(c->d_eoff, s->f_edge_off, 4ull * (N + 1)));
-    CK(h2d(c->d_edges, s->edges, 4ull * E));
+    if (!stream) {          // (a streamed step's sweep reads these from the caller's memory)
+        CK(h2d(c->d_state, s->f_state, N));
+        CK(h2d(c->d_type, s->f_type, N));
+        CK(h2d(c->d_round, s->f_round, N));
+        CK(h2d(c->d_exec, s->f_executor, 2ull * N));
+        CK(h2d(c->d_pin, s->f_pin, 2ull * N));
+        CK(h2d(c->d_eoff, s->f_edge_off, 4ull * (N + 1)));
+        CK(h2d(c->d_edges, s->edges, 4ull * E));
+    }
     CK(h2d(c->d_itype, s->i_type, I));
     CK(h2d(c->d_icap, s->i_cap, 4ull * I));
     CK(h2d(c->d_ibase, s->i_base_load, 4ull * I));
@@ -1124,6 +1216,14 @@ static int upload_impl(nalar_ctx* c, const nalar_snapshot* s, int64_t* err_row, 
     c->blocks_valid = true;
     c->blocks_T = T;
     if (trace) tt[3] = now();
+    if (stream) {
+        // K1 checks the rows (K0's contract) as it stages them; K4 publishes
+        // a failure into h_err, read after the step's synchronisation
+        c->h_err[0] = ~0ull;
+        c->h_err[1] = 0ull;
+        c->uploaded = true;
+        return NALAR_OK;
+    }
     rc = validate_table(c, err_row, nullptr, sync);
     if (trace) {
         tt[4] = now();
@@ -1372,6 +1472,12 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
     for (uint8_t a : c->h_taff) th = (th ^ a) * 1099511628211ull;
     Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->params_gen, c->smem, c->d_state,
             (c->have_mig ? 1u : 0u) | (c->have_method ? 2u : 0u), th, c->max_inst_per_type};
+    if (c->streaming) {
+        const void* a[7] = {c->sin.state, c->sin.type, c->sin.round, c->sin.pin, c->sin.exec, c->sin.eoff, c->sin.edges};
+        uint64_t h = 1469598103934665603ull;
+        for (const void* x : a) h = (h ^ (uint64_t)(uintptr_t)x) * 1099511628211ull;
+        key.stream_key = h | 1ull;
+    }
     // a graph pays off only for a shape that repeats (not after every delta)
     const bool repeat = c->last_key_set && c->last_key == key;
     const bool cached = c->gexec[policy] && c->gkey[policy] == key;

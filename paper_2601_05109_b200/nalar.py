@@ -33,6 +33,7 @@ EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
            "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile",
+           "nalar_debug_last_step_streamed",
            "nalar_delta_apply", "nalar_set_policy_params", "nalar_peer_buffer", "nalar_peer_connect",
            "nalar_step")
 NALAR_DELTA_APPLY_ASSIGNED = 1
@@ -125,6 +126,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_epoch_stats_get.argtypes = [C.c_void_p, P(nalar_epoch_stats)]
     lib.nalar_debug_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]
     lib.nalar_debug_profile.restype = C.c_int
+    lib.nalar_debug_last_step_streamed.argtypes = [C.c_void_p]
+    lib.nalar_debug_last_step_streamed.restype = C.c_int
     lib.nalar_delta_apply.argtypes = [C.c_void_p, P(nalar_delta), P(C.c_int64)]
     lib.nalar_delta_apply.restype = C.c_int
     lib.nalar_set_policy_params.argtypes = [C.c_void_p, P(nalar_policy_params)]
@@ -513,6 +516,11 @@ class Context:
             e.err_row = row.value
             raise e
         return self._results(bufs, d)
+
+    def last_step_streamed(self) -> bool:
+        """Whether the last step() staged the table straight from the
+        caller's pinned arrays (nalar_step's streamed path)."""
+        return bool(_lib.nalar_debug_last_step_streamed(self.h))
 
     def _decisions(self, bufs, cache):
         N, W, I = self.n
