@@ -247,9 +247,11 @@ typedef struct {
     int16_t*  ra_prov;    /* [T]                                               */
     uint32_t  t_cap;      /* elements of the four arrays above (>= T)          */
     uint32_t  n_reassign; /* out                                               */
-    /* HoL migration (only with nalar_policy_params.migrate,
-     * world == 1): migrate_to[f] = destination instance of a QUEUED future
-     * (a SESSION future carries its session: re-home its pin), -1 none.      */
+    /* HoL migration (only with nalar_policy_params.migrate):
+     * migrate_to[f] = destination instance of a QUEUED future (a SESSION
+     * future carries its session: re-home its pin), -1 none.  world > 1: the
+     * rank's own rows; i_mig_in / i_mig_out / n_migrated are global (the same
+     * on every rank).                                                         */
     int16_t*  migrate_to; /* [N] (capacity f_cap)                              */
     uint32_t* i_mig_in;   /* [I] (capacity i_cap)                              */
     uint32_t* i_mig_out;  /* [I]                                               */
@@ -286,7 +288,11 @@ typedef struct {
      * least-backlogged (load + assigned) unblocked instance of its type while
      * that backlog + delta <= the source's; STATEFUL futures never move, a
      * SESSION future only as its session's sole queued work with nothing of
-     * the session running.  E_NOTIMPL with world > 1. */
+     * the session running.  world > 1: every rank's candidates travel in the
+     * epoch's one exchange (a list region per rank after the (row base, rows)
+     * pairs; nalar_exchange_buffer's n_words covers it) and every rank runs
+     * the same greedy; more than 8127 candidates on one rank: the fetch /
+     * stats return E_NOTIMPL. */
     uint32_t migrate;              /* 0 off, 1 on                                  */
     uint32_t theta_wait, theta_head, delta;
     /* batch coalescing (NEXT-4): the `batchable` directive as a per-type

@@ -276,8 +276,37 @@ struct FetchParams {
 
 // K5 HoL migration (NEXT-1, k_migrate.cu); G == 1
 constexpr uint32_t kK5MaxInst = 256;    // instances per type the migration pass supports
+// World > 1, HoL migration on (NEXT-1): every rank's migration candidates
+// travel in the ONE exchange of the epoch, as a list region per rank after the
+// (row base, rows) pairs: word 0 = entries (kListOverflow: too many), words
+// [1, 1 + kMaxTypesDev) = entries per type, then per type in order the rank's
+// candidates in row order, each its bucket item's second word (level | (executor
+// + 1) << 16).  Regions of other ranks are zero in a rank's own buffer, so the
+// allreduce (sum) is an allgather.
+constexpr uint32_t kListWords = 8192;
+constexpr uint32_t kMaxTypesDev = 64;
+constexpr uint32_t kListHdr = 1 + kMaxTypesDev;
+constexpr uint32_t kListOverflow = 0xFFFFFFFFu;
+
+struct ListParams {
+    const uint32_t* tot_loc;    // [Rh] this rank's bucket totals
+    const uint32_t* cnt_rb;     // [Rh][B]
+    const uint32_t* off_rb;
+    const uint32_t* blk_row0;
+    const uint2* items;
+    uint32_t* list;             // this rank's list region (kListWords)
+    uint32_t* mrow;             // [kListWords] this rank's row of each list entry
+    uint32_t R, B, n_types;
+};
+cudaError_t launch_lists(const ListParams& p, cudaStream_t s);
+
 struct MigrateParams {
     const unsigned long long* verdict;
+    // world > 1: every rank's list region ([G][kListWords]) and this rank's rows
+    const uint32_t* lists;
+    const uint32_t* mrow;
+    uint32_t G, rank;
+    unsigned long long* list_err;      // mapped host word: a rank's list overflowed
     const uint32_t* H;          // [Rh][Lv] (this rank's slot == the sum when G == 1)
     const uint32_t* tot;        // [Rh]
     const uint32_t* cnt_rb;     // [Rh][B]
@@ -322,6 +351,8 @@ constexpr uint32_t kPeerPoison = 0xFFFFFFFFu;   // flag value of a rank whose ex
 constexpr uint32_t kPeerLocalWords = 8;         // epoch, push ctr, gather ctr, wait ok, sticky failed
 struct PeerParams {
     uint32_t* peers[kPeerMaxRanks];   // every rank's receive buffer (own included)
+    uint32_t lw;                      // list words per rank (kListWords when lists travel, else 0)
+    const uint32_t* list_mine;        // this rank's list region
     const uint32_t* slot;             // this rank's H slot [Rh*Lv]
     const uint32_t* load;             // this rank's partial load [I]
     const uint32_t* tot;              // this rank's partial totals [Rh]
@@ -332,7 +363,7 @@ struct PeerParams {
     uint32_t G, rank, rh_lv, I, Rh;
 };
 inline size_t peer_par_words(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
-    return (size_t)G * (Rhmax * Lv + Imax + Rhmax + 2);
+    return (size_t)G * (Rhmax * Lv + Imax + Rhmax + 2 + kListWords);
 }
 inline size_t peer_buffer_bytes(uint32_t G, size_t Rhmax, uint32_t Lv, size_t Imax) {
     return 4 * (kPeerFlagWords + 2 * peer_par_words(G, Rhmax, Lv, Imax) + kPeerLocalWords);

@@ -23,6 +23,14 @@
 //      (level_j only grows, backlog_s - m no longer shrinks), so it is retired
 //      and the batch is re-evaluated from the next lane.  Each pass decides at
 //      least one lane; a batch takes at most (1 + retired sources) passes.
+//
+// World > 1: the candidates of every rank arrive in the epoch's one exchange
+// (k_lists below writes this rank's into its list region before the
+// collective).  The global O4 order is (level desc, rank asc, row asc) -- the
+// shards are consecutive in the row order -- so every rank walks all ranks'
+// lists in rank order with the same counting sort, runs the same greedy on the
+// same (global) backlogs and reaches the same moves; it writes migrate_to for
+// its own rows only.
 #include "internal.h"
 
 namespace nalar {
@@ -54,9 +62,11 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
     __shared__ uint2 s_c[kMigWin];                          // (row, local source) by rank - w0
     __shared__ uint32_t s_nt, s_lmin;
 
+    __shared__ uint32_t s_loff[kPeerMaxRanks], s_lcnt[kPeerMaxRanks + 1], s_lerr;
     if (*p.verdict) return;              // an invalid table (K0)
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t t = blockIdx.x, r = p.R + t, Lv = p.levels, B = p.B;
+    const uint32_t G = p.G > 1 ? p.G : 1u;
     // ---- static: the type's instances, blocked flags (before the PDL wait) --
     const uint32_t k0 = p.type_off[t], ni = p.type_off[t + 1] - k0;
     for (uint32_t k = tid; k < ni; k += kK5Threads) {
@@ -68,9 +78,33 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    const uint32_t n = p.tot[r];                              // candidates of type t
+    const uint32_t n = p.tot[r];                              // candidates of type t (all ranks)
     uint32_t hl = 0;
-    if (tid < Lv) hl = p.H[(size_t)r * Lv + tid];
+    if (tid < Lv)
+        for (uint32_t s = 0; s < G; ++s) hl += p.H[((size_t)s * p.Rh + r) * Lv + tid];
+    if (G > 1) {
+        // each rank's list segment of type t: offset and count
+        if (tid == 0) s_lerr = 0;
+        if (tid < G) {
+            const uint32_t* L = p.lists + (size_t)tid * kListWords;
+            uint32_t off = 0;
+            for (uint32_t u = 0; u < t; ++u) off += L[1 + u];
+            s_loff[tid] = kListHdr + off;
+            s_lcnt[tid] = L[1 + t];
+            if (L[0] == kListOverflow) s_lerr = 1u;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t c = 0;
+            for (uint32_t s = 0; s < G; ++s) { const uint32_t x = s_lcnt[s]; s_lcnt[s] = c; c += x; }
+            s_lcnt[G] = c;
+        }
+        __syncthreads();
+        if (s_lerr) {                          // some rank's candidates did not fit its list
+            if (tid == 0 && t == 0 && p.list_err) *(volatile unsigned long long*)p.list_err = 1ull;
+            return;
+        }
+    }
     for (uint32_t k = tid; k < ni; k += kK5Threads) {
         const uint32_t i = s_inst[k];
         const uint64_t b = (uint64_t)p.i_load[i] + p.i_assigned[i];
@@ -126,7 +160,42 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
 
     for (uint32_t w0 = 0; w0 < n; w0 += kMigWin) {
         // ---- 1. place the candidates of ranks [w0, w0 + kMigWin) ------------
-        for (uint32_t b0 = 0; b0 < B; b0 += kK5Threads) {
+        if (G > 1) {
+            // every rank's list, in rank order: one global sequence in row order
+            const uint32_t total = s_lcnt[G];
+            for (uint32_t q0 = 0; q0 < total; q0 += kK5Threads) {
+                const uint32_t q = q0 + tid;
+                const bool ok = q < total;
+                uint32_t lv = 0x100u + tid, row = 0xFFFFFFFFu, src = 0;
+                if (ok) {
+                    uint32_t s = 0;
+                    while (s + 1 < G && s_lcnt[s + 1] <= q) ++s;
+                    const uint32_t k = q - s_lcnt[s];
+                    const uint32_t e = p.lists[(size_t)s * kListWords + s_loff[s] + k];
+                    lv = e & 0xFFu;
+                    src = s_lk[(e >> 16) - 1u];
+                    if (s == p.rank) row = p.mrow[s_loff[s] - kListHdr + k];
+                }
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, lv);
+                if (ok && (__ffs(peers) - 1) == (int)lane) s_wc[warp][lv] = __popc(peers);
+                __syncthreads();
+                if (ok) {
+                    uint32_t rank = s_run[lv] + __popc(peers & lanemask_lt());
+                    for (uint32_t k = 0; k < warp; ++k) rank += s_wc[k][lv];
+                    const uint32_t g = s_A[lv] + rank;
+                    if (g >= w0 && g < w0 + kMigWin) s_c[g - w0] = make_uint2(row, src);
+                }
+                __syncthreads();
+                {
+                    uint32_t add = 0;
+#pragma unroll
+                    for (int k = 0; k < kK5Warps; ++k) { add += s_wc[k][tid]; s_wc[k][tid] = 0; }
+                    s_run[tid] += add;
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t b0 = 0; G == 1 && b0 < B; b0 += kK5Threads) {
             const uint32_t bb = b0 + tid;
             const uint32_t c = bb < B ? p.cnt_rb[(size_t)r * B + bb] : 0u;
             if (bb < B) s_base[tid] = p.blk_row0[bb] + p.off_rb[(size_t)r * B + bb];
@@ -208,7 +277,7 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
                     const uint32_t commit = A & (first == 32u ? 0xFFFFFFFFu : ((1u << first) - 1u));
                     const bool me = (commit >> lane) & 1u;
                     if (me) {
-                        p.migrate_to[cx.x] = (int16_t)s_inst[kt];
+                        if (cx.x != 0xFFFFFFFFu) p.migrate_to[cx.x] = (int16_t)s_inst[kt];   // own rows only
                         atomicAdd(&s_in[kt], 1u);
                     }
                     // per source: its moves in this pass, added once by its lowest lane
@@ -237,6 +306,68 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
     if (tid == 0 && n_moves) atomicAdd(&p.counters[C_MIGRATED], n_moves);
 }
 
+// this rank's migration candidates into its list region of the exchange
+// (world > 1), one block per type: the type's bucket items over the K1 blocks
+// in row order; block 0 writes the header
+__global__ void __launch_bounds__(256) k_lists(ListParams p) {
+    __shared__ uint32_t s_pref[257], s_base[256], s_red[8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t t = blockIdx.x, r = p.R + t, B = p.B;
+    uint32_t off = 0, total = 0;
+    for (uint32_t u = 0; u < p.n_types; ++u) {
+        const uint32_t c = p.tot_loc[p.R + u];
+        off += u < t ? c : 0u;
+        total += c;
+    }
+    if (kListHdr + total > kListWords) {
+        if (t == 0 && tid == 0) p.list[0] = kListOverflow;
+        return;
+    }
+    if (t == 0)
+        for (uint32_t u = tid; u < kListHdr; u += blockDim.x)
+            p.list[u] = u == 0 ? total : (u - 1 < p.n_types ? p.tot_loc[p.R + u - 1] : 0u);
+    uint32_t done = 0;
+    for (uint32_t b0 = 0; b0 < B; b0 += 256) {
+        const uint32_t bb = b0 + tid;
+        const uint32_t c = bb < B ? p.cnt_rb[(size_t)r * B + bb] : 0u;
+        if (bb < B) s_base[tid] = p.blk_row0[bb] + p.off_rb[(size_t)r * B + bb];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        __syncthreads();
+        if (lane == 31) s_red[warp] = incl;
+        __syncthreads();
+        uint32_t wb = 0;
+        for (uint32_t k = 0; k < warp; ++k) wb += s_red[k];
+        s_pref[tid] = wb + incl - c;
+        if (tid == 255) s_pref[256] = wb + incl;
+        __syncthreads();
+        const uint32_t n = s_pref[256], nb = min(256u, B - b0);
+        for (uint32_t q = tid; q < n; q += 256) {
+            uint32_t lo = 0, hi = nb - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (s_pref[mid] <= q) lo = mid;
+                else hi = mid - 1;
+            }
+            const uint2 x = p.items[s_base[lo] + (q - s_pref[lo])];
+            p.list[kListHdr + off + done + q] = x.y;
+            p.mrow[off + done + q] = x.x;
+        }
+        done += n;
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_lists(const ListParams& p, cudaStream_t s) {
+    if (p.n_types == 0) return cudaSuccess;
+    k_lists<<<p.n_types, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s) {
     if (p.n_types == 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
@@ -258,6 +389,7 @@ cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s) {
 cudaError_t preload_k_migrate() {
     cudaFuncAttributes a;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k5_migrate)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k_lists)) return e;
     return cudaSuccess;
 }
 

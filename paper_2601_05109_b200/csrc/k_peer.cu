@@ -56,7 +56,7 @@ __device__ __forceinline__ uint64_t gtimer_ns() {
 __global__ void __launch_bounds__(256) k_peer_push(PeerParams p) {
     uint32_t* loc = p.peers[p.rank] + kPeerFlagWords + 2 * p.par_words;   // local words
     const uint32_t e = loc[0] + 1u, par = e & 1u;
-    const uint32_t nh = p.rh_lv, n = nh + p.I + p.Rh + 2;  // words sent to each peer
+    const uint32_t nh = p.rh_lv, n = nh + p.I + p.Rh + 2 + p.lw;  // words sent to each peer
     const uint64_t total = (uint64_t)n * p.G;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = (uint32_t)(j / n), w = (uint32_t)(j % n);
@@ -72,9 +72,13 @@ __global__ void __launch_bounds__(256) k_peer_push(PeerParams p) {
         } else if (w < nh + p.I + p.Rh) {
             v = p.tot[w - nh - p.I];
             o = (size_t)p.G * (nh + p.I) + (size_t)p.rank * p.Rh + (w - nh - p.I);
-        } else {
+        } else if (w < nh + p.I + p.Rh + 2) {
             v = p.rb_mine[w - nh - p.I - p.Rh];
             o = (size_t)p.G * (nh + p.I + p.Rh) + 2ull * p.rank + (w - nh - p.I - p.Rh);
+        } else {                                  // this rank's list region (NEXT-1 candidates)
+            const uint32_t k = w - nh - p.I - p.Rh - 2;
+            v = p.list_mine[k];
+            o = (size_t)p.G * (nh + p.I + p.Rh + 2) + (size_t)p.rank * p.lw + k;
         }
         dst[o] = v;
     }
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(256) k_peer_gather(PeerParams p) {
     const bool s_ok = loc[3] != 0u;
     const uint32_t* src = own + kPeerFlagWords + par * p.par_words;
     const uint32_t nh = p.rh_lv;
-    const uint64_t nH = (uint64_t)p.G * nh, n = nH + p.I + p.Rh + 2ull * p.G;
+    const uint64_t nH = (uint64_t)p.G * nh, n = nH + p.I + p.Rh + 2ull * p.G + (uint64_t)p.G * p.lw;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t v = 0;
         if (j < nH) {
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(256) k_peer_gather(PeerParams p) {
         } else if (j < nH + p.I + p.Rh) {
             const uint32_t r = (uint32_t)(j - nH - p.I);
             for (uint32_t s = 0; s < p.G; ++s) v += src[nH + (size_t)p.G * p.I + (size_t)s * p.Rh + r];
-        } else {                                  // (row base, rows) pairs, by rank
+        } else {                                  // (row base, rows) pairs, then the list regions, by rank
             v = src[nH + (size_t)p.G * (p.I + p.Rh) + (j - nH - p.I - p.Rh)];
         }
         p.x[j] = s_ok ? v : 0u;
@@ -159,14 +163,14 @@ static uint32_t peer_grid(uint64_t words) {
 }
 
 cudaError_t launch_peer_exchange(const PeerParams& p, cudaStream_t s) {
-    const uint64_t n = (uint64_t)p.rh_lv + p.I + p.Rh + 2;
+    const uint64_t n = (uint64_t)p.rh_lv + p.I + p.Rh + 2 + p.lw;
     k_peer_push<<<peer_grid(n * p.G), 256, 0, s>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     k_peer_wait<<<1, 32, 0, s>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_peer_gather<<<peer_grid((uint64_t)p.G * p.rh_lv + p.I + p.Rh + 2ull * p.G), 256, 0, s>>>(p);
+    k_peer_gather<<<peer_grid((uint64_t)p.G * p.rh_lv + p.I + p.Rh + 2ull * p.G + (uint64_t)p.G * p.lw), 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 

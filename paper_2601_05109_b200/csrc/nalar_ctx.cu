@@ -144,6 +144,7 @@ struct nalar_ctx {
     uint2* d_items = nullptr;
     uint32_t *d_cnt_rb = nullptr, *d_off_rb = nullptr;
     uint32_t* d_x = nullptr;          // exchange: H[G][R][Lv] then load[I]
+    uint32_t* d_mrow = nullptr;       // world > 1: this rank's row of each entry of its list region
     size_t x_words = 0;
     uint32_t* d_scr = nullptr;        // counters[C_NUM], n_adm[Rmax], tot_loc[Rmax]; contiguous with d_x
     size_t zero_bytes = 0;            // bytes to clear per epoch from d_x
@@ -249,7 +250,7 @@ struct Plan {
     size_t kvh, kvl, kvhome, tmin, tmax, tstat, tbusy, tcap, rakill, raprov, age, head, migto, migin, migout;
     size_t tmaxb, method, bhead;
     size_t items, cnt_rb, off_rb, x, scr, err;
-    size_t x_words, total;
+    size_t x_words, total, mrow;
     uint32_t Rmax, Rhmax, Bmax;
 };
 
@@ -323,7 +324,9 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->items = L.take<uint2>(N);
     p->cnt_rb = L.take<uint32_t>((size_t)p->Rhmax * p->Bmax);
     p->off_rb = L.take<uint32_t>((size_t)p->Rhmax * p->Bmax);
-    p->x_words = (size_t)G * p->Rhmax * Lv + I + p->Rhmax + 2ull * G;   // + (row base, rows) per rank
+    p->x_words = (size_t)G * p->Rhmax * Lv + I + p->Rhmax + 2ull * G    // + (row base, rows) per rank
+                 + (G > 1 ? (size_t)G * kListWords : 0);                  // + list regions (NEXT-1)
+    p->mrow = L.take<uint32_t>(G > 1 ? kListWords : 1);
     // exchange buffer and scratch are contiguous so one memset clears both
     p->x = L.off;
     L.off += p->x_words * 4;
@@ -577,9 +580,17 @@ int run_k4(nalar_ctx* c) {
 
 
 
+// world > 1 with HoL migration: every rank's candidates travel in the exchange
+bool lists_on(nalar_ctx* c) { return c->cfg.world > 1 && c->mig_active(); }
+// the list regions [G][kListWords], right after the (row base, rows) pairs
+uint32_t* x_lists(nalar_ctx* c) {
+    const uint32_t G = (uint32_t)c->cfg.world;
+    return c->d_x + (size_t)G * c->Rh * c->Lv + c->I + c->Rh + 2ull * G;
+}
+
 size_t x_used_words(nalar_ctx* c) {
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
-    return (size_t)G * c->Rh * c->Lv + c->I + c->Rh + 2ull * G;
+    return (size_t)G * c->Rh * c->Lv + c->I + c->Rh + 2ull * G + (lists_on(c) ? (size_t)G * kListWords : 0);
 }
 
 
@@ -602,6 +613,15 @@ int enqueue_first_half(nalar_ctx* c, int policy) {
     if (timing) CK(record_ev(c, 0));
     int rc = run_k1(c, policy);
     if (rc) return rc;
+    if (lists_on(c)) {               // this rank's migration candidates -> its list region
+        ListParams l{};
+        l.tot_loc = c->d_scr + C_NUM + c->Rmax;
+        l.cnt_rb = c->d_cnt_rb; l.off_rb = c->d_off_rb; l.blk_row0 = c->d_blk_row0; l.items = c->d_items;
+        l.list = x_lists(c) + (size_t)c->cfg.rank * kListWords;
+        l.mrow = c->d_mrow;
+        l.R = c->R; l.B = c->B; l.n_types = c->T;
+        CK(launch_lists(l, c->stream));
+    }
     if (timing) CK(record_ev(c, 1));
     return NALAR_OK;
 }
@@ -622,6 +642,8 @@ int enqueue_collective(nalar_ctx* c) {
         p.rb_mine = x_rb(c) + 2 * p.rank;
         p.err = c->peer_err_dev;
         p.par_words = c->peer_par_words;
+        p.lw = lists_on(c) ? kListWords : 0u;
+        p.list_mine = x_lists(c) + (size_t)p.rank * kListWords;
         CK(launch_peer_exchange(p, c->stream));
         return NALAR_OK;
     }
@@ -648,7 +670,12 @@ int enqueue_second_tail(nalar_ctx* c) {
     if (c->mig_active()) {          // K5 HoL migration (NEXT-1), after admission
         MigrateParams m{};
         m.verdict = c->d_err + 5;
-        m.H = c->d_x; m.tot = c->d_x + (size_t)c->Rh * c->Lv + c->I;
+        const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
+        m.H = c->d_x; m.tot = c->d_x + (size_t)G * c->Rh * c->Lv + c->I;
+        m.G = G; m.rank = c->cfg.world > 1 ? (uint32_t)c->cfg.rank : 0u;
+        m.lists = G > 1 ? x_lists(c) : nullptr;
+        m.mrow = c->d_mrow;
+        m.list_err = c->h_err_dev + 7;
         m.cnt_rb = c->d_cnt_rb; m.off_rb = c->d_off_rb; m.blk_row0 = c->d_blk_row0; m.items = c->d_items;
         m.type_off = c->d_type_off; m.type_inst = c->d_type_inst;
         m.i_load = c->d_iload; m.i_assigned = c->d_iasg; m.i_head_rem = c->d_head;
@@ -915,6 +942,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
     c->d_ispare = at<uint32_t>(a, p.ispare); c->d_iasg = at<uint32_t>(a, p.iasg); c->d_arow = at<uint32_t>(a, p.arow);
     c->d_items = at<uint2>(a, p.items); c->d_cnt_rb = at<uint32_t>(a, p.cnt_rb); c->d_off_rb = at<uint32_t>(a, p.off_rb);
     c->d_x = at<uint32_t>(a, p.x); c->d_scr = at<uint32_t>(a, p.scr);
+    c->d_mrow = at<uint32_t>(a, p.mrow);
     c->d_err = at<unsigned long long>(a, p.err);
     if (cfg->stream) {
         c->stream = (cudaStream_t)cfg->stream;
@@ -939,6 +967,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         if (cudaEventCreate(&e) != cudaSuccess) return bail(NALAR_E_CUDA);
     c->h_err[4] = 0;
     c->h_err[6] = 0;
+    c->h_err[7] = 0;
     c->h_err_dev = (unsigned long long*)mapped_view(c->h_err);
     if (!c->h_err_dev) return bail(NALAR_E_CUDA);
     {   // K0's device words: min bad row ~0, structural 0, block counter 0
@@ -1548,6 +1577,11 @@ static int peer_check(nalar_ctx* c, int rc) {
         c->h_err[6] = 0;
         return fail(c, NALAR_E_INVAL, "ranks' workflow ranges out of order (global_row_base)");
     }
+    if (rc == NALAR_OK && c->h_err[7]) {        // K5: a rank's candidate list overflowed (world > 1)
+        c->h_err[7] = 0;
+        return fail(c, NALAR_E_NOTIMPL, "HoL migration: more than %u candidates on a rank (world > 1)",
+                    kListWords - kListHdr);
+    }
     return rc;
 }
 
@@ -1773,8 +1807,6 @@ int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
     CK(cudaMemcpyAsync(c->d_tmin, mn.data(), 2ull * mn.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_tmax, mx.data(), 2ull * mx.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (p->migrate && c->cfg.world > 1)
-        return fail(c, NALAR_E_NOTIMPL, "HoL migration is single-rank (world == 1) in this version");
     bool batch = false;
     std::vector<uint16_t> mbt(c->cfg.max_types, 0);
     for (uint32_t t = 0; p->t_max_batch && t < p->n_types; ++t) {
