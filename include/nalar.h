@@ -256,11 +256,12 @@ typedef struct {
     uint32_t* i_mig_in;   /* [I] (capacity i_cap)                              */
     uint32_t* i_mig_out;  /* [I]                                               */
     uint32_t  n_migrated; /* out                                               */
-    /* Batch coalescing (only with a max_batch > 1, world
-     * == 1): batch_head[f] = row of the first future of f's batch -- the
-     * futures assigned to one instance this epoch with one method, in
-     * priority order, cut into batches of max_batch (
-     * SPEC S:281) -- or -1.                                                  */
+    /* Batch coalescing (only with a max_batch > 1):
+     * batch_head[f] = GLOBAL row (snapshot global_row_base + row) of the
+     * first future of f's batch -- the futures assigned to one instance this
+     * epoch with one method, in priority order, cut into batches of max_batch
+     * -- or -1.  world > 1: the rank's own
+     * rows (a head may be another rank's row); n_batches is global.          */
     int32_t*  batch_head; /* [N] (capacity f_cap)                              */
     uint32_t  n_batches;  /* out                                               */
 } nalar_decisions;
@@ -298,8 +299,11 @@ typedef struct {
     /* batch coalescing (NEXT-4): the `batchable` directive as a per-type
      * max_batch (<= 1: not batchable; Table 1).  A batchable type
      * must have affinity NONE ("cannot be combined with batchable agents",
-     * PAPER.md:576): the epoch returns E_INVAL otherwise.  E_NOTIMPL with
-     * world > 1. */
+     * PAPER.md:576): the epoch returns E_INVAL otherwise.  world > 1: every
+     * rank's eligible futures of the batchable resources travel in the
+     * epoch's one exchange (the list region, as for migration) and every rank
+     * re-derives their admission; E_STATE after a delta (global row base
+     * unknown), E_NOTIMPL at the fetch when a rank's list overflows. */
     const uint16_t* t_max_batch;   /* [n_types] or NULL (no batching)              */
 } nalar_policy_params;
 

@@ -276,19 +276,32 @@ struct FetchParams {
 
 // K5 HoL migration (NEXT-1, k_migrate.cu); G == 1
 constexpr uint32_t kK5MaxInst = 256;    // instances per type the migration pass supports
-// World > 1, HoL migration on (NEXT-1): every rank's migration candidates
-// travel in the ONE exchange of the epoch, as a list region per rank after the
-// (row base, rows) pairs: word 0 = entries (kListOverflow: too many), words
-// [1, 1 + kMaxTypesDev) = entries per type, then per type in order the rank's
-// candidates in row order, each its bucket item's second word (level | (executor
-// + 1) << 16).  Regions of other ranks are zero in a rank's own buffer, so the
-// allreduce (sum) is an allgather.
-constexpr uint32_t kListWords = 8192;
+// World > 1 with HoL migration (NEXT-1) or batch coalescing (NEXT-4) on: the
+// lists these passes need from every rank travel in the ONE exchange of the
+// epoch, as a region of kListWords per rank after the (row base, rows) pairs.
+// Regions of other ranks are zero in a rank's own buffer, so the allreduce
+// (sum) is an allgather.
+//  [0, kMigWords) migration: word 0 = entries (kListOverflow: too many), words
+//    [1, 1 + kMaxTypesDev) = entries per type, then per type in order the
+//    rank's candidates in row order, each its bucket item's second word
+//    (level | (executor + 1) << 16);
+//  [kMigWords, kListWords) batching: word 0 = entries (or kListOverflow),
+//    words [1, 1 + R) = entries per resource (batchable ones only), then per
+//    resource in order the rank's eligible futures in row order, two words
+//    each: level | method << 8, global row.
+constexpr uint32_t kListWords = 16384;
+constexpr uint32_t kMigWords = 8192;
 constexpr uint32_t kMaxTypesDev = 64;
 constexpr uint32_t kListHdr = 1 + kMaxTypesDev;
 constexpr uint32_t kListOverflow = 0xFFFFFFFFu;
 
 struct ListParams {
+    uint32_t mig, batch;        // which sections to write
+    const uint8_t* i_type;      // batching: which resources are batchable
+    const uint16_t* t_max_batch;
+    const uint8_t* f_method;    // [N] or null (method 0)
+    const uint8_t* level;       // [N] (K1's levels)
+    uint32_t row_base;          // this rank's global row base
     const uint32_t* tot_loc;    // [Rh] this rank's bucket totals
     const uint32_t* cnt_rb;     // [Rh][B]
     const uint32_t* off_rb;
@@ -296,7 +309,7 @@ struct ListParams {
     const uint2* items;
     uint32_t* list;             // this rank's list region (kListWords)
     uint32_t* mrow;             // [kListWords] this rank's row of each list entry
-    uint32_t R, B, n_types;
+    uint32_t R, B, n_types, n_inst;
 };
 cudaError_t launch_lists(const ListParams& p, cudaStream_t s);
 
@@ -329,6 +342,16 @@ cudaError_t launch_migrate(const MigrateParams& p, cudaStream_t s);
 // K6 batch coalescing (NEXT-4, k_batch.cu); G == 1
 struct BatchParams {
     const unsigned long long* verdict;
+    uint32_t row_base;             // batch_head holds global rows (row_base + row)
+    // world > 1 (K6 over every rank's lists, k_batch.cu k6_batch_ranks)
+    uint32_t G, n_rows, R, levels, Rh;
+    const uint32_t* lists;         // [G][kListWords]
+    const uint32_t* H;             // [G][Rh][Lv] exchange
+    const uint32_t* tot;           // [Rh] global eligible per resource
+    const uint32_t* i_spare;       // [I] global (K4)
+    const uint32_t* type_off;
+    const uint32_t* type_inst;
+    unsigned long long* list_err;  // mapped host word
     const uint8_t* i_type;
     const uint16_t* t_max_batch;   // [T]
     const uint8_t* f_method;       // [N] or null

@@ -306,26 +306,73 @@ __global__ void __launch_bounds__(kK5Threads, 1) k5_migrate(MigrateParams p) {
     if (tid == 0 && n_moves) atomicAdd(&p.counters[C_MIGRATED], n_moves);
 }
 
-// this rank's migration candidates into its list region of the exchange
-// (world > 1), one block per type: the type's bucket items over the K1 blocks
-// in row order; block 0 writes the header
+// this rank's lists for the exchange (world > 1), written after the sweep:
+// blocks [0, T) the migration candidates of type t (NEXT-1), blocks [T, T + R)
+// (or [0, R) without migration) the eligible futures of batchable resource r
+// (NEXT-4); each walks its resource's bucket items over the K1 blocks in row
+// order.  See internal.h (kListWords) for the layout.
 __global__ void __launch_bounds__(256) k_lists(ListParams p) {
     __shared__ uint32_t s_pref[257], s_base[256], s_red[8];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t t = blockIdx.x, r = p.R + t, B = p.B;
-    uint32_t off = 0, total = 0;
-    for (uint32_t u = 0; u < p.n_types; ++u) {
-        const uint32_t c = p.tot_loc[p.R + u];
-        off += u < t ? c : 0u;
-        total += c;
+    const uint32_t B = p.B;
+    const uint32_t nm = p.mig ? p.n_types : 0u;
+    const bool is_mig = blockIdx.x < nm;
+    uint32_t r, off, total, n_loc;
+    uint32_t* L;
+    if (is_mig) {
+        const uint32_t t = blockIdx.x;
+        r = p.R + t;
+        off = 0; total = 0;
+        for (uint32_t u = 0; u < p.n_types; ++u) {
+            const uint32_t c = p.tot_loc[p.R + u];
+            off += u < t ? c : 0u;
+            total += c;
+        }
+        L = p.list;
+        if (kListHdr + total > kMigWords) {
+            if (t == 0 && tid == 0) L[0] = kListOverflow;
+            return;
+        }
+        if (t == 0)
+            for (uint32_t u = tid; u < kListHdr; u += blockDim.x)
+                L[u] = u == 0 ? total : (u - 1 < p.n_types ? p.tot_loc[p.R + u - 1] : 0u);
+        n_loc = p.tot_loc[r];
+    } else {
+        r = blockIdx.x - nm;
+        auto batchable = [&](uint32_t q) {
+            const uint32_t t = q < p.n_inst ? p.i_type[q] : q - p.n_inst;
+            return p.t_max_batch[t] > 1u;
+        };
+        // offset of r's entries and the total, over the batchable resources
+        uint32_t o = 0, tt = 0;
+        for (uint32_t q = tid; q < p.R; q += blockDim.x) {
+            const uint32_t c = batchable(q) ? p.tot_loc[q] : 0u;
+            o += q < r ? c : 0u;
+            tt += c;
+        }
+#pragma unroll
+        for (int k = 16; k > 0; k >>= 1) {
+            o += __shfl_xor_sync(0xFFFFFFFFu, o, k);
+            tt += __shfl_xor_sync(0xFFFFFFFFu, tt, k);
+        }
+        if (lane == 0) { s_red[warp] = o; s_pref[warp] = tt; }
+        __syncthreads();
+        off = 0; total = 0;
+        for (uint32_t k = 0; k < 8; ++k) { off += s_red[k]; total += s_pref[k]; }
+        __syncthreads();
+        L = p.list + kMigWords;
+        const uint32_t hdr = 1 + p.R;
+        if (hdr + 2 * total > kListWords - kMigWords) {
+            if (r == 0 && tid == 0) L[0] = kListOverflow;
+            return;
+        }
+        if (r == 0)
+            for (uint32_t q = tid; q < hdr; q += blockDim.x)
+                L[q] = q == 0 ? total : (batchable(q - 1) ? p.tot_loc[q - 1] : 0u);
+        n_loc = batchable(r) ? p.tot_loc[r] : 0u;
+        off = hdr + 2 * off;
     }
-    if (kListHdr + total > kListWords) {
-        if (t == 0 && tid == 0) p.list[0] = kListOverflow;
-        return;
-    }
-    if (t == 0)
-        for (uint32_t u = tid; u < kListHdr; u += blockDim.x)
-            p.list[u] = u == 0 ? total : (u - 1 < p.n_types ? p.tot_loc[p.R + u - 1] : 0u);
+    if (n_loc == 0) return;
     uint32_t done = 0;
     for (uint32_t b0 = 0; b0 < B; b0 += 256) {
         const uint32_t bb = b0 + tid;
@@ -354,8 +401,14 @@ __global__ void __launch_bounds__(256) k_lists(ListParams p) {
                 else hi = mid - 1;
             }
             const uint2 x = p.items[s_base[lo] + (q - s_pref[lo])];
-            p.list[kListHdr + off + done + q] = x.y;
-            p.mrow[off + done + q] = x.x;
+            if (is_mig) {
+                L[kListHdr + off + done + q] = x.y;
+                p.mrow[off + done + q] = x.x;
+            } else {
+                const uint32_t m = p.f_method ? p.f_method[x.x] : 0u;
+                L[off + 2 * (done + q)] = (x.y & 0xFFu) | (m << 8);
+                L[off + 2 * (done + q) + 1] = p.row_base + x.x;
+            }
         }
         done += n;
         __syncthreads();
@@ -363,8 +416,9 @@ __global__ void __launch_bounds__(256) k_lists(ListParams p) {
 }
 
 cudaError_t launch_lists(const ListParams& p, cudaStream_t s) {
-    if (p.n_types == 0) return cudaSuccess;
-    k_lists<<<p.n_types, 256, 0, s>>>(p);
+    const uint32_t nb = (p.mig ? p.n_types : 0u) + (p.batch ? p.R : 0u);
+    if (nb == 0) return cudaSuccess;
+    k_lists<<<nb, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 

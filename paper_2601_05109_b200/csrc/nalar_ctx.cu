@@ -581,7 +581,7 @@ int run_k4(nalar_ctx* c) {
 
 
 // world > 1 with HoL migration: every rank's candidates travel in the exchange
-bool lists_on(nalar_ctx* c) { return c->cfg.world > 1 && c->mig_active(); }
+bool lists_on(nalar_ctx* c) { return c->cfg.world > 1 && (c->mig_active() || c->batch_on); }
 // the list regions [G][kListWords], right after the (row base, rows) pairs
 uint32_t* x_lists(nalar_ctx* c) {
     const uint32_t G = (uint32_t)c->cfg.world;
@@ -615,6 +615,13 @@ int enqueue_first_half(nalar_ctx* c, int policy) {
     if (rc) return rc;
     if (lists_on(c)) {               // this rank's migration candidates -> its list region
         ListParams l{};
+        l.mig = c->mig_active() ? 1u : 0u;
+        l.batch = c->batch_on ? 1u : 0u;
+        l.i_type = c->d_itype; l.t_max_batch = c->d_tmaxb;
+        l.f_method = c->have_method ? c->d_method : nullptr;
+        l.level = c->d_level;
+        l.row_base = (uint32_t)c->row_base;
+        l.n_inst = c->I;
         l.tot_loc = c->d_scr + C_NUM + c->Rmax;
         l.cnt_rb = c->d_cnt_rb; l.off_rb = c->d_off_rb; l.blk_row0 = c->d_blk_row0; l.items = c->d_items;
         l.list = x_lists(c) + (size_t)c->cfg.rank * kListWords;
@@ -691,6 +698,13 @@ int enqueue_second_tail(nalar_ctx* c) {
         bp.level = c->d_level; bp.n_adm = c->d_scr + C_NUM; bp.tot_loc = c->d_scr + C_NUM + c->Rmax;
         bp.arow = c->d_arow; bp.ainst = c->d_ainst; bp.n_inst = c->I;
         bp.batch_head = c->d_bhead; bp.counters = c->d_scr;
+        const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
+        bp.row_base = (uint32_t)c->row_base;
+        bp.G = G; bp.n_rows = c->N; bp.R = c->R; bp.levels = c->Lv; bp.Rh = c->Rh;
+        bp.lists = G > 1 ? x_lists(c) : nullptr;
+        bp.H = c->d_x; bp.tot = c->d_x + (size_t)G * c->Rh * c->Lv + c->I;
+        bp.i_spare = c->d_ispare; bp.type_off = c->d_type_off; bp.type_inst = c->d_type_inst;
+        bp.list_err = c->h_err_dev + 7;
         CK(launch_batch(bp, c->stream));
     }
     if (timing) CK(record_ev(c, 3));
@@ -707,6 +721,9 @@ int epoch_checks(nalar_ctx* c) {
         for (uint32_t t = 0; t < c->T && t < c->h_tmaxb.size(); ++t)
             if (c->h_tmaxb[t] > 1 && c->h_taff[t] != NALAR_AFF_NONE)
                 return fail(c, NALAR_E_INVAL, "type %u: batchable with managed state (PAPER.md:576)", t);
+    if (c->batch_on && c->cfg.world > 1 && !c->row_base_known)
+        return fail(c, NALAR_E_STATE, "batch coalescing across ranks needs the snapshot's global_row_base "
+                    "(upload a snapshot after a delta)");
     if (c->mig_active() && c->max_inst_per_type > kK5MaxInst)
         return fail(c, NALAR_E_NOTIMPL, "HoL migration supports <= %u instances per type", kK5MaxInst);
     return NALAR_OK;
@@ -1579,8 +1596,8 @@ static int peer_check(nalar_ctx* c, int rc) {
     }
     if (rc == NALAR_OK && c->h_err[7]) {        // K5: a rank's candidate list overflowed (world > 1)
         c->h_err[7] = 0;
-        return fail(c, NALAR_E_NOTIMPL, "HoL migration: more than %u candidates on a rank (world > 1)",
-                    kListWords - kListHdr);
+        return fail(c, NALAR_E_NOTIMPL, "HoL migration / batching: more candidates on a rank than its exchange "
+                    "list holds (world > 1)");
     }
     return rc;
 }
@@ -1813,8 +1830,6 @@ int nalar_set_policy_params(nalar_ctx* c, const nalar_policy_params* p) {
         mbt[t] = p->t_max_batch[t];
         batch |= mbt[t] > 1;
     }
-    if (batch && c->cfg.world > 1)
-        return fail(c, NALAR_E_NOTIMPL, "batch coalescing is single-rank (world == 1) in this version");
     CK(cudaMemcpyAsync(c->d_tmaxb, mbt.data(), 2ull * mbt.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->batch_on = batch;

@@ -109,16 +109,13 @@ def test_reassign_sharded_identical_on_every_rank(G):
         ctx.close()
 
 
-def test_single_rank_passes_refuse_multi_rank():
-    """NEXT-4 is single-rank in this version: E_NOTIMPL, not a wrong answer
-    (NEXT-1 runs across ranks: tests/test_migrate_gpu.py)."""
+def test_next_rows_accepted_multi_rank():
+    """NEXT-1 / NEXT-2 / NEXT-4 all run across ranks (tests/test_migrate_gpu.py,
+    tests/test_batch_gpu.py, above)."""
     nalar = _nalar()
     s = c2(1)
     ctx = nalar.Context.for_snapshot(s, world=2, rank=0, collective=nalar.NALAR_COLL_EXTERNAL)
     ctx.set_policy_params(migrate=True)
-    ctx.set_policy_params()
-    with pytest.raises(nalar.NalarError) as e:
-        ctx.set_policy_params(t_max_batch=[4, 0, 0, 0], n_types=4)
-    assert e.value.code == nalar.NALAR_E_NOTIMPL
-    ctx.set_policy_params(reassign=True)            # NEXT-2 is multi-rank
+    ctx.set_policy_params(t_max_batch=[4, 0, 0, 0], n_types=4)
+    ctx.set_policy_params(reassign=True)
     ctx.close()
