@@ -406,12 +406,14 @@ def main():
     ms_ra = timed_epochs(max(args.steps // 4, 10), True)
     ra_out = ctx.fetch(("reassign", "kv"))
     ctx.set_policy_params(reassign=False)
-    # HoL migration (NEXT-1, single rank): the same table with synthetic wait
-    # ages / head-job times (nalar_gen.with_hol_inputs, SPEC delta = 2)
+    # HoL migration (NEXT-1): the same table with synthetic wait ages /
+    # head-job times (nalar_gen.with_hol_inputs on the global table, then this
+    # rank's shard; SPEC delta = 2)
     mig = {}
-    if world == 1:
+    if True:
         from nalar_gen import with_hol_inputs
-        sh = with_hol_inputs(s)
+        sh = with_hol_inputs(table)
+        sh = sh.slice_workflows(w0, w1) if world > 1 else sh
         ctx.set_policy_params(migrate=True, theta_wait=50, theta_head=50, delta=2)
         ctx.upload(sh)
         timed_epochs(args.warmup, True)
@@ -420,10 +422,11 @@ def main():
         ctx.set_policy_params(migrate=False)
         ctx.upload(s)
         mig = {"migrate_on_epoch_us": float(np.mean(ms_mig)) * 1e3, "migrated": int(mo["n_migrated"])}
-        # batch coalescing (NEXT-4, single rank): max_batch 4 on the NONE-affinity
-        # types, three methods drawn per future
-        sb = s.copy()
-        sb.f_method = np.random.default_rng(3).integers(0, 3, s.n_futures).astype(np.uint8)
+        # batch coalescing (NEXT-4): max_batch 4 on the NONE-affinity types,
+        # three methods drawn per future (global table, then this rank's shard)
+        sb = table.copy()
+        sb.f_method = np.random.default_rng(3).integers(0, 3, table.n_futures).astype(np.uint8)
+        sb = sb.slice_workflows(w0, w1) if world > 1 else sb
         ctx.set_policy_params(t_max_batch=np.where(s.t_affinity == 0, 4, 0), n_types=s.n_types)
         ctx.upload(sb)
         timed_epochs(args.warmup, True)

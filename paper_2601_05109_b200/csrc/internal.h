@@ -49,6 +49,15 @@ size_t k1_fixed_smem(uint32_t n_types, uint32_t n_inst, uint32_t R);
 // staged, with its rows / edges)
 // (inline: the host partition evaluates it once per workflow per cut)
 __host__ __device__ inline size_t k1_align16(size_t x) { return (x + 15) & ~(size_t)15; }
+// an upper bound of k1_block_smem(.., staged = true) without the per-array
+// 16-B rounding (each of its 26 terms rounds up by < 16 B): the partition's
+// cheap first test
+inline size_t k1_block_smem_upper(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T) {
+    const size_t w = wfs, r = rows;
+    return w * (8 * (size_t)T + 8) + 4 * w + 4 * (w + 1) + 4 * w + 32 * w + 8 * w * T + 8 * w * T + 8 * w +
+           3 * (r + 32) + 2 * (2 * r + 32) + (4 * (r + 1) + 32) + (4 * (size_t)edges + 32) + (4 * (w + 1) + 32) +
+           (4 * w + 32) + 2 * r + 2 * r + 4 * 4 * r + 2 * r + 26 * 16;
+}
 inline size_t k1_block_smem(uint32_t rows, uint32_t edges, uint32_t wfs, uint32_t T, bool staged) {
     auto align16 = k1_align16;
 
@@ -79,6 +88,9 @@ struct ValidateParams {
     unsigned long long* err;   // [0] = min bad row (init ~0), [1] = structural flag (device)
     uint32_t* done;            // block-completion counter (0 between launches)
     unsigned long long* host_err;   // mapped host words: the last block publishes err here and re-arms it
+    // after a delta: the delta's update errors (device words, ~0 = none) are
+    // published to host_err[2], [3] and re-armed by the same last block
+    unsigned long long* delta_err;
     unsigned long long* verdict;    // device word: 1 if the table is invalid (the epoch kernels skip)
 };
 
@@ -247,6 +259,7 @@ struct DeltaParams {
     uint32_t n_inst_upd, n_inst; const uint32_t* inst_id; const uint32_t* inst_cap; const uint32_t* inst_base;
     uint32_t* i_cap; uint32_t* i_base;
     unsigned long long* err;     // [0] bad update index, [1] bad prio / instance update index
+    uint32_t n_fut_new, n_edges_new;   // tails of the new offset arrays (written by KD3)
 };
 
 // host <-> device segment copies (k_io.cu): src / dst are device-accessible

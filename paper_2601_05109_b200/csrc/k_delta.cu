@@ -57,6 +57,10 @@ __global__ void kd3_rebuild(DeltaParams p) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (w >= p.n_wf_new) return;
+    if (w == 0 && lane == 0) {               // tails of the new offset arrays
+        p.n_wf_off[p.n_wf_new] = p.n_fut_new;
+        p.n_eoff[p.n_fut_new] = p.n_edges_new;
+    }
     const RebuildPlan pl = p.plan[w];
     // workflow arrays
     if (lane == 0) {

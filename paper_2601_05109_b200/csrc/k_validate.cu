@@ -102,6 +102,10 @@ __global__ void __launch_bounds__(kK0Threads) k0_validate(ValidateParams p) {
             volatile unsigned long long* h = p.host_err;
             h[0] = bad;
             h[1] = structural;
+            if (p.delta_err) {                   // a delta's update errors (KD2 / KD4), then re-armed
+                h[2] = atomicExch(&p.delta_err[0], ~0ull);
+                h[3] = atomicExch(&p.delta_err[1], ~0ull);
+            }
             // the epoch kernels of a combined step (nalar_step) may already be
             // queued behind this one: they read this word and skip an invalid table
             *p.verdict = (bad != ~0ull || structural) ? 1ull : 0ull;

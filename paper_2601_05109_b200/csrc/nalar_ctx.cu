@@ -199,6 +199,7 @@ struct nalar_ctx {
     std::vector<uint64_t> m_wf_id;
     std::vector<uint32_t> m_wf_off, m_wf_eoff;
     std::vector<uint32_t> m_perm;          // per-block task order (set_blocks)
+    std::vector<RebuildPlan> m_plan;       // delta scratch (nalar_delta_apply)
     bool blocks_valid = false;              // device block tables match m_wf_off / m_wf_eoff
     uint32_t blocks_T = 0;
     bool assign_valid = false;        // last epoch's assignment regions match the table
@@ -436,7 +437,8 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
             while (w < W) {
                 const uint32_t wr = wf_off[w + 1] - wf_off[w];
                 const uint32_t e_if = wf_eoff[w + 1] - wf_eoff[ws];
-                if (w > ws && (k1_block_smem(rows + wr, e_if, w - ws + 1, c->T, true) > kStageBudget ||
+                if (w > ws && ((k1_block_smem_upper(rows + wr, e_if, w - ws + 1, c->T) > kStageBudget &&
+                                k1_block_smem(rows + wr, e_if, w - ws + 1, c->T, true) > kStageBudget) ||
                                w - ws + 1 > kMaxWfPerBlock || is_deep(w)))
                     break;
                 rows += wr;
@@ -836,7 +838,8 @@ int validate_verdict(nalar_ctx* c, int64_t* err_row) {
     return NALAR_OK;
 }
 
-int validate_table(nalar_ctx* c, int64_t* err_row, const char*, bool sync = true) {
+int validate_table(nalar_ctx* c, int64_t* err_row, const char*, bool sync = true,
+                   unsigned long long* delta_err = nullptr) {
     cudaStream_t st = c->stream;
     c->h_err[0] = ~0ull;                  // the verdict when there is nothing to check
     c->h_err[1] = 0ull;
@@ -848,6 +851,7 @@ int validate_table(nalar_ctx* c, int64_t* err_row, const char*, bool sync = true
     v.done = (uint32_t*)(c->d_err + 4);
     v.host_err = c->h_err_dev;            // K0 publishes [0] / [1] here
     v.verdict = c->d_err + 5;
+    v.delta_err = delta_err;
     CK(launch_validate(v, st));
     if (!sync) return NALAR_OK;           // nalar_step: the verdict is read after its one sync
     CK(cudaStreamSynchronize(st));
@@ -1331,7 +1335,8 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
         }
         groups.push_back({d->app_wf_id[j], j, 1});
     }
-    std::vector<RebuildPlan> plan;
+    std::vector<RebuildPlan>& plan = c->m_plan;      // reused across deltas (no allocation)
+    plan.clear();
     plan.reserve(W + groups.size());
     const uint64_t max_live = W ? c->m_wf_id.back() : 0;
     size_t g = 0;
@@ -1406,7 +1411,6 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     const size_t s_aed = S.take<uint32_t>(nae);
     const size_t s_pid = S.take<uint64_t>(np), s_pvl = S.take<int32_t>(np);
     const size_t s_iid = S.take<uint32_t>(ni), s_icp = S.take<uint32_t>(ni), s_ibl = S.take<uint32_t>(ni);
-    const size_t s_tail = S.take<uint32_t>(2);
     if (S.off > c->h_dstage_bytes) {
         if (c->h_dstage) cudaFreeHost(c->h_dstage);
         c->h_dstage = nullptr;
@@ -1439,12 +1443,9 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     CK(h2d(s_aed, d->app_edges, 4ull * nae));
     CK(h2d(s_pid, d->prio_wf_id, 8ull * np)); CK(h2d(s_pvl, d->prio_value, 4ull * np));
     CK(h2d(s_iid, d->inst_id, 4ull * ni)); CK(h2d(s_icp, d->inst_cap, 4ull * ni)); CK(h2d(s_ibl, d->inst_base_load, 4ull * ni));
-    {
-        const uint32_t tails[2] = {N2, E2};        // tails of the new offset arrays
-        CK(h2d(s_tail, tails, 8));
-    }
     CK(cudaMemcpyAsync(sb, c->h_dstage, S.off, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(c->d_err, 0xFF, 16, st));
+    // (the update-error words d_err[0], [1] are armed (~0); K0's last block
+    // publishes them to h_err[2], [3] after this delta and re-arms them)
     DeltaParams p{};
     p.wf_off = c->d_wf_off; p.wf_prio = c->d_wf_prio; p.wf_id = c->d_wf_id;
     p.state = c->d_state; p.type = c->d_type; p.round = c->d_round; p.exec = c->d_exec; p.pin = c->d_pin;
@@ -1463,12 +1464,12 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     p.n_inst_upd = ni; p.n_inst = c->I; p.inst_id = at<uint32_t>(sb, s_iid); p.inst_cap = at<uint32_t>(sb, s_icp);
     p.inst_base = at<uint32_t>(sb, s_ibl); p.i_cap = c->d_icap; p.i_base = c->d_ibase;
     p.err = c->d_err;
+    p.n_fut_new = N2; p.n_edges_new = E2;               // KD3 writes the offset tails
     CK(launch_delta(p, apply_asg, c->R, st));
-    CK(cudaMemcpyAsync(c->alt.wf_off + W2, sb + s_tail, 4, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(c->alt.eoff + N2, sb + s_tail + 4, 4, cudaMemcpyDeviceToDevice, st));
-    // the update errors travel to pinned slots 2, 3 now and are checked after
-    // the single synchronisation below (validation reuses d_err)
-    CK(cudaMemcpyAsync(c->h_err + 2, c->d_err, 16, cudaMemcpyDeviceToHost, st));
+    if (W2 == 0) {                                       // (no KD3 block: write them here)
+        CK(cudaMemsetAsync(c->alt.wf_off, 0, 4, st));
+        CK(cudaMemsetAsync(c->alt.eoff, 0, 4, st));
+    }
     c->assign_valid = false;
     if (trace) tt[2] = now();
     // ---- swap in the new table, re-partition, validate ------------------------
@@ -1486,8 +1487,16 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     c->have_method = false;          // so are the batch methods (d_method is in pre-delta row order)
     int rc = set_blocks(c, nullptr, /*fill_sms=*/false);
     if (trace) tt[3] = now();
-    if (!rc) rc = validate_table(c, err_index, nullptr);       // synchronises
-    else cudaStreamSynchronize(st);
+    c->h_err[2] = ~0ull;
+    c->h_err[3] = ~0ull;
+    if (!rc && N2 && W2) {
+        rc = validate_table(c, err_index, nullptr, true, c->d_err);   // synchronises; publishes the update errors
+    } else {
+        if (!rc) rc = validate_table(c, err_index, nullptr, false);   // (nothing to check: clears the verdict)
+        cudaMemcpyAsync(c->h_err + 2, c->d_err, 16, cudaMemcpyDeviceToHost, st);
+        cudaMemsetAsync(c->d_err, 0xFF, 16, st);
+        cudaStreamSynchronize(st);
+    }
     if (trace) {
         tt[4] = now();
         fprintf(stderr, "[nalar delta] plan %.1f us, stage+launch %.1f, swap+partition %.1f, validate+sync %.1f, "

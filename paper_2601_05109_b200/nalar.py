@@ -299,18 +299,23 @@ _DELTA_ARRAYS = {"upd_wf_id": np.uint64, "upd_seq": np.uint32, "upd_state": np.u
 
 
 def delta_struct(dl) -> tuple:
-    """nalar_delta over a nalar_gen.Delta-like object (numpy arrays)."""
-    keep = {k: np.ascontiguousarray(getattr(dl, k), dtype=dt) for k, dt in _DELTA_ARRAYS.items()}
+    """nalar_delta over a nalar_gen.Delta-like object (numpy arrays).  Empty
+    arrays stay NULL (numpy's .ctypes.data costs ~2 us per array)."""
     d = nalar_delta()
     d.flags = int(dl.flags)
-    d.n_updates = len(keep["upd_seq"])
-    d.n_retired = len(keep["retired_wf_id"])
-    d.n_append = len(keep["app_wf_id"])
-    d.n_append_edges = len(keep["app_edges"])
-    d.n_prio = len(keep["prio_wf_id"])
-    d.n_inst = len(keep["inst_id"])
-    for k, a in keep.items():
-        setattr(d, k, _ptr(a))
+    keep = []
+    for k, dt in _DELTA_ARRAYS.items():
+        a = getattr(dl, k)
+        if len(a):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            setattr(d, k, a.ctypes.data)
+    d.n_updates = len(dl.upd_seq)
+    d.n_retired = len(dl.retired_wf_id)
+    d.n_append = len(dl.app_wf_id)
+    d.n_append_edges = len(dl.app_edges)
+    d.n_prio = len(dl.prio_wf_id)
+    d.n_inst = len(dl.inst_id)
     return d, keep
 
 
@@ -525,8 +530,11 @@ class Context:
     def _decisions(self, bufs, cache):
         N, W, I = self.n
         # the marshalled struct is reused while the caller passes the same
-        # output arrays (they stay referenced by the cache, so ids are stable)
-        key = (N, W, I, tuple((k, id(v), len(v)) for k, v in bufs.items()))
+        # output arrays (they stay referenced by the cache, so ids are stable);
+        # the table sizes only matter for groups without buffers (their
+        # pointers are null), so a delta-mode table that changes size every
+        # epoch keeps the cache
+        key = tuple((k, id(v), len(v)) for k, v in bufs.items())
         cached = getattr(self, "_out_cache", None)
         if cached is not None and cached[0] == key:
             d = cached[1]
