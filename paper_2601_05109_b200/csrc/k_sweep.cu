@@ -40,14 +40,26 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
+__device__ __forceinline__ void k1_entry(const SweepParams& p, uint8_t* smem) {
     // an invalid table (K0's verdict, complete before the zero kernel ran)
     // is never swept: nalar_step queues this kernel before the host has seen it
     if (!p.stream_in && *p.verdict) return;
     const uint32_t b = p.blk_order[blockIdx.x];
     if (p.blk_staged[b]) k1_body<true>(p, smem, b);
     else k1_body<false>(p, smem, b);
+}
+
+// one CTA per SM: the latency-bound single-wave case (C4: 142 blocks)
+__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    k1_entry(p, smem);
+}
+
+// two CTAs per SM (64 registers): tables of several waves (C5, 2^20 futures),
+// where a second resident block hides the sweeps' dependent latencies
+__global__ void __launch_bounds__(kK1Threads, 2) k1_sweep_x2(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    k1_entry(p, smem);
 }
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once
@@ -76,8 +88,13 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k1_sweep_x2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
         configured = smem;
     }
+    // more blocks than one wave and two fit an SM: the 2-per-SM build
+    static const int x2_env = [] { const char* e = getenv("NALAR_K1_X2"); return e ? atoi(e) : -1; }();
+    const bool x2 = x2_env >= 0 ? x2_env != 0 : (p.B > 148u && 2 * (smem + 1024) <= 228 * 1024);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.B);
     cfg.blockDim = dim3(kK1Threads);
@@ -95,7 +112,7 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     // NALAR_K1_TRIGGER=0 / 1 / 2 = entry / after P2 / before P5)
     static const uint32_t trig = [] { const char* e = getenv("NALAR_K1_TRIGGER"); return e ? (uint32_t)atoi(e) : 2u; }();
     p.trig = trig;
-    return cudaLaunchKernelEx(&cfg, k1_sweep, p);
+    return x2 ? cudaLaunchKernelEx(&cfg, k1_sweep_x2, p) : cudaLaunchKernelEx(&cfg, k1_sweep, p);
 }
 
 
@@ -104,6 +121,7 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
 cudaError_t preload_k_sweep() {
     cudaFuncAttributes a;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_x2)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k_zero)) return e;
     return cudaSuccess;
 }
