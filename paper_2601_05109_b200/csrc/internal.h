@@ -15,13 +15,19 @@ constexpr int kK1Threads = 512;          // sweep: warp per workflow inside a bl
 constexpr int kK1Warps = kK1Threads / 32;
 constexpr uint32_t kLongSteps = 6;      // workflows of >= 6 steps use the transfer decomposition
 // the threshold in rows (kLongSteps steps; NALAR_LONG_STEPS to experiment)
-inline uint32_t long_rows() {
-    static const uint32_t v = [] {
+// rows from which a workflow is composed from step transfers.  A one-wave
+// table (latency-bound: C4) uses kLongSteps; a table of several waves
+// (throughput-bound: a transfer costs ~2.3x an ordinary step) kLongStepsWaves
+// -- measured at C5: 6 / 10 / 16 / 24 steps -> 145 / 140 / 141 / 146 us.
+// NALAR_LONG_STEPS overrides both.
+constexpr uint32_t kLongStepsWaves = 10;
+inline uint32_t long_rows(bool waves = false) {
+    static const int env = [] {
         const char* e = getenv("NALAR_LONG_STEPS");
-        const int s = e ? atoi(e) : (int)kLongSteps;
-        return 32u * (uint32_t)(s > 1 ? s : 1);
+        return e ? atoi(e) : 0;
     }();
-    return v;
+    const int s = env > 0 ? env : (int)(waves ? kLongStepsWaves : kLongSteps);
+    return 32u * (uint32_t)(s > 1 ? s : 1);
 }
 constexpr uint32_t kMaxIface = 7;       // interface rows per step in a transfer
 constexpr int kK4Threads = 256;          // assign: one block per resource

@@ -204,6 +204,7 @@ struct nalar_ctx {
     uint32_t blocks_T = 0;
     bool assign_valid = false;        // last epoch's assignment regions match the table
     bool all_staged = false;          // every K1 block stages its rows in shared memory
+    uint32_t long_rows = 0;           // compose threshold of the current partition (long_rows())
     // streamed step (nalar_step, pinned snapshot): K1 reads the per-row arrays
     // from the caller's host memory, validates them and writes the device copy
     bool streaming = false;
@@ -498,7 +499,7 @@ SweepParams sweep_params(nalar_ctx* c, int policy) {
     p.verdict = c->d_err + 5;
     p.stream_in = c->streaming ? 1u : 0u;
     p.src = c->sin;
-    p.long_rows = long_rows();
+    p.long_rows = c->long_rows;
     p.wf_fut_off = c->d_wf_off; p.wf_prio = c->d_wf_prio;
     p.f_state = c->d_state; p.f_type = c->d_type; p.f_round = c->d_round;
     p.f_exec = c->d_exec; p.f_pin = c->d_pin; p.f_edge_off = c->d_eoff; p.edges = c->d_edges;
@@ -752,6 +753,8 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     partition(c, c->m_wf_off.data(), c->m_wf_eoff.data(), bw, br, be, bs, &mx, fill_sms);
     const double t1 = trace ? now() : 0;
     c->B = (uint32_t)bs.size();
+    c->long_rows = long_rows(c->B > kSmSplit);      // several waves: throughput-bound
+    const uint32_t lr = c->long_rows;
     c->all_staged = std::all_of(bs.begin(), bs.end(), [](uint8_t x) { return x != 0; });
     c->fixed_smem = k1_fixed_smem(c->T, c->I, c->Rh);
     c->smem = c->fixed_smem + mx;
@@ -775,8 +778,8 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
             // many small workflows (a delta-mode table): only the long ones
             // need to start first -- a stable O(n) partition keeps the host
             // cost flat (a full sort per block is ~25 ns per workflow here)
-            std::stable_partition(o, o + (we - ws), [off](uint32_t x) {
-                return off[x + 1] - off[x] >= long_rows();
+            std::stable_partition(o, o + (we - ws), [off, lr](uint32_t x) {
+                return off[x + 1] - off[x] >= lr;
             });
         }
     }
