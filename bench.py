@@ -507,13 +507,16 @@ def main():
 
     def pin_alloc(n, dt):
         return pinned_like(np.zeros(n, dt))
-    outb = ctx.output_buffers(("status", "instance", "assign"), alloc=pin_alloc)
+    # the decisions a controller acts on: status, instance, the ordered
+    # assignment list, new_pin (SESSION homes to record, Q13) and level
+    E2E_FIELDS = ("status", "level", "instance", "new_pin", "assign")
+    outb = ctx.output_buffers(E2E_FIELDS, alloc=pin_alloc)
     e2e_t, split_t = [], []
     n_asg = 0
     for i in range(3 + args.e2e_steps):
         barrier()
         t0 = time.perf_counter()
-        r = ctx.step(sp, pol, ("status", "instance", "assign"), out=outb)
+        r = ctx.step(sp, pol, E2E_FIELDS, out=outb)
         dt = time.perf_counter() - t0
         n_asg = r["n_assigned"]
         streamed = ctx.last_step_streamed()
@@ -524,7 +527,7 @@ def main():
         t0 = time.perf_counter()
         ctx.upload(sp)
         ctx.epoch(pol)
-        ctx.fetch(("status", "instance", "assign"), out=outb)
+        ctx.fetch(E2E_FIELDS, out=outb)
         if i >= 3:
             split_t.append(time.perf_counter() - t0)
     # where the e2e step goes (separately timed, wall clock, same buffers)
@@ -536,7 +539,7 @@ def main():
         ctx.epoch(pol)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
-        ctx.fetch(("status", "instance", "assign"), out=outb)
+        ctx.fetch(E2E_FIELDS, out=outb)
         t3 = time.perf_counter()
         if i >= 3:
             parts["upload"].append(t1 - t0); parts["epoch_sync"].append(t2 - t1); parts["fetch"].append(t3 - t2)
@@ -546,7 +549,7 @@ def main():
         et = et.cuda()
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_mean = float(et.cpu().mean())
-    d2h = 3 * s.n_futures + 6 * n_asg + 32
+    d2h = 5 * s.n_futures + 6 * n_asg + 4 * 9   # status, level, new_pin (1 B), instance (2 B); list; counters
 
     line = {"metric": METRIC, "value": value, "unit": "futures/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
@@ -567,7 +570,7 @@ def main():
             "roofline": roof,
             "e2e": {"value": total_fut / e2e_mean, "unit": "futures/s", "ms_per_step": e2e_mean * 1e3,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "nalar_step",
-                    "streamed": streamed,
+                    "fields": list(E2E_FIELDS), "streamed": streamed,
                     "split_calls_ms_per_step": float(np.mean(split_t) * 1e3), "parts": e2e_parts},
             # per epoch: k_zero (exchange buffer + counters), k1_sweep, k4_assign
             "gpu_launches": 3 * args.steps,

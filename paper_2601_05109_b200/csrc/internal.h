@@ -128,6 +128,13 @@ struct SweepParams {
     const uint32_t* blk_order;
     uint32_t* stage_ctr;
     uint32_t stage_window;
+    // nalar_step with pinned outputs: the per-row outputs also go straight to
+    // the caller's mapped host arrays as they are produced (null: not wanted)
+    uint8_t* o_status;
+    uint8_t* o_level;
+    uint16_t* o_depth;
+    int16_t* o_instance;
+    uint8_t* o_new_pin;
     uint32_t* rb_mine;           // world > 1: this rank's (global_row_base, rows) words of the exchange
     uint32_t row_base, n_rows;
     uint32_t long_rows;          // workflows of >= long_rows rows are composed from step transfers
@@ -189,6 +196,9 @@ struct AssignParams {
     uint32_t stream_in;
     unsigned long long* err;             // [0] min bad row, [1] structural (device)
     unsigned long long* host_err;        // mapped host words [0], [1]
+    uint8_t* o_status;                   // streamed outputs (see SweepParams), admitted rows
+    int16_t* o_instance;
+    uint8_t* o_new_pin;
     const uint32_t* rb;                  // world > 1: every rank's (global_row_base, rows)
     unsigned long long* order_err;       // mapped host word: set when the ranks' row ranges are out of order
     const uint32_t* H;          // [G][R][Lv] summed over ranks

@@ -1025,6 +1025,14 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
             if (staged) { p.level[g] = (uint8_t)lv; p.depth[g] = (uint16_t)d; }
             p.instance[g] = inst;
             p.new_pin[g] = 0;
+            // streamed outputs: straight to the caller's pinned arrays (the
+            // PCIe writes overlap the rest of the epoch; K4 patches the
+            // admitted rows, P4 the fence winners)
+            if (p.o_status) p.o_status[g] = (uint8_t)status;
+            if (p.o_level) p.o_level[g] = (uint8_t)lv;
+            if (p.o_depth) p.o_depth[g] = (uint16_t)d;
+            if (p.o_instance) p.o_instance[g] = inst;
+            if (p.o_new_pin) p.o_new_pin[g] = 0;
             if (elig) {
                 const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
                 atomicAdd(&p.H[(size_t)r * Lv + lv], 1u);
@@ -1127,6 +1135,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         if (f != 0xFFFFFFFFu) {
             flg[f] |= FL_ELIG;
             p.status[r0 + f] = 6;
+            if (p.o_status) p.o_status[r0 + f] = 6;
             const int pinf = pn[f];
             const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + t;
             atomicAdd(&p.H[(size_t)r * Lv + lev[f]], 1u);

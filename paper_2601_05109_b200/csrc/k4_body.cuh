@@ -656,6 +656,9 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
                     p.status[row] = 7;
                     p.instance[row] = inst;
                     p.new_pin[row] = (uint8_t)(is_type && aff != 0);
+                    if (p.o_status) p.o_status[row] = 7;
+                    if (p.o_instance) p.o_instance[row] = inst;
+                    if (p.o_new_pin) p.o_new_pin[row] = (uint8_t)(is_type && aff != 0);
                     const uint32_t pos = list_base + s_LA[lv] + rank;
                     p.assign_row[pos] = row;
                     p.assign_inst[pos] = inst;

@@ -210,6 +210,13 @@ struct nalar_ctx {
     bool streaming = false;
     bool last_streamed = false;
     StreamIn sin{};
+    // nalar_step with pinned per-row outputs: K1 / K4 write them straight to
+    // the caller's memory; the step's fetch then skips them
+    struct StreamOut {
+        uint8_t* status = nullptr; uint8_t* level = nullptr; uint16_t* depth = nullptr;
+        int16_t* instance = nullptr; uint8_t* new_pin = nullptr;
+    } sout;
+    bool sout_on = false;
     Key last_key{};
     bool last_key_set = false;
     unsigned long long* d_prof = nullptr;
@@ -499,6 +506,10 @@ SweepParams sweep_params(nalar_ctx* c, int policy) {
     p.verdict = c->d_err + 5;
     p.stream_in = c->streaming ? 1u : 0u;
     p.src = c->sin;
+    if (c->sout_on) {
+        p.o_status = c->sout.status; p.o_level = c->sout.level; p.o_depth = c->sout.depth;
+        p.o_instance = c->sout.instance; p.o_new_pin = c->sout.new_pin;
+    }
     p.long_rows = c->long_rows;
     p.wf_fut_off = c->d_wf_off; p.wf_prio = c->d_wf_prio;
     p.f_state = c->d_state; p.f_type = c->d_type; p.f_round = c->d_round;
@@ -550,6 +561,7 @@ AssignParams assign_params(nalar_ctx* c) {
     p.stream_in = c->streaming ? 1u : 0u;
     p.err = c->d_err + 2;
     p.host_err = c->h_err_dev;
+    if (c->sout_on) { p.o_status = c->sout.status; p.o_instance = c->sout.instance; p.o_new_pin = c->sout.new_pin; }
     const uint32_t G = c->cfg.world > 1 ? (uint32_t)c->cfg.world : 1u;
     p.H = c->d_x;
     p.rb = c->cfg.world > 1 ? x_rb(c) : nullptr;
@@ -1146,15 +1158,35 @@ int nalar_step(nalar_ctx* c, const nalar_snapshot* s, int policy, nalar_decision
     }
     c->streaming = stream;
     c->last_streamed = stream;
+    // streamed outputs: every requested per-row output pinned and large enough
+    {
+        static const bool sout_env = [] { const char* e = getenv("NALAR_STREAM_OUT"); return !e || atoi(e) != 0; }();
+        nalar_ctx::StreamOut& q = c->sout;
+        q = nalar_ctx::StreamOut{};
+        bool ok = sout_env && c->N && out->f_cap >= c->N &&
+                  (out->status || out->level || out->depth || out->instance || out->new_pin);
+        auto view = [&](void* h) -> void* {
+            if (!h) return nullptr;
+            void* v = mapped_view(h);
+            if (!v) ok = false;
+            return v;
+        };
+        q.status = (uint8_t*)view(out->status); q.level = (uint8_t*)view(out->level);
+        q.depth = (uint16_t*)view(out->depth); q.instance = (int16_t*)view(out->instance);
+        q.new_pin = (uint8_t*)view(out->new_pin);
+        if (!ok) q = nalar_ctx::StreamOut{};
+        c->sout_on = ok;
+    }
     static const bool trace = getenv("NALAR_TRACE_STEP") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::micro>(
                         std::chrono::steady_clock::now().time_since_epoch()).count(); };
     const double t1 = trace ? now() : 0;
     rc = nalar_policy_epoch(c, policy);                // kernels skip an invalid table on the device
     c->streaming = false;
-    if (rc) { c->uploaded = false; return rc; }
+    if (rc) { c->uploaded = false; c->sout_on = false; return rc; }
     const double t2 = trace ? now() : 0;
-    rc = fetch_impl(c, out);                           // the one synchronisation
+    rc = fetch_impl(c, out);                           // the one synchronisation (skips streamed outputs)
+    c->sout_on = false;
     if (trace) fprintf(stderr, "[nalar step] upload queued %.1f us, epoch queued %.1f, fetch+sync %.1f (streamed %d)\n",
                        t1 - t0, t2 - t1, now() - t2, (int)stream);
     const int vr = validate_verdict(c, err_row);       // K0 ran before everything above
@@ -1530,9 +1562,11 @@ int nalar_policy_epoch(nalar_ctx* c, int policy) {
     for (uint8_t a : c->h_taff) th = (th ^ a) * 1099511628211ull;
     Key key{c->N, c->E, c->W, c->I, c->T, c->B, c->R, (uint32_t)policy, c->params_gen, c->smem, c->d_state,
             (c->have_mig ? 1u : 0u) | (c->have_method ? 2u : 0u), th, c->max_inst_per_type};
-    if (c->streaming) {
-        const void* a[7] = {c->sin.state, c->sin.type, c->sin.round, c->sin.pin, c->sin.exec, c->sin.eoff, c->sin.edges};
-        uint64_t h = 1469598103934665603ull;
+    if (c->streaming || c->sout_on) {
+        const void* a[12] = {c->sin.state, c->sin.type, c->sin.round, c->sin.pin, c->sin.exec, c->sin.eoff,
+                             c->sin.edges, c->sout.status, c->sout.level, c->sout.depth, c->sout.instance,
+                             c->sout.new_pin};
+        uint64_t h = 1469598103934665603ull ^ (c->streaming ? 7ull : 0ull);
         for (const void* x : a) h = (h ^ (uint64_t)(uintptr_t)x) * 1099511628211ull;
         key.stream_key = h | 1ull;
     }
@@ -1712,8 +1746,12 @@ static int fetch_impl(nalar_ctx* c, nalar_decisions* o) {
         const bool tbad = (o->t_busy || o->t_capsum || o->ra_kill || o->ra_prov) && o->t_cap < c->T;
         bool mapped = !(fbad || wbad || ibad || kbad || tbad);
         CopyBatch cb(st);
+        const bool so = c->sout_on;      // nalar_step: K1 / K4 wrote these already
         for (const Out& q : outs) {
             if (!mapped || !q.h || !q.bytes) continue;
+            if (so && (q.h == (void*)o->status || q.h == (void*)o->level || q.h == (void*)o->depth ||
+                       q.h == (void*)o->instance || q.h == (void*)o->new_pin))
+                continue;
             void* v = mapped_view(q.h);
             if (!v) mapped = false;
             else cb.p.seg[cb.p.n++] = CopySeg{q.d, v, (uint64_t)q.bytes};

@@ -250,3 +250,49 @@ def test_streamed_step_off_for_pageable_and_next_rows():
     assert np.array_equal(g["batch_head"], ob["batch_head"])
     assert not ctx.last_step_streamed()
     ctx.close()
+
+
+# ---- streamed outputs: with every per-row output pinned, K1 / K4 write them
+# straight to the caller's memory during the epoch (the fetch skips them) ----
+
+@pytest.mark.parametrize("mk", [c1, lambda: c2(1), c4, lambda: random_table(33, n_workflows=30, max_rows=40),
+                                lambda: swe_table(20000, seed=5)])
+@pytest.mark.parametrize("policy", ["srtf", "lpt"])
+def test_streamed_outputs_all_fields(mk, policy):
+    nalar = _nalar()
+    keep = []
+    s = mk()
+    o = oracle_epoch(s, policy)
+    sp = _pinned_snapshot(s, keep)
+    ctx = nalar.Context.for_snapshot(s)
+    out = ctx.output_buffers(("status", "level", "depth", "instance", "new_pin", "wf_agg", "i_load", "i_spare",
+                              "i_assigned", "assign", "kv"),
+                             alloc=lambda n, dt: pinned_like(np.zeros(n, dt), keep), like=s)
+    for k in ("status", "level", "depth", "instance", "new_pin"):
+        out[k][...] = 0x5A                     # poison: every row must be written
+    for _ in range(3):                         # direct launch, graph capture, replay
+        g = ctx.step(sp, policy, out=out)
+        same(o, g, f"{s.name} {policy} streamed outputs")
+    # a split fetch afterwards (the plain copy path) agrees
+    ctx.epoch(policy)
+    same(o, ctx.fetch(), "split after streamed outputs")
+    ctx.close()
+
+
+def test_streamed_outputs_pageable_inputs_and_reassign():
+    """Pageable inputs (plain upload) with pinned outputs still stream the outputs."""
+    nalar = _nalar()
+    keep = []
+    s = c4(2)
+    prm = {"u_hi_pct": 80, "u_lo_pct": 30}
+    o = oracle_epoch(s, "srtf", reassign=prm)
+    ctx = nalar.Context.for_snapshot(s)
+    ctx.set_policy_params(reassign=True, **prm)
+    out = ctx.output_buffers(("status", "level", "depth", "instance", "new_pin", "assign", "reassign"),
+                             alloc=lambda n, dt: pinned_like(np.zeros(n, dt), keep), like=s)
+    for _ in range(2):
+        g = ctx.step(s, "srtf", out=out)
+        for k in ("status", "level", "depth", "instance", "new_pin", "assign_row", "assign_inst"):
+            assert np.array_equal(np.asarray(g[k]), np.asarray(o[k])), k
+        assert np.array_equal(g["ra_kill"], o["ra_kill"])
+    ctx.close()
