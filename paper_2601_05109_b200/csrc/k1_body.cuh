@@ -150,7 +150,7 @@ __device__ __forceinline__ bool doom_closure(bool doom, bool pend, uint32_t need
 // The body is instantiated twice: for a staged block every table pointer
 // derives from the shared-memory window, so the compiler emits LDS/STS; for an
 // unstaged (oversized) block they point into global memory.
-template <bool kStaged>
+template <bool kStaged, bool kOut = false>
 __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uint32_t b) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Rh = p.Rh, Lv = p.levels;
@@ -1028,11 +1028,13 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
             // streamed outputs: straight to the caller's pinned arrays (the
             // PCIe writes overlap the rest of the epoch; K4 patches the
             // admitted rows, P4 the fence winners)
-            if (p.o_status) p.o_status[g] = (uint8_t)status;
-            if (p.o_level) p.o_level[g] = (uint8_t)lv;
-            if (p.o_depth) p.o_depth[g] = (uint16_t)d;
-            if (p.o_instance) p.o_instance[g] = inst;
-            if (p.o_new_pin) p.o_new_pin[g] = 0;
+            if (kOut) {
+                if (p.o_status) p.o_status[g] = (uint8_t)status;
+                if (p.o_level) p.o_level[g] = (uint8_t)lv;
+                if (p.o_depth) p.o_depth[g] = (uint16_t)d;
+                if (p.o_instance) p.o_instance[g] = inst;
+                if (p.o_new_pin) p.o_new_pin[g] = 0;
+            }
             if (elig) {
                 const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + tyf;
                 atomicAdd(&p.H[(size_t)r * Lv + lv], 1u);
@@ -1135,7 +1137,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         if (f != 0xFFFFFFFFu) {
             flg[f] |= FL_ELIG;
             p.status[r0 + f] = 6;
-            if (p.o_status) p.o_status[r0 + f] = 6;
+            if (kOut && p.o_status) p.o_status[r0 + f] = 6;
             const int pinf = pn[f];
             const uint32_t r = pinf >= 0 ? (uint32_t)pinf : I + t;
             atomicAdd(&p.H[(size_t)r * Lv + lev[f]], 1u);

@@ -40,26 +40,35 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
+template <bool kOut>
 __device__ __forceinline__ void k1_entry(const SweepParams& p, uint8_t* smem) {
     // an invalid table (K0's verdict, complete before the zero kernel ran)
     // is never swept: nalar_step queues this kernel before the host has seen it
     if (!p.stream_in && *p.verdict) return;
     const uint32_t b = p.blk_order[blockIdx.x];
-    if (p.blk_staged[b]) k1_body<true>(p, smem, b);
-    else k1_body<false>(p, smem, b);
+    if (p.blk_staged[b]) k1_body<true, kOut>(p, smem, b);
+    else k1_body<false, kOut>(p, smem, b);
 }
 
 // one CTA per SM: the latency-bound single-wave case (C4: 142 blocks)
 __global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry(p, smem);
+    k1_entry<false>(p, smem);
+}
+
+// the same, also writing the per-row outputs to the caller's pinned arrays
+// (nalar_step's streamed outputs; a separate build so the plain epoch keeps
+// its code -- the stores in P3 cost the plain epoch 1.2 us when compiled in)
+__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep_out(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    k1_entry<true>(p, smem);
 }
 
 // two CTAs per SM (64 registers): tables of several waves (C5, 2^20 futures),
 // where a second resident block hides the sweeps' dependent latencies
 __global__ void __launch_bounds__(kK1Threads, 2) k1_sweep_x2(SweepParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry(p, smem);
+    k1_entry<false>(p, smem);
 }
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once
@@ -90,6 +99,8 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(k1_sweep_x2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k1_sweep_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
         configured = smem;
     }
     // more blocks than one wave and two fit an SM: the 2-per-SM build
@@ -112,6 +123,8 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     // NALAR_K1_TRIGGER=0 / 1 / 2 = entry / after P2 / before P5)
     static const uint32_t trig = [] { const char* e = getenv("NALAR_K1_TRIGGER"); return e ? (uint32_t)atoi(e) : 2u; }();
     p.trig = trig;
+    if (p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin)
+        return cudaLaunchKernelEx(&cfg, k1_sweep_out, p);      // (one wave only: the host checks)
     return x2 ? cudaLaunchKernelEx(&cfg, k1_sweep_x2, p) : cudaLaunchKernelEx(&cfg, k1_sweep, p);
 }
 
@@ -122,6 +135,7 @@ cudaError_t preload_k_sweep() {
     cudaFuncAttributes a;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_x2)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_out)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k_zero)) return e;
     return cudaSuccess;
 }

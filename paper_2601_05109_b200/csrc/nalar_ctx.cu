@@ -1163,7 +1163,7 @@ int nalar_step(nalar_ctx* c, const nalar_snapshot* s, int policy, nalar_decision
         static const bool sout_env = [] { const char* e = getenv("NALAR_STREAM_OUT"); return !e || atoi(e) != 0; }();
         nalar_ctx::StreamOut& q = c->sout;
         q = nalar_ctx::StreamOut{};
-        bool ok = sout_env && c->N && out->f_cap >= c->N &&
+        bool ok = sout_env && c->N && out->f_cap >= c->N && c->B <= kSmSplit &&   // one-wave tables (K1 build)
                   (out->status || out->level || out->depth || out->instance || out->new_pin);
         auto view = [&](void* h) -> void* {
             if (!h) return nullptr;
