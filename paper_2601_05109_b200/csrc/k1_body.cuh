@@ -150,8 +150,12 @@ __device__ __forceinline__ bool doom_closure(bool doom, bool pend, uint32_t need
 // The body is instantiated twice: for a staged block every table pointer
 // derives from the shared-memory window, so the compiler emits LDS/STS; for an
 // unstaged (oversized) block they point into global memory.
-template <bool kStaged, bool kOut = false>
+template <bool kStaged, bool kOut = false, bool kProf = false>
 __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uint32_t b) {
+    // NALAR_F_PROFILE stamps only in the profiling build: a null pointer known
+    // at compile time removes every stamp and its branch from the production
+    // sweep (code in P3 costs the plain epoch even when it never runs)
+    unsigned long long* const prof = kProf ? p.prof : nullptr;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Rh = p.Rh, Lv = p.levels;
 
@@ -160,7 +164,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
     const uint32_t nr = r1 - r0, ne = e1 - e0, nw = w1 - w0;
     constexpr bool staged = kStaged;
-    unsigned long long* bprof = p.prof ? p.prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;
+    unsigned long long* bprof = prof ? prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;
     if (bprof && tid == 0) bprof[3] = gtimer();
     // the point where the assignment kernel may launch (PDL) is p.trig; it
     // waits for this grid's completion before reading anything the sweep writes
@@ -438,20 +442,20 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     auto wf_begin = [&](uint32_t wi) {
         m_dep = m_rnd = 0;
         cyc_edge = cyc_round = cyc_rest = cyc_wait = 0;
-        cyc_t = p.prof ? clock64() : 0;
+        cyc_t = prof ? clock64() : 0;
         n_rounds = 0;
         n_kp = 0;
-        if (p.prof && lane == 0) p.prof[(size_t)(w0 + wi) * 2] = gtimer();
+        if (prof && lane == 0) prof[(size_t)(w0 + wi) * 2] = gtimer();
     };
     auto wf_end = [&](uint32_t wi) {
         const uint32_t w = w0 + wi;
         m_dep = __reduce_max_sync(0xFFFFFFFFu, m_dep);
         m_rnd = __reduce_max_sync(0xFFFFFFFFu, m_rnd);
         if (lane == 0) { s_wrnd[wi] = m_rnd; s_agg[wi * 8 + 7] = m_dep; }
-        if (p.prof && lane == 0) {
-            p.prof[(size_t)w * 2 + 1] = gtimer();
+        if (prof && lane == 0) {
+            prof[(size_t)w * 2 + 1] = gtimer();
             cyc_rest += clock64() - cyc_t;
-            unsigned long long* c = p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)w * 4;
+            unsigned long long* c = prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)w * 4;
             c[0] = cyc_edge; c[1] = cyc_round; c[2] = cyc_rest;
             c[3] = cyc_wait ? (unsigned long long)cyc_wait << 32 : (n_rounds | n_kp);
         }
@@ -519,7 +523,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         s3 = np > 3 ? s3 : s0;
         const bool pend = stf == 0u;
         bool doom = pend && dm;
-        if (p.prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
+        if (prof) { const long long t = clock64(); cyc_edge += t - cyc_t; cyc_t = t; }
         // in-step settling: Bellman-Ford rounds on registers, depths moving
         // by shuffles (four rounds per convergence vote); then doom, a
         // boolean closure over in-step DEP edges, by ballots
@@ -532,7 +536,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
                 // the common case: at most 4 slots, and only as many shuffles
                 // per round as the step's widest row needs
                 const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
-                if (p.prof) n_kp += 1ull << (16 + 12 * ((K < 4 ? K : 4) - 1));
+                if (prof) n_kp += 1ull << (16 + 12 * ((K < 4 ? K : 4) - 1));
                 auto settle = [&](auto round) {
                     for (;;) {
                         round();
@@ -612,7 +616,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         d_out = min(d, 65535u);
         doom_out = doom;
         allres_out = allres;
-        if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
+        if (prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
     };
     // a whole short workflow, step by step
     auto sweep_workflow = [&](uint32_t wi) {
@@ -633,7 +637,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         };
         prefetch(fa);
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
-            if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
+            if (prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
             const uint32_t stf = q_st, eb = q_eb, ee = q_ee, rdf = q_rd;
@@ -649,7 +653,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     // P2a: the transfer function of one step of a long workflow
     // NALAR_F_PROFILE: per-block cycle sums of the transfer phases
     unsigned long long* tprof =
-        p.prof ? p.prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)p.n_wf * 4 + b * 8 : nullptr;
+        prof ? prof + (size_t)p.n_wf * 2 + (size_t)p.B * 8 + (size_t)p.R * 8 + (size_t)p.n_wf * 4 + b * 8 : nullptr;
     long long tt = 0;
     auto tstamp = [&](int j) {
         if (tprof) {
@@ -823,12 +827,12 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         auto wait_flag = [&](uint32_t c0) {
             uint32_t v = ld_acquire_u16(&aux[c0]);
             if (!(v & kStepDone)) {
-                const long long tw = p.prof ? clock64() : 0;
+                const long long tw = prof ? clock64() : 0;
                 do {
                     __nanosleep(20);
                     v = ld_acquire_u16(&aux[c0]);
                 } while (!(v & kStepDone));
-                if (p.prof) cyc_wait += clock64() - tw;
+                if (prof) cyc_wait += clock64() - tw;
             }
             return v;
         };
@@ -853,7 +857,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         a0 = wait_flag(fa);
         load_step(fa);
         for (uint32_t c0 = fa; c0 < fb; c0 += 32) {
-            if (p.prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
+            if (prof) { const long long t = clock64(); cyc_rest += t - cyc_t; cyc_t = t; }
             const uint32_t f = c0 + lane;
             const bool valid = f < fb;
             const uint32_t c_rdf = rdf, c_stf = stf;
@@ -882,13 +886,13 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
                 best = c7 ? max(best, c7 - 1u) : best;
                 d = min(best, 65535u);
                 allres = (c_av & 0x100u) != 0;
-                if (p.prof) { const long long t = clock64() + (long long)d; cyc_edge += t - cyc_t; cyc_t = t; }
+                if (prof) { const long long t = clock64() + (long long)d; cyc_edge += t - cyc_t; cyc_t = t; }
                 {   // in-step closure from the transfer's ancestor masks
                     const bool seed = c_stf == 0u && dm;
                     const uint32_t D = __ballot_sync(0xFFFFFFFFu, seed);
                     doom = seed || (c_stf == 0u && (c_nd & D) != 0u);
                 }
-                if (p.prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
+                if (prof) { const long long t = clock64(); cyc_round += t - cyc_t; cyc_t = t; }
             } else {
                 const uint32_t eb = valid ? eo[f] - e0 : 0u, ee = valid ? eo[f + 1] - e0 : 0u;
                 const uint32_t pva = eb < ee ? ed[eb] : 0u, pvb = eb + 1 < ee ? ed[eb + 1] : 0u;

@@ -40,14 +40,14 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-template <bool kOut>
+template <bool kOut, bool kProf = false>
 __device__ __forceinline__ void k1_entry(const SweepParams& p, uint8_t* smem) {
     // an invalid table (K0's verdict, complete before the zero kernel ran)
     // is never swept: nalar_step queues this kernel before the host has seen it
     if (!p.stream_in && *p.verdict) return;
     const uint32_t b = p.blk_order[blockIdx.x];
-    if (p.blk_staged[b]) k1_body<true, kOut>(p, smem, b);
-    else k1_body<false, kOut>(p, smem, b);
+    if (p.blk_staged[b]) k1_body<true, kOut, kProf>(p, smem, b);
+    else k1_body<false, kOut, kProf>(p, smem, b);
 }
 
 // one CTA per SM: the latency-bound single-wave case (C4: 142 blocks)
@@ -62,6 +62,16 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
 __global__ void __launch_bounds__(kK1Threads, 1) k1_sweep_out(SweepParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     k1_entry<true>(p, smem);
+}
+
+// NALAR_F_PROFILE builds (the stamps compiled in; one / two CTAs per SM)
+__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep_prof(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    k1_entry<false, true>(p, smem);
+}
+__global__ void __launch_bounds__(kK1Threads, 2) k1_sweep_x2_prof(SweepParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    k1_entry<false, true>(p, smem);
 }
 
 // two CTAs per SM (64 registers): tables of several waves (C5, 2^20 futures),
@@ -101,6 +111,10 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(k1_sweep_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k1_sweep_prof, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k1_sweep_x2_prof, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
         configured = smem;
     }
     // more blocks than one wave and two fit an SM: the 2-per-SM build
@@ -123,6 +137,7 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     // NALAR_K1_TRIGGER=0 / 1 / 2 = entry / after P2 / before P5)
     static const uint32_t trig = [] { const char* e = getenv("NALAR_K1_TRIGGER"); return e ? (uint32_t)atoi(e) : 2u; }();
     p.trig = trig;
+    if (p.prof) return x2 ? cudaLaunchKernelEx(&cfg, k1_sweep_x2_prof, p) : cudaLaunchKernelEx(&cfg, k1_sweep_prof, p);
     if (p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin)
         return cudaLaunchKernelEx(&cfg, k1_sweep_out, p);      // (one wave only: the host checks)
     return x2 ? cudaLaunchKernelEx(&cfg, k1_sweep_x2, p) : cudaLaunchKernelEx(&cfg, k1_sweep, p);
@@ -136,6 +151,8 @@ cudaError_t preload_k_sweep() {
     if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_x2)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_out)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_prof)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_x2_prof)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k_zero)) return e;
     return cudaSuccess;
 }
