@@ -150,7 +150,9 @@ __device__ __forceinline__ bool doom_closure(bool doom, bool pend, uint32_t need
 // The body is instantiated twice: for a staged block every table pointer
 // derives from the shared-memory window, so the compiler emits LDS/STS; for an
 // unstaged (oversized) block they point into global memory.
-template <bool kStaged, bool kOut = false, bool kProf = false>
+// kIn: streamed-step staging / validation; kNext: HoL-migration candidates and
+// batch-head presets (the NEXT-1 / NEXT-4 modes) -- compiled in only where used
+template <bool kStaged, bool kOut = false, bool kProf = false, bool kIn = false, bool kNext = false>
 __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uint32_t b) {
     // NALAR_F_PROFILE stamps only in the profiling build: a null pointer known
     // at compile time removes every stamp and its branch from the production
@@ -231,7 +233,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     uint16_t* aux;        //   DEP-from-interface mask, FAILED pred, all-resolved, k, ok
     if (staged) {
         // a streamed step stages the rows from the caller's pinned host arrays
-        const bool si = p.stream_in != 0u;
+        const bool si = kIn && p.stream_in != 0u;
         const Win ws = window(si ? p.src.state : p.f_state, 1, r0, r1);
         const Win wt = window(si ? p.src.type : p.f_type, 1, r0, r1);
         const Win wr = window(si ? p.src.round : p.f_round, 1, r0, r1);
@@ -259,7 +261,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         aux = (uint16_t*)q;
         if (tid == 0) {
             mbar_init(mbar, 1);
-            if (p.stream_in && blockIdx.x >= p.stage_window) {
+            if (kIn && p.stream_in && blockIdx.x >= p.stage_window) {
                 // pacing of a streamed step's host reads (see SweepParams)
                 asm volatile("griddepcontrol.wait;" ::: "memory");   // the counter is the zero kernel's
                 const uint32_t need = blockIdx.x - p.stage_window;
@@ -335,11 +337,11 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     }
     __syncthreads();
     if (staged) mbar_wait(mbar, 0);
-    if (staged && p.stream_in && tid == 0) {
+    if (kIn && staged && p.stream_in && tid == 0) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
         atomicAdd(p.stage_ctr, 1u);
     }
-    if (staged && p.stream_in) {
+    if (kIn && staged && p.stream_in) {
         // K0's input contract (k_validate.cu validate_row, Q1) on the
         // staged rows: an edge points to an earlier row of the same workflow,
         // states / types in range, pins and executors name an instance of the
@@ -1002,7 +1004,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
             // past theta_head; STATEFUL never moves; a SESSION future only as
             // its session's sole queued work with nothing running (decided in P4)
             bool mig = false;
-            if (p.mig_on) {
+            if (kNext && p.mig_on) {
                 if (stf == 1u && aff != 2u) {
                     const bool c = p.f_age[r0 + f] > p.theta_wait && p.i_head_rem[ex[f]] > p.theta_head;
                     if (aff == 0u) {
@@ -1015,8 +1017,8 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
                 if (stf == 2u && aff == 1u) atomicOr(&s_mrun[2 * wl + (tyf >> 5)], 1u << (tyf & 31u));
                 p.migrate_to[r0 + f] = -1;
             }
-            if (p.batch_head) p.batch_head[r0 + f] = -1;
-            if (p.mig_on) {
+            if (kNext && p.batch_head) p.batch_head[r0 + f] = -1;
+            if (kNext && p.mig_on) {
                 if (mig) {
                     atomicAdd(&p.H[(size_t)(R + tyf) * Lv + lv], 1u);
                     atomicAdd(&s_rcnt[R + tyf], 1u);
@@ -1131,7 +1133,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
         } else if (aff == 1u) {
             f = s_wfru[k];
         }
-        if (p.mig_on && aff == 1u && s_mq[k] == 1u && !((s_mrun[2 * wl + (t >> 5)] >> (t & 31u)) & 1u) &&
+        if (kNext && p.mig_on && aff == 1u && s_mq[k] == 1u && !((s_mrun[2 * wl + (t >> 5)] >> (t & 31u)) & 1u) &&
             (s_mqrow[k] & 0x80000000u)) {
             const uint32_t fm = s_mqrow[k] & 0x7FFFFFFFu;   // the session's sole queued future moves
             flg[fm] |= FL_MIG;

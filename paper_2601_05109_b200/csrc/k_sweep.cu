@@ -40,46 +40,36 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-template <bool kOut, bool kProf = false>
+template <bool kOut, bool kProf, bool kIn, bool kNext>
 __device__ __forceinline__ void k1_entry(const SweepParams& p, uint8_t* smem) {
     // an invalid table (K0's verdict, complete before the zero kernel ran)
     // is never swept: nalar_step queues this kernel before the host has seen it
     if (!p.stream_in && *p.verdict) return;
     const uint32_t b = p.blk_order[blockIdx.x];
-    if (p.blk_staged[b]) k1_body<true, kOut, kProf>(p, smem, b);
-    else k1_body<false, kOut, kProf>(p, smem, b);
+    if (p.blk_staged[b]) k1_body<true, kOut, kProf, kIn, kNext>(p, smem, b);
+    else k1_body<false, kOut, kProf, kIn, kNext>(p, smem, b);
 }
 
-// one CTA per SM: the latency-bound single-wave case (C4: 142 blocks)
-__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry<false>(p, smem);
-}
-
-// the same, also writing the per-row outputs to the caller's pinned arrays
-// (nalar_step's streamed outputs; a separate build so the plain epoch keeps
-// its code -- the stores in P3 cost the plain epoch 1.2 us when compiled in)
-__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep_out(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry<true>(p, smem);
-}
-
-// NALAR_F_PROFILE builds (the stamps compiled in; one / two CTAs per SM)
-__global__ void __launch_bounds__(kK1Threads, 1) k1_sweep_prof(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry<false, true>(p, smem);
-}
-__global__ void __launch_bounds__(kK1Threads, 2) k1_sweep_x2_prof(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry<false, true>(p, smem);
-}
-
-// two CTAs per SM (64 registers): tables of several waves (C5, 2^20 futures),
-// where a second resident block hides the sweeps' dependent latencies
-__global__ void __launch_bounds__(kK1Threads, 2) k1_sweep_x2(SweepParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    k1_entry<false>(p, smem);
-}
+// K1 builds.  Code compiled into the sweep costs the plain epoch even when a
+// runtime flag skips it (measured: streamed-output stores in P3 +1.2 us at C4,
+// the NALAR_F_PROFILE stamps +1.1 us at C4 and +7.5 us at C5), so each mode
+// has its own build: <outputs to host, profile stamps, streamed staging,
+// NEXT-1/4 marks> x {one CTA per SM (a one-wave table, C4), two (several
+// waves, C5: 64 registers)}.
+#define NALAR_K1_KERNEL(NAME, MINB, OUT, PROF, IN, NEXT)                        \
+    __global__ void __launch_bounds__(kK1Threads, MINB) NAME(SweepParams p) {    \
+        extern __shared__ __align__(128) uint8_t smem[];                         \
+        k1_entry<OUT, PROF, IN, NEXT>(p, smem);                                  \
+    }
+NALAR_K1_KERNEL(k1_sweep, 1, false, false, false, false)          // the plain epoch
+NALAR_K1_KERNEL(k1_sweep_x2, 2, false, false, false, false)
+NALAR_K1_KERNEL(k1_sweep_step, 1, true, false, true, false)       // nalar_step (streamed in / out)
+NALAR_K1_KERNEL(k1_sweep_step_x2, 2, false, false, true, false)
+NALAR_K1_KERNEL(k1_sweep_next, 1, false, false, false, true)      // HoL migration / batching on
+NALAR_K1_KERNEL(k1_sweep_next_x2, 2, false, false, false, true)
+NALAR_K1_KERNEL(k1_sweep_prof, 1, true, true, true, true)         // NALAR_F_PROFILE (every mode)
+NALAR_K1_KERNEL(k1_sweep_x2_prof, 2, true, true, true, true)
+#undef NALAR_K1_KERNEL
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once
 __global__ void k_zero(uint32_t* __restrict__ x, size_t n, unsigned long long* verdict) {
@@ -104,17 +94,13 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     int dev = 0;
     if (cudaError_t e = cudaGetDevice(&dev)) return e;
     size_t& configured = configured_dev[dev & 63];
+    static void* const kernels[8] = {(void*)k1_sweep, (void*)k1_sweep_x2, (void*)k1_sweep_step,
+                                     (void*)k1_sweep_step_x2, (void*)k1_sweep_next, (void*)k1_sweep_next_x2,
+                                     (void*)k1_sweep_prof, (void*)k1_sweep_x2_prof};
     if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k1_sweep_x2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k1_sweep_out, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k1_sweep_prof, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k1_sweep_x2_prof, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+        for (void* k : kernels)
+            if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+                return e;
         configured = smem;
     }
     // more blocks than one wave and two fit an SM: the 2-per-SM build
@@ -137,10 +123,14 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     // NALAR_K1_TRIGGER=0 / 1 / 2 = entry / after P2 / before P5)
     static const uint32_t trig = [] { const char* e = getenv("NALAR_K1_TRIGGER"); return e ? (uint32_t)atoi(e) : 2u; }();
     p.trig = trig;
-    if (p.prof) return x2 ? cudaLaunchKernelEx(&cfg, k1_sweep_x2_prof, p) : cudaLaunchKernelEx(&cfg, k1_sweep_prof, p);
-    if (p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin)
-        return cudaLaunchKernelEx(&cfg, k1_sweep_out, p);      // (one wave only: the host checks)
-    return x2 ? cudaLaunchKernelEx(&cfg, k1_sweep_x2, p) : cudaLaunchKernelEx(&cfg, k1_sweep, p);
+    // the build for this epoch's modes (streamed outputs: one-wave tables only, the host checks)
+    int k = 0;
+    if (p.prof) k = 6;
+    else if (p.stream_in || p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin) k = 2;
+    else if (p.mig_on || p.batch_head) k = 4;
+    if (x2 && !(k == 2 && (p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin))) ++k;
+    void* args[] = {&p};
+    return cudaLaunchKernelExC(&cfg, kernels[k], args);
 }
 
 
@@ -148,11 +138,10 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
 // launch, which waits for the device: see nalar_create, NALAR_COLL_PEER)
 cudaError_t preload_k_sweep() {
     cudaFuncAttributes a;
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep)) return e;
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_x2)) return e;
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_out)) return e;
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_prof)) return e;
-    if (cudaError_t e = cudaFuncGetAttributes(&a, k1_sweep_x2_prof)) return e;
+    for (const void* k : {(const void*)k1_sweep, (const void*)k1_sweep_x2, (const void*)k1_sweep_step,
+                          (const void*)k1_sweep_step_x2, (const void*)k1_sweep_next, (const void*)k1_sweep_next_x2,
+                          (const void*)k1_sweep_prof, (const void*)k1_sweep_x2_prof})
+        if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k_zero)) return e;
     return cudaSuccess;
 }
