@@ -237,7 +237,10 @@ __device__ void reassign_finish(const AssignParams& p, uint32_t blk, uint32_t* s
 
 }  // namespace
 
-template <bool kFused>
+// kAll: the NALAR_F_PROFILE stamps, resource reassignment (NEXT-2) and the
+// streamed-step paths compiled in; the plain epoch's build has none of them
+// (code in the body costs the epoch even when a runtime flag skips it)
+template <bool kFused, bool kAll = true, bool kProf = kAll>
 __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     __shared__ uint32_t s_inst[NALAR_MAX_INSTANCES_DEV];
     __shared__ uint32_t s_spare[NALAR_MAX_INSTANCES_DEV];   // spare before phase A
@@ -264,14 +267,14 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     unsigned long long ra_busy = 0, ra_cap = 0;      // NEXT-2 partials of this thread's instances
     uint64_t ra_best = ~0ull;
 
-    if (!p.stream_in && *p.verdict) return;   // an invalid table (K0): nothing to assign
+    if (!(kAll && p.stream_in) && *p.verdict) return;   // an invalid table (K0): nothing to assign
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     // type resources (the longest walks: phase B of a whole type) take the
     // lowest block indices, so they are the first to find a free SM while K1
     // is still running (PDL early launch)
     const uint32_t r = blk < p.n_types ? p.n_inst + blk : blk - p.n_types;
-    unsigned long long* prof = p.prof ? p.prof + (size_t)r * 8 : nullptr;
+    unsigned long long* prof = (kProf && p.prof) ? p.prof + (size_t)r * 8 : nullptr;
     if (prof && tid == 0) prof[0] = gtimer2();
     const bool is_type = r >= I;
     // ---- static data first: this kernel is a programmatic dependent of the
@@ -291,13 +294,13 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     const uint32_t cap_r = is_type ? 0u : p.i_cap[r], base_r = is_type ? 0u : p.i_base[r];
     const uint8_t aff = is_type ? p.t_aff[t] : 0;
     const uint32_t blk0 = tid < B ? p.blk_row0[tid] : 0u;
-    if (p.ra_on && tid < 64u && tid < p.n_types) {       // NEXT-2 directives (static)
+    if (kAll && p.ra_on && tid < 64u && tid < p.n_types) {       // NEXT-2 directives (static)
         s_tmin[tid] = p.t_min_inst ? p.t_min_inst[tid] : 0u;
         s_tmax[tid] = p.t_max_inst ? p.t_max_inst[tid] : 0xFFFFu;
     }
     // everything below reads the sweep's results
     if (!kFused) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (p.stream_in && *p.verdict) {
+    if (kAll && p.stream_in && *p.verdict) {
         // a streamed step's sweep found an invalid row: publish K0's words to
         // the host (read after the step's one synchronisation) and re-arm them
         if (blk == 0 && threadIdx.x == 0) {
@@ -342,7 +345,7 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     const uint32_t off0 = tid < B ? p.off_rb[(size_t)r * B + tid] : 0u;
     uint32_t ls0 = 0, ha0 = 0;
     uint64_t my_load = 0;                     // load of instance k == tid of the type (kept for NEXT-2)
-    const uint32_t ha_unp = (is_type && p.ra_on && tid == 0) ? p.tot[r] : 0u;   // unpinned eligible of t
+    const uint32_t ha_unp = (kAll && is_type && p.ra_on && tid == 0) ? p.tot[r] : 0u;   // unpinned eligible of t
     if (is_type) {
         if (tid < ni) { ls0 = p.load_sum[s_inst[tid]]; ha0 = p.tot[s_inst[tid]]; }
     } else if (tid == 0) {
@@ -529,10 +532,10 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
         }
     }
     if (prof && tid == 0) prof[2] = gtimer2();
-    if (p.ra_on) reassign_stats<kFused>(p, is_type, t, ni, ha_unp, ra_busy, ra_cap, ra_best, s_rb, s_rc, s_rbest);
+    if (kAll && p.ra_on) reassign_stats<kFused>(p, is_type, t, ni, ha_unp, ra_busy, ra_cap, ra_best, s_rb, s_rc, s_rbest);
     if (n_adm == 0) {
         if (prof && tid == 0) prof[3] = gtimer2();
-        if (p.ra_on) reassign_finish<kFused>(p, blk, &s_last, s_ts, s_tmin, s_tmax);
+        if (kAll && p.ra_on) reassign_finish<kFused>(p, blk, &s_last, s_ts, s_tmin, s_tmax);
         return;
     }
     k4_sync<kFused>();
@@ -656,9 +659,11 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
                     p.status[row] = 7;
                     p.instance[row] = inst;
                     p.new_pin[row] = (uint8_t)(is_type && aff != 0);
-                    if (p.o_status) p.o_status[row] = 7;
-                    if (p.o_instance) p.o_instance[row] = inst;
-                    if (p.o_new_pin) p.o_new_pin[row] = (uint8_t)(is_type && aff != 0);
+                    if (kAll) {
+                        if (p.o_status) p.o_status[row] = 7;
+                        if (p.o_instance) p.o_instance[row] = inst;
+                        if (p.o_new_pin) p.o_new_pin[row] = (uint8_t)(is_type && aff != 0);
+                    }
                     const uint32_t pos = list_base + s_LA[lv] + rank;
                     p.assign_row[pos] = row;
                     p.assign_inst[pos] = inst;
@@ -668,7 +673,7 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
         }
     }
     if (prof && tid == 0) prof[3] = gtimer2();
-    if (p.ra_on) reassign_finish<kFused>(p, blk, &s_last, s_ts, s_tmin, s_tmax);
+    if (kAll && p.ra_on) reassign_finish<kFused>(p, blk, &s_last, s_ts, s_tmin, s_tmax);
 }
 
 }  // namespace nalar

@@ -27,7 +27,12 @@
 
 namespace nalar {
 
-__global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) { k4_body<false>(p, blockIdx.x); }
+// the plain epoch's build, and one with the profile stamps, resource
+// reassignment (NEXT-2) and the streamed-step paths (see k4_body)
+__global__ void __launch_bounds__(kK4Threads, 1) k4_assign(AssignParams p) { k4_body<false, false>(p, blockIdx.x); }
+__global__ void __launch_bounds__(kK4Threads, 1) k4_assign_all(AssignParams p) { k4_body<false, true>(p, blockIdx.x); }
+// the plain build plus the profile stamps (what bench.py's spans time)
+__global__ void __launch_bounds__(kK4Threads, 1) k4_assign_prof(AssignParams p) { k4_body<false, false, true>(p, blockIdx.x); }
 
 
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
@@ -47,7 +52,9 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
     // 0.6 us faster (scripts/trig_sweep.sh).  NALAR_K4_PDL=0: plain launch.
     static const bool pdl = [] { const char* e = getenv("NALAR_K4_PDL"); return !e || atoi(e) != 0; }();
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k4_assign, p);
+    const bool all = p.ra_on || p.stream_in || p.o_status || p.o_instance || p.o_new_pin;
+    if (all) return cudaLaunchKernelEx(&cfg, k4_assign_all, p);
+    return p.prof ? cudaLaunchKernelEx(&cfg, k4_assign_prof, p) : cudaLaunchKernelEx(&cfg, k4_assign, p);
 }
 
 
@@ -56,6 +63,8 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s) {
 cudaError_t preload_k_assign() {
     cudaFuncAttributes a;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k4_assign)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k4_assign_all)) return e;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k4_assign_prof)) return e;
     return cudaSuccess;
 }
 

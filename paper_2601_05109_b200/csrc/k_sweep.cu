@@ -67,8 +67,9 @@ NALAR_K1_KERNEL(k1_sweep_step, 1, true, false, true, false)       // nalar_step 
 NALAR_K1_KERNEL(k1_sweep_step_x2, 2, false, false, true, false)
 NALAR_K1_KERNEL(k1_sweep_next, 1, false, false, false, true)      // HoL migration / batching on
 NALAR_K1_KERNEL(k1_sweep_next_x2, 2, false, false, false, true)
-NALAR_K1_KERNEL(k1_sweep_prof, 1, true, true, true, true)         // NALAR_F_PROFILE (every mode)
-NALAR_K1_KERNEL(k1_sweep_x2_prof, 2, true, true, true, true)
+NALAR_K1_KERNEL(k1_sweep_prof, 1, false, true, false, false)      // NALAR_F_PROFILE: the plain build + stamps
+NALAR_K1_KERNEL(k1_sweep_x2_prof, 2, false, true, false, false)   //   (what bench.py's spans time)
+NALAR_K1_KERNEL(k1_sweep_prof_all, 1, true, true, true, true)     // NALAR_F_PROFILE, any other mode
 #undef NALAR_K1_KERNEL
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once
@@ -94,9 +95,9 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     int dev = 0;
     if (cudaError_t e = cudaGetDevice(&dev)) return e;
     size_t& configured = configured_dev[dev & 63];
-    static void* const kernels[8] = {(void*)k1_sweep, (void*)k1_sweep_x2, (void*)k1_sweep_step,
+    static void* const kernels[9] = {(void*)k1_sweep, (void*)k1_sweep_x2, (void*)k1_sweep_step,
                                      (void*)k1_sweep_step_x2, (void*)k1_sweep_next, (void*)k1_sweep_next_x2,
-                                     (void*)k1_sweep_prof, (void*)k1_sweep_x2_prof};
+                                     (void*)k1_sweep_prof, (void*)k1_sweep_x2_prof, (void*)k1_sweep_prof_all};
     if (smem > 48 * 1024 && smem > configured) {
         for (void* k : kernels)
             if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
@@ -124,11 +125,13 @@ cudaError_t launch_sweep(const SweepParams& p_in, size_t smem, cudaStream_t s) {
     static const uint32_t trig = [] { const char* e = getenv("NALAR_K1_TRIGGER"); return e ? (uint32_t)atoi(e) : 2u; }();
     p.trig = trig;
     // the build for this epoch's modes (streamed outputs: one-wave tables only, the host checks)
+    const bool out = p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin;
+    const bool next = p.mig_on || p.batch_head;
     int k = 0;
-    if (p.prof) k = 6;
-    else if (p.stream_in || p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin) k = 2;
-    else if (p.mig_on || p.batch_head) k = 4;
-    if (x2 && !(k == 2 && (p.o_status || p.o_level || p.o_depth || p.o_instance || p.o_new_pin))) ++k;
+    if (p.prof) k = (p.stream_in || out || next) ? 8 : 6;
+    else if (p.stream_in || out) k = 2;
+    else if (next) k = 4;
+    if (x2 && k != 8 && !(k == 2 && out)) ++k;
     void* args[] = {&p};
     return cudaLaunchKernelExC(&cfg, kernels[k], args);
 }
@@ -140,7 +143,7 @@ cudaError_t preload_k_sweep() {
     cudaFuncAttributes a;
     for (const void* k : {(const void*)k1_sweep, (const void*)k1_sweep_x2, (const void*)k1_sweep_step,
                           (const void*)k1_sweep_step_x2, (const void*)k1_sweep_next, (const void*)k1_sweep_next_x2,
-                          (const void*)k1_sweep_prof, (const void*)k1_sweep_x2_prof})
+                          (const void*)k1_sweep_prof, (const void*)k1_sweep_x2_prof, (const void*)k1_sweep_prof_all})
         if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return e;
     if (cudaError_t e = cudaFuncGetAttributes(&a, k_zero)) return e;
     return cudaSuccess;
