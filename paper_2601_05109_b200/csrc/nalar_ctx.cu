@@ -411,9 +411,11 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
         const char* e = getenv("NALAR_LONG_WEIGHT");
         return e ? atof(e) : kLongWeight;
     }();
+    const bool unit_w = long_w == 1.0;          // the default: cost = rows
+    const uint32_t lr = long_rows();
     auto cost = [&](uint32_t w) {
         const uint32_t wr = wf_off[w + 1] - wf_off[w];
-        return wr >= long_rows() ? (uint64_t)(wr * long_w) : (uint64_t)wr;
+        return (unit_w || wr < lr) ? (uint64_t)wr : (uint64_t)(wr * long_w);
     };
     uint64_t total = 0;
     for (uint32_t w = 0; w < W; ++w) total += cost(w);
@@ -436,6 +438,8 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     // one greedy cut at a given per-block target; returns the block count
     auto cut = [&](uint64_t target) -> size_t {
         bw.clear(); br.clear(); be.clear(); bs.clear();
+        const size_t guess = (size_t)(total / std::max<uint64_t>(target, 1)) + 8;
+        bw.reserve(guess); br.reserve(guess); be.reserve(guess); bs.reserve(guess);
         size_t mx = 0;
         uint32_t w = 0;
         while (w < W) {
@@ -804,7 +808,9 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     // longest workflow's 32-row steps, then rows); CTAs are dispatched in
     // index order and a streamed step stages them in this order
     std::vector<uint32_t> order(c->B);
-    {
+    if (!fill_sms) {                 // a delta's layout (no streamed step): row order
+        for (uint32_t b = 0; b < c->B; ++b) order[b] = b;
+    } else {
         std::vector<uint64_t> cost(c->B);
         for (uint32_t b = 0; b < c->B; ++b) {
             uint32_t mx = 0;
