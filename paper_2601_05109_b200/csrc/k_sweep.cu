@@ -27,7 +27,7 @@
 // assignment pass (and, for G > 1, the allreduce) consumes.
 #include <algorithm>
 
-#include "k1_body.cuh"
+#include "internal.h"
 
 namespace nalar {
 
@@ -40,37 +40,19 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     return (b + 127) & ~(size_t)127;
 }
 
-template <bool kOut, bool kProf, bool kIn, bool kNext>
-__device__ __forceinline__ void k1_entry(const SweepParams& p, uint8_t* smem) {
-    // an invalid table (K0's verdict, complete before the zero kernel ran)
-    // is never swept: nalar_step queues this kernel before the host has seen it
-    if (!p.stream_in && *p.verdict) return;
-    const uint32_t b = p.blk_order[blockIdx.x];
-    if (p.blk_staged[b]) k1_body<true, kOut, kProf, kIn, kNext>(p, smem, b);
-    else k1_body<false, kOut, kProf, kIn, kNext>(p, smem, b);
-}
-
-// K1 builds.  Code compiled into the sweep costs the plain epoch even when a
-// runtime flag skips it (measured: streamed-output stores in P3 +1.2 us at C4,
-// the NALAR_F_PROFILE stamps +1.1 us at C4 and +7.5 us at C5), so each mode
-// has its own build: <outputs to host, profile stamps, streamed staging,
-// NEXT-1/4 marks> x {one CTA per SM (a one-wave table, C4), two (several
-// waves, C5: 64 registers)}.
-#define NALAR_K1_KERNEL(NAME, MINB, OUT, PROF, IN, NEXT)                        \
-    __global__ void __launch_bounds__(kK1Threads, MINB) NAME(SweepParams p) {    \
-        extern __shared__ __align__(128) uint8_t smem[];                         \
-        k1_entry<OUT, PROF, IN, NEXT>(p, smem);                                  \
-    }
-NALAR_K1_KERNEL(k1_sweep, 1, false, false, false, false)          // the plain epoch
-NALAR_K1_KERNEL(k1_sweep_x2, 2, false, false, false, false)
-NALAR_K1_KERNEL(k1_sweep_step, 1, true, false, true, false)       // nalar_step (streamed in / out)
-NALAR_K1_KERNEL(k1_sweep_step_x2, 2, false, false, true, false)
-NALAR_K1_KERNEL(k1_sweep_next, 1, false, false, false, true)      // HoL migration / batching on
-NALAR_K1_KERNEL(k1_sweep_next_x2, 2, false, false, false, true)
-NALAR_K1_KERNEL(k1_sweep_prof, 1, false, true, false, false)      // NALAR_F_PROFILE: the plain build + stamps
-NALAR_K1_KERNEL(k1_sweep_x2_prof, 2, false, true, false, false)   //   (what bench.py's spans time)
-NALAR_K1_KERNEL(k1_sweep_prof_all, 1, true, true, true, true)     // NALAR_F_PROFILE, any other mode
-#undef NALAR_K1_KERNEL
+// The nine K1 builds live in k1_kernels.cu, compiled once per build
+// (-DNALAR_K1_PART=0..8) so the objects compile in parallel.
+#define NALAR_K1_DECL(NAME) __global__ void NAME(SweepParams p);
+NALAR_K1_DECL(k1_sweep)
+NALAR_K1_DECL(k1_sweep_x2)
+NALAR_K1_DECL(k1_sweep_step)
+NALAR_K1_DECL(k1_sweep_step_x2)
+NALAR_K1_DECL(k1_sweep_next)
+NALAR_K1_DECL(k1_sweep_next_x2)
+NALAR_K1_DECL(k1_sweep_prof)
+NALAR_K1_DECL(k1_sweep_x2_prof)
+NALAR_K1_DECL(k1_sweep_prof_all)
+#undef NALAR_K1_DECL
 
 // clears the per-epoch exchange buffer and counters; lets the sweep launch at once
 __global__ void k_zero(uint32_t* __restrict__ x, size_t n, unsigned long long* verdict) {
