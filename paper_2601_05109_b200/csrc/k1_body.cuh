@@ -535,8 +535,31 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
             // saturation is applied once after convergence: with D the
             // unsaturated depth, min(M, 1 + max min(M, D_p)) = min(M, D_f)
             if (!wide) {
-                // the common case: at most 4 slots, and only as many shuffles
-                // per round as the step's widest row needs
+                // the common case: at most 4 slots (unused ones repeat slot
+                // 0).  One settle loop for every fan-in: K-specialised copies
+                // spread the step loop over more code than the SMSP's L0
+                // instruction cache holds
+#ifndef NALAR_K_VARIANTS
+                if (prof) n_kp += 1ull << (16 + 12 * 3);
+                for (;;) {
+                    uint32_t before = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (k == 3) before = d;    // converged once a round changes nothing
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile(
+                            "shfl.sync.idx.b32 %0, %4, %5, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %1, %4, %6, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %2, %4, %7, 31, -1;\n\t"
+                            "shfl.sync.idx.b32 %3, %4, %8, 31, -1;"
+                            : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                            : "r"(d), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
+                        d = has ? max(d, max(max(x0, x1), max(x2, x3)) + 1u) : d;
+                    }
+                    n_rounds += 4;
+                    if (!__any_sync(0xFFFFFFFFu, d != before)) break;
+                }
+#else
                 const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, np);
                 if (prof) n_kp += 1ull << (16 + 12 * ((K < 4 ? K : 4) - 1));
                 auto settle = [&](auto round) {
@@ -588,6 +611,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
                         d = has ? max(d, max(max(x0, x1), max(x2, x3)) + 1u) : d;
                     });
                 }
+#endif
             } else {
                 // a row with more than four in-step predecessors (a fan-in,
                 // e.g. the aggregate of many subtasks) reads the extra ones
@@ -770,6 +794,12 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
             const uint32_t am = pendf ? (((need_dep >> s0) & 1u) | (((need_dep >> s1) & 1u) << 1) |
                                          (((need_dep >> s2) & 1u) << 2) | (((need_dep >> s3) & 1u) << 3))
                                       : 0u;
+#ifndef NALAR_K_VARIANTS
+            // one settle per (NP, doomable): unused slots repeat slot 0, so
+            // K = 4 serves every fan-in (K-specialised copies cost more in
+            // instruction fetch than their spared shuffles, measured)
+#define NALAR_SETTLE2(NP_, A_) nit = settle_pairs<4, NP_, A_>(h0, h1, h2, h3, has, s0, s1, s2, s3, anc, am);
+#else
 #define NALAR_SETTLE2(NP_, A_)                                                                          \
             switch (K) {                                                                                \
                 case 1: nit = settle_pairs<1, NP_, A_>(h0, h1, h2, h3, has, s0, s1, s2, s3, anc, am); break;   \
@@ -777,6 +807,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
                 case 3: nit = settle_pairs<3, NP_, A_>(h0, h1, h2, h3, has, s0, s1, s2, s3, anc, am); break;   \
                 default: nit = settle_pairs<4, NP_, A_>(h0, h1, h2, h3, has, s0, s1, s2, s3, anc, am); break;  \
             }
+#endif
 #define NALAR_SETTLE(NP_) if (doomable) { NALAR_SETTLE2(NP_, true) } else { NALAR_SETTLE2(NP_, false) }
             if (NPw == 1u) { NALAR_SETTLE(1) }
             else if (NPw == 2u) { NALAR_SETTLE(2) }
