@@ -425,6 +425,11 @@ int nalar_epoch_stats_get(nalar_ctx* ctx, nalar_epoch_stats* stats);
  * *n_words = 2W + 8B + 8R + 4W + 8B. */
 int nalar_debug_profile(nalar_ctx* ctx, uint64_t* host, size_t cap_words, size_t* n_words);
 
+/* Diagnostics: the K1 block table of the uploaded table -- block b sweeps
+ * workflows [blk_wf[b], blk_wf[b + 1]); *n_words = B + 1.  NALAR_E_SIZE if
+ * cap_words is smaller (then *n_words says how many). */
+int nalar_debug_blocks(nalar_ctx* ctx, uint32_t* blk_wf, size_t cap_words, size_t* n_words);
+
 /* Device stream the ctx runs on (cudaStream_t). */
 void* nalar_stream(nalar_ctx* ctx);
 

@@ -57,7 +57,7 @@ NcclApi g_nccl;
 thread_local std::string g_create_err;   // nalar_last_error(NULL) after a failed nalar_create
 
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
-constexpr double kLongWeight = 1.0;             // cost per row of a long workflow (partition)
+constexpr double kLongWeight = 1.75;            // cost per row of a long workflow (partition)
 // K1 blocks of one wave (NALAR_K1_BLOCKS): a few SMs stay free for the
 // early-launched (PDL) K4 blocks; measured at C4: 148 blocks 48.5 us / epoch,
 // 145 46.1, 142 45.8, 138 48.8
@@ -405,8 +405,12 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
                bool fill_sms) {
     const uint32_t W = c->W;
     // balance by estimated cost, not rows: a long workflow's rows cost more
-    // (transfer + compose) and its compose chain is serial (weight 1 by
-    // default: measured neutral on C4; NALAR_LONG_WEIGHT to experiment)
+    // (a step transfer is ~3x a sweep step, and its compose chain is serial).
+    // Weight 1.75 (NALAR_LONG_WEIGHT): C4 epoch over four seeds 41.0 -> 39.9
+    // us mean (1.25: 40.4, 1.5: 40.0, 2: 39.9, 2.5: 40.3, 3: 39.9;
+    // scripts/part_sweep.py); C5 unchanged (120.5 us).  Without it a block
+    // could take two deep workflows and five short ones (1,418 rows), whose
+    // short sweeps then wait ~9 us behind the transfers for a warp
     static const double long_w = [] {
         const char* e = getenv("NALAR_LONG_WEIGHT");
         return e ? atof(e) : kLongWeight;
@@ -435,6 +439,9 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
     for (uint32_t w = 0; deep_alone && w < W; ++w) n_deep += wf_off[w + 1] - wf_off[w] >= 32u * deep_alone;
     const bool alone = deep_alone && n_deep <= kDeepAloneMax;
     auto is_deep = [&](uint32_t w) { return alone && wf_off[w + 1] - wf_off[w] >= 32u * deep_alone; };
+    // a workflow that would take a block further past the target than the
+    // block falls short without it starts the next block (NALAR_CUT_NEAREST)
+    static const bool nearest = [] { const char* e = getenv("NALAR_CUT_NEAREST"); return e && atoi(e) != 0; }();
     // one greedy cut at a given per-block target; returns the block count
     auto cut = [&](uint64_t target) -> size_t {
         bw.clear(); br.clear(); be.clear(); bs.clear();
@@ -451,7 +458,8 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
                 const uint32_t e_if = wf_eoff[w + 1] - wf_eoff[ws];
                 if (w > ws && ((k1_block_smem_upper(rows + wr, e_if, w - ws + 1, c->T) > kStageBudget &&
                                 k1_block_smem(rows + wr, e_if, w - ws + 1, c->T, true) > kStageBudget) ||
-                               w - ws + 1 > kMaxWfPerBlock || is_deep(w)))
+                               w - ws + 1 > kMaxWfPerBlock || is_deep(w) ||
+                               (nearest && cst + cost(w) > target && cst + cost(w) - target > target - cst)))
                     break;
                 rows += wr;
                 cst += cost(w);
@@ -1094,6 +1102,17 @@ int nalar_debug_profile(nalar_ctx* c, uint64_t* host, size_t cap, size_t* n_word
     if (!host || cap < c->prof_words) return NALAR_E_SIZE;
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(host, c->d_prof, 8 * c->prof_words, cudaMemcpyDeviceToHost));
+    return NALAR_OK;
+}
+
+int nalar_debug_blocks(nalar_ctx* c, uint32_t* host, size_t cap, size_t* n_words) {
+    if (!c || !n_words) return NALAR_E_INVAL;
+    DevGuard dg(c->cfg.device);
+    if (!c->uploaded) return fail(c, NALAR_E_STATE, "no table uploaded");
+    *n_words = (size_t)c->B + 1;
+    if (!host || cap < *n_words) return NALAR_E_SIZE;
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(host, c->d_blk_wf, 4 * *n_words, cudaMemcpyDeviceToHost));
     return NALAR_OK;
 }
 

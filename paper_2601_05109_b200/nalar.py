@@ -33,7 +33,7 @@ EXPORTS = ("nalar_abi_version", "nalar_workspace_bytes", "nalar_nccl_unique_id",
            "nalar_destroy", "nalar_snapshot_upload", "nalar_policy_epoch", "nalar_epoch_begin",
            "nalar_exchange_buffer", "nalar_epoch_finish", "nalar_fetch_decisions",
            "nalar_epoch_stats_get", "nalar_stream", "nalar_last_error", "nalar_debug_profile",
-           "nalar_debug_last_step_streamed",
+           "nalar_debug_last_step_streamed", "nalar_debug_blocks",
            "nalar_delta_apply", "nalar_set_policy_params", "nalar_peer_buffer", "nalar_peer_connect",
            "nalar_step")
 NALAR_DELTA_APPLY_ASSIGNED = 1
@@ -126,6 +126,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.nalar_epoch_stats_get.argtypes = [C.c_void_p, P(nalar_epoch_stats)]
     lib.nalar_debug_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]
     lib.nalar_debug_profile.restype = C.c_int
+    lib.nalar_debug_blocks.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_size_t)]
+    lib.nalar_debug_blocks.restype = C.c_int
     lib.nalar_debug_last_step_streamed.argtypes = [C.c_void_p]
     lib.nalar_debug_last_step_streamed.restype = C.c_int
     lib.nalar_delta_apply.argtypes = [C.c_void_p, P(nalar_delta), P(C.c_int64)]
@@ -279,6 +281,14 @@ def nalar_epoch_stats_get(h) -> nalar_epoch_stats:
     s = nalar_epoch_stats()
     _check(h, _lib.nalar_epoch_stats_get(h, C.byref(s)), "epoch_stats_get")
     return s
+
+
+def nalar_debug_blocks(h) -> np.ndarray:
+    n = C.c_size_t(0)
+    _lib.nalar_debug_blocks(h, None, 0, C.byref(n))
+    buf = np.zeros(n.value, np.uint32)
+    _check(h, _lib.nalar_debug_blocks(h, buf.ctypes.data, buf.size, C.byref(n)), "debug_blocks")
+    return buf
 
 
 def nalar_debug_profile(h) -> np.ndarray:

@@ -66,3 +66,17 @@ for j in (0, 4, 7, 1, 2, 5, 6, 3):
     if len(v):
         d = (v - k1_end) / 1e3
         print(f"  {names[j]:7s} med {np.median(d):6.2f} max {d.max():6.2f} n {len(v)}")
+bw = nalar.nalar_debug_blocks(ctx.h).astype(np.int64)
+blk_of = np.searchsorted(bw, np.arange(W), side="right") - 1
+maxd = None
+try:
+    from oracle import oracle_epoch
+    maxd = oracle_epoch(s, "srtf")["wf_agg"][:, 8]
+except Exception:
+    pass
+print("slowest blocks (p2 end), their workflows: rows/depth start-end us wait_kcyc")
+for b in np.argsort(-(blk[:, 7] - t0))[:5]:
+    ws = range(bw[b], bw[b + 1])
+    desc = "  ".join(f"{rows[w]}/{maxd[w] if maxd is not None else '?'} {start[w]:.1f}-{end[w]:.1f} w{(cyc[w, 3] >> 32) // 1000}"
+                     for w in ws)
+    print(f" blk {b} p2end {(blk[b, 7] - t0) / 1e3:.2f} rows {off[bw[b + 1]] - off[bw[b]]}: {desc}")
