@@ -121,7 +121,10 @@ struct SweepParams {
     const unsigned long long* verdict;   // K0's verdict: nonzero = invalid table, do nothing
     uint32_t stream_in;          // 1: rows come from `src` (host), validated here (verdict unused at entry)
     StreamIn src;
-    // CTA i sweeps block blk_order[i] (costliest first).  A streamed step paces
+    // CTA i sweeps block blk_order[8 i] (costliest first); words 8 i + 1..7
+    // are that block's first / end workflow, row and edge and its staged
+    // flag, so a CTA starts with one round trip of independent loads (not a
+    // chain through the block tables).  A streamed step paces
     // its host reads: CTA i >= stage_window issues its copies once
     // stage_ctr >= i - stage_window CTAs have staged (bounded wait), so the
     // costly blocks' rows cross PCIe first and their sweeps overlap the rest.

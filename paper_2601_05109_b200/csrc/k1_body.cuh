@@ -153,7 +153,8 @@ __device__ __forceinline__ bool doom_closure(bool doom, bool pend, uint32_t need
 // kIn: streamed-step staging / validation; kNext: HoL-migration candidates and
 // batch-head presets (the NEXT-1 / NEXT-4 modes) -- compiled in only where used
 template <bool kStaged, bool kOut = false, bool kProf = false, bool kIn = false, bool kNext = false>
-__device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uint32_t b) {
+__device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, const uint4 ca, const uint4 cb) {
+    const uint32_t b = ca.x;
     // NALAR_F_PROFILE stamps only in the profiling build: a null pointer known
     // at compile time removes every stamp and its branch from the production
     // sweep (code in P3 costs the plain epoch even when it never runs)
@@ -161,9 +162,9 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, uin
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t T = p.n_types, I = p.n_inst, R = p.R, Rh = p.Rh, Lv = p.levels;
 
-    const uint32_t w0 = p.blk_wf[b], w1 = p.blk_wf[b + 1];
-    const uint32_t r0 = p.blk_row0[b], r1 = p.blk_row0[b + 1];
-    const uint32_t e0 = p.blk_edge0[b], e1 = p.blk_edge0[b + 1];
+    const uint32_t w0 = ca.y, w1 = ca.z;
+    const uint32_t r0 = ca.w, r1 = cb.x;
+    const uint32_t e0 = cb.y, e1 = cb.z;
     const uint32_t nr = r1 - r0, ne = e1 - e0, nw = w1 - w0;
     constexpr bool staged = kStaged;
     unsigned long long* bprof = prof ? prof + (size_t)p.n_wf * 2 + b * 8 : nullptr;

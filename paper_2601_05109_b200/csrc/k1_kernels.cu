@@ -9,10 +9,12 @@ template <bool kOut, bool kProf, bool kIn, bool kNext>
 __device__ __forceinline__ void k1_entry(const SweepParams& p, uint8_t* smem) {
     // an invalid table (K0's verdict, complete before the zero kernel ran)
     // is never swept: nalar_step queues this kernel before the host has seen it
+    // this CTA's block record and the verdict: independent loads, one round trip
+    const uint4* rec = reinterpret_cast<const uint4*>(p.blk_order) + 2 * (size_t)blockIdx.x;
+    const uint4 ca = rec[0], cb = rec[1];
     if (!p.stream_in && *p.verdict) return;
-    const uint32_t b = p.blk_order[blockIdx.x];
-    if (p.blk_staged[b]) k1_body<true, kOut, kProf, kIn, kNext>(p, smem, b);
-    else k1_body<false, kOut, kProf, kIn, kNext>(p, smem, b);
+    if (cb.w) k1_body<true, kOut, kProf, kIn, kNext>(p, smem, ca, cb);
+    else k1_body<false, kOut, kProf, kIn, kNext>(p, smem, ca, cb);
 }
 
 // K1 builds.  Code compiled into the sweep costs the plain epoch even when a

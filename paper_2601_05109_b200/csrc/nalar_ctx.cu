@@ -199,6 +199,7 @@ struct nalar_ctx {
     std::vector<uint64_t> m_wf_id;
     std::vector<uint32_t> m_wf_off, m_wf_eoff;
     std::vector<uint32_t> m_perm;          // per-block task order (set_blocks)
+    std::vector<uint32_t> m_cta_rec;       // per-CTA K1 block records (set_blocks)
     std::vector<RebuildPlan> m_plan;       // delta scratch (nalar_delta_apply)
     bool blocks_valid = false;              // device block tables match m_wf_off / m_wf_eoff
     uint32_t blocks_T = 0;
@@ -290,7 +291,7 @@ bool plan_layout(const nalar_config* cfg, Plan* p) {
     p->blk_row0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_edge0 = L.take<uint32_t>(p->Bmax + 1);
     p->blk_staged = L.take<uint8_t>(p->Bmax);
-    p->blk_order = L.take<uint32_t>(p->Bmax);
+    p->blk_order = L.take<uint32_t>(8 * (size_t)p->Bmax);   // per-CTA block records (SweepParams)
     p->wf_perm = L.take<uint32_t>(W);
     p->type_off = L.take<uint32_t>(T + 1);
     p->type_inst = L.take<uint32_t>(I);
@@ -830,10 +831,19 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
             return cost[x] != cost[y] ? cost[x] > cost[y] : x < y;
         });
     }
+    // per-CTA block records: {block, w0, w1, r0, r1, e0, e1, staged}
+    std::vector<uint32_t>& rec = c->m_cta_rec;
+    rec.resize(8ull * c->B);
+    for (uint32_t i = 0; i < c->B; ++i) {
+        const uint32_t b = order[i];
+        uint32_t* o = rec.data() + 8ull * i;
+        o[0] = b; o[1] = bw[b]; o[2] = bw[b + 1]; o[3] = br[b];
+        o[4] = br[b + 1]; o[5] = be[b]; o[6] = be[b + 1]; o[7] = bs[b];
+    }
     const Part parts[6] = {
         {2, bw.data(), 4ull * bw.size(), c->d_blk_wf}, {3, br.data(), 4ull * br.size(), c->d_blk_row0},
         {4, be.data(), 4ull * be.size(), c->d_blk_edge0}, {5, bs.data(), bs.size(), c->d_blk_staged},
-        {6, c->m_perm.data(), 4ull * c->W, c->d_wf_perm}, {7, order.data(), 4ull * c->B, c->d_blk_order}};
+        {6, c->m_perm.data(), 4ull * c->W, c->d_wf_perm}, {7, rec.data(), 4ull * rec.size(), c->d_blk_order}};
     for (const Part& q : parts) {
         if (!q.bytes) continue;
         memcpy(c->h_tab + c->tab_off[q.slot], q.src, q.bytes);
@@ -1005,7 +1015,7 @@ int nalar_create(nalar_ctx** out, const nalar_config* cfg) {
         return bail(NALAR_E_NOMEM);
     {
         const size_t Tm = cfg->max_types, Im = cfg->max_instances, Wm = cfg->max_workflows, Bm = c->Bmax;
-        const size_t sz[8] = {4 * (Tm + 1), 4 * Im, 4 * (Bm + 1), 4 * (Bm + 1), 4 * (Bm + 1), Bm, 4 * Wm, 4 * Bm};
+        const size_t sz[8] = {4 * (Tm + 1), 4 * Im, 4 * (Bm + 1), 4 * (Bm + 1), 4 * (Bm + 1), Bm, 4 * Wm, 32 * Bm};
         size_t o = 0;
         for (int k = 0; k < 8; ++k) { c->tab_off[k] = o; o += (sz[k] + 15) & ~(size_t)15; }
         if (cudaMallocHost(&c->h_tab, std::max<size_t>(o, 16)) != cudaSuccess) return bail(NALAR_E_NOMEM);
