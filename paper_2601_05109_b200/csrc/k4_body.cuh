@@ -267,7 +267,8 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     unsigned long long ra_busy = 0, ra_cap = 0;      // NEXT-2 partials of this thread's instances
     uint64_t ra_best = ~0ull;
 
-    if (!(kAll && p.stream_in) && *p.verdict) return;   // an invalid table (K0): nothing to assign
+    // the verdict is loaded with the first static loads below (one round trip)
+    const unsigned long long verdict = (kAll && p.stream_in) ? 0ull : *p.verdict;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t I = p.n_inst, R = p.R, Lv = p.levels, G = p.G, B = p.B;
     // type resources (the longest walks: phase B of a whole type) take the
@@ -279,11 +280,15 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
     const bool is_type = r >= I;
     // ---- static data first: this kernel is a programmatic dependent of the
     // sweep (PDL) and runs this part while the sweep is still working --------
+    // (this prologue runs beside K1's last ~2 us: its dependent loads are
+    // kept to verdict || type list bounds -> list -> caps, base loads)
     const uint32_t t = is_type ? r - I : p.i_type[r];
-    uint32_t ni = 0, k0 = 0;
+    const uint32_t k0 = is_type ? p.type_off[t] : 0u;
+    const uint32_t kend = is_type ? p.type_off[t + 1] : 0u;
+    const uint32_t cap_r = is_type ? 0u : p.i_cap[r], base_r = is_type ? 0u : p.i_base[r];
+    if (verdict) return;   // an invalid table (K0): nothing to assign
+    const uint32_t ni = kend - k0;
     if (is_type) {
-        k0 = p.type_off[t];
-        ni = p.type_off[t + 1] - k0;
         for (uint32_t k = tid; k < ni; k += kK4Threads) {
             const uint32_t i = p.type_inst[k0 + k];
             s_inst[k] = i;
@@ -291,7 +296,6 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
             s_sp2[k] = p.i_base[i];           // base load for now
         }
     }
-    const uint32_t cap_r = is_type ? 0u : p.i_cap[r], base_r = is_type ? 0u : p.i_base[r];
     const uint8_t aff = is_type ? p.t_aff[t] : 0;
     const uint32_t blk0 = tid < B ? p.blk_row0[tid] : 0u;
     if (kAll && p.ra_on && tid < 64u && tid < p.n_types) {       // NEXT-2 directives (static)
