@@ -91,6 +91,25 @@ double time_graph(cudaStream_t st, F enqueue, int reps = 200, bool flush = true)
     return t[reps / 2] * 1e3;
 }
 
+template <class F>
+double time_plain(cudaStream_t st, F enqueue, int reps = 200) {
+    std::vector<cudaEvent_t> ev(2 * reps);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (int i = 0; i < 10; ++i) enqueue();
+    for (int i = 0; i < reps; ++i) {
+        CK(cudaMemsetAsync(g_flush, i & 0xFF, kFlush, st));
+        CK(cudaEventRecord(ev[2 * i], st));
+        enqueue();
+        CK(cudaEventRecord(ev[2 * i + 1], st));
+    }
+    CK(cudaStreamSynchronize(st));
+    std::vector<float> t(reps);
+    double sum = 0;
+    for (int i = 0; i < reps; ++i) { CK(cudaEventElapsedTime(&t[i], ev[2 * i], ev[2 * i + 1])); sum += t[i]; }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return sum / reps * 1e3;
+}
+
 static void launch_pdl(void (*k)(), cudaStream_t st, int blocks, int threads) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
@@ -122,6 +141,12 @@ int main() {
     CK(cudaMalloc(&src, 148ull << 16));
     CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
 
+    printf("plain stream launches, event to event, MEAN of 200, L2 flushed before each (us):\n");
+    printf("  1 empty kernel, 148x512             %7.2f\n", time_plain(st, [&] { k_empty<<<148, 512, 0, st>>>(); }));
+    printf("  3 empty kernels, 148x512            %7.2f\n", time_plain(st, [&] { for (int j = 0; j < 3; ++j) k_empty<<<148, 512, 0, st>>>(); }));
+    printf("  3 PDL kernels, 148x512              %7.2f\n", time_plain(st, [&] {
+               k_empty<<<148, 512, 0, st>>>();
+               for (int j = 1; j < 3; ++j) launch_pdl(k_pdl_empty, st, 148, 512); }));
     printf("graph, event to event, median of 200, L2 flushed before each (us):\n");
     printf("  1 empty kernel, 1 block             %7.2f\n", time_graph(st, [&] { k_empty<<<1, 32, 0, st>>>(); }));
     printf("  1 empty kernel, 148x512             %7.2f\n", time_graph(st, [&] { k_empty<<<148, 512, 0, st>>>(); }));
