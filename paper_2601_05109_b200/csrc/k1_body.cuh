@@ -908,16 +908,21 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
                     a0 = wait_flag(c0 + 32);
                     load_step(c0 + 32);
                 }
-                uint32_t best = 0;
-                bool dm = (c_av & 0x80u) != 0;
+                // (max,+) evaluation as a tree (the terms are independent; a
+                // slot >= k has byte 0): the step chain's longest ALU run
+                uint32_t a[kMaxIface + 1];
+                uint32_t dmk = 0;
 #pragma unroll
                 for (uint32_t i = 0; i < kMaxIface; ++i) {
                     const uint32_t by = i < 4 ? (c_tl >> (8 * i)) & 0xFFu : (c_th >> (8 * (i - 4))) & 0xFFu;
-                    best = (i < k && by) ? max(best, dx[i] + by - 1u) : best;
-                    dm |= i < k && ((c_av >> i) & 1u) && (fx[i] & FL_DOOMED);
+                    a[i] = by ? dx[i] + by - 1u : 0u;
+                    dmk |= (fx[i] & FL_DOOMED) ? 1u << i : 0u;
                 }
                 const uint32_t c7 = c_th >> 24;
-                best = c7 ? max(best, c7 - 1u) : best;
+                a[kMaxIface] = c7 ? c7 - 1u : 0u;
+                static_assert(kMaxIface == 7, "the tree below takes 8 terms");
+                const uint32_t best = max(max(max(a[0], a[1]), max(a[2], a[3])), max(max(a[4], a[5]), max(a[6], a[7])));
+                const bool dm = (c_av & 0x80u) != 0 || (dmk & c_av & ((1u << k) - 1u) & 0x7Fu) != 0;
                 d = min(best, 65535u);
                 allres = (c_av & 0x100u) != 0;
                 if (prof) { const long long t = clock64() + (long long)d; cyc_edge += t - cyc_t; cyc_t = t; }
