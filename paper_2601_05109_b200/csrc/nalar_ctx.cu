@@ -199,6 +199,10 @@ struct nalar_ctx {
     std::vector<uint64_t> m_wf_id;
     std::vector<uint32_t> m_wf_off, m_wf_eoff;
     std::vector<uint32_t> m_perm;          // per-block task order (set_blocks)
+    std::vector<uint32_t> m_tmp;           // set_blocks scratch
+    std::vector<uint64_t> m_spare_id;      // delta: the previous mirror, reused
+    std::vector<uint32_t> m_spare_off, m_spare_eoff;
+    std::vector<uint8_t> m_retired;
     std::vector<uint32_t> m_cta_rec;       // per-CTA K1 block records (set_blocks)
     std::vector<RebuildPlan> m_plan;       // delta scratch (nalar_delta_apply)
     bool blocks_valid = false;              // device block tables match m_wf_off / m_wf_eoff
@@ -787,6 +791,7 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     // task order inside each block: largest workflow first (longest-processing-
     // time-first list scheduling of workflows onto the block's warps)
     c->m_perm.resize(c->W);
+    if (c->m_tmp.size() < c->W) c->m_tmp.resize(c->W);
     for (size_t b = 0; b + 1 < bw.size(); ++b) {
         const uint32_t ws = bw[b], we = bw[b + 1];
         uint32_t* o = c->m_perm.data() + ws;
@@ -803,9 +808,19 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
             // many small workflows (a delta-mode table): only the long ones
             // need to start first -- a stable O(n) partition keeps the host
             // cost flat (a full sort per block is ~25 ns per workflow here)
-            std::stable_partition(o, o + (we - ws), [off, lr](uint32_t x) {
-                return off[x + 1] - off[x] >= lr;
-            });
+            // (by hand: std::stable_partition allocates a buffer per call,
+            // ~50 ns x 145 blocks per delta)
+            uint32_t n_long = 0;
+            for (uint32_t k = 0; k < we - ws; ++k) n_long += off[k + 1] - off[k] >= lr;
+            if (n_long && n_long < we - ws) {
+                uint32_t* tmp = c->m_tmp.data();
+                uint32_t a = 0, z = n_long;
+                for (uint32_t k = 0; k < we - ws; ++k) {
+                    if (off[k + 1] - off[k] >= lr) o[a++] = k;
+                    else tmp[z++ - n_long] = k;
+                }
+                std::copy(tmp, tmp + (we - ws - n_long), o + n_long);
+            }
         }
     }
     const double t2 = trace ? now() : 0;
@@ -1378,7 +1393,8 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
         return fail(c, NALAR_E_INVAL, "null delta array");
     const uint32_t W = c->W;
     // ---- host: the new workflow list (old minus retired, plus appended) ----
-    std::vector<uint8_t> retired(W, 0);
+    std::vector<uint8_t>& retired = c->m_retired;
+    retired.assign(W, 0);
     for (uint32_t k = 0; k < d->n_retired; ++k) {
         const auto it = std::lower_bound(c->m_wf_id.begin(), c->m_wf_id.end(), d->retired_wf_id[k]);
         if (it == c->m_wf_id.end() || *it != d->retired_wf_id[k]) {
@@ -1547,8 +1563,13 @@ int nalar_delta_apply(nalar_ctx* c, const nalar_delta* d, int64_t* err_index) {
     std::swap(c->d_state, c->alt.state); std::swap(c->d_type, c->alt.type); std::swap(c->d_round, c->alt.round);
     std::swap(c->d_exec, c->alt.exec); std::swap(c->d_pin, c->alt.pin); std::swap(c->d_eoff, c->alt.eoff);
     std::swap(c->d_edges, c->alt.edges);
-    std::vector<uint64_t> nid(W2);
-    std::vector<uint32_t> noff(W2 + 1), neoff(W2 + 1);
+    // the new host mirror (into the spare vectors of the last delta: no allocation)
+    std::vector<uint64_t>& nid = c->m_spare_id;
+    std::vector<uint32_t>& noff = c->m_spare_off;
+    std::vector<uint32_t>& neoff = c->m_spare_eoff;
+    nid.resize(W2);
+    noff.resize(W2 + 1);
+    neoff.resize(W2 + 1);
     for (uint32_t w = 0; w < W2; ++w) { nid[w] = plan[w].wf_id; noff[w] = plan[w].new_row0; neoff[w] = plan[w].new_edge0; }
     noff[W2] = N2; neoff[W2] = E2;
     c->m_wf_id.swap(nid); c->m_wf_off.swap(noff); c->m_wf_eoff.swap(neoff);
