@@ -59,9 +59,11 @@ thread_local std::string g_create_err;   // nalar_last_error(NULL) after a faile
 constexpr uint32_t kSmSplit = 148;              // B200 SMs: K1 grid target
 constexpr double kLongWeight = 1.75;            // cost per row of a long workflow (partition)
 // K1 blocks of one wave (NALAR_K1_BLOCKS): a few SMs stay free for the
-// early-launched (PDL) K4 blocks; measured at C4: 148 blocks 48.5 us / epoch,
-// 145 46.1, 142 45.8, 138 48.8
-constexpr uint32_t kK1Wave = 142;
+// early-launched (PDL) K4 blocks; measured at C4 (round 1): 148 blocks 48.5 us
+// / epoch, 145 46.1, 142 45.8, 138 48.8; re-measured after the round-2 K1
+// changes over four C4 seeds (scripts/part_sweep.py): 142 37.6-37.9 us, 143
+// 37.4, 144 36.9-37.4, 145 37.1, 147 37.6, 148 37.4
+constexpr uint32_t kK1Wave = 144;
 constexpr uint32_t kDeepAlone = 20;      // steps: a workflow this deep gets its own K1 block
 constexpr uint32_t kDeepAloneMax = 16;   // ... while there are at most this many
 constexpr size_t kStageBudget = 96 * 1024;      // max staged smem per K1 block
