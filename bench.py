@@ -305,6 +305,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--c3-epochs", type=int, default=60)
     ap.add_argument("--c5", type=int, default=1, help="also time the 2^20-future C5 table at N=1 (c5_g1)")
+    ap.add_argument("--c4-survey", type=int, default=1,
+                    help="also time C4 generated with SURVEY 8(d)'s recipe as written (c4_survey_recipe)")
     ap.add_argument("--collective", default="nccl", choices=["peer", "nccl"],
                     help="rank exchange for N > 1: the library's NCCL allreduce (default; the "
                          "north_star's collective), or kernels storing into peer memory (CUDA IPC)")
@@ -616,6 +618,40 @@ def main():
                          "kernels_us": sp5,
                          "roofline": roofline_of(s5, st5.n_eligible, sp5.get("k1_span"), None)}
         line["c5_g1"]["roofline"]["traffic"] = load_traffic("k1_sweep_c5")
+    if rank == 0 and world == 1 and args.c4_survey:
+        # C4 generated with SURVEY §8(d)'s recipe as written (base_load
+        # U{0..16}, rounds 1 + Geometric(0.3)) beside the benched, parity-tested
+        # generator (DESIGN.md §6 states the drift); same timing as the C4 line;
+        # its parity with the oracle is tests/test_parity_gpu.py::test_c4_survey_recipe
+        from nalar_gen import swe_table
+        sv = swe_table(1 << 17, args.seed, recipe="survey")
+        svctx = nalar.Context.for_snapshot(sv, device=local)
+        svctx.upload(sv)
+        svs = torch.cuda.ExternalStream(svctx.stream)
+        nsv = min(args.steps, 500)
+        evs = []
+        with torch.cuda.stream(svs):
+            for i in range(max(args.warmup, 3) + nsv):
+                flush.zero_()
+                a6, b6 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a6.record(svs)
+                svctx.epoch(pol)
+                b6.record(svs)
+                if i >= max(args.warmup, 3):
+                    evs.append((a6, b6))
+        torch.cuda.synchronize()
+        ussv = [x.elapsed_time(y) * 1e3 for x, y in evs]
+        stsv = svctx.stats()
+        svctx.close()
+        line["c4_survey_recipe"] = {
+            "workload": "C4 with SURVEY 8(d)'s generator recipe as written (base_load U{0..16}, "
+                        "rounds 1 + Geometric(0.3), cap 8)",
+            "futures": sv.n_futures, "workflows": sv.n_workflows, "edges": sv.n_edges, "epochs": nsv,
+            "epoch_us_mean": float(np.mean(ussv)), "epoch_us_p50": nearest_rank(ussv, 50),
+            "epoch_us_p99": nearest_rank(ussv, 99), "value": sv.n_futures / (float(np.mean(ussv)) * 1e-6),
+            "unit": "futures/s",
+            "counts": {"ready": stsv.n_ready, "eligible": stsv.n_eligible, "assigned": stsv.n_assigned,
+                       "doomed": stsv.n_doomed}}
     if rank == 0 and world == 1:
         from oracle import build_oracle
         build_oracle()

@@ -163,7 +163,7 @@ _ZIPF = np.array([1.0 / (k ** 1.1) for k in range(1, 9)])
 _ZIPF = _ZIPF / _ZIPF.sum()
 
 
-def _swe_workflow(rng, deep):
+def _swe_workflow(rng, deep, survey=False):
     """Returns (types, rounds, dep_preds, call_preds) in creation order."""
     types, rounds, deps, calls = [], [], [], []
 
@@ -177,7 +177,8 @@ def _swe_workflow(rng, deep):
         Rs = [int(rng.integers(40, 65)) for _ in range(S)]
     else:
         S = int(rng.integers(4, 13))
-        Rs = [min(8, int(rng.geometric(0.48))) for _ in range(S)]
+        # (survey: SURVEY.md 8(d) C4 as written, R = 1 + Geometric(0.3), cap 8)
+        Rs = [min(8, (1 + int(rng.geometric(0.3))) if survey else int(rng.geometric(0.48))) for _ in range(S)]
     last_run = [None] * S
     last_review = [None] * S
     for r in range(max(Rs)):
@@ -199,12 +200,18 @@ def _swe_workflow(rng, deep):
     return types, rounds, deps, calls
 
 
-def swe_table(n_futures: int, seed: int = 1, name: str = "C4", p_deep: float = 0.05) -> Snapshot:
+def swe_table(n_futures: int, seed: int = 1, name: str = "C4", p_deep: float = 0.05,
+              recipe: str = "default") -> Snapshot:
+    """recipe "default": the parity-tested and benched generator (DESIGN.md 6:
+    base_load U{0..4}, rounds Geometric(0.48)); "survey": SURVEY.md 8(d)'s C4
+    as written (base_load U{0..16}, rounds 1 + Geometric(0.3), both cap 8)."""
+    assert recipe in ("default", "survey")
+    survey = recipe == "survey"
     rng = np.random.default_rng(seed)
     n_inst = 64
     i_type = np.repeat(np.arange(8), 8)
     cap = np.full(n_inst, 16)
-    base = rng.integers(0, 5, n_inst)
+    base = rng.integers(0, 17 if survey else 5, n_inst)
     tb = TableBuilder(i_type=i_type, i_cap=cap, i_base_load=base, t_affinity=C4_AFFINITY,
                       name=f"{name}s{seed}")
     load = base.astype(np.int64).copy()
@@ -213,7 +220,7 @@ def swe_table(n_futures: int, seed: int = 1, name: str = "C4", p_deep: float = 0
     while tb.n_rows < n_futures:
         wid += 1
         deep = rng.random() < p_deep
-        types, rounds, deps, calls = _swe_workflow(rng, deep)
+        types, rounds, deps, calls = _swe_workflow(rng, deep, survey)
         n = len(types)
         left = n_futures - tb.n_rows
         if n > left:                      # truncate the last workflow to a row prefix

@@ -88,6 +88,13 @@ def test_c5_full_size():
     check(c5(1), "srtf")
 
 
+@pytest.mark.parametrize("pol", ["srtf", "lpt", "fcfs"])
+def test_c4_survey_recipe(pol):
+    """C4 generated with SURVEY 8(d)'s recipe as written (base_load U{0..16},
+    rounds 1 + Geometric(0.3)): bench.py's c4_survey_recipe table."""
+    check(swe_table(1 << 17, 1, recipe="survey"), pol)
+
+
 @pytest.mark.parametrize("flags", [2, 4, 6, 1])        # NO_GRAPH, FORCE_UNSTAGED, both, TIMING
 def test_launch_variants(flags):
     check(c2(1), "srtf", flags=flags)
