@@ -405,6 +405,28 @@ void destroy_graphs(nalar_ctx* c) {
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
 }
 
+// The compose threshold of a one-wave table.  A table whose long workflows
+// would give its blocks more than one round of step transfers (> 16 per
+// block of a full wave on average: the composers then wait for a second
+// ~3.5 us round) composes from one more step: C4 by SURVEY 8(d)'s recipe (80 %
+// of rows in workflows of >= 6 steps, 24.7 transfers per block) 42.7 -> 40.5 us
+// over four seeds at 7 steps (8: 41.0, 10: 43.4); the benched C4 generator
+// (9.8 per block) keeps 6 steps (7: +0.4 us).  Used by the partition's cost
+// model and the kernel alike.  NALAR_LONG_STEPS fixes the threshold;
+// NALAR_LONG_ADAPT=0 disables the rule.
+uint32_t one_wave_long_rows(const nalar_ctx* c, const uint32_t* wf_off) {
+    static const bool fixed = getenv("NALAR_LONG_STEPS") != nullptr;
+    static const bool adapt = [] { const char* e = getenv("NALAR_LONG_ADAPT"); return !e || atoi(e) != 0; }();
+    const uint32_t lr = long_rows();
+    if (!adapt || fixed) return lr;
+    uint64_t steps = 0;
+    for (uint32_t w = 0; w < c->W; ++w) {
+        const uint32_t r = wf_off[w + 1] - wf_off[w];
+        if (r >= lr) steps += (r + 31) / 32;
+    }
+    return steps > 16ull * kK1Wave ? lr + 32 : lr;
+}
+
 // Greedy partition of whole workflows into K1 blocks, balanced by rows.
 // wf_off[W+1]: first row of each workflow; wf_eoff[W+1]: first edge of each workflow
 void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, std::vector<uint32_t>& bw,
@@ -423,7 +445,7 @@ void partition(nalar_ctx* c, const uint32_t* wf_off, const uint32_t* wf_eoff, st
         return e ? atof(e) : kLongWeight;
     }();
     const bool unit_w = long_w == 1.0;          // the default: cost = rows
-    const uint32_t lr = long_rows();
+    const uint32_t lr = fill_sms ? one_wave_long_rows(c, wf_off) : long_rows();
     auto cost = [&](uint32_t w) {
         const uint32_t wr = wf_off[w + 1] - wf_off[w];
         return (unit_w || wr < lr) ? (uint64_t)wr : (uint64_t)(wr * long_w);
@@ -785,6 +807,7 @@ int set_blocks(nalar_ctx* c, CopyBatch* batch, bool fill_sms = true) {
     const double t1 = trace ? now() : 0;
     c->B = (uint32_t)bs.size();
     c->long_rows = long_rows(c->B > kSmSplit);      // several waves: throughput-bound
+    if (c->B <= kSmSplit) c->long_rows = one_wave_long_rows(c, c->m_wf_off.data());
     const uint32_t lr = c->long_rows;
     c->all_staged = std::all_of(bs.begin(), bs.end(), [](uint8_t x) { return x != 0; });
     c->fixed_smem = k1_fixed_smem(c->T, c->I, c->Rh);

@@ -1,4 +1,5 @@
-"""C4 epoch (4 seeds) under partition knobs, one process per setting:
+"""C4 epoch (4 seeds) under partition knobs, one process per setting
+(SWEEP_RECIPE=survey: SURVEY 8(d)'s generator recipe):
 NALAR_CUT_NEAREST, NALAR_LONG_WEIGHT, NALAR_DEEP_ALONE.  python scripts/part_sweep.py"""
 import os
 import subprocess
@@ -12,7 +13,7 @@ from paper_2601_05109_b200 import nalar
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 out = []
 for seed in (1, 2, 3, 4):
-    s = swe_table(1 << 17, seed)
+    s = swe_table(1 << 17, seed, recipe=os.environ.get("SWEEP_RECIPE", "default"))
     ctx = nalar.Context.for_snapshot(s); ctx.upload(s)
     st = torch.cuda.ExternalStream(ctx.stream); ev = []
     with torch.cuda.stream(st):
