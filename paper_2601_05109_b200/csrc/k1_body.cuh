@@ -413,12 +413,15 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
     // do not fit (wide interface / fan-in) fall back to the ordinary sweep step
     // in P2b.
     auto is_long = [&](uint32_t wi) { return wfo[wi + 1] - wfo[wi] >= p.long_rows; };
-    // long-step task prefix over workflows (warp 0), s_lpref[nw] = total
+    // long-step task prefix over the workflows in task order (s_perm: largest
+    // first, so the early composers' transfers lead the tickets; warp 0),
+    // s_lpref[nw] = total
     if (warp == 0) {
         uint32_t carry = 0, nlong = 0;
         for (uint32_t b0 = 0; b0 < nw; b0 += 32) {
-            const uint32_t wi = b0 + lane;
-            const uint32_t n = (wi < nw && is_long(wi)) ? (wfo[wi + 1] - wfo[wi] + 31u) / 32u : 0u;
+            const uint32_t j = b0 + lane;
+            const uint32_t wi = j < nw ? s_perm[j] : 0u;
+            const uint32_t n = (j < nw && is_long(wi)) ? (wfo[wi + 1] - wfo[wi] + 31u) / 32u : 0u;
             nlong += __popc(__ballot_sync(0xFFFFFFFFu, n != 0u));
             uint32_t incl = n;
 #pragma unroll
@@ -426,7 +429,7 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
                 const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
                 if (lane >= (uint32_t)o) incl += y;
             }
-            if (wi < nw) s_lpref[wi] = carry + incl - n;
+            if (j < nw) s_lpref[j] = carry + incl - n;
             carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
         if (lane == 0) { s_lpref[nw] = carry; s_cnt[3] = nlong; }
@@ -959,13 +962,28 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
         if (lane == 0) t = atomicAdd(s_ticket, 1u);
         t = __shfl_sync(0xFFFFFFFFu, t, 0);
         if (t < n_long_tasks) {
-            uint32_t lo = 0, hi = nw - 1;            // last workflow with s_lpref <= t
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) >> 1;
-                if (s_lpref[mid] <= t) lo = mid;
-                else hi = mid - 1;
+            // the two early composers' steps alternate (each composer gets its
+            // next step every other ticket), then the rest in task order
+            const uint32_t nA = s_lpref[1], nB = nw > 1 ? s_lpref[2] - s_lpref[1] : 0u;
+            const uint32_t m = min(nA, nB);
+            uint32_t wi, k;
+            if (t < 2u * m) {
+                wi = s_perm[t & 1u];
+                k = t >> 1;
+            } else if (t < nA + nB) {
+                wi = s_perm[nA > nB ? 0 : 1];
+                k = m + (t - 2u * m);
+            } else {
+                uint32_t lo = 2, hi = nw - 1;        // last position with s_lpref <= t
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    if (s_lpref[mid] <= t) lo = mid;
+                    else hi = mid - 1;
+                }
+                wi = s_perm[lo];
+                k = t - s_lpref[lo];
             }
-            transfer_step(wfo[lo] - r0 + 32u * (t - s_lpref[lo]), wfo[lo + 1] - r0);
+            transfer_step(wfo[wi] - r0 + 32u * k, wfo[wi + 1] - r0);
             continue;
         }
         if (t - n_long_tasks + n_early >= nw) break;
