@@ -950,8 +950,10 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
     };
 
     // Tasks by ticket (after the early composes above): every step transfer of
-    // the block's long workflows (P2a), then the remaining workflows largest
-    // first -- a long one is composed, a short one swept.  A composing warp
+    // the block's long workflows (P2a; the two early composers' steps
+    // alternating, then the other long workflows largest first), then the
+    // remaining workflows largest first -- a long one is composed, a short
+    // one swept.  A composing warp
     // follows its transfers step by step, waiting on the producer's release
     // flag.  Deadlock-free: a compose only ever waits on transfers, and every
     // transfer is claimed by one of the >= 14 warps not composing early, none

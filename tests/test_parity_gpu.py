@@ -88,6 +88,16 @@ def test_c5_full_size():
     check(c5(1), "srtf")
 
 
+@pytest.mark.parametrize("seed", [2, 3, 5, 8])
+def test_many_long_workflows_per_block(seed):
+    """Blocks holding several long (composed) workflows of unequal lengths:
+    the transfer tickets alternate between the two early composers' steps,
+    then follow the other long workflows largest first; also the adaptive
+    compose threshold (the survey recipe's transfer load)."""
+    for n in (24000, 50000):
+        check(swe_table(n, seed, recipe="survey"), ("srtf", "lpt", "fcfs")[seed % 3])
+
+
 @pytest.mark.parametrize("pol", ["srtf", "lpt", "fcfs"])
 def test_c4_survey_recipe(pol):
     """C4 generated with SURVEY 8(d)'s recipe as written (base_load U{0..16},
