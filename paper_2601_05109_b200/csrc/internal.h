@@ -13,6 +13,7 @@ namespace nalar {
 constexpr int kK0Threads = 256;          // validate: warp per workflow
 constexpr int kK1Threads = 512;          // sweep: warp per workflow inside a block
 constexpr int kK1Warps = kK1Threads / 32;
+constexpr int kP5Chunks = 4;             // K1 P5 buckets up to this many 512-row chunks in one pass
 constexpr uint32_t kLongSteps = 6;      // workflows of >= 6 steps use the transfer decomposition
 // the threshold in rows (kLongSteps steps; NALAR_LONG_STEPS to experiment)
 // rows from which a workflow is composed from step transfers.  A one-wave

@@ -189,6 +189,8 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
     sp += 4 * kK1Threads;
     uint32_t* s_wc = (uint32_t*)sp;
     sp += 4 * kK1Warps;
+    uint32_t* s_wcc = (uint32_t*)sp;                 // [kP5Chunks][kK1Warps] eligible counts (P5)
+    sp += 4 * kP5Chunks * kK1Warps;
     uint8_t* s_aff = sp;
 
     // ---- per-workflow tables (always in smem) -------------------------------
@@ -1242,10 +1244,82 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
         }
         __syncthreads();
     }
-    for (uint32_t t0 = 0; t0 < nr; t0 += kK1Threads) {
+    // Every 512-row chunk at once when the block has <= kP5Chunks of them and
+    // <= 512 eligible rows (one compaction, two barriers; chunk by chunk it
+    // took three barriers per chunk): per-(chunk, warp) counts, their
+    // exclusive prefix in (chunk, warp) = row order, the row-ordered list,
+    // then warp 0 buckets it by resource as below.
+    // (one-wave tables only: several waves are throughput-bound, where the
+    // extra reductions cost -- C5 +2.5 us)
+    const uint32_t nch = (nr + kK1Threads - 1) / kK1Threads;
+    bool p5_done = false;
+    if (p.B <= 148u && nch <= (uint32_t)kP5Chunks) {
+        uint32_t balc[kP5Chunks];
+        uint32_t ecnt = 0;
+#pragma unroll
+        for (int c = 0; c < kP5Chunks; ++c) {
+            balc[c] = 0u;
+            if ((uint32_t)c < nch) {
+                const uint32_t f = (uint32_t)c * kK1Threads + tid;
+                const uint32_t fl = f < nr ? flg[f] : 0u;
+                ecnt += __popc(__ballot_sync(0xFFFFFFFFu, (fl & FL_ELIG) != 0u));
+                balc[c] = __ballot_sync(0xFFFFFFFFu, (fl & (FL_ELIG | FL_MIG)) != 0u);
+                if (lane == 0) s_wcc[c * kK1Warps + warp] = __popc(balc[c]);
+            }
+        }
+        if (lane == 0 && ecnt) atomicAdd(&s_cnt[1], ecnt);
+        __syncthreads();
+        // the (chunk, warp) counts, four per lane, in row order
+        const uint32_t ncw = nch * kK1Warps;
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = lane * 4u + q < ncw ? s_wcc[lane * 4u + q] : 0u;
+        const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, v[0] + v[1] + v[2] + v[3]);
+        if (tot <= (uint32_t)kK1Threads) {
+#pragma unroll
+            for (int c = 0; c < kP5Chunks; ++c) {
+                if ((uint32_t)c >= nch) break;
+                const uint32_t e = (uint32_t)c * kK1Warps + warp;      // this warp's entry
+                // exclusive prefix of entry e: whole lanes before e / 4, then part of lane e / 4
+                uint32_t part = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) part += lane * 4u + q < e ? v[q] : 0u;
+                const uint32_t base = __reduce_add_sync(0xFFFFFFFFu, part);
+                const uint32_t f = (uint32_t)c * kK1Threads + tid;
+                if ((balc[c] >> lane) & 1u) s_list[base + __popc(balc[c] & ((1u << lane) - 1u))] = f;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                for (uint32_t j0 = 0; j0 < tot; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    const bool ok = j < tot;
+                    uint32_t r = 0xFFFFFFFFu, ff = 0;
+                    bool mg = false;
+                    if (ok) {
+                        ff = s_list[j];
+                        mg = !(flg[ff] & FL_ELIG);                  // a HoL candidate (NEXT-1)
+                        const int pinf = pn[ff];
+                        r = mg ? R + ty[ff] : (pinf >= 0 ? (uint32_t)pinf : I + ty[ff]);
+                    }
+                    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, r);
+                    const uint32_t rank = ok ? s_rcnt[r] + __popc(peers & ((1u << lane) - 1u)) : 0u;
+                    __syncwarp();
+                    if (ok) {
+                        p.items[r0 + s_roff[r] + rank] =
+                            make_uint2(r0 + ff, lev[ff] | (mg ? (uint32_t)(ex[ff] + 1) << 16 : 0u));
+                        if ((__ffs(peers) - 1) == (int)lane) s_rcnt[r] += __popc(peers);
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            p5_done = true;
+        }
+    }
+    for (uint32_t t0 = 0; !p5_done && t0 < nr; t0 += kK1Threads) {
         const uint32_t f = t0 + tid;
         const bool el = f < nr && (flg[f] & (FL_ELIG | FL_MIG));
-        {
+        if (p.B > 148u || nch > (uint32_t)kP5Chunks) {   // (counted above otherwise)
             const uint32_t be = __ballot_sync(0xFFFFFFFFu, f < nr && (flg[f] & FL_ELIG));
             if (lane == 0 && be) atomicAdd(&s_cnt[1], __popc(be));
         }

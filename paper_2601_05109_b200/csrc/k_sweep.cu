@@ -36,6 +36,7 @@ size_t k1_fixed_smem(uint32_t T, uint32_t I, uint32_t R) {
     b += 4 * (size_t)I;                             // in-flight counts
     b += 8 * (size_t)R;                             // per-resource count / offset
     b += 4 * (size_t)kK1Threads + 4 * kK1Warps;     // compaction list + warp counts
+    b += 4 * (size_t)kP5Chunks * kK1Warps;          // per-(chunk, warp) eligible counts (P5)
     b += (size_t)T;                                 // affinity
     return (b + 127) & ~(size_t)127;
 }
