@@ -1230,8 +1230,8 @@ __device__ __forceinline__ void k1_body(const SweepParams& p, uint8_t* smem, con
         }
         if (lane == 31) s_wc[warp] = incl;
         __syncthreads();
-        uint32_t wbase = 0;
-        for (uint32_t k = 0; k < warp; ++k) wbase += s_wc[k];
+        // the warps before this one, one lane each, summed by one reduction
+        const uint32_t wbase = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? s_wc[lane] : 0u);
         uint32_t run = wbase + incl - sum;
         for (uint32_t r = lo; r < hi; ++r) {
             const uint32_t c = s_rcnt[r];
