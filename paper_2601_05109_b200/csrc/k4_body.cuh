@@ -431,20 +431,25 @@ __device__ __forceinline__ void k4_body(const AssignParams& p, uint32_t blk) {
             base_part += s_wc[2][k];
         }
         bound = is_type ? bs : s_bound;
+        // number of this rank's futures admitted on r (closed form per level:
+        // every input is this thread's own), reduced across the barrier below
+        uint32_t adm_lv = 0;
+        if (tid < Lv) {
+            const uint64_t pre = (uint64_t)ag + s_before[tid];
+            if (pre < bound) {
+                const uint64_t room = bound - pre;
+                adm_lv = (uint32_t)(room < hl ? room : hl);
+            }
+        }
+        adm_lv = __reduce_add_sync(0xFFFFFFFFu, adm_lv);
+        if (lane == 0) s_red32[warp] = adm_lv;
         k4_sync<kFused>();
         if (tid < 3 * kK4Warps) s_wc[tid >> 3][tid & 7] = 0;
     }
     const uint32_t list_base = base_part;
-    // number of this rank's futures admitted on r (closed form per level)
-    uint32_t adm_lv = 0;
-    if (tid < Lv) {
-        const uint64_t pre = (uint64_t)s_A[tid] + s_before[tid];
-        if (pre < bound) {
-            const uint64_t room = bound - pre;
-            adm_lv = (uint32_t)(room < s_Hl[tid] ? room : s_Hl[tid]);
-        }
-    }
-    const uint32_t n_adm = block_sum<kFused, uint32_t>(adm_lv, s_red32);
+    uint32_t n_adm = 0;
+#pragma unroll
+    for (int k = 0; k < kK4Warps; ++k) n_adm += s_red32[k];
     if (prof && tid == 0) prof[1] = gtimer2();
     if (tid == 0) {
         p.n_adm[r] = n_adm;
