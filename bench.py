@@ -62,7 +62,8 @@ def workload_config(n_gpus, table, policy, collective="peer"):
                 if n_gpus > 1 else ""),
             "recipe_deviation": "generator drift from SURVEY §8(d) C4 (DESIGN.md §6): base_load U{0..4} "
                                 "(survey U{0..16}), rounds R = min(8, Geometric(0.48)) (survey 1 + "
-                                "Geometric(0.3), cap 8); the benched table is the parity-tested one"}
+                                "Geometric(0.3), cap 8); the benched table is the parity-tested one; "
+                                "the recipe as written is timed as c4_survey_recipe (N=1)"}
 
 
 def profile_spans(nalar, make_ctx, s, pol, flush, n=8):
